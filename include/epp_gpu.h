@@ -1,0 +1,151 @@
+/* epp-b200: C ABI of the B200 stage executor (libepp_gpu.so, sm_100a).
+ *
+ * The reference has no GPU code; this is the thin C ABI the
+ * paper's runtime would sit on.  One `epp_stage` owns the
+ * weights, gradients, optimizer state, per-sequence KV / dKV buffers (the
+ * paper's "global buffer for KV intermediate activations")
+ * and the saved activations of in-flight chunks for a contiguous range of
+ * transformer layers on one device.  The caller (one host thread / process
+ * per GPU) replays a plan document's per-stage op list: forward and backward
+ * calls per chunk, in the order of the reference schedule
+ * (proj/src/pipeline.cpp:96-297), moving the [T, hidden] activation /
+ * gradient between adjacent stages.
+ *
+ * Conventions
+ *   - return 0 on success, else EPP_GPU_E*; message in epp_gpu_last_error()
+ *     (thread-local).
+ *   - `stream` arguments are cudaStream_t passed as void*; all work is
+ *     stream-ordered, nothing synchronises unless stated.
+ *   - activations/gradients exchanged between stages: [T, hidden] row-major in
+ *     the stage dtype (bf16 or fp32); the caller owns them.
+ *   - a stage handle is single-threaded; distinct handles are independent.
+ */
+#ifndef EPP_GPU_H_
+#define EPP_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { EPP_GPU_OK = 0, EPP_GPU_EARG = 1, EPP_GPU_ECUDA = 2, EPP_GPU_ESTATE = 3, EPP_GPU_EOTHER = 4 };
+enum { EPP_ARCH_GPT = 0, EPP_ARCH_LLAMA = 1 };
+enum { EPP_DTYPE_F32 = 0, EPP_DTYPE_BF16 = 1 };
+/* chunk kinds, numbered as epp::ChunkKind (proj/include/epp/chunk.hpp:18) */
+enum { EPP_CHUNK_BATCHED = 0, EPP_CHUNK_SPLIT = 1, EPP_CHUNK_HYBRID = 2 };
+
+typedef struct epp_model_desc {
+    int32_t arch;        /* EPP_ARCH_GPT: LayerNorm+GELU+MHA; EPP_ARCH_LLAMA: RMSNorm+SwiGLU+GQA */
+    int32_t layers;      /* whole model */
+    int32_t hidden;
+    int32_t heads;
+    int32_t kv_heads;
+    int32_t head_dim;    /* 64 or 128 in bf16 mode */
+    int32_t ffn;         /* GELU: hidden -> ffn -> hidden; SwiGLU: gate/up of width ffn */
+    int32_t vocab;
+    float rope_theta;
+    float norm_eps;
+} epp_model_desc;
+
+/* One heterogeneous micro-batch, i.e. one epp::Chunk (chunk.hpp:32-46) plus
+ * the executor-side facts the plan document implies. */
+typedef struct epp_chunk_desc {
+    int32_t id;
+    int32_t seq;           /* owning long sequence of slices[0], -1 for Batched */
+    int32_t kind;          /* EPP_CHUNK_* */
+    int32_t tail;          /* no later slice of `seq` exists */
+    int64_t context;       /* tokens of `seq` before slices[0] */
+    int64_t seq_len;       /* total length of `seq` (sizes its KV buffer) */
+    int32_t nslices;
+    const int64_t* slices; /* host array, slices[0] primary */
+    int32_t ckpt_layers;   /* plan ckpt[stage][pos]: recompute this many layers */
+    float loss_scale;      /* last stage: d(loss)/d(sum of token losses) */
+    const int32_t* token_ids;   /* device [T]; required on the embedding stage */
+    const int32_t* target_ids;  /* device [T]; last stage; -1 = no target */
+} epp_chunk_desc;
+
+typedef struct epp_param_info {
+    const char* name;
+    int64_t numel;
+    float* master;     /* fp32 master weights (device) */
+    void* work;        /* working copy in the stage dtype (== master for fp32) */
+    float* grad;       /* fp32 gradient accumulator (device) */
+} epp_param_info;
+
+typedef struct epp_stage epp_stage;
+
+int epp_gpu_set_device(int device);
+
+int epp_stage_create(const epp_model_desc* model, int first_layer, int num_layers,
+                     int has_embed, int has_head, int dtype, epp_stage** out);
+int epp_stage_destroy(epp_stage* st);
+
+/* Deterministic N(0, 0.02) init (output projections scaled by 1/sqrt(2L)),
+ * norm weights 1, biases 0. */
+int epp_stage_init_weights(epp_stage* st, uint64_t seed, void* stream);
+int epp_stage_num_params(epp_stage* st, int32_t* n);
+int epp_stage_param(epp_stage* st, int32_t idx, epp_param_info* info);
+/* Re-derive working copies after the caller wrote `master` buffers. */
+int epp_stage_sync_weights(epp_stage* st, void* stream);
+
+/* Forward of one chunk over this stage's layers.  act_in: [T, hidden]
+ * (ignored on the embedding stage, which reads token_ids); act_out: [T,
+ * hidden] (ignored on the last stage, which computes the loss and the
+ * LM-head gradient instead).  Layers [0, ckpt_layers) of the stage keep only
+ * their inputs and are recomputed by the backward. */
+int epp_stage_forward(epp_stage* st, const epp_chunk_desc* chunk, const void* act_in,
+                      void* act_out, void* stream);
+/* Backward of one chunk: grad_in = d(loss)/d(act_out) (ignored on the last
+ * stage), grad_out = d(loss)/d(act_in) (ignored on the embedding stage).
+ * Accumulates parameter gradients; frees the chunk's saved activations, and
+ * the sequence's KV/dKV buffers once its first slice (context 0) is done. */
+int epp_stage_backward(epp_stage* st, const epp_chunk_desc* chunk, const void* grad_in,
+                       void* grad_out, void* stream);
+/* Explicit release of a sequence's KV / dKV buffers (normally automatic). */
+int epp_seq_release(epp_stage* st, int32_t seq);
+
+/* Last stage: accumulated (sum of token losses, #targets) since the last
+ * reset.  Synchronises `stream`. */
+int epp_stage_loss(epp_stage* st, double out[2], int32_t reset, void* stream);
+int epp_stage_zero_grads(epp_stage* st, void* stream);
+/* AdamW on fp32 masters (bias-corrected, step >= 1); zeroes the grads. */
+int epp_stage_adamw_step(epp_stage* st, float lr, float beta1, float beta2, float eps,
+                         float weight_decay, int32_t step, void* stream);
+/* Device bytes held by this stage's in-flight chunks and sequences. */
+int epp_stage_memory(epp_stage* st, int64_t* live_bytes, int64_t* peak_bytes);
+
+/* ---- kernel-level entry points (unit tests, benchmarks) ------------------ */
+/* C[M,N] = epi(A(m,k) B(n,k)); *_kmajor selects the operand layout
+ * (kernels.h GemmArgs); epi: 0 store, 1 fp32 accumulate, 2 add residual R,
+ * 3 store fp32. */
+int epp_kernel_gemm(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda,
+                    int32_t a_kmajor, const void* B, int64_t ldb, int32_t b_kmajor, void* C,
+                    int64_t ldc, const void* R, int64_t ldr, int32_t epi, int32_t dtype,
+                    void* stream);
+/* Slice-causal attention over nseg segments (host arrays).  Segment i: query
+ * rows [q_start[i], +q_len[i]) of q/o, keys at k[i]/v[i] (row stride
+ * Hkv*hd), kv_ctx[i] context keys before the first query. lse: [H, T] log2. */
+int epp_kernel_attention_fwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, float scale,
+                             int32_t nseg, const int32_t* q_start, const int32_t* q_len,
+                             const int32_t* kv_ctx, const void* const* k, const void* const* v,
+                             const void* q, void* o, float* lse, int32_t dtype, void* stream);
+/* Backward; dk/dv (fp32, per segment, same row layout as k/v) are ACCUMULATED
+ * into, dq (fp32 [T,H,hd]) is written. */
+int epp_kernel_attention_bwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, float scale,
+                             int32_t nseg, const int32_t* q_start, const int32_t* q_len,
+                             const int32_t* kv_ctx, const void* const* k, const void* const* v,
+                             float* const* dk, float* const* dv, const void* q, const void* o,
+                             const float* lse, const void* dout, float* dq, int32_t dtype,
+                             void* stream);
+
+const char* epp_gpu_last_error(void);
+/* Kernel launches issued by this library in this process (for bench claims). */
+int64_t epp_gpu_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EPP_GPU_H_ */

@@ -97,7 +97,7 @@ def build_gpu(force: bool = False) -> Path | None:
         list(ex.map(_run, jobs))
     if force or jobs or _stale(GPU_SO, objs):
         _run([NVCC, "-shared"] + GPU_ARCH + ["-o", str(GPU_SO)] + [str(o) for o in objs]
-             + ["-lcuda", "-lcublas"])
+ )
     return GPU_SO
 
 

@@ -1,0 +1,141 @@
+// epp-b200: kernel-level C ABI (include/epp_gpu.h epp_kernel_*) used by the
+// unit tests and micro-benchmarks to drive single kernels on raw pointers.
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "epp_gpu.h"
+#include "kernels.h"
+
+namespace eppk {
+namespace {
+thread_local std::string g_kerr;
+
+template <typename F>
+int kguard(F&& f) {
+    g_kerr.clear();
+    try {
+        f();
+        return EPP_GPU_OK;
+    } catch (const CudaError& e) {
+        g_kerr = e.what();
+        return EPP_GPU_ECUDA;
+    } catch (const std::invalid_argument& e) {
+        g_kerr = e.what();
+        return EPP_GPU_EARG;
+    } catch (const std::exception& e) {
+        g_kerr = e.what();
+        return EPP_GPU_EOTHER;
+    }
+}
+
+// Build + upload segment table and work lists for a standalone attention call.
+struct AttnTables {
+    void* segs = nullptr;
+    void* qw = nullptr;
+    void* kw = nullptr;
+    int nq = 0, nk = 0;
+    cudaStream_t s;
+    AttnTables(int nseg, const int32_t* q_start, const int32_t* q_len, const int32_t* kv_ctx,
+               const void* const* k, const void* const* v, float* const* dk, float* const* dv,
+               cudaStream_t st)
+        : s(st) {
+        std::vector<AttnSeg> sg(nseg);
+        std::vector<AttnWork> q, kk;
+        for (int i = 0; i < nseg; ++i) {
+            sg[i] = AttnSeg{};
+            sg[i].q_start = q_start[i];
+            sg[i].q_len = q_len[i];
+            sg[i].kv_ctx = kv_ctx[i];
+            sg[i].k = k[i];
+            sg[i].v = v[i];
+            sg[i].dk = dk ? dk[i] : nullptr;
+            sg[i].dv = dv ? dv[i] : nullptr;
+            for (int b = 0; b * kAttnBlock < q_len[i]; ++b) q.push_back({i, b});
+            for (int b = 0; b * kAttnBlock < kv_ctx[i] + q_len[i]; ++b) kk.push_back({i, b});
+        }
+        nq = static_cast<int>(q.size());
+        nk = static_cast<int>(kk.size());
+        EPP_CUDA(cudaMalloc(&segs, sizeof(AttnSeg) * (nseg ? nseg : 1)));
+        EPP_CUDA(cudaMalloc(&qw, sizeof(AttnWork) * (nq ? nq : 1)));
+        EPP_CUDA(cudaMalloc(&kw, sizeof(AttnWork) * (nk ? nk : 1)));
+        EPP_CUDA(cudaMemcpy(segs, sg.data(), sizeof(AttnSeg) * nseg, cudaMemcpyHostToDevice));
+        EPP_CUDA(cudaMemcpy(qw, q.data(), sizeof(AttnWork) * nq, cudaMemcpyHostToDevice));
+        EPP_CUDA(cudaMemcpy(kw, kk.data(), sizeof(AttnWork) * nk, cudaMemcpyHostToDevice));
+    }
+    ~AttnTables() {
+        cudaStreamSynchronize(s);
+        cudaFree(segs);
+        cudaFree(qw);
+        cudaFree(kw);
+    }
+};
+}  // namespace
+}  // namespace eppk
+
+extern "C" {
+
+int epp_kernel_gemm(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_kmajor,
+                    const void* B, int64_t ldb, int32_t b_kmajor, void* C, int64_t ldc,
+                    const void* R, int64_t ldr, int32_t epi, int32_t dtype, void* stream) {
+    return eppk::kguard([&] {
+        eppk::GemmArgs g;
+        g.M = M; g.N = N; g.K = K;
+        g.A = A; g.lda = lda; g.a_kmajor = a_kmajor != 0;
+        g.B = B; g.ldb = ldb; g.b_kmajor = b_kmajor != 0;
+        g.C = C; g.ldc = ldc; g.R = R; g.ldr = ldr;
+        EPP_REQUIRE(epi >= 0 && epi <= 3, "bad epilogue");
+        g.epi = static_cast<eppk::Epi>(epi);
+        g.dtype = static_cast<eppk::DType>(dtype);
+        eppk::gemm(g, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int epp_kernel_attention_fwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, float scale, int32_t nseg,
+                             const int32_t* q_start, const int32_t* q_len, const int32_t* kv_ctx,
+                             const void* const* k, const void* const* v, const void* q, void* o,
+                             float* lse, int32_t dtype, void* stream) {
+    return eppk::kguard([&] {
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        eppk::AttnTables tb(nseg, q_start, q_len, kv_ctx, k, v, nullptr, nullptr, s);
+        eppk::AttnArgs a;
+        a.segs = static_cast<const eppk::AttnSeg*>(tb.segs);
+        a.nseg = nseg;
+        a.qwork = static_cast<const eppk::AttnWork*>(tb.qw);
+        a.nqwork = tb.nq;
+        a.kwork = static_cast<const eppk::AttnWork*>(tb.kw);
+        a.nkwork = tb.nk;
+        a.T = T; a.H = H; a.Hkv = Hkv; a.hd = hd; a.layer = 0; a.scale = scale;
+        a.dtype = static_cast<eppk::DType>(dtype);
+        a.q = q; a.o = o; a.lse = lse;
+        eppk::attn_fwd(a, s);
+    });
+}
+
+int epp_kernel_attention_bwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, float scale, int32_t nseg,
+                             const int32_t* q_start, const int32_t* q_len, const int32_t* kv_ctx,
+                             const void* const* k, const void* const* v, float* const* dk,
+                             float* const* dv, const void* q, const void* o, const float* lse,
+                             const void* dout, float* dq, int32_t dtype, void* stream) {
+    return eppk::kguard([&] {
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        eppk::AttnTables tb(nseg, q_start, q_len, kv_ctx, k, v, dk, dv, s);
+        float* delta = nullptr;
+        EPP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&delta), sizeof(float) * H * (T ? T : 1), s));
+        eppk::AttnArgs a;
+        a.segs = static_cast<const eppk::AttnSeg*>(tb.segs);
+        a.nseg = nseg;
+        a.qwork = static_cast<const eppk::AttnWork*>(tb.qw);
+        a.nqwork = tb.nq;
+        a.kwork = static_cast<const eppk::AttnWork*>(tb.kw);
+        a.nkwork = tb.nk;
+        a.T = T; a.H = H; a.Hkv = Hkv; a.hd = hd; a.layer = 0; a.scale = scale;
+        a.dtype = static_cast<eppk::DType>(dtype);
+        a.q = q; a.o = const_cast<void*>(o); a.lse = const_cast<float*>(lse);
+        a.dout = dout; a.delta = delta; a.dq = dq;
+        eppk::attn_bwd(a, s);
+        EPP_CUDA(cudaFreeAsync(delta, s));
+    });
+}
+
+}  // extern "C"

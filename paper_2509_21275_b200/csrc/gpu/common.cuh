@@ -1,0 +1,78 @@
+// epp-b200 GPU executor: shared device helpers (sm_100a only).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace eppk {
+
+typedef __nv_bfloat16 bf16;
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define EPP_CUDA(call)                                                                   \
+    do {                                                                                 \
+        cudaError_t err_ = (call);                                                       \
+        if (err_ != cudaSuccess)                                                         \
+            throw ::eppk::CudaError(std::string(#call " failed: ") +                    \
+                                    cudaGetErrorString(err_) + " at " __FILE__ ":" +     \
+                                    std::to_string(__LINE__));                           \
+    } while (0)
+
+// Every kernel launch is followed by EPP_CHECK_LAUNCH(), which also feeds the
+// process-wide launch counter reported by epp_gpu_kernel_launches().
+long long& launch_counter();
+#define EPP_CHECK_LAUNCH()                                                               \
+    do {                                                                                 \
+        EPP_CUDA(cudaGetLastError());                                                    \
+        ++::eppk::launch_counter();                                                      \
+    } while (0)
+
+#define EPP_REQUIRE(cond, msg)                                                           \
+    do {                                                                                 \
+        if (!(cond)) throw std::invalid_argument(std::string("epp: ") + (msg));          \
+    } while (0)
+
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(bf16 x) { return __bfloat162float(x); }
+template <typename T> __device__ __forceinline__ T from_f(float x);
+template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ bf16 from_f<bf16>(float x) { return __float2bfloat16_rn(x); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide sum for blockDim.x <= 1024; `scratch` holds >= 32 floats.
+__device__ __forceinline__ float block_sum(float v, float* scratch) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    const int nw = (blockDim.x + 31) >> 5;
+    v = (threadIdx.x < nw) ? scratch[threadIdx.x] : 0.f;
+    if (wid == 0) v = warp_sum(v);
+    if (threadIdx.x == 0) scratch[0] = v;
+    __syncthreads();
+    const float r = scratch[0];
+    __syncthreads();
+    return r;
+}
+
+inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace eppk

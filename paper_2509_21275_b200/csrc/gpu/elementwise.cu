@@ -1,0 +1,720 @@
+// epp-b200: HBM-bound kernels of the stage executor — embedding, LayerNorm /
+// RMSNorm (fwd, bwd with fused residual add, recompute), RoPE + QKV scatter
+// into the per-segment KV rows and its inverse gather, GELU / SwiGLU, fused
+// softmax cross-entropy, AdamW and initialisation.  All are vectorised
+// (16-byte accesses), one CTA per row where a row reduction is needed.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace eppk {
+
+namespace {
+
+// ---- 8-wide vector load/store for float and bf16 -----------------------
+__device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load8(const bf16* p, float (&v)[8]) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(h[i]);
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+    }
+}
+__device__ __forceinline__ void store8(float* p, const float (&v)[8]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void store8(bf16* p, const float (&v)[8]) {
+    uint4 raw;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = raw;
+}
+
+template <typename F>
+void dispatch_t(DType t, F&& f) {
+    if (t == DType::F32) f(float{});
+    else f(bf16{});
+}
+
+int grid_for(long long n, int threads) {
+    const long long b = (n + threads - 1) / threads;
+    return static_cast<int>(b < 1 ? 1 : (b > 1048576 ? 1048576 : b));
+}
+
+// ------------------------------------------------------------ embedding ---
+template <typename T>
+__global__ void embed_fwd_k(const int32_t* ids, const T* table, T* out, int Tn, int D) {
+    const int t = blockIdx.x;
+    const T* src = table + static_cast<long long>(ids[t]) * D;
+    T* dst = out + static_cast<long long>(t) * D;
+    for (int c = threadIdx.x * 8; c < D; c += blockDim.x * 8) {
+        float v[8];
+        load8(src + c, v);
+        store8(dst + c, v);
+    }
+}
+template <typename T>
+__global__ void embed_bwd_k(const int32_t* ids, const T* dout, float* dtable, int Tn, int D) {
+    const int t = blockIdx.x;
+    float* dst = dtable + static_cast<long long>(ids[t]) * D;
+    const T* src = dout + static_cast<long long>(t) * D;
+    for (int c = threadIdx.x * 8; c < D; c += blockDim.x * 8) {
+        float v[8];
+        load8(src + c, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) atomicAdd(dst + c + i, v[i]);
+    }
+}
+
+// ---------------------------------------------------------------- norms ---
+// One CTA per row, two passes (mean, then centred variance), fp32 math.
+template <typename T>
+__global__ void norm_fwd_k(bool rms, const T* x, const T* w, const T* b, T* y, float* mean,
+                           float* rstd, int D, float eps) {
+    __shared__ float scratch[32];
+    const long long row = blockIdx.x;
+    const T* xr = x + row * D;
+    float s = 0.f;
+    for (int c = threadIdx.x * 8; c < D; c += blockDim.x * 8) {
+        float v[8];
+        load8(xr + c, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += v[i];
+    }
+    const float mu = rms ? 0.f : block_sum(s, scratch) / D;
+    float q = 0.f;
+    for (int c = threadIdx.x * 8; c < D; c += blockDim.x * 8) {
+        float v[8];
+        load8(xr + c, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) q += (v[i] - mu) * (v[i] - mu);
+    }
+    const float rs = rsqrtf(block_sum(q, scratch) / D + eps);
+    if (threadIdx.x == 0) {
+        if (mean) mean[row] = mu;
+        rstd[row] = rs;
+    }
+    for (int c = threadIdx.x * 8; c < D; c += blockDim.x * 8) {
+        float v[8], wv[8], bv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        load8(xr + c, v);
+        load8(w + c, wv);
+        if (b) load8(b + c, bv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = (v[i] - mu) * rs * wv[i] + bv[i];
+        store8(y + row * D + c, v);
+    }
+}
+
+template <typename T>
+__global__ void norm_apply_k(bool rms, const T* x, const T* w, const T* b, const float* mean,
+                             const float* rstd, T* y, int D) {
+    const long long row = blockIdx.x;
+    const float mu = rms ? 0.f : mean[row];
+    const float rs = rstd[row];
+    for (int c = threadIdx.x * 8; c < D; c += blockDim.x * 8) {
+        float v[8], wv[8], bv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        load8(x + row * D + c, v);
+        load8(w + c, wv);
+        if (b) load8(b + c, bv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = (v[i] - mu) * rs * wv[i] + bv[i];
+        store8(y + row * D + c, v);
+    }
+}
+
+constexpr int kNormRows = 16;     // rows per CTA in the backward (dw/db partials)
+constexpr int kNormMaxG = 8;      // vec8 groups per thread -> D <= 8192 at 128 threads
+
+template <typename T>
+__global__ void norm_bwd_k(bool rms, const T* x, const T* w, const T* dy, const float* mean,
+                           const float* rstd, const T* dres, T* dx, float* pw, float* pb,
+                           int Tn, int D) {
+    __shared__ float scratch[32];
+    float aw[kNormMaxG][8], ab[kNormMaxG][8];
+#pragma unroll
+    for (int g = 0; g < kNormMaxG; ++g)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) aw[g][i] = ab[g][i] = 0.f;
+    const int r0 = blockIdx.x * kNormRows;
+    for (int r = r0; r < min(Tn, r0 + kNormRows); ++r) {
+        const long long off = static_cast<long long>(r) * D;
+        const float mu = rms ? 0.f : mean[r];
+        const float rs = rstd[r];
+        float s1 = 0.f, s2 = 0.f;   // sum(dxhat), sum(dxhat * xhat)
+#pragma unroll
+        for (int g = 0; g < kNormMaxG; ++g) {
+            const int c = (g * blockDim.x + threadIdx.x) * 8;
+            if (c >= D) break;
+            float xv[8], wv[8], gv[8];
+            load8(x + off + c, xv);
+            load8(w + c, wv);
+            load8(dy + off + c, gv);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float xh = (xv[i] - mu) * rs;
+                const float dxh = gv[i] * wv[i];
+                s1 += dxh;
+                s2 += dxh * xh;
+                aw[g][i] += gv[i] * xh;
+                ab[g][i] += gv[i];
+            }
+        }
+        const float m1 = rms ? 0.f : block_sum(s1, scratch) / D;
+        const float m2 = block_sum(s2, scratch) / D;
+#pragma unroll
+        for (int g = 0; g < kNormMaxG; ++g) {
+            const int c = (g * blockDim.x + threadIdx.x) * 8;
+            if (c >= D) break;
+            float xv[8], wv[8], gv[8], out[8], rv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            load8(x + off + c, xv);
+            load8(w + c, wv);
+            load8(dy + off + c, gv);
+            if (dres) load8(dres + off + c, rv);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float xh = (xv[i] - mu) * rs;
+                out[i] = rv[i] + rs * (gv[i] * wv[i] - m1 - xh * m2);
+            }
+            store8(dx + off + c, out);
+        }
+    }
+    float* prow_w = pw + static_cast<long long>(blockIdx.x) * D;
+    float* prow_b = pb ? pb + static_cast<long long>(blockIdx.x) * D : nullptr;
+#pragma unroll
+    for (int g = 0; g < kNormMaxG; ++g) {
+        const int c = (g * blockDim.x + threadIdx.x) * 8;
+        if (c >= D) break;
+        store8(prow_w + c, aw[g]);
+        if (prow_b) store8(prow_b + c, ab[g]);
+    }
+}
+
+// dst[c] += sum_g part[g, c]  (deterministic column reduction)
+__global__ void col_reduce_add(const float* part, int G, int D, float* dst) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= D) return;
+    float s = 0.f;
+    for (int g = 0; g < G; ++g) s += part[static_cast<long long>(g) * D + c];
+    dst[c] += s;
+}
+
+// ----------------------------------------------------------------- RoPE ---
+// Rotate-half RoPE.  cos/sin come from a per-position table built in double
+// precision (positions reach ~2e5, where float angle products lose accuracy).
+struct RopeTable {
+    float2* cs = nullptr;   // [max_pos, hd/2] (cos, sin)
+    int max_pos = 0;
+    int half = 0;
+    float theta = 0.f;
+};
+
+__global__ void rope_table_k(float2* cs, int max_pos, int half, double theta) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<long long>(max_pos) * half) return;
+    const int pos = static_cast<int>(i / half), j = static_cast<int>(i % half);
+    const double inv = pow(theta, -2.0 * j / (2.0 * half));
+    double s, c;
+    sincos(pos * inv, &s, &c);
+    cs[i] = make_float2(static_cast<float>(c), static_cast<float>(s));
+}
+
+template <typename T>
+__global__ void rope_scatter_k(const T* qkv, T* q_out, const AttnSeg* segs, const int* tok_seg,
+                               const int* tok_pos, const float2* cs, int Tn, int H, int Hkv,
+                               int hd, int layer) {
+    const int half = hd / 2;
+    const int slots = H + 2 * Hkv;
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<long long>(Tn) * slots * half) return;
+    const int j = static_cast<int>(idx % half);
+    const int slot = static_cast<int>((idx / half) % slots);
+    const long long t = idx / (static_cast<long long>(half) * slots);
+    const T* src = qkv + t * slots * hd + static_cast<long long>(slot) * hd;
+    const int pos = tok_pos[t];
+    const AttnSeg& sg = segs[tok_seg[t]];
+    const long long kvrow = static_cast<long long>(pos) * Hkv * hd;
+    float x1 = to_f(src[j]), x2 = to_f(src[j + half]);
+    if (slot < H + Hkv) {
+        const float2 c = cs[static_cast<long long>(pos) * half + j];
+        const float y1 = x1 * c.x - x2 * c.y;
+        const float y2 = x2 * c.x + x1 * c.y;
+        x1 = y1;
+        x2 = y2;
+    }
+    T* dst;
+    if (slot < H) {
+        dst = q_out + (t * H + slot) * hd;
+    } else if (slot < H + Hkv) {
+        dst = const_cast<T*>(static_cast<const T*>(sg.k)) + layer * sg.kv_layer_stride + kvrow +
+              static_cast<long long>(slot - H) * hd;
+    } else {
+        dst = const_cast<T*>(static_cast<const T*>(sg.v)) + layer * sg.kv_layer_stride + kvrow +
+              static_cast<long long>(slot - H - Hkv) * hd;
+    }
+    dst[j] = from_f<T>(x1);
+    dst[j + half] = from_f<T>(x2);
+}
+
+template <typename T>
+__global__ void rope_gather_grad_k(const float* dq, const AttnSeg* segs, const int* tok_seg,
+                                   const int* tok_pos, const float2* cs, T* dqkv, int Tn, int H,
+                                   int Hkv, int hd, int layer) {
+    const int half = hd / 2;
+    const int slots = H + 2 * Hkv;
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<long long>(Tn) * slots * half) return;
+    const int j = static_cast<int>(idx % half);
+    const int slot = static_cast<int>((idx / half) % slots);
+    const long long t = idx / (static_cast<long long>(half) * slots);
+    const int pos = tok_pos[t];
+    const AttnSeg& sg = segs[tok_seg[t]];
+    const long long kvrow = static_cast<long long>(pos) * Hkv * hd;
+    const float* src;
+    if (slot < H)
+        src = dq + (t * H + slot) * hd;
+    else if (slot < H + Hkv)
+        src = sg.dk + layer * sg.dkv_layer_stride + kvrow + static_cast<long long>(slot - H) * hd;
+    else
+        src = sg.dv + layer * sg.dkv_layer_stride + kvrow +
+              static_cast<long long>(slot - H - Hkv) * hd;
+    float g1 = src[j], g2 = src[j + half];
+    if (slot < H + Hkv) {
+        const float2 c = cs[static_cast<long long>(pos) * half + j];
+        const float y1 = g1 * c.x + g2 * c.y;
+        const float y2 = g2 * c.x - g1 * c.y;
+        g1 = y1;
+        g2 = y2;
+    }
+    T* dst = dqkv + t * slots * hd + static_cast<long long>(slot) * hd;
+    dst[j] = from_f<T>(g1);
+    dst[j + half] = from_f<T>(g2);
+}
+
+// ------------------------------------------------------------ activation ---
+__device__ __forceinline__ float gelu_tanh(float x) {
+    const float k = 0.7978845608028654f;
+    return 0.5f * x * (1.f + tanhf(k * (x + 0.044715f * x * x * x)));
+}
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+    const float k = 0.7978845608028654f;
+    const float u = k * (x + 0.044715f * x * x * x);
+    const float t = tanhf(u);
+    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k * (1.f + 3.f * 0.044715f * x * x);
+}
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+
+template <typename T>
+__global__ void act_fwd_k(int act, const T* h, T* out, long long Tn, int F) {
+    const long long n8 = Tn * F / 8;
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n8;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long e = i * 8;
+        float v[8];
+        if (act == 0) {
+            load8(h + e, v);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = gelu_tanh(v[k]);
+        } else {
+            const long long t = e / F;
+            const int c = static_cast<int>(e % F);
+            float g[8], u[8];
+            load8(h + t * 2 * F + c, g);
+            load8(h + t * 2 * F + F + c, u);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = g[k] * sigmoidf_(g[k]) * u[k];
+        }
+        store8(out + e, v);
+    }
+}
+
+template <typename T>
+__global__ void act_bwd_k(int act, const T* h, const T* da, T* dh, long long Tn, int F) {
+    const long long n8 = Tn * F / 8;
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n8;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long e = i * 8;
+        float d[8];
+        load8(da + e, d);
+        if (act == 0) {
+            float x[8];
+            load8(h + e, x);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) d[k] *= gelu_tanh_grad(x[k]);
+            store8(dh + e, d);
+        } else {
+            const long long t = e / F;
+            const int c = static_cast<int>(e % F);
+            float g[8], u[8], dg[8], du[8];
+            load8(h + t * 2 * F + c, g);
+            load8(h + t * 2 * F + F + c, u);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float sg = sigmoidf_(g[k]);
+                const float si = g[k] * sg;
+                du[k] = d[k] * si;
+                dg[k] = d[k] * u[k] * sg * (1.f + g[k] * (1.f - sg));
+            }
+            store8(dh + t * 2 * F + c, dg);
+            store8(dh + t * 2 * F + F + c, du);
+        }
+    }
+}
+
+// -------------------------------------------------------- cross entropy ---
+// One CTA per row; logits overwritten with grad_scale * (softmax - onehot).
+template <typename T>
+__global__ void ce_k(T* logits, const int32_t* targets, float* loss_acc, int V, float gscale) {
+    __shared__ float scratch[32];
+    __shared__ float red_m[32], red_s[32];
+    const long long row = blockIdx.x;
+    T* lr = logits + row * V;
+    const int tgt = targets[row];
+    float m = -INFINITY, s = 0.f;
+    for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
+        float v[8];
+        load8(lr + c, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float mn = fmaxf(m, v[i]);
+            s = s * __expf(m - mn) + __expf(v[i] - mn);
+            m = mn;
+        }
+    }
+    // combine (m, s) across the block
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        const float mn = fmaxf(m, m2);
+        s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
+        m = mn;
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        red_m[wid] = m;
+        red_s[wid] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float M = -INFINITY, S = 0.f;
+        for (int i = 0; i < (blockDim.x + 31) / 32; ++i) {
+            const float mn = fmaxf(M, red_m[i]);
+            S = (M == -INFINITY ? 0.f : S * __expf(M - mn)) +
+                (red_m[i] == -INFINITY ? 0.f : red_s[i] * __expf(red_m[i] - mn));
+            M = mn;
+        }
+        scratch[0] = M;
+        scratch[1] = S;
+    }
+    __syncthreads();
+    const float M = scratch[0];
+    const float lse = M + logf(scratch[1]);
+    const bool valid = tgt >= 0;
+    if (threadIdx.x == 0 && valid) {
+        const float xt = to_f(lr[tgt]);
+        atomicAdd(loss_acc, lse - xt);
+        atomicAdd(loss_acc + 1, 1.f);
+    }
+    __syncthreads();   // target logit read before overwrite
+    for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
+        float v[8];
+        load8(lr + c, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float p = valid ? __expf(v[i] - lse) : 0.f;
+            if (valid && c + i == tgt) p -= 1.f;
+            v[i] = p * gscale;
+        }
+        store8(lr + c, v);
+    }
+}
+
+// ---------------------------------------------------------------- misc ----
+template <typename T>
+__global__ void cast_k(const float* src, T* dst, long long n) {
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        dst[i] = from_f<T>(src[i]);
+}
+
+template <typename T>
+__global__ void add_k(T* y, const T* x, long long n) {
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        y[i] = from_f<T>(to_f(y[i]) + to_f(x[i]));
+}
+
+template <typename T>
+__global__ void adamw_k(float* master, T* work, float* grad, float* m, float* v, long long n,
+                        float lr, float b1, float b2, float eps, float wd, float bc1, float bc2) {
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const float g = grad[i];
+        const float mi = b1 * m[i] + (1.f - b1) * g;
+        const float vi = b2 * v[i] + (1.f - b2) * g * g;
+        m[i] = mi;
+        v[i] = vi;
+        float p = master[i];
+        p -= lr * (wd * p + (mi / bc1) / (sqrtf(vi / bc2) + eps));
+        master[i] = p;
+        work[i] = from_f<T>(p);
+        grad[i] = 0.f;
+    }
+}
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+__global__ void init_normal_k(float* dst, long long n, float std, unsigned long long seed) {
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const unsigned long long r = mix64(seed ^ mix64(static_cast<unsigned long long>(i)));
+        const float u1 = (static_cast<float>(r >> 40) + 0.5f) * (1.f / 16777216.f);
+        const float u2 = (static_cast<float>((r >> 16) & 0xFFFFFF) + 0.5f) * (1.f / 16777216.f);
+        dst[i] = std * sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+    }
+}
+
+__global__ void init_const_k(float* dst, long long n, float v) {
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        dst[i] = v;
+}
+
+// Lazily grown RoPE table (one per process; positions only ever grow).
+RopeTable g_rope;
+
+const float2* rope_table(int max_pos, int hd, float theta, cudaStream_t s) {
+    const int half = hd / 2;
+    if (g_rope.cs && g_rope.max_pos >= max_pos && g_rope.half == half && g_rope.theta == theta)
+        return g_rope.cs;
+    if (max_pos <= 0) throw CudaError("rope table used before rope_reserve()");
+    int want = 4096;
+    while (want < max_pos) want *= 2;
+    if (g_rope.cs) {
+        EPP_CUDA(cudaStreamSynchronize(s));
+        EPP_CUDA(cudaFree(g_rope.cs));
+    }
+    EPP_CUDA(cudaMalloc(&g_rope.cs, sizeof(float2) * want * half));
+    const long long n = static_cast<long long>(want) * half;
+    rope_table_k<<<grid_for(n, 256), 256, 0, s>>>(g_rope.cs, want, half, theta);
+    EPP_CHECK_LAUNCH();
+    g_rope.max_pos = want;
+    g_rope.half = half;
+    g_rope.theta = theta;
+    return g_rope.cs;
+}
+
+int norm_threads(int D) {
+    int t = D / 8;
+    if (t > 128) t = 128;
+    if (t < 32) t = 32;
+    return t;
+}
+
+}  // namespace
+
+// =========================================================================
+void embed_fwd(DType t, const int32_t* ids, const void* table, void* out, int T, int D,
+               cudaStream_t s) {
+    if (T == 0) return;
+    dispatch_t(t, [&](auto z) {
+        using E = decltype(z);
+        embed_fwd_k<E><<<T, norm_threads(D), 0, s>>>(ids, static_cast<const E*>(table),
+                                                     static_cast<E*>(out), T, D);
+    });
+    EPP_CHECK_LAUNCH();
+}
+
+void embed_bwd(DType t, const int32_t* ids, const void* dout, float* dtable, int T, int D,
+               cudaStream_t s) {
+    if (T == 0) return;
+    dispatch_t(t, [&](auto z) {
+        using E = decltype(z);
+        embed_bwd_k<E><<<T, norm_threads(D), 0, s>>>(ids, static_cast<const E*>(dout), dtable, T, D);
+    });
+    EPP_CHECK_LAUNCH();
+}
+
+void norm_fwd(DType t, bool rms, const void* x, const void* w, const void* b, void* y, float* mean,
+              float* rstd, int T, int D, float eps, cudaStream_t s) {
+    EPP_REQUIRE(D % 8 == 0, "norm: D must be a multiple of 8");
+    if (T == 0) return;
+    dispatch_t(t, [&](auto z) {
+        using E = decltype(z);
+        norm_fwd_k<E><<<T, norm_threads(D), 0, s>>>(rms, static_cast<const E*>(x),
+                                                    static_cast<const E*>(w),
+                                                    static_cast<const E*>(b), static_cast<E*>(y),
+                                                    mean, rstd, D, eps);
+    });
+    EPP_CHECK_LAUNCH();
+}
+
+void norm_apply(DType t, bool rms, const void* x, const void* w, const void* b, const float* mean,
+                const float* rstd, void* y, int T, int D, cudaStream_t s) {
+    if (T == 0) return;
+    dispatch_t(t, [&](auto z) {
+        using E = decltype(z);
+        norm_apply_k<E><<<T, norm_threads(D), 0, s>>>(rms, static_cast<const E*>(x),
+                                                      static_cast<const E*>(w),
+                                                      static_cast<const E*>(b), mean, rstd,
+                                                      static_cast<E*>(y), D);
+    });
+    EPP_CHECK_LAUNCH();
+}
+
+void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy, const float* mean,
+              const float* rstd, const void* dres, void* dx, float* dw, float* db, int T, int D,
+              cudaStream_t s) {
+    EPP_REQUIRE(D % 8 == 0 && D <= 8 * 128 * kNormMaxG, "norm_bwd: unsupported D");
+    if (T == 0) return;
+    const int G = ceil_div(T, kNormRows);
+    float* part = nullptr;
+    EPP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * 2 * G * D, s));
+    float* pw = part;
+    float* pb = db ? part + static_cast<long long>(G) * D : nullptr;
+    dispatch_t(t, [&](auto z) {
+        using E = decltype(z);
+        norm_bwd_k<E><<<G, norm_threads(D), 0, s>>>(
+            rms, static_cast<const E*>(x), static_cast<const E*>(w), static_cast<const E*>(dy),
+            mean, rstd, static_cast<const E*>(dres), static_cast<E*>(dx), pw, pb, T, D);
+    });
+    EPP_CHECK_LAUNCH();
+    col_reduce_add<<<ceil_div(D, 256), 256, 0, s>>>(pw, G, D, dw);
+    if (db) col_reduce_add<<<ceil_div(D, 256), 256, 0, s>>>(pb, G, D, db);
+    EPP_CHECK_LAUNCH();
+    EPP_CUDA(cudaFreeAsync(part, s));
+}
+
+void rope_qkv_scatter(DType t, const void* qkv, void* q_out, const AttnSeg* segs_dev, int nseg,
+                      const int* tok_seg, const int* tok_pos, int T, int H, int Hkv, int hd,
+                      int layer, float theta, cudaStream_t s) {
+    (void)nseg;
+    if (T == 0) return;
+    EPP_REQUIRE(hd % 2 == 0, "rope: head_dim must be even");
+    const float2* cs = rope_table(0, hd, theta, s);
+    const long long n = static_cast<long long>(T) * (H + 2 * Hkv) * (hd / 2);
+    dispatch_t(t, [&](auto z) {
+        using E = decltype(z);
+        rope_scatter_k<E><<<grid_for(n, 256), 256, 0, s>>>(static_cast<const E*>(qkv),
+                                                           static_cast<E*>(q_out), segs_dev,
+                                                           tok_seg, tok_pos, cs, T, H, Hkv, hd,
+                                                           layer);
+    });
+    EPP_CHECK_LAUNCH();
+}
+
+void rope_qkv_gather_grad(DType t, const float* dq, const AttnSeg* segs_dev, const int* tok_seg,
+                          const int* tok_pos, void* dqkv, int T, int H, int Hkv, int hd, int layer,
+                          float theta, cudaStream_t s) {
+    if (T == 0) return;
+    const float2* cs = rope_table(0, hd, theta, s);
+    const long long n = static_cast<long long>(T) * (H + 2 * Hkv) * (hd / 2);
+    dispatch_t(t, [&](auto z) {
+        using E = decltype(z);
+        rope_gather_grad_k<E><<<grid_for(n, 256), 256, 0, s>>>(dq, segs_dev, tok_seg, tok_pos, cs,
+                                                               static_cast<E*>(dqkv), T, H, Hkv,
+                                                               hd, layer);
+    });
+    EPP_CHECK_LAUNCH();
+}
+
+void act_fwd(DType t, int act, const void* h, void* a, int T, int F, cudaStream_t s) {
+    EPP_REQUIRE(F % 8 == 0, "act: F must be a multiple of 8");
+    if (T == 0) return;
+    const long long n8 = static_cast<long long>(T) * F / 8;
+    dispatch_t(t, [&](auto z) {
+        using E = decltype(z);
+        act_fwd_k<E><<<grid_for(n8, 256), 256, 0, s>>>(act, static_cast<const E*>(h),
+                                                       static_cast<E*>(a), T, F);
+    });
+    EPP_CHECK_LAUNCH();
+}
+
+void act_bwd(DType t, int act, const void* h, const void* da, void* dh, int T, int F,
+             cudaStream_t s) {
+    if (T == 0) return;
+    const long long n8 = static_cast<long long>(T) * F / 8;
+    dispatch_t(t, [&](auto z) {
+        using E = decltype(z);
+        act_bwd_k<E><<<grid_for(n8, 256), 256, 0, s>>>(act, static_cast<const E*>(h),
+                                                       static_cast<const E*>(da),
+                                                       static_cast<E*>(dh), T, F);
+    });
+    EPP_CHECK_LAUNCH();
+}
+
+void cross_entropy(DType t, void* logits, const int32_t* targets, float* loss_acc, int T, int V,
+                   float grad_scale, cudaStream_t s) {
+    EPP_REQUIRE(V % 8 == 0, "ce: V must be a multiple of 8");
+    if (T == 0) return;
+    dispatch_t(t, [&](auto z) {
+        using E = decltype(z);
+        ce_k<E><<<T, 256, 0, s>>>(static_cast<E*>(logits), targets, loss_acc, V, grad_scale);
+    });
+    EPP_CHECK_LAUNCH();
+}
+
+void fill_zero(void* p, size_t bytes, cudaStream_t s) {
+    if (bytes) EPP_CUDA(cudaMemsetAsync(p, 0, bytes, s));
+}
+
+void cast_f32_to(DType t, const float* src, void* dst, long long n, cudaStream_t s) {
+    if (n == 0) return;
+    dispatch_t(t, [&](auto z) {
+        using E = decltype(z);
+        cast_k<E><<<grid_for(n, 256), 256, 0, s>>>(src, static_cast<E*>(dst), n);
+    });
+    EPP_CHECK_LAUNCH();
+}
+
+void add_inplace(DType t, void* y, const void* x, long long n, cudaStream_t s) {
+    if (n == 0) return;
+    dispatch_t(t, [&](auto z) {
+        using E = decltype(z);
+        add_k<E><<<grid_for(n, 256), 256, 0, s>>>(static_cast<E*>(y), static_cast<const E*>(x), n);
+    });
+    EPP_CHECK_LAUNCH();
+}
+
+void adamw(float* master, void* work, DType t, float* grad, float* m, float* v, long long n,
+           float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
+           cudaStream_t s) {
+    if (n == 0) return;
+    dispatch_t(t, [&](auto z) {
+        using E = decltype(z);
+        adamw_k<E><<<grid_for(n, 256), 256, 0, s>>>(master, static_cast<E*>(work), grad, m, v, n,
+                                                     lr, b1, b2, eps, wd, bc1, bc2);
+    });
+    EPP_CHECK_LAUNCH();
+}
+
+void init_normal(float* dst, long long n, float std, unsigned long long seed, cudaStream_t s) {
+    if (n == 0) return;
+    init_normal_k<<<grid_for(n, 256), 256, 0, s>>>(dst, n, std, seed);
+    EPP_CHECK_LAUNCH();
+}
+
+void init_const(float* dst, long long n, float v, cudaStream_t s) {
+    if (n == 0) return;
+    init_const_k<<<grid_for(n, 256), 256, 0, s>>>(dst, n, v);
+    EPP_CHECK_LAUNCH();
+}
+
+void rope_reserve(int max_pos, int hd, float theta, cudaStream_t s) {
+    rope_table(max_pos, hd, theta, s);
+}
+
+}  // namespace eppk

@@ -1,0 +1,512 @@
+// epp-b200: GEMMs for the stage executor.
+//
+// BF16 path: tcgen05.mma (kind::f16, cta_group::1, M=128, N=BN) with the fp32
+// accumulator in TMEM, operands staged by TMA (cp.async.bulk.tensor, 128-byte
+// swizzle) through a STAGES-deep mbarrier ring.  Warp roles per CTA:
+//   warp 0  TMA producer (one elected lane)
+//   warp 1  TMEM allocator + MMA issuer (one elected lane)
+//   warps 2-5  epilogue: tcgen05.ld -> registers -> fused epilogue -> global
+// Both operands may be K-major or MN-major (transposed) in global memory, so
+// forward (X W^T), data-gradient (dY W) and weight-gradient (dY^T X) GEMMs all
+// run without materialised transposes.
+//
+// F32 path (parity mode): a register-tiled SIMT kernel with the same operand
+// conventions.
+#include <cuda.h>
+
+#include <atomic>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace eppk {
+
+static std::atomic<long long> g_gemm_launches{0};
+long long gemm_launch_count() { return g_gemm_launches.load(); }
+
+// =========================================================================
+// Device-side PTX wrappers
+// =========================================================================
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// 32 lanes x 32 consecutive fp32 columns per warp: thread t gets row
+// (lane base + t), columns [col, col+32).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory matrix descriptor, SWIZZLE_128B, sm100 version bits.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((addr >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+    d |= 1ull << 46;              // descriptor version (Blackwell)
+    d |= 2ull << 61;              // layout: SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor: BF16 x BF16 -> F32, M=128, N=n.
+__host__ __device__ constexpr uint32_t instr_desc(int n, bool a_mn, bool b_mn) {
+    return (1u << 4)                             // D format F32
+           | (1u << 7)                           // A format BF16
+           | (1u << 10)                          // B format BF16
+           | ((a_mn ? 1u : 0u) << 15)            // A major
+           | ((b_mn ? 1u : 0u) << 16)            // B major
+           | (static_cast<uint32_t>(n >> 3) << 17)
+           | (static_cast<uint32_t>(128 >> 4) << 24);
+}
+
+}  // namespace tc
+
+// =========================================================================
+// tcgen05 kernel
+// =========================================================================
+constexpr int kBM = 128;
+constexpr int kBK = 64;              // one 128-byte swizzle atom of bf16
+constexpr int kThreads = 192;
+
+template <int BN, int STAGES>
+struct TcSmem {
+    static constexpr int kABytes = kBM * kBK * 2;     // 16 KB
+    static constexpr int kBBytes = BN * kBK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kBarOffset = STAGES * kStageBytes;
+    static constexpr int kTotal = kBarOffset + (2 * STAGES + 1) * 8 + 16 + 1024;  // + align slack
+};
+
+struct TcParams {
+    int M, N, K;
+    void* C;
+    long long ldc;
+    const bf16* R;
+    long long ldr;
+};
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_b, const TcParams p) {
+    using L = TcSmem<BN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+    uint64_t* empty = full + STAGES;
+    uint64_t* acc_full = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int n0 = blockIdx.x * BN;
+    const int m0 = blockIdx.y * kBM;
+    const int nk = (p.K + kBK - 1) / kBK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        tc::mbar_init(acc_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+    }
+    constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         tc::smem_u32(tmem_slot)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int kb = 0; kb < nk; ++kb) {
+                tc::mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* sa = smem + stage * L::kStageBytes;
+                uint8_t* sb = sa + L::kABytes;
+                tc::mbar_expect_tx(&full[stage], L::kStageBytes);
+                const int k0 = kb * kBK;
+                if (A_MN) {
+#pragma unroll
+                    for (int i = 0; i < kBM / 64; ++i)
+                        tc::tma_load_2d(sa + i * 8192, &map_a, &full[stage], m0 + 64 * i, k0);
+                } else {
+                    tc::tma_load_2d(sa, &map_a, &full[stage], k0, m0);
+                }
+                if (B_MN) {
+#pragma unroll
+                    for (int i = 0; i < BN / 64; ++i)
+                        tc::tma_load_2d(sb + i * 8192, &map_b, &full[stage], n0 + 64 * i, k0);
+                } else {
+                    tc::tma_load_2d(sb, &map_b, &full[stage], k0, n0);
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        constexpr uint32_t idesc = tc::instr_desc(BN, A_MN, B_MN);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kb = 0; kb < nk; ++kb) {
+            tc::mbar_wait(&full[stage], phase);
+            tc::fence_after();
+            if (lane == 0) {
+                const uint32_t sa = tc::smem_u32(smem + stage * L::kStageBytes);
+                const uint32_t sb = sa + L::kABytes;
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk) {
+                    // K-major: advance 32 B inside the swizzle atom; SBO = 8 rows.
+                    // MN-major: advance 16 K-rows (2 atoms); LBO = 64-col block.
+                    const uint64_t ad = A_MN ? tc::smem_desc(sa + kk * 2048, 8192, 1024)
+                                             : tc::smem_desc(sa + kk * 32, 16, 1024);
+                    const uint64_t bd = B_MN ? tc::smem_desc(sb + kk * 2048, 8192, 1024)
+                                             : tc::smem_desc(sb + kk * 32, 16, 1024);
+                    tc::mma_bf16(tmem, ad, bd, idesc, (kb | kk) != 0);
+                }
+                tc::commit(&empty[stage]);
+            }
+            __syncwarp();
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+        if (lane == 0) tc::commit(acc_full);
+        __syncwarp();
+    } else {
+        // ---------------- epilogue (warps 2..5) ----------------
+        const int quarter = warp & 3;                  // TMEM lane quarter
+        const int row = m0 + quarter * 32 + lane;
+        if (nk > 0) tc::mbar_wait(acc_full, 0);
+        tc::fence_after();
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+            float v[32];
+            if (nk > 0) {
+                tc::tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c, v);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            }
+            const int col = n0 + c;
+            if (row >= p.M || col >= p.N) continue;
+            if (EPI == static_cast<int>(Epi::AccumF32) || EPI == static_cast<int>(Epi::StoreF32)) {
+                float* dst = static_cast<float*>(p.C) + static_cast<long long>(row) * p.ldc + col;
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                    float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                    if (EPI == static_cast<int>(Epi::AccumF32)) {
+                        const float4 old = *reinterpret_cast<const float4*>(dst + i);
+                        o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+                    }
+                    *reinterpret_cast<float4*>(dst + i) = o;
+                }
+            } else {
+                if (EPI == static_cast<int>(Epi::AddRes)) {
+                    const bf16* r = p.R + static_cast<long long>(row) * p.ldr + col;
+#pragma unroll
+                    for (int i = 0; i < 32; i += 8) {
+                        const uint4 raw = *reinterpret_cast<const uint4*>(r + i);
+                        const bf16* rb = reinterpret_cast<const bf16*>(&raw);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) v[i + j] += __bfloat162float(rb[j]);
+                    }
+                }
+                bf16* dst = static_cast<bf16*>(p.C) + static_cast<long long>(row) * p.ldc + col;
+#pragma unroll
+                for (int i = 0; i < 32; i += 8) {
+                    uint4 raw;
+                    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        h[j] = __floats2bfloat162_rn(v[i + 2 * j], v[i + 2 * j + 1]);
+                    *reinterpret_cast<uint4*>(dst + i) = raw;
+                }
+            }
+        }
+        tc::fence_before();
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc::fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(kTmemCols)
+                     : "memory");
+    }
+}
+
+// =========================================================================
+// Host side: tensor maps + dispatch
+// =========================================================================
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        EPP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p)
+            throw CudaError("cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// 2-D bf16 tensor [rows, cols] (cols contiguous, row pitch ld elements),
+// box = [box_cols (inner), box_rows].
+CUtensorMap make_map(const void* base, long long rows, long long cols, long long ld,
+                     int box_cols, int box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+    return m;
+}
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
+void launch_tc(const GemmArgs& g, cudaStream_t s) {
+    using L = TcSmem<BN, STAGES>;
+    auto kern = gemm_tc_kernel<BN, STAGES, A_MN, B_MN, EPI>;
+    static bool configured = false;   // per instantiation
+    if (!configured) {
+        EPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
+        configured = true;
+    }
+    // A: K-major -> tensor [M, K]; MN-major -> tensor [K, M].
+    const CUtensorMap ma = A_MN ? make_map(g.A, g.K, g.M, g.lda, 64, kBK)
+                                : make_map(g.A, g.M, g.K, g.lda, kBK, kBM);
+    const CUtensorMap mb = B_MN ? make_map(g.B, g.K, g.N, g.ldb, 64, kBK)
+                                : make_map(g.B, g.N, g.K, g.ldb, kBK, BN);
+    TcParams p{g.M, g.N, g.K, g.C, g.ldc, static_cast<const bf16*>(g.R), g.ldr};
+    dim3 grid(ceil_div(g.N, BN), ceil_div(g.M, kBM));
+    kern<<<grid, kThreads, L::kTotal, s>>>(ma, mb, p);
+    EPP_CHECK_LAUNCH();
+    g_gemm_launches.fetch_add(1);
+}
+
+
+template <int BN, int STAGES, int EPI>
+void dispatch_major(const GemmArgs& g, cudaStream_t s) {
+    const bool a_mn = !g.a_kmajor, b_mn = !g.b_kmajor;
+    if (!a_mn && !b_mn) launch_tc<BN, STAGES, false, false, EPI>(g, s);
+    else if (!a_mn && b_mn) launch_tc<BN, STAGES, false, true, EPI>(g, s);
+    else if (a_mn && !b_mn) launch_tc<BN, STAGES, true, false, EPI>(g, s);
+    else launch_tc<BN, STAGES, true, true, EPI>(g, s);
+}
+
+template <int BN, int STAGES>
+void dispatch_epi(const GemmArgs& g, cudaStream_t s) {
+    switch (g.epi) {
+        case Epi::Store: dispatch_major<BN, STAGES, 0>(g, s); break;
+        case Epi::AccumF32: dispatch_major<BN, STAGES, 1>(g, s); break;
+        case Epi::AddRes: dispatch_major<BN, STAGES, 2>(g, s); break;
+        case Epi::StoreF32: dispatch_major<BN, STAGES, 3>(g, s); break;
+    }
+}
+
+// ---------------------------------------------------------------- SIMT f32
+template <typename T>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
+    constexpr int TM = 64, TN = 64, TK = 16;
+    __shared__ float As[TK][TM + 1];
+    __shared__ float Bs[TK][TN + 1];
+    const T* A = static_cast<const T*>(g.A);
+    const T* B = static_cast<const T*>(g.B);
+    const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    float acc[4][4] = {};
+    for (int k0 = 0; k0 < g.K; k0 += TK) {
+        for (int i = threadIdx.x; i < TK * TM; i += 256) {
+            const int kk = g.a_kmajor ? i % TK : i / TM;
+            const int mm = g.a_kmajor ? i / TK : i % TM;
+            const int m = m0 + mm, k = k0 + kk;
+            float v = 0.f;
+            if (m < g.M && k < g.K)
+                v = to_f(g.a_kmajor ? A[static_cast<long long>(m) * g.lda + k]
+                                    : A[static_cast<long long>(k) * g.lda + m]);
+            As[kk][mm] = v;
+        }
+        for (int i = threadIdx.x; i < TK * TN; i += 256) {
+            const int kk = g.b_kmajor ? i % TK : i / TN;
+            const int nn = g.b_kmajor ? i / TK : i % TN;
+            const int n = n0 + nn, k = k0 + kk;
+            float v = 0.f;
+            if (n < g.N && k < g.K)
+                v = to_f(g.b_kmajor ? B[static_cast<long long>(n) * g.ldb + k]
+                                    : B[static_cast<long long>(k) * g.ldb + n]);
+            Bs[kk][nn] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < TK; ++kk) {
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int m = m0 + ty + 16 * i;
+        if (m >= g.M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = n0 + tx + 16 * j;
+            if (n >= g.N) continue;
+            const long long off = static_cast<long long>(m) * g.ldc + n;
+            float v = acc[i][j];
+            if (g.epi == Epi::AccumF32) {
+                static_cast<float*>(g.C)[off] += v;
+            } else if (g.epi == Epi::StoreF32) {
+                static_cast<float*>(g.C)[off] = v;
+            } else {
+                if (g.epi == Epi::AddRes)
+                    v += to_f(static_cast<const T*>(g.R)[static_cast<long long>(m) * g.ldr + n]);
+                static_cast<T*>(g.C)[off] = from_f<T>(v);
+            }
+        }
+    }
+}
+
+}  // namespace
+
+void gemm(const GemmArgs& g, cudaStream_t s) {
+    EPP_REQUIRE(g.M >= 0 && g.N >= 0 && g.K >= 0, "gemm: negative extent");
+    if (g.M == 0 || g.N == 0) return;
+    if (g.dtype == DType::F32) {
+        dim3 grid(ceil_div(g.N, 64), ceil_div(g.M, 64));
+        gemm_simt_kernel<float><<<grid, 256, 0, s>>>(g);
+        EPP_CHECK_LAUNCH();
+        g_gemm_launches.fetch_add(1);
+        return;
+    }
+    EPP_REQUIRE(g.N % 32 == 0, "gemm(bf16): N must be a multiple of 32");
+    EPP_REQUIRE(g.lda % 8 == 0 && g.ldb % 8 == 0, "gemm(bf16): lda/ldb must be multiples of 8");
+    EPP_REQUIRE(g.ldc % 8 == 0, "gemm(bf16): ldc must be a multiple of 8");
+    EPP_REQUIRE((reinterpret_cast<uintptr_t>(g.A) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(g.B) & 15) == 0,
+                "gemm(bf16): operands must be 16-byte aligned");
+    if (g.K == 0) {
+        // Empty reduction: Store/StoreF32 write zeros, AddRes copies R, AccumF32 no-op.
+        if (g.epi == Epi::AccumF32) return;
+    }
+    // Wide tiles keep the tensor pipe fed (128x256 per MMA); narrow problems
+    // use 128-wide tiles to expose more CTAs.
+    const long long tiles256 = static_cast<long long>(ceil_div(g.N, 256)) * ceil_div(g.M, kBM);
+    if (g.N % 256 == 0 && tiles256 >= 120)
+        dispatch_epi<256, 4>(g, s);
+    else
+        dispatch_epi<128, 6>(g, s);
+}
+
+}  // namespace eppk

@@ -1,0 +1,142 @@
+// epp-b200 GPU executor: host-side launch interface of every kernel family.
+// All launches are stream-ordered; pointers are device pointers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace eppk {
+
+enum class DType : int { F32 = 0, BF16 = 1 };
+
+inline size_t dtype_size(DType t) { return t == DType::F32 ? 4 : 2; }
+
+// ---------------------------------------------------------------- GEMM ----
+// C[M,N] = epilogue( sum_k A(m,k) * B(n,k) )
+//   A(m,k) = a_kmajor ? A[m*lda + k] : A[k*lda + m]
+//   B(n,k) = b_kmajor ? B[n*ldb + k] : B[k*ldb + n]
+// Operand/output element type follows `dtype` (F32: all fp32; BF16: A/B bf16,
+// fp32 accumulation, C bf16 for Store/AddRes, fp32 for AccumF32/StoreF32).
+enum class Epi : int {
+    Store = 0,      // C = acc
+    AccumF32 = 1,   // C(fp32) += acc          (weight-gradient accumulation)
+    AddRes = 2,     // C = acc + R             (residual stream update)
+    StoreF32 = 3,   // C(fp32) = acc
+};
+
+struct GemmArgs {
+    int M = 0, N = 0, K = 0;
+    const void* A = nullptr; long long lda = 0; bool a_kmajor = true;
+    const void* B = nullptr; long long ldb = 0; bool b_kmajor = true;
+    void* C = nullptr; long long ldc = 0;
+    const void* R = nullptr; long long ldr = 0;
+    Epi epi = Epi::Store;
+    DType dtype = DType::BF16;
+};
+
+void gemm(const GemmArgs& a, cudaStream_t s);
+// Number of GEMM kernel launches issued so far on this process (bench counter).
+long long gemm_launch_count();
+
+// ----------------------------------------------------------- attention ----
+// Segment of a chunk's token layout.  Queries are rows [q_start, q_start+q_len)
+// of the chunk; they sit at key positions [kv_ctx, kv_ctx+q_len) of the
+// segment's key/value rows, which live at k/v (+ layer * kv_layer_stride),
+// row stride Hkv*hd elements.  Key j is visible to query i iff j <= kv_ctx+i.
+struct AttnSeg {
+    int q_start;
+    int q_len;
+    int kv_ctx;
+    int pad_;
+    const void* k;       // layer-0 base
+    const void* v;
+    float* dk;           // fp32 gradient accumulators (backward), may be null in fwd
+    float* dv;
+    long long kv_layer_stride;    // elements between layers
+    long long dkv_layer_stride;
+};
+
+// Work item (segment index, 64-row block index).
+struct AttnWork {
+    int seg;
+    int block;
+};
+constexpr int kAttnBlock = 64;
+
+struct AttnArgs {
+    const AttnSeg* segs = nullptr;   // device array
+    int nseg = 0;
+    const AttnWork* qwork = nullptr;   // query blocks (fwd, dq)
+    int nqwork = 0;
+    const AttnWork* kwork = nullptr;   // key blocks (dk/dv)
+    int nkwork = 0;
+    int T = 0;
+    int H = 0, Hkv = 0, hd = 0;
+    int layer = 0;
+    float scale = 0.f;
+    DType dtype = DType::BF16;
+    // forward
+    const void* q = nullptr;   // [T, H, hd]
+    void* o = nullptr;         // [T, H, hd]
+    float* lse = nullptr;      // [H, T], log2 domain: max2 + log2(sum)
+    // backward
+    const void* dout = nullptr;   // [T, H, hd]
+    float* delta = nullptr;       // [H, T] scratch
+    float* dq = nullptr;          // [T, H, hd] fp32 (fully written by attn_bwd)
+};
+
+void attn_fwd(const AttnArgs& a, cudaStream_t s);
+void attn_bwd(const AttnArgs& a, cudaStream_t s);
+
+// ------------------------------------------------------- elementwise ------
+void embed_fwd(DType t, const int32_t* ids, const void* table, void* out, int T, int D,
+               cudaStream_t s);
+void embed_bwd(DType t, const int32_t* ids, const void* dout, float* dtable, int T, int D,
+               cudaStream_t s);
+// LayerNorm (has_bias, rms=false) or RMSNorm (rms=true): y = norm(x)*w (+b)
+void norm_fwd(DType t, bool rms, const void* x, const void* w, const void* b, void* y,
+              float* mean, float* rstd, int T, int D, float eps, cudaStream_t s);
+// dx = dres + norm_bwd(dy);  dw/db accumulated (fp32) via per-block partials
+void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy,
+              const float* mean, const float* rstd, const void* dres, void* dx, float* dw,
+              float* db, int T, int D, cudaStream_t s);
+// Recompute y = norm(x) from saved stats.
+void norm_apply(DType t, bool rms, const void* x, const void* w, const void* b,
+                const float* mean, const float* rstd, void* y, int T, int D, cudaStream_t s);
+
+// Ensure the RoPE cos/sin table covers positions [0, max_pos).
+void rope_reserve(int max_pos, int hd, float theta, cudaStream_t s);
+// RoPE + scatter of a packed [T, (H+2Hkv)*hd] QKV row block: q -> q_out [T,H,hd],
+// k/v -> each segment's key/value rows for `layer`.
+void rope_qkv_scatter(DType t, const void* qkv, void* q_out, const AttnSeg* segs_dev, int nseg,
+                      const int* tok_seg, const int* tok_pos, int T, int H, int Hkv, int hd,
+                      int layer, float theta, cudaStream_t s);
+// Inverse: dq (fp32 [T,H,hd]) and segment dk/dv (fp32) -> dqkv [T,(H+2Hkv)hd],
+// un-rotating dq/dk.
+void rope_qkv_gather_grad(DType t, const float* dq, const AttnSeg* segs_dev, const int* tok_seg,
+                          const int* tok_pos, void* dqkv, int T, int H, int Hkv, int hd,
+                          int layer, float theta, cudaStream_t s);
+
+// act: 0 = GELU(tanh), 1 = SwiGLU (input [T,2F] gate|up -> [T,F])
+void act_fwd(DType t, int act, const void* h, void* a, int T, int F, cudaStream_t s);
+// dh from da; for SwiGLU dh is [T,2F].  Writes dh (may alias nothing).
+void act_bwd(DType t, int act, const void* h, const void* da, void* dh, int T, int F,
+             cudaStream_t s);
+
+// Cross entropy over logits rows [T, V] (in place: logits -> dlogits * scale).
+// loss_acc[0] += sum of losses over valid targets; loss_acc[1] += #valid.
+void cross_entropy(DType t, void* logits, const int32_t* targets, float* loss_acc, int T, int V,
+                   float grad_scale, cudaStream_t s);
+
+void fill_zero(void* p, size_t bytes, cudaStream_t s);
+void cast_f32_to(DType t, const float* src, void* dst, long long n, cudaStream_t s);
+void add_inplace(DType t, void* y, const void* x, long long n, cudaStream_t s);
+// AdamW on fp32 master weights; writes the working copy (bf16 or fp32).
+void adamw(float* master, void* work, DType t, float* grad, float* m, float* v, long long n,
+           float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
+           cudaStream_t s);
+// Deterministic normal(0, std) init from (seed, offset) counter-based hashing.
+void init_normal(float* dst, long long n, float std, unsigned long long seed, cudaStream_t s);
+void init_const(float* dst, long long n, float v, cudaStream_t s);
+
+}  // namespace eppk

@@ -1,0 +1,837 @@
+// epp-b200: the per-stage executor behind include/epp_gpu.h.
+//
+// Runs a contiguous range of transformer layers of one pipeline stage on
+// heterogeneous EPP chunks (Batched / Split / Hybrid, proj/include/epp/
+// chunk.hpp:16-46), with the memory contract the planner assumes
+// (proj/src/cost_model.cpp:47-66):
+//   * non-checkpointed layers keep full activations until the chunk's
+//     backward;  the first `ckpt_layers` layers of the stage keep only their
+//     input and are re-run layer by layer right before their backward;
+//   * K/V of a long sequence's slices live in a per-(stage, sequence) buffer
+//     that later slices attend to (and that checkpointed layers therefore
+//     never drop); dK/dV of those keys accumulate in fp32 across the
+//     sequence's chunks, whose backwards run last-slice-first
+//     (proj/src/pipeline.cpp:119-131);
+//   * the buffers are released after the sequence's first slice (context 0)
+//     finishes its backward.
+// Memory comes from the CUDA stream-ordered allocator on the stage's stream.
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "epp_gpu.h"
+#include "kernels.h"
+
+namespace eppk {
+
+long long& launch_counter() {
+    static long long n = 0;
+    return n;
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+// ----------------------------------------------------------- allocation ----
+struct Pool {
+    long long live = 0;
+    long long peak = 0;
+};
+
+// Stream-ordered device buffer.
+class Buf {
+public:
+    Buf() = default;
+    Buf(Pool* pool, size_t bytes, cudaStream_t s, bool zero = false) : pool_(pool), bytes_(bytes), s_(s) {
+        if (bytes_ == 0) return;
+        EPP_CUDA(cudaMallocAsync(&p_, bytes_, s_));
+        if (zero) EPP_CUDA(cudaMemsetAsync(p_, 0, bytes_, s_));
+        pool_->live += static_cast<long long>(bytes_);
+        if (pool_->live > pool_->peak) pool_->peak = pool_->live;
+    }
+    Buf(const Buf&) = delete;
+    Buf& operator=(const Buf&) = delete;
+    Buf(Buf&& o) noexcept { *this = std::move(o); }
+    Buf& operator=(Buf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_; bytes_ = o.bytes_; s_ = o.s_; pool_ = o.pool_;
+            o.p_ = nullptr; o.bytes_ = 0;
+        }
+        return *this;
+    }
+    ~Buf() { release(); }
+    void release() {
+        if (p_) {
+            cudaFreeAsync(p_, s_);
+            pool_->live -= static_cast<long long>(bytes_);
+            p_ = nullptr;
+            bytes_ = 0;
+        }
+    }
+    template <typename T = void> T* get() const { return static_cast<T*>(p_); }
+    explicit operator bool() const { return p_ != nullptr; }
+
+private:
+    Pool* pool_ = nullptr;
+    void* p_ = nullptr;
+    size_t bytes_ = 0;
+    cudaStream_t s_ = nullptr;
+};
+
+// Pinned host staging for small per-chunk tables (segment descriptors, token
+// maps, work lists): a two-half ring so H2D copies stay asynchronous.  When
+// the ring moves into a half, it first waits for the copies that last read
+// from that half.
+class PinnedRing {
+public:
+    explicit PinnedRing(size_t bytes) : cap_(bytes) {
+        EPP_CUDA(cudaMallocHost(&base_, cap_));
+        for (auto& e : done_) EPP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    ~PinnedRing() {
+        for (auto& e : done_) cudaEventDestroy(e);
+        cudaFreeHost(base_);
+    }
+    void* stage(const void* src, size_t bytes, cudaStream_t s) {
+        const size_t half = cap_ / 2;
+        EPP_REQUIRE(bytes <= half, "staging request too large");
+        const size_t aligned = (bytes + 255) & ~static_cast<size_t>(255);
+        if (off_ + aligned > (cur_ + 1) * half) {
+            EPP_CUDA(cudaEventRecord(done_[cur_], s));
+            cur_ ^= 1;
+            if (used_[cur_]) EPP_CUDA(cudaEventSynchronize(done_[cur_]));
+            off_ = cur_ * half;
+        }
+        used_[cur_] = true;
+        void* dst = base_ + off_;
+        std::memcpy(dst, src, bytes);
+        off_ += aligned;
+        return dst;
+    }
+
+private:
+    char* base_ = nullptr;
+    size_t cap_;
+    size_t off_ = 0;
+    int cur_ = 0;
+    bool used_[2] = {false, false};
+    cudaEvent_t done_[2];
+};
+
+struct Param {
+    std::string name;
+    long long numel = 0;
+    float* master = nullptr;
+    void* work = nullptr;
+    float* grad = nullptr;
+    float* m = nullptr;
+    float* v = nullptr;
+    float init_std = 0.f;   // 0 -> constant init_val
+    float init_val = 0.f;
+};
+
+struct LayerParams {
+    int ln1_w = -1, ln1_b = -1, wqkv = -1, wo = -1, ln2_w = -1, ln2_b = -1, w1 = -1, w2 = -1;
+};
+
+// Saved per-layer activations of one chunk.
+struct LayerSaved {
+    Buf x_out;        // output of this layer (= next layer's input); last layer -> act_out
+    Buf mean1, rstd1, mean2, rstd2;
+    Buf q, o, lse, x_mid, h;
+    bool full = false;   // q/o/lse/x_mid/h present
+};
+
+struct ChunkState {
+    int T = 0;
+    std::vector<AttnSeg> segs;     // host copy
+    Buf segs_dev, tok_seg, tok_pos, qwork, kwork;
+    Buf kv_local;                  // [K|V][layer][T][Hkv*hd] rows of packed segments
+    Buf dkv_local;                 // fp32 [dK|dV][T][Hkv*hd], one layer, re-zeroed per layer
+    int nqwork = 0, nkwork = 0;
+    Buf x_in;                      // stage input (copy of act_in or embedding)
+    std::vector<LayerSaved> layers;
+    Buf meanf, rstdf, dxf;         // last stage: final-norm stats + d(final norm out)
+    int ckpt = 0;
+};
+
+struct SeqKV {
+    long long len = 0;
+    Buf kv;          // [layers][len][Hkv*hd] K then V halves: k at 0, v at layers*len*kvw
+    Buf dkv;         // fp32, same layout
+};
+
+}  // namespace
+
+// ===========================================================================
+class StageImpl {
+public:
+    StageImpl(const epp_model_desc& m, int first, int nl, bool embed, bool head, DType dt)
+        : m_(m), first_(first), nl_(nl), has_embed_(embed), has_head_(head), dt_(dt) {
+        EPP_REQUIRE(m.heads > 0 && m.kv_heads > 0 && m.heads % m.kv_heads == 0, "bad head counts");
+        EPP_REQUIRE(m.head_dim * m.heads == m.hidden, "head_dim * heads must equal hidden");
+        EPP_REQUIRE(first >= 0 && nl >= 0 && first + nl <= m.layers, "bad layer range");
+        EPP_REQUIRE(m.hidden % 64 == 0 && m.ffn % 64 == 0 && m.vocab % 64 == 0,
+                    "hidden/ffn/vocab must be multiples of 64");
+        EPP_REQUIRE(dt == DType::F32 || m.head_dim == 64 || m.head_dim == 128,
+                    "bf16 attention supports head_dim 64 or 128");
+        D_ = m.hidden;
+        H_ = m.heads;
+        Hkv_ = m.kv_heads;
+        hd_ = m.head_dim;
+        llama_ = m.arch == EPP_ARCH_LLAMA;
+        F_ = m.ffn;
+        F1_ = llama_ ? 2 * F_ : F_;
+        Nqkv_ = (H_ + 2 * Hkv_) * hd_;
+        const float std0 = 0.02f;
+        const float std_out = 0.02f / std::sqrt(2.0f * m.layers);
+        if (has_embed_) emb_ = add("embed.weight", static_cast<long long>(m.vocab) * D_, std0);
+        for (int j = 0; j < nl; ++j) {
+            const std::string pre = "layers." + std::to_string(first + j) + ".";
+            LayerParams lp;
+            lp.ln1_w = add(pre + "norm1.weight", D_, 0.f, 1.f);
+            if (!llama_) lp.ln1_b = add(pre + "norm1.bias", D_, 0.f, 0.f);
+            lp.wqkv = add(pre + "attn.wqkv", static_cast<long long>(Nqkv_) * D_, std0);
+            lp.wo = add(pre + "attn.wo", static_cast<long long>(D_) * H_ * hd_, std_out);
+            lp.ln2_w = add(pre + "norm2.weight", D_, 0.f, 1.f);
+            if (!llama_) lp.ln2_b = add(pre + "norm2.bias", D_, 0.f, 0.f);
+            lp.w1 = add(pre + (llama_ ? "mlp.w13" : "mlp.w1"), static_cast<long long>(F1_) * D_, std0);
+            lp.w2 = add(pre + "mlp.w2", static_cast<long long>(D_) * F_, std_out);
+            lps_.push_back(lp);
+        }
+        if (has_head_) {
+            lnf_w_ = add("final_norm.weight", D_, 0.f, 1.f);
+            if (!llama_) lnf_b_ = add("final_norm.bias", D_, 0.f, 0.f);
+            lm_ = add("lm_head.weight", static_cast<long long>(m.vocab) * D_, std0);
+        }
+        for (Param& p : params_) {
+            EPP_CUDA(cudaMalloc(&p.master, sizeof(float) * p.numel));
+            EPP_CUDA(cudaMalloc(&p.grad, sizeof(float) * p.numel));
+            EPP_CUDA(cudaMalloc(&p.m, sizeof(float) * p.numel));
+            EPP_CUDA(cudaMalloc(&p.v, sizeof(float) * p.numel));
+            EPP_CUDA(cudaMemset(p.grad, 0, sizeof(float) * p.numel));
+            EPP_CUDA(cudaMemset(p.m, 0, sizeof(float) * p.numel));
+            EPP_CUDA(cudaMemset(p.v, 0, sizeof(float) * p.numel));
+            if (dt_ == DType::F32) {
+                p.work = p.master;
+            } else {
+                EPP_CUDA(cudaMalloc(&p.work, 2 * p.numel));
+            }
+        }
+        EPP_CUDA(cudaMalloc(&loss_acc_, sizeof(float) * 2));
+        EPP_CUDA(cudaMemset(loss_acc_, 0, sizeof(float) * 2));
+        // Keep freed chunk memory in the pool instead of returning it to the OS.
+        int dev = 0;
+        EPP_CUDA(cudaGetDevice(&dev));
+        cudaMemPool_t mp;
+        EPP_CUDA(cudaDeviceGetDefaultMemPool(&mp, dev));
+        uint64_t thresh = UINT64_MAX;
+        EPP_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thresh));
+    }
+
+    ~StageImpl() {
+        chunks_.clear();
+        seqs_.clear();
+        cudaDeviceSynchronize();
+        for (Param& p : params_) {
+            cudaFree(p.master);
+            cudaFree(p.grad);
+            cudaFree(p.m);
+            cudaFree(p.v);
+            if (p.work != p.master) cudaFree(p.work);
+        }
+        cudaFree(loss_acc_);
+    }
+
+    std::vector<Param>& params() { return params_; }
+    Pool& pool() { return pool_; }
+
+    void init_weights(unsigned long long seed, cudaStream_t s) {
+        for (size_t i = 0; i < params_.size(); ++i) {
+            Param& p = params_[i];
+            if (p.init_std > 0.f) {
+                // Seed folds in the global parameter name so stages agree
+                // irrespective of how layers are partitioned.
+                unsigned long long h = seed * 0x100000001b3ULL;
+                for (char c : p.name) h = (h ^ static_cast<unsigned char>(c)) * 0x100000001b3ULL;
+                init_normal(p.master, p.numel, p.init_std, h, s);
+            } else {
+                init_const(p.master, p.numel, p.init_val, s);
+            }
+        }
+        sync_weights(s);
+    }
+
+    void sync_weights(cudaStream_t s) {
+        if (dt_ == DType::F32) return;
+        for (Param& p : params_) cast_f32_to(dt_, p.master, p.work, p.numel, s);
+    }
+
+    void zero_grads(cudaStream_t s) {
+        for (Param& p : params_) fill_zero(p.grad, sizeof(float) * p.numel, s);
+    }
+
+    void adamw_step(float lr, float b1, float b2, float eps, float wd, int step, cudaStream_t s) {
+        EPP_REQUIRE(step >= 1, "adamw step must be >= 1");
+        const float bc1 = 1.f - std::pow(b1, static_cast<float>(step));
+        const float bc2 = 1.f - std::pow(b2, static_cast<float>(step));
+        for (Param& p : params_) {
+            // no weight decay on norms / biases
+            const bool decay = p.init_std > 0.f;
+            adamw(p.master, p.work, dt_, p.grad, p.m, p.v, p.numel, lr, b1, b2, eps,
+                  decay ? wd : 0.f, bc1, bc2, s);
+        }
+    }
+
+    void loss(double out[2], bool reset, cudaStream_t s) {
+        float h[2];
+        EPP_CUDA(cudaMemcpyAsync(h, loss_acc_, sizeof(h), cudaMemcpyDeviceToHost, s));
+        EPP_CUDA(cudaStreamSynchronize(s));
+        out[0] = h[0];
+        out[1] = h[1];
+        if (reset) EPP_CUDA(cudaMemsetAsync(loss_acc_, 0, sizeof(float) * 2, s));
+    }
+
+    void release_seq(int seq) { seqs_.erase(seq); }
+
+    // ------------------------------------------------------------------
+    void forward(const epp_chunk_desc& c, const void* act_in, void* act_out, cudaStream_t s) {
+        EPP_REQUIRE(chunks_.find(c.id) == chunks_.end(), "chunk already in flight on this stage");
+        EPP_REQUIRE(c.ckpt_layers >= 0 && c.ckpt_layers <= nl_, "ckpt_layers out of range");
+        ChunkState& cs = chunks_[c.id];
+        try {
+            setup_chunk(cs, c, s);
+            cs.ckpt = c.ckpt_layers;
+            const size_t act_bytes = static_cast<size_t>(cs.T) * D_ * esz();
+            cs.x_in = Buf(&pool_, act_bytes, s);
+            if (has_embed_) {
+                EPP_REQUIRE(c.token_ids != nullptr, "embedding stage needs token_ids");
+                embed_fwd(dt_, c.token_ids, work(emb_), cs.x_in.get(), cs.T, D_, s);
+            } else {
+                EPP_REQUIRE(act_in != nullptr, "act_in is null");
+                EPP_CUDA(cudaMemcpyAsync(cs.x_in.get(), act_in, act_bytes, cudaMemcpyDeviceToDevice, s));
+            }
+            cs.layers.resize(nl_);
+            const void* x = cs.x_in.get();
+            for (int j = 0; j < nl_; ++j) {
+                LayerSaved& L = cs.layers[j];
+                const bool last = j == nl_ - 1;
+                L.x_out = Buf(&pool_, act_bytes, s);
+                layer_forward(cs, j, x, L, /*out=*/L.x_out.get(), /*skip_out=*/false, s);
+                if (j < cs.ckpt) drop_full(L);
+                x = L.x_out.get();
+                (void)last;
+            }
+            if (has_head_) {
+                head_forward(cs, c, x, s);
+            } else {
+                EPP_REQUIRE(act_out != nullptr, "act_out is null");
+                EPP_CUDA(cudaMemcpyAsync(act_out, x, act_bytes, cudaMemcpyDeviceToDevice, s));
+            }
+            // The last layer's output is only needed downstream (or by the
+            // head, already consumed); keep it only where the final norm's
+            // backward needs it (last stage).
+            if (!has_head_ && nl_ > 0) cs.layers[nl_ - 1].x_out.release();
+        } catch (...) {
+            chunks_.erase(c.id);
+            throw;
+        }
+    }
+
+    void backward(const epp_chunk_desc& c, const void* grad_in, void* grad_out, cudaStream_t s) {
+        auto it = chunks_.find(c.id);
+        EPP_REQUIRE(it != chunks_.end(), "backward of a chunk that was not forwarded");
+        ChunkState& cs = it->second;
+        const size_t act_bytes = static_cast<size_t>(cs.T) * D_ * esz();
+        // d(stage output)
+        Buf dy(&pool_, act_bytes, s);
+        if (has_head_) {
+            const void* xl = nl_ > 0 ? cs.layers[nl_ - 1].x_out.get() : cs.x_in.get();
+            norm_bwd(dt_, llama_, xl, work(lnf_w_), cs.dxf.get(), cs.meanf.get<float>(),
+                     cs.rstdf.get<float>(), nullptr, dy.get(), grad(lnf_w_),
+                     lnf_b_ >= 0 ? grad(lnf_b_) : nullptr, cs.T, D_, s);
+            cs.dxf.release();
+        } else {
+            EPP_REQUIRE(grad_in != nullptr, "grad_in is null");
+            EPP_CUDA(cudaMemcpyAsync(dy.get(), grad_in, act_bytes, cudaMemcpyDeviceToDevice, s));
+        }
+        attach_dkv(cs, c, s);
+
+        for (int j = nl_ - 1; j >= 0; --j) {
+            LayerSaved& L = cs.layers[j];
+            const void* x = j == 0 ? cs.x_in.get() : cs.layers[j - 1].x_out.get();
+            if (!L.full) layer_forward(cs, j, x, L, nullptr, /*skip_out=*/true, s);   // recompute
+            Buf dx(&pool_, act_bytes, s);
+            layer_backward(cs, j, x, L, dy.get(), dx.get(), s);
+            drop_full(L);
+            L.x_out.release();
+            dy = std::move(dx);
+        }
+        if (has_embed_) {
+            embed_bwd(dt_, c.token_ids, dy.get(), grad(emb_), cs.T, D_, s);
+        } else {
+            EPP_REQUIRE(grad_out != nullptr, "grad_out is null");
+            EPP_CUDA(cudaMemcpyAsync(grad_out, dy.get(), act_bytes, cudaMemcpyDeviceToDevice, s));
+        }
+        dy.release();
+        const bool first_slice = c.seq >= 0 && c.context == 0;
+        const int seq = c.seq;
+        chunks_.erase(it);
+        if (first_slice) seqs_.erase(seq);
+    }
+
+private:
+    int add(const std::string& name, long long numel, float std, float val = 0.f) {
+        Param p;
+        p.name = name;
+        p.numel = numel;
+        p.init_std = std;
+        p.init_val = val;
+        params_.push_back(p);
+        return static_cast<int>(params_.size()) - 1;
+    }
+    void* work(int i) const { return params_[i].work; }
+    float* grad(int i) const { return params_[i].grad; }
+    size_t esz() const { return dtype_size(dt_); }
+    long long kvw() const { return static_cast<long long>(Hkv_) * hd_; }
+
+    void drop_full(LayerSaved& L) {
+        L.q.release(); L.o.release(); L.lse.release(); L.x_mid.release(); L.h.release();
+        L.full = false;
+    }
+
+    // Segment table, token maps and attention work lists of one chunk.
+    void setup_chunk(ChunkState& cs, const epp_chunk_desc& c, cudaStream_t s) {
+        EPP_REQUIRE(c.nslices >= 1 && c.slices != nullptr, "chunk has no slices");
+        long long T = 0;
+        for (int i = 0; i < c.nslices; ++i) {
+            EPP_REQUIRE(c.slices[i] > 0, "slice length must be positive");
+            T += c.slices[i];
+        }
+        EPP_REQUIRE(T < (1LL << 31), "chunk too large");
+        cs.T = static_cast<int>(T);
+        const bool seq_chunk = c.seq >= 0;
+        if (seq_chunk) {
+            EPP_REQUIRE(c.seq_len >= c.context + c.slices[0], "seq_len shorter than the slice");
+            SeqKV& sk = seqs_[c.seq];
+            if (!sk.kv) {
+                sk.len = c.seq_len;
+                sk.kv = Buf(&pool_, 2 * static_cast<size_t>(nl_) * sk.len * kvw() * esz(), s);
+            }
+            EPP_REQUIRE(sk.len == c.seq_len, "seq_len changed between slices");
+        } else {
+            EPP_REQUIRE(c.context == 0, "context without a sequence");
+        }
+        cs.kv_local = Buf(&pool_, 2 * static_cast<size_t>(nl_) * T * kvw() * esz(), s);
+        int max_pos = 0;
+        long long q_start = 0;
+        cs.segs.clear();
+        for (int i = 0; i < c.nslices; ++i) {
+            AttnSeg sg{};
+            sg.q_start = static_cast<int>(q_start);
+            sg.q_len = static_cast<int>(c.slices[i]);
+            if (i == 0 && seq_chunk) {
+                SeqKV& sk = seqs_[c.seq];
+                sg.kv_ctx = static_cast<int>(c.context);
+                sg.k = sk.kv.get<uint8_t>();
+                sg.v = sk.kv.get<uint8_t>() + static_cast<size_t>(nl_) * sk.len * kvw() * esz();
+                sg.kv_layer_stride = sk.len * kvw();
+                sg.dkv_layer_stride = sk.len * kvw();
+            } else {
+                // Packed document: K/V rows in the chunk-local buffer (layer
+                // strided like the sequence buffers); dK/dV in a one-layer
+                // scratch (dkv stride 0), bound at backward.
+                sg.kv_ctx = 0;
+                const size_t row0 = static_cast<size_t>(q_start) * kvw();
+                sg.k = cs.kv_local.get<uint8_t>() + row0 * esz();
+                sg.v = cs.kv_local.get<uint8_t>() + (static_cast<size_t>(nl_) * T * kvw() + row0) * esz();
+                sg.kv_layer_stride = T * kvw();
+                sg.dkv_layer_stride = 0;
+            }
+            max_pos = std::max(max_pos, sg.kv_ctx + sg.q_len);
+            cs.segs.push_back(sg);
+            q_start += c.slices[i];
+        }
+        rope_reserve(max_pos, hd_, m_.rope_theta, s);
+        std::vector<int> tseg(cs.T), tpos(cs.T);
+        std::vector<AttnWork> qw, kw;
+        for (int i = 0; i < static_cast<int>(cs.segs.size()); ++i) {
+            const AttnSeg& sg = cs.segs[i];
+            for (int t = 0; t < sg.q_len; ++t) {
+                tseg[sg.q_start + t] = i;
+                tpos[sg.q_start + t] = sg.kv_ctx + t;
+            }
+            for (int b = 0; b * kAttnBlock < sg.q_len; ++b) qw.push_back({i, b});
+            for (int b = 0; b * kAttnBlock < sg.kv_ctx + sg.q_len; ++b) kw.push_back({i, b});
+        }
+        cs.nqwork = static_cast<int>(qw.size());
+        cs.nkwork = static_cast<int>(kw.size());
+        cs.tok_seg = upload(tseg.data(), tseg.size() * sizeof(int), s);
+        cs.tok_pos = upload(tpos.data(), tpos.size() * sizeof(int), s);
+        cs.qwork = upload(qw.data(), qw.size() * sizeof(AttnWork), s);
+        cs.kwork = upload(kw.data(), kw.size() * sizeof(AttnWork), s);
+        cs.segs_dev = upload(cs.segs.data(), cs.segs.size() * sizeof(AttnSeg), s);
+    }
+
+    Buf upload(const void* host, size_t bytes, cudaStream_t s) {
+        Buf b(&pool_, bytes, s);
+        if (bytes) copy_h2d(b.get(), host, bytes, s);
+        return b;
+    }
+    void copy_h2d(void* dst, const void* host, size_t bytes, cudaStream_t s) {
+        const void* src = ring_.stage(host, bytes, s);
+        EPP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    }
+
+    // Bind dK/dV accumulators into the segment table: the sequence's
+    // persistent fp32 buffer for segment 0 of a Split/Hybrid chunk, a
+    // one-layer chunk-local scratch for packed documents.
+    void attach_dkv(ChunkState& cs, const epp_chunk_desc& c, cudaStream_t s) {
+        const size_t half = static_cast<size_t>(cs.T) * kvw();
+        cs.dkv_local = Buf(&pool_, 2 * half * sizeof(float), s);
+        for (size_t i = 0; i < cs.segs.size(); ++i) {
+            AttnSeg& sg = cs.segs[i];
+            if (i == 0 && c.seq >= 0) {
+                SeqKV& sk = seqs_[c.seq];
+                if (!sk.dkv)
+                    sk.dkv = Buf(&pool_, 2 * static_cast<size_t>(nl_) * sk.len * kvw() * sizeof(float),
+                                 s, /*zero=*/true);
+                sg.dk = sk.dkv.get<float>();
+                sg.dv = sk.dkv.get<float>() + static_cast<size_t>(nl_) * sk.len * kvw();
+            } else {
+                const size_t row0 = static_cast<size_t>(sg.q_start) * kvw();
+                sg.dk = cs.dkv_local.get<float>() + row0;
+                sg.dv = cs.dkv_local.get<float>() + half + row0;
+            }
+        }
+        copy_h2d(cs.segs_dev.get(), cs.segs.data(), cs.segs.size() * sizeof(AttnSeg), s);
+    }
+
+    AttnArgs attn_args(ChunkState& cs, int j) const {
+        AttnArgs a;
+        a.segs = cs.segs_dev.get<AttnSeg>();
+        a.nseg = static_cast<int>(cs.segs.size());
+        a.qwork = cs.qwork.get<AttnWork>();
+        a.nqwork = cs.nqwork;
+        a.kwork = cs.kwork.get<AttnWork>();
+        a.nkwork = cs.nkwork;
+        a.T = cs.T;
+        a.H = H_;
+        a.Hkv = Hkv_;
+        a.hd = hd_;
+        a.layer = j;
+        a.scale = 1.f / std::sqrt(static_cast<float>(hd_));
+        a.dtype = dt_;
+        return a;
+    }
+
+    // Forward of stage layer j on input x.  Writes the saved activations into
+    // L (q, o, lse, x_mid, h, kv_local, norm stats) and, unless skip_out, the
+    // layer output to `out`.
+    void layer_forward(ChunkState& cs, int j, const void* x, LayerSaved& L, void* out, bool skip_out,
+                       cudaStream_t s) {
+        const LayerParams& P = lps_[j];
+        const int T = cs.T;
+        const size_t e = esz();
+        if (!L.mean1) {
+            L.mean1 = Buf(&pool_, sizeof(float) * T, s);
+            L.rstd1 = Buf(&pool_, sizeof(float) * T, s);
+            L.mean2 = Buf(&pool_, sizeof(float) * T, s);
+            L.rstd2 = Buf(&pool_, sizeof(float) * T, s);
+        }
+        L.q = Buf(&pool_, static_cast<size_t>(T) * H_ * hd_ * e, s);
+        L.o = Buf(&pool_, static_cast<size_t>(T) * H_ * hd_ * e, s);
+        L.lse = Buf(&pool_, sizeof(float) * H_ * T, s);
+        L.x_mid = Buf(&pool_, static_cast<size_t>(T) * D_ * e, s);
+        L.h = Buf(&pool_, static_cast<size_t>(T) * F1_ * e, s);
+        L.full = true;
+
+        Buf xn(&pool_, static_cast<size_t>(T) * D_ * e, s);
+        norm_fwd(dt_, llama_, x, work(P.ln1_w), P.ln1_b >= 0 ? work(P.ln1_b) : nullptr, xn.get(),
+                 llama_ ? nullptr : L.mean1.get<float>(), L.rstd1.get<float>(), T, D_,
+                 m_.norm_eps, s);
+        Buf qkv(&pool_, static_cast<size_t>(T) * Nqkv_ * e, s);
+        gemm(mk(T, Nqkv_, D_, xn.get(), D_, true, work(P.wqkv), D_, true, qkv.get(), Nqkv_), s);
+        rope_qkv_scatter(dt_, qkv.get(), L.q.get(), cs.segs_dev.get<AttnSeg>(),
+                         static_cast<int>(cs.segs.size()), cs.tok_seg.get<int>(),
+                         cs.tok_pos.get<int>(), T, H_, Hkv_, hd_, j, m_.rope_theta, s);
+        qkv.release();
+        AttnArgs a = attn_args(cs, j);
+        a.q = L.q.get();
+        a.o = L.o.get();
+        a.lse = L.lse.get<float>();
+        attn_fwd(a, s);
+        // x_mid = x + o Wo^T
+        GemmArgs g = mk(T, D_, H_ * hd_, L.o.get(), H_ * hd_, true, work(P.wo), H_ * hd_, true,
+                        L.x_mid.get(), D_);
+        g.epi = Epi::AddRes;
+        g.R = x;
+        g.ldr = D_;
+        gemm(g, s);
+        norm_fwd(dt_, llama_, L.x_mid.get(), work(P.ln2_w), P.ln2_b >= 0 ? work(P.ln2_b) : nullptr,
+                 xn.get(), llama_ ? nullptr : L.mean2.get<float>(), L.rstd2.get<float>(), T, D_,
+                 m_.norm_eps, s);
+        gemm(mk(T, F1_, D_, xn.get(), D_, true, work(P.w1), D_, true, L.h.get(), F1_), s);
+        xn.release();
+        if (!skip_out) {
+            Buf act(&pool_, static_cast<size_t>(T) * F_ * e, s);
+            act_fwd(dt_, llama_ ? 1 : 0, L.h.get(), act.get(), T, F_, s);
+            GemmArgs g2 = mk(T, D_, F_, act.get(), F_, true, work(P.w2), F_, true, out, D_);
+            g2.epi = Epi::AddRes;
+            g2.R = L.x_mid.get();
+            g2.ldr = D_;
+            gemm(g2, s);
+        }
+    }
+
+    void layer_backward(ChunkState& cs, int j, const void* x, LayerSaved& L, const void* dy,
+                        void* dx, cudaStream_t s) {
+        const LayerParams& P = lps_[j];
+        const int T = cs.T;
+        const size_t e = esz();
+        const int Dq = H_ * hd_;
+        // ---- MLP ----
+        Buf act(&pool_, static_cast<size_t>(T) * F_ * e, s);
+        act_fwd(dt_, llama_ ? 1 : 0, L.h.get(), act.get(), T, F_, s);
+        Buf da(&pool_, static_cast<size_t>(T) * F_ * e, s);
+        gemm(mk(T, F_, D_, dy, D_, true, work(P.w2), F_, false, da.get(), F_), s);        // dA = dY W2
+        wgrad(D_, F_, T, dy, D_, act.get(), F_, grad(P.w2), s);                            // dW2 += dY^T A
+        act.release();
+        Buf dh(&pool_, static_cast<size_t>(T) * F1_ * e, s);
+        act_bwd(dt_, llama_ ? 1 : 0, L.h.get(), da.get(), dh.get(), T, F_, s);
+        da.release();
+        Buf dxn(&pool_, static_cast<size_t>(T) * D_ * e, s);
+        gemm(mk(T, D_, F1_, dh.get(), F1_, true, work(P.w1), D_, false, dxn.get(), D_), s);  // dXn2
+        Buf xn(&pool_, static_cast<size_t>(T) * D_ * e, s);
+        norm_apply(dt_, llama_, L.x_mid.get(), work(P.ln2_w), P.ln2_b >= 0 ? work(P.ln2_b) : nullptr,
+                   llama_ ? nullptr : L.mean2.get<float>(), L.rstd2.get<float>(), xn.get(), T, D_, s);
+        wgrad(F1_, D_, T, dh.get(), F1_, xn.get(), D_, grad(P.w1), s);                     // dW1
+        dh.release();
+        Buf dxm(&pool_, static_cast<size_t>(T) * D_ * e, s);
+        norm_bwd(dt_, llama_, L.x_mid.get(), work(P.ln2_w), dxn.get(),
+                 llama_ ? nullptr : L.mean2.get<float>(), L.rstd2.get<float>(), dy, dxm.get(),
+                 grad(P.ln2_w), P.ln2_b >= 0 ? grad(P.ln2_b) : nullptr, T, D_, s);
+        // ---- attention ----
+        Buf dout(&pool_, static_cast<size_t>(T) * Dq * e, s);
+        gemm(mk(T, Dq, D_, dxm.get(), D_, true, work(P.wo), Dq, false, dout.get(), Dq), s);  // dO
+        wgrad(D_, Dq, T, dxm.get(), D_, L.o.get(), Dq, grad(P.wo), s);                       // dWo
+        Buf dq(&pool_, sizeof(float) * static_cast<size_t>(T) * Dq, s);
+        Buf delta(&pool_, sizeof(float) * static_cast<size_t>(H_) * T, s);
+        fill_zero(cs.dkv_local.get(), 2 * static_cast<size_t>(T) * kvw() * sizeof(float), s);
+        AttnArgs a = attn_args(cs, j);
+        a.q = L.q.get();
+        a.o = L.o.get();
+        a.lse = L.lse.get<float>();
+        a.dout = dout.get();
+        a.delta = delta.get<float>();
+        a.dq = dq.get<float>();
+        attn_bwd(a, s);
+        dout.release();
+        delta.release();
+        Buf dqkv(&pool_, static_cast<size_t>(T) * Nqkv_ * e, s);
+        rope_qkv_gather_grad(dt_, dq.get<float>(), cs.segs_dev.get<AttnSeg>(), cs.tok_seg.get<int>(),
+                             cs.tok_pos.get<int>(), dqkv.get(), T, H_, Hkv_, hd_, j, m_.rope_theta, s);
+        dq.release();
+        gemm(mk(T, D_, Nqkv_, dqkv.get(), Nqkv_, true, work(P.wqkv), D_, false, dxn.get(), D_), s);
+        norm_apply(dt_, llama_, x, work(P.ln1_w), P.ln1_b >= 0 ? work(P.ln1_b) : nullptr,
+                   llama_ ? nullptr : L.mean1.get<float>(), L.rstd1.get<float>(), xn.get(), T, D_, s);
+        wgrad(Nqkv_, D_, T, dqkv.get(), Nqkv_, xn.get(), D_, grad(P.wqkv), s);
+        dqkv.release();
+        xn.release();
+        norm_bwd(dt_, llama_, x, work(P.ln1_w), dxn.get(), llama_ ? nullptr : L.mean1.get<float>(),
+                 L.rstd1.get<float>(), dxm.get(), dx, grad(P.ln1_w),
+                 P.ln1_b >= 0 ? grad(P.ln1_b) : nullptr, T, D_, s);
+    }
+
+    // Last stage: final norm, LM head, cross-entropy and its backward through
+    // the head, in row blocks so the [rows, vocab] logits stay bounded.
+    void head_forward(ChunkState& cs, const epp_chunk_desc& c, const void* x, cudaStream_t s) {
+        EPP_REQUIRE(c.target_ids != nullptr, "last stage needs target_ids");
+        const int T = cs.T;
+        const size_t e = esz();
+        const int V = m_.vocab;
+        cs.meanf = Buf(&pool_, sizeof(float) * T, s);
+        cs.rstdf = Buf(&pool_, sizeof(float) * T, s);
+        Buf xf(&pool_, static_cast<size_t>(T) * D_ * e, s);
+        norm_fwd(dt_, llama_, x, work(lnf_w_), lnf_b_ >= 0 ? work(lnf_b_) : nullptr, xf.get(),
+                 llama_ ? nullptr : cs.meanf.get<float>(), cs.rstdf.get<float>(), T, D_, m_.norm_eps,
+                 s);
+        cs.dxf = Buf(&pool_, static_cast<size_t>(T) * D_ * e, s);
+        const int rows = std::max(1, std::min(T, static_cast<int>((512LL << 20) / (static_cast<long long>(V) * e))));
+        Buf logits(&pool_, static_cast<size_t>(rows) * V * e, s);
+        for (int r0 = 0; r0 < T; r0 += rows) {
+            const int n = std::min(rows, T - r0);
+            const uint8_t* xr = xf.get<uint8_t>() + static_cast<size_t>(r0) * D_ * e;
+            gemm(mk(n, V, D_, xr, D_, true, work(lm_), D_, true, logits.get(), V), s);
+            cross_entropy(dt_, logits.get(), c.target_ids + r0, loss_acc_, n, V, c.loss_scale, s);
+            // dXf = dLogits Wlm ; dWlm += dLogits^T Xf
+            gemm(mk(n, D_, V, logits.get(), V, true, work(lm_), D_, false,
+                    cs.dxf.get<uint8_t>() + static_cast<size_t>(r0) * D_ * e, D_), s);
+            wgrad(V, D_, n, logits.get(), V, xr, D_, grad(lm_), s);
+        }
+    }
+
+    GemmArgs mk(int M, int N, int K, const void* A, long long lda, bool ak, const void* B,
+                long long ldb, bool bk, void* C, long long ldc) const {
+        GemmArgs g;
+        g.M = M; g.N = N; g.K = K;
+        g.A = A; g.lda = lda; g.a_kmajor = ak;
+        g.B = B; g.ldb = ldb; g.b_kmajor = bk;
+        g.C = C; g.ldc = ldc;
+        g.dtype = dt_;
+        return g;
+    }
+    // dW[M,N] += sum_t dY[t, m] X[t, n]  (both operands MN-major)
+    void wgrad(int M, int N, int T, const void* dy, long long ldy, const void* x, long long ldx,
+               float* dw, cudaStream_t s) const {
+        GemmArgs g = mk(M, N, T, dy, ldy, false, x, ldx, false, dw, N);
+        g.epi = Epi::AccumF32;
+        gemm(g, s);
+    }
+
+    epp_model_desc m_;
+    int first_, nl_;
+    bool has_embed_, has_head_;
+    DType dt_;
+    int D_ = 0, H_ = 0, Hkv_ = 0, hd_ = 0, F_ = 0, F1_ = 0, Nqkv_ = 0;
+    bool llama_ = false;
+    std::vector<Param> params_;
+    std::vector<LayerParams> lps_;
+    int emb_ = -1, lnf_w_ = -1, lnf_b_ = -1, lm_ = -1;
+    float* loss_acc_ = nullptr;
+    Pool pool_;
+    PinnedRing ring_{32u << 20};
+    std::map<int, ChunkState> chunks_;
+    std::map<int, SeqKV> seqs_;
+};
+
+}  // namespace eppk
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+struct epp_stage {
+    std::unique_ptr<eppk::StageImpl> impl;
+};
+
+namespace {
+
+template <typename F>
+int guard(F&& f) {
+    eppk::g_err.clear();
+    try {
+        f();
+        return EPP_GPU_OK;
+    } catch (const eppk::CudaError& e) {
+        eppk::g_err = e.what();
+        return EPP_GPU_ECUDA;
+    } catch (const std::invalid_argument& e) {
+        eppk::g_err = e.what();
+        return EPP_GPU_EARG;
+    } catch (const std::exception& e) {
+        eppk::g_err = e.what();
+        return EPP_GPU_EOTHER;
+    }
+}
+
+cudaStream_t S(void* p) { return static_cast<cudaStream_t>(p); }
+
+}  // namespace
+
+extern "C" {
+
+int epp_gpu_set_device(int device) {
+    return guard([&] { EPP_CUDA(cudaSetDevice(device)); });
+}
+
+int epp_stage_create(const epp_model_desc* model, int first_layer, int num_layers, int has_embed,
+                     int has_head, int dtype, epp_stage** out) {
+    return guard([&] {
+        EPP_REQUIRE(model && out, "null argument");
+        EPP_REQUIRE(dtype == EPP_DTYPE_F32 || dtype == EPP_DTYPE_BF16, "bad dtype");
+        auto* st = new epp_stage;
+        try {
+            st->impl = std::make_unique<eppk::StageImpl>(*model, first_layer, num_layers, has_embed != 0,
+                                                         has_head != 0, static_cast<eppk::DType>(dtype));
+        } catch (...) {
+            delete st;
+            throw;
+        }
+        *out = st;
+    });
+}
+
+int epp_stage_destroy(epp_stage* st) {
+    return guard([&] { delete st; });
+}
+
+int epp_stage_init_weights(epp_stage* st, uint64_t seed, void* stream) {
+    return guard([&] { st->impl->init_weights(seed, S(stream)); });
+}
+
+int epp_stage_num_params(epp_stage* st, int32_t* n) {
+    return guard([&] { *n = static_cast<int32_t>(st->impl->params().size()); });
+}
+
+int epp_stage_param(epp_stage* st, int32_t idx, epp_param_info* info) {
+    return guard([&] {
+        auto& ps = st->impl->params();
+        EPP_REQUIRE(idx >= 0 && idx < static_cast<int32_t>(ps.size()), "param index out of range");
+        const auto& p = ps[idx];
+        info->name = p.name.c_str();
+        info->numel = p.numel;
+        info->master = p.master;
+        info->work = p.work;
+        info->grad = p.grad;
+    });
+}
+
+int epp_stage_sync_weights(epp_stage* st, void* stream) {
+    return guard([&] { st->impl->sync_weights(S(stream)); });
+}
+
+int epp_stage_forward(epp_stage* st, const epp_chunk_desc* chunk, const void* act_in, void* act_out,
+                      void* stream) {
+    return guard([&] { st->impl->forward(*chunk, act_in, act_out, S(stream)); });
+}
+
+int epp_stage_backward(epp_stage* st, const epp_chunk_desc* chunk, const void* grad_in,
+                       void* grad_out, void* stream) {
+    return guard([&] { st->impl->backward(*chunk, grad_in, grad_out, S(stream)); });
+}
+
+int epp_seq_release(epp_stage* st, int32_t seq) {
+    return guard([&] { st->impl->release_seq(seq); });
+}
+
+int epp_stage_loss(epp_stage* st, double out[2], int32_t reset, void* stream) {
+    return guard([&] { st->impl->loss(out, reset != 0, S(stream)); });
+}
+
+int epp_stage_zero_grads(epp_stage* st, void* stream) {
+    return guard([&] { st->impl->zero_grads(S(stream)); });
+}
+
+int epp_stage_adamw_step(epp_stage* st, float lr, float beta1, float beta2, float eps,
+                         float weight_decay, int32_t step, void* stream) {
+    return guard([&] { st->impl->adamw_step(lr, beta1, beta2, eps, weight_decay, step, S(stream)); });
+}
+
+int epp_stage_memory(epp_stage* st, int64_t* live_bytes, int64_t* peak_bytes) {
+    return guard([&] {
+        if (live_bytes) *live_bytes = st->impl->pool().live;
+        if (peak_bytes) *peak_bytes = st->impl->pool().peak;
+    });
+}
+
+const char* epp_gpu_last_error(void) { return eppk::g_err.c_str(); }
+
+int64_t epp_gpu_kernel_launches(void) { return eppk::launch_counter(); }
+
+}  // extern "C"

@@ -1,0 +1,186 @@
+"""Replays a plan document on stage executors — the EPP training step.
+
+    plan_{i} = planner.make_plan(lengths_i)        (CPU, can be pre-solved)
+    for unit in plan.units:                        (sequential 1F1B pipelines,
+        every stage runs stage_ops(...)             gradient-accumulated)
+    optimizer step on every stage
+
+Two drivers share the op-list logic (schedule.stage_ops):
+  * LocalPipeline — every stage in this process (one GPU running d_p stages,
+    or the d_p = 1 single-GPU configuration); ops are issued in a
+    dependency-respecting round robin over the stages' op lists.
+  * DistributedPipeline — one stage per rank (torch.distributed, NCCL on
+    B200s, gloo in the CPU tests).  Activations go p -> p+1 and gradients
+    p+1 -> p over two separate process groups per adjacent pair, so the
+    forward and backward streams of messages can never block each other;
+    both sides derive every message size from the plan, no handshake.
+
+A stage is any object with forward(chunk, act_in) / backward(chunk, grad_in)
+(gpu.CudaStage on the product path).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from .schedule import ChunkLayout, Plan, chunk_token_arrays, stage_ops
+
+
+@dataclass
+class ChunkOp:
+    """Per-(stage, chunk) call arguments (mirrors epp_chunk_desc)."""
+    id: int
+    seq: int
+    kind: int
+    tail: bool
+    context: int
+    seq_len: int
+    slices: List[int]
+    ckpt_layers: int
+    loss_scale: float
+    token_ids: Optional[torch.Tensor]
+    target_ids: Optional[torch.Tensor]
+
+
+def stage_layers(layers: int, pp_degree: int, stage: int):
+    """(first layer, count) of 0-based `stage` — contiguous L/d_p blocks
+    (proj/src/config.cpp:25-26 requires L % d_p == 0)."""
+    per = layers // pp_degree
+    return stage * per, per
+
+
+class _ChunkTokens:
+    """Token ids / targets of every chunk of a step, staged from pinned host
+    memory to the device (counted as the step's H2D bytes)."""
+
+    def __init__(self, plan: Plan, tokens: Sequence[np.ndarray], device: torch.device, need_ids: bool,
+                 need_targets: bool):
+        self.ids: Dict[int, torch.Tensor] = {}
+        self.tgt: Dict[int, torch.Tensor] = {}
+        self.h2d_bytes = 0
+        pin = device.type == "cuda"
+        for cid, lay in plan.chunks.items():
+            ids, tgt = chunk_token_arrays(lay, tokens)
+            if need_ids:
+                t = torch.from_numpy(ids)
+                if pin:
+                    t = t.pin_memory()
+                self.ids[cid] = t.to(device, non_blocking=True)
+                self.h2d_bytes += t.numel() * 4
+            if need_targets:
+                t = torch.from_numpy(tgt)
+                if pin:
+                    t = t.pin_memory()
+                self.tgt[cid] = t.to(device, non_blocking=True)
+                self.h2d_bytes += t.numel() * 4
+
+
+def _op(plan: Plan, unit, pos: int, stage: int, toks: _ChunkTokens) -> ChunkOp:
+    lay: ChunkLayout = plan.chunks[unit.chunks[pos]]
+    return ChunkOp(lay.id, lay.seq, lay.kind, lay.tail, lay.context, lay.seq_len, lay.slices,
+                   unit.ckpt[stage][pos], 1.0 / max(1, plan.total_targets),
+                   toks.ids.get(lay.id), toks.tgt.get(lay.id))
+
+
+class LocalPipeline:
+    def __init__(self, stages: Sequence, device: torch.device):
+        self.stages = list(stages)
+        self.device = device
+
+    def run_step(self, plan: Plan, tokens: Sequence[np.ndarray]) -> dict:
+        dp = len(self.stages)
+        if dp != plan.pp_degree:
+            raise ValueError(f"plan is for {plan.pp_degree} stages, executor has {dp}")
+        toks = _ChunkTokens(plan, tokens, self.device, True, True)
+        for unit in plan.units:
+            self._run_unit(plan, unit, toks)
+        return {"h2d_bytes": toks.h2d_bytes}
+
+    def _run_unit(self, plan: Plan, unit, toks: _ChunkTokens):
+        dp = len(self.stages)
+        n = len(unit.chunks)
+        order = unit.backward_order
+        ops = [stage_ops(n, unit.n_prefill, dp, p + 1, order) for p in range(dp)]
+        idx = [0] * dp
+        acts: Dict[tuple, torch.Tensor] = {}
+        grads: Dict[tuple, torch.Tensor] = {}
+        remaining = sum(len(o) for o in ops)
+        while remaining:
+            progressed = False
+            for p in range(dp):
+                while idx[p] < len(ops[p]):
+                    kind, pos = ops[p][idx[p]]
+                    if kind == "F":
+                        if p > 0 and (p - 1, pos) not in acts:
+                            break
+                        act_in = acts.pop((p - 1, pos)) if p > 0 else None
+                        out = self.stages[p].forward(_op(plan, unit, pos, p, toks), act_in)
+                        if p + 1 < dp:
+                            acts[(p, pos)] = out
+                    else:
+                        if p + 1 < dp and (p + 1, pos) not in grads:
+                            break
+                        g_in = grads.pop((p + 1, pos)) if p + 1 < dp else None
+                        g_out = self.stages[p].backward(_op(plan, unit, pos, p, toks), g_in)
+                        if p > 0:
+                            grads[(p, pos)] = g_out
+                    idx[p] += 1
+                    remaining -= 1
+                    progressed = True
+            if not progressed:
+                raise RuntimeError("pipeline op lists deadlocked (plan/op-list mismatch)")
+
+
+class DistributedPipeline:
+    """One stage per rank of the default process group (rank = stage)."""
+
+    def __init__(self, stage, rank: int, world: int, device: torch.device, hidden: int,
+                 act_dtype: torch.dtype):
+        import torch.distributed as dist
+        self.dist = dist
+        self.stage, self.rank, self.world = stage, rank, world
+        self.device, self.hidden, self.act_dtype = device, hidden, act_dtype
+        # One group per adjacent pair and direction; every rank creates all of
+        # them in the same order (new_group is collective).
+        self.fwd_groups, self.bwd_groups = [], []
+        for p in range(world - 1):
+            self.fwd_groups.append(dist.new_group([p, p + 1]))
+            self.bwd_groups.append(dist.new_group([p, p + 1]))
+        self.p2p_bytes = 0
+
+    def run_step(self, plan: Plan, tokens: Sequence[np.ndarray]) -> dict:
+        p, dp = self.rank, self.world
+        if dp != plan.pp_degree:
+            raise ValueError(f"plan is for {plan.pp_degree} stages, world size is {dp}")
+        toks = _ChunkTokens(plan, tokens, self.device, need_ids=(p == 0), need_targets=(p == dp - 1))
+        pending = []
+        for unit in plan.units:
+            n = len(unit.chunks)
+            for kind, pos in stage_ops(n, unit.n_prefill, dp, p + 1, unit.backward_order):
+                T = plan.chunks[unit.chunks[pos]].tokens
+                op = _op(plan, unit, pos, p, toks)
+                if kind == "F":
+                    act_in = None
+                    if p > 0:
+                        act_in = torch.empty((T, self.hidden), dtype=self.act_dtype, device=self.device)
+                        self.dist.irecv(act_in, src=p - 1, group=self.fwd_groups[p - 1]).wait()
+                    out = self.stage.forward(op, act_in)
+                    if p + 1 < dp:
+                        pending.append((self.dist.isend(out, dst=p + 1, group=self.fwd_groups[p]), out))
+                        self.p2p_bytes += out.numel() * out.element_size()
+                else:
+                    g_in = None
+                    if p + 1 < dp:
+                        g_in = torch.empty((T, self.hidden), dtype=self.act_dtype, device=self.device)
+                        self.dist.irecv(g_in, src=p + 1, group=self.bwd_groups[p]).wait()
+                    g_out = self.stage.backward(op, g_in)
+                    if p > 0:
+                        pending.append((self.dist.isend(g_out, dst=p - 1, group=self.bwd_groups[p - 1]), g_out))
+                        self.p2p_bytes += g_out.numel() * g_out.element_size()
+            for w, _ in pending:
+                w.wait()
+            pending.clear()
+        return {"h2d_bytes": toks.h2d_bytes}

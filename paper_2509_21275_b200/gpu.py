@@ -1,0 +1,233 @@
+"""ctypes binding of libepp_gpu.so (include/epp_gpu.h) with torch plumbing.
+
+torch provides device memory and streams; all compute goes through the CUDA
+library.  Loading fails loudly when the library is missing — there is no CPU
+fallback on the product path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+from typing import Dict, Optional
+
+import numpy as np
+import torch
+
+from .model import ModelConfig
+
+_LIB_PATH = Path(__file__).resolve().parent / "libepp_gpu.so"
+_lib = None
+
+DTYPES = {"f32": 0, "bf16": 1}
+TORCH_DTYPES = {"f32": torch.float32, "bf16": torch.bfloat16}
+
+
+class EppGpuError(RuntimeError):
+    pass
+
+
+class ModelDesc(ctypes.Structure):
+    _fields_ = [("arch", ctypes.c_int32), ("layers", ctypes.c_int32), ("hidden", ctypes.c_int32),
+                ("heads", ctypes.c_int32), ("kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("ffn", ctypes.c_int32), ("vocab", ctypes.c_int32), ("rope_theta", ctypes.c_float),
+                ("norm_eps", ctypes.c_float)]
+
+
+class ChunkDesc(ctypes.Structure):
+    _fields_ = [("id", ctypes.c_int32), ("seq", ctypes.c_int32), ("kind", ctypes.c_int32),
+                ("tail", ctypes.c_int32), ("context", ctypes.c_int64), ("seq_len", ctypes.c_int64),
+                ("nslices", ctypes.c_int32), ("slices", ctypes.POINTER(ctypes.c_int64)),
+                ("ckpt_layers", ctypes.c_int32), ("loss_scale", ctypes.c_float),
+                ("token_ids", ctypes.c_void_p), ("target_ids", ctypes.c_void_p)]
+
+
+class ParamInfo(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char_p), ("numel", ctypes.c_int64), ("master", ctypes.c_void_p),
+                ("work", ctypes.c_void_p), ("grad", ctypes.c_void_p)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise ImportError(f"{_LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
+        L = ctypes.CDLL(str(_LIB_PATH), mode=os.RTLD_LOCAL)
+        vp, i32, i64, f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
+        sig = {
+            "epp_gpu_set_device": [ctypes.c_int],
+            "epp_stage_create": [ctypes.POINTER(ModelDesc), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                 ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
+            "epp_stage_destroy": [vp],
+            "epp_stage_init_weights": [vp, ctypes.c_uint64, vp],
+            "epp_stage_num_params": [vp, ctypes.POINTER(i32)],
+            "epp_stage_param": [vp, i32, ctypes.POINTER(ParamInfo)],
+            "epp_stage_sync_weights": [vp, vp],
+            "epp_stage_forward": [vp, ctypes.POINTER(ChunkDesc), vp, vp, vp],
+            "epp_stage_backward": [vp, ctypes.POINTER(ChunkDesc), vp, vp, vp],
+            "epp_seq_release": [vp, i32],
+            "epp_stage_loss": [vp, ctypes.POINTER(ctypes.c_double), i32, vp],
+            "epp_stage_zero_grads": [vp, vp],
+            "epp_stage_adamw_step": [vp, f32, f32, f32, f32, f32, i32, vp],
+            "epp_stage_memory": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)],
+            "epp_kernel_gemm": [i32, i32, i32, vp, i64, i32, vp, i64, i32, vp, i64, vp, i64, i32, i32, vp],
+            "epp_kernel_attention_fwd": [i32, i32, i32, i32, f32, i32, ctypes.POINTER(i32),
+                                         ctypes.POINTER(i32), ctypes.POINTER(i32),
+                                         ctypes.POINTER(vp), ctypes.POINTER(vp), vp, vp, vp, i32, vp],
+            "epp_kernel_attention_bwd": [i32, i32, i32, i32, f32, i32, ctypes.POINTER(i32),
+                                         ctypes.POINTER(i32), ctypes.POINTER(i32),
+                                         ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                         ctypes.POINTER(vp), vp, vp, vp, vp, vp, i32, vp],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        L.epp_gpu_last_error.restype = ctypes.c_char_p
+        L.epp_gpu_kernel_launches.restype = ctypes.c_int64
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise EppGpuError(lib().epp_gpu_last_error().decode())
+
+
+def kernel_launches() -> int:
+    return int(lib().epp_gpu_kernel_launches())
+
+
+def stream_ptr(stream: Optional[torch.cuda.Stream] = None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+class CudaStage:
+    """One pipeline stage on the current CUDA device (the CUDA executor)."""
+
+    def __init__(self, model: ModelConfig, first: int, num: int, has_embed: bool, has_head: bool,
+                 dtype: str = "bf16", device: Optional[int] = None):
+        self.model, self.first, self.num = model, first, num
+        self.has_embed, self.has_head = has_embed, has_head
+        self.dtype = dtype
+        self.tdtype = TORCH_DTYPES[dtype]
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        L = lib()
+        check(L.epp_gpu_set_device(self.device.index))
+        desc = ModelDesc(1 if model.llama else 0, model.layers, model.hidden, model.heads,
+                         model.kv_heads, model.head_dim, model.ffn, model.vocab,
+                         model.rope_theta, model.norm_eps)
+        h = ctypes.c_void_p()
+        check(L.epp_stage_create(ctypes.byref(desc), first, num, int(has_embed), int(has_head),
+                                 DTYPES[dtype], ctypes.byref(h)))
+        self.h = h
+        self._keep = {}
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            check(lib().epp_stage_destroy(self.h))
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- parameters ----------------------------------------------------------
+    def params(self) -> Dict[str, dict]:
+        L = lib()
+        n = ctypes.c_int32()
+        check(L.epp_stage_num_params(self.h, ctypes.byref(n)))
+        out = {}
+        for i in range(n.value):
+            info = ParamInfo()
+            check(L.epp_stage_param(self.h, i, ctypes.byref(info)))
+            out[info.name.decode()] = {"numel": info.numel, "master": info.master, "work": info.work,
+                                       "grad": info.grad}
+        return out
+
+    def init_weights(self, seed: int):
+        check(lib().epp_stage_init_weights(self.h, seed, stream_ptr()))
+
+    def load_weights(self, weights: Dict[str, torch.Tensor]):
+        for name, p in self.params().items():
+            src = weights[name].detach().to(self.device, torch.float32).contiguous().view(-1)
+            assert src.numel() == p["numel"], name
+            _wrap_ptr(p["master"], p["numel"], torch.float32, self.device).copy_(src)
+        check(lib().epp_stage_sync_weights(self.h, stream_ptr()))
+
+    def grads(self) -> Dict[str, torch.Tensor]:
+        return {name: _wrap_ptr(p["grad"], p["numel"], torch.float32, self.device).clone()
+                for name, p in self.params().items()}
+
+    def zero_grads(self):
+        check(lib().epp_stage_zero_grads(self.h, stream_ptr()))
+
+    def adamw_step(self, lr, step, b1=0.9, b2=0.95, eps=1e-8, wd=0.1):
+        check(lib().epp_stage_adamw_step(self.h, lr, b1, b2, eps, wd, step, stream_ptr()))
+
+    def loss(self, reset: bool = False):
+        out = (ctypes.c_double * 2)()
+        check(lib().epp_stage_loss(self.h, out, int(reset), stream_ptr()))
+        return out[0], out[1]
+
+    def memory(self):
+        live, peak = ctypes.c_int64(), ctypes.c_int64()
+        check(lib().epp_stage_memory(self.h, ctypes.byref(live), ctypes.byref(peak)))
+        return live.value, peak.value
+
+    # -- chunk ops -------------------------------------------------------------
+    def _desc(self, c) -> ChunkDesc:
+        slices = (ctypes.c_int64 * len(c.slices))(*c.slices)
+        self._keep[c.id] = slices
+        return ChunkDesc(c.id, c.seq, c.kind, int(c.tail), c.context, c.seq_len, len(c.slices),
+                         slices, c.ckpt_layers, c.loss_scale, _ptr(c.token_ids), _ptr(c.target_ids))
+
+    def forward(self, c, act_in: Optional[torch.Tensor]) -> Optional[torch.Tensor]:
+        T = sum(c.slices)
+        out = None
+        if not self.has_head:
+            out = torch.empty((T, self.model.hidden), dtype=self.tdtype, device=self.device)
+        d = self._desc(c)
+        check(lib().epp_stage_forward(self.h, ctypes.byref(d), _ptr(act_in), _ptr(out), stream_ptr()))
+        return out
+
+    def backward(self, c, grad_in: Optional[torch.Tensor]) -> Optional[torch.Tensor]:
+        T = sum(c.slices)
+        out = None
+        if not self.has_embed:
+            out = torch.empty((T, self.model.hidden), dtype=self.tdtype, device=self.device)
+        d = self._desc(c)
+        check(lib().epp_stage_backward(self.h, ctypes.byref(d), _ptr(grad_in), _ptr(out), stream_ptr()))
+        self._keep.pop(c.id, None)
+        return out
+
+
+def _wrap_ptr(ptr: int, numel: int, dtype: torch.dtype, device: torch.device) -> torch.Tensor:
+    """Zero-copy tensor over device memory owned by the library."""
+    class _Holder:
+        pass
+    h = _Holder()
+    h.__cuda_array_interface__ = {
+        "shape": (int(numel),),
+        "typestr": {torch.float32: "<f4", torch.bfloat16: "<V2"}[dtype],
+        "data": (int(ptr), False),
+        "version": 3,
+        "strides": None,
+    }
+    if dtype == torch.bfloat16:
+        raw = torch.as_tensor(_I16Holder(ptr, numel), device=device)
+        return raw.view(torch.bfloat16)
+    return torch.as_tensor(h, device=device)
+
+
+class _I16Holder:
+    def __init__(self, ptr, numel):
+        self.__cuda_array_interface__ = {"shape": (int(numel),), "typestr": "<i2",
+                                         "data": (int(ptr), False), "version": 3, "strides": None}

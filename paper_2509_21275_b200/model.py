@@ -1,0 +1,147 @@
+"""Model shapes of the BASELINE.json configs and the planner memory/cost
+model for them on B200.
+
+The planner only sees a model through SystemConfig (proj/include/epp/
+config.hpp:30-60): layers, hidden, bytes per token of activations and model
+state per stage.  `planner_config()` derives those numbers from what the CUDA
+stage executor (csrc/gpu/stage.cu) actually keeps resident, so the MILP's
+memory rows describe the real executor.
+"""
+from __future__ import annotations
+
+from dataclasses import asdict, dataclass
+from typing import Dict, Optional
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    name: str
+    arch: str            # "gpt" | "llama"
+    layers: int
+    hidden: int
+    heads: int
+    kv_heads: int
+    ffn: int
+    vocab: int
+    rope_theta: float = 10000.0
+    norm_eps: float = 1e-5
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden // self.heads
+
+    @property
+    def llama(self) -> bool:
+        return self.arch == "llama"
+
+    def params_per_layer(self) -> int:
+        D, hd = self.hidden, self.head_dim
+        qkv = (self.heads + 2 * self.kv_heads) * hd * D
+        wo = D * self.heads * hd
+        mlp = (3 if self.llama else 2) * D * self.ffn
+        norms = (2 if self.llama else 4) * D
+        return qkv + wo + mlp + norms
+
+    def num_params(self) -> int:
+        return self.layers * self.params_per_layer() + 2 * self.vocab * self.hidden + 2 * self.hidden
+
+    def linear_flops_per_token_layer(self) -> float:
+        """Forward matmul FLOPs per token per layer (2 x MACs)."""
+        D, hd = self.hidden, self.head_dim
+        qkv = 2 * D * (self.heads + 2 * self.kv_heads) * hd
+        wo = 2 * self.heads * hd * D
+        mlp = 2 * D * self.ffn * (3 if self.llama else 2)
+        return qkv + wo + mlp
+
+    def attn_flops_per_pair_layer(self) -> float:
+        """Forward FLOPs per (query, visible key) pair per layer: QK^T + PV."""
+        return 4.0 * self.heads * self.head_dim
+
+    def to_spec_dict(self) -> Dict:
+        d = asdict(self)
+        d.pop("name")
+        d["head_dim"] = self.head_dim
+        return d
+
+
+MODELS: Dict[str, ModelConfig] = {
+    # configs[0]: tiny GPT on the CPU reference (BASELINE.json)
+    "tiny": ModelConfig("tiny", "gpt", layers=4, hidden=256, heads=4, kv_heads=4, ffn=1024, vocab=4096),
+    # configs[1]: GPT-1.3B shape
+    "gpt-1.3b": ModelConfig("gpt-1.3b", "gpt", layers=24, hidden=2048, heads=16, kv_heads=16,
+                            ffn=8192, vocab=50304),
+    # configs[2]: GPT-7B shape
+    "gpt-7b": ModelConfig("gpt-7b", "gpt", layers=32, hidden=4096, heads=32, kv_heads=32,
+                          ffn=16384, vocab=50304),
+    # configs[3]: Llama-style 7B (GQA, RMSNorm, SwiGLU)
+    "llama-7b": ModelConfig("llama-7b", "llama", layers=32, hidden=4096, heads=32, kv_heads=8,
+                            ffn=11008, vocab=32000),
+    # small test shapes for the GPU parity suite
+    "tiny-llama": ModelConfig("tiny-llama", "llama", layers=4, hidden=256, heads=4, kv_heads=2,
+                              ffn=512, vocab=4096),
+    "small-gpt": ModelConfig("small-gpt", "gpt", layers=4, hidden=512, heads=4, kv_heads=4,
+                             ffn=2048, vocab=8192),
+}
+
+
+def activation_bytes_per_token(m: ModelConfig, elem_bytes: int = 2) -> float:
+    """Bytes the CUDA stage keeps per token per NON-checkpointed layer until
+    the chunk's backward (stage.cu LayerSaved + chunk-local K/V): layer output
+    x (D), q (H*hd), o (H*hd), x_mid (D), h (F or 2F), K and V (2*Hkv*hd),
+    plus fp32 norm stats and LSE."""
+    D, hd = m.hidden, m.head_dim
+    f1 = 2 * m.ffn if m.llama else m.ffn
+    elems = D + m.heads * hd + m.heads * hd + D + f1 + 2 * m.kv_heads * hd
+    return elems * elem_bytes + 4 * 4 + 4 * m.heads
+
+
+def state_bytes_per_param(dtype: str = "bf16") -> float:
+    """fp32 master + fp32 grad + fp32 Adam m, v (+ bf16 working copy)."""
+    return 16.0 + (2.0 if dtype == "bf16" else 0.0)
+
+
+def planner_config(m: ModelConfig, pp_degree: int, mem_capacity: float = 180e9,
+                   cost: Optional[Dict[str, float]] = None, reserve_bytes: float = 12e9,
+                   dtype: str = "bf16") -> Dict:
+    """SystemConfig document for the planner (proj/src/config.cpp:76-113).
+
+    token_act_bytes: whole-model, unsharded activation bytes per token;
+    stage_state_bytes: parameters/optimizer of each stage + a fixed reserve
+    for workspaces (GEMM/attention scratch, logits blocks, allocator slack).
+    """
+    L = m.layers
+    assert L % pp_degree == 0, "layers must divide by pp_degree"
+    per_layer = m.params_per_layer()
+    sbp = state_bytes_per_param(dtype)
+    states = []
+    for p in range(pp_degree):
+        n = per_layer * (L // pp_degree)
+        if p == 0:
+            n += m.vocab * m.hidden
+        if p == pp_degree - 1:
+            n += m.vocab * m.hidden + 2 * m.hidden
+        states.append(n * sbp + reserve_bytes)
+    cost = dict(cost or default_cost(m))
+    return {
+        "cluster": {"num_gpus": pp_degree, "pp_degree": pp_degree, "sp_degree": 1,
+                    "mem_capacity": float(mem_capacity),
+                    "all2all_bandwidth": {}, "all2all_latency": {}},
+        "model": {"layers": L, "hidden_dim": m.hidden, "elem_bytes": 2.0,
+                  "token_act_bytes": float(activation_bytes_per_token(m) * L),
+                  "stage_state_bytes": [float(x) for x in states]},
+        "cost": cost,
+    }
+
+
+def default_cost(m: ModelConfig, tflops: float = 700e12, attn_tflops: float = 450e12,
+                 fixed_per_layer: float = 60e-6) -> Dict[str, float]:
+    """Analytic Eq. 1 coefficients (whole model, per GPU count folded in by
+    the cost model) before closed-loop fitting: linear work at `tflops`,
+    attention pair work at `attn_tflops`, a fixed per-pass overhead."""
+    L = m.layers
+    a1 = m.linear_flops_per_token_layer() * L / tflops
+    # Eq. 1 charges (C+s)^2 - C^2 = 2Cs + s^2 ~ 2 x causal pairs
+    a2 = 0.5 * m.attn_flops_per_pair_layer() * L / attn_tflops
+    return {"fwd_sec_per_token2": a2, "fwd_sec_per_token": a1, "fwd_sec_fixed": fixed_per_layer * L,
+            "bwd_sec_per_token2": 2.5 * a2, "bwd_sec_per_token": 2.0 * a1,
+            "bwd_sec_fixed": 2.0 * fixed_per_layer * L, "layer_fwd_seconds": 0.0}

@@ -1,0 +1,154 @@
+"""Kernel-level numerics on the GPU, through the C ABI (libepp_gpu.so):
+tcgen05 GEMMs in every operand layout / epilogue vs a fp32 torch reference,
+slice-causal attention fwd/bwd vs the fp32 oracle math."""
+import ctypes
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def G():
+    from paper_2509_21275_b200 import gpu
+    return gpu
+
+
+def ref_gemm(A, B, a_k, b_k, M, N, K):
+    Am = A.float() if a_k else A.float().T
+    Bm = B.float() if b_k else B.float().T
+    return Am[:M, :K] @ Bm[:N, :K].T
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("a_k,b_k", [(True, True), (True, False), (False, True), (False, False)])
+@pytest.mark.parametrize("M,N,K", [(256, 512, 256), (300, 384, 320), (1000, 256, 192), (4096, 1024, 1024)])
+def test_gemm_layouts(dtype, a_k, b_k, M, N, K):
+    g = G()
+    td = torch.bfloat16 if dtype == "bf16" else torch.float32
+    torch.manual_seed(0)
+    A = (torch.randn((M, K) if a_k else (K, M), device="cuda") * 0.5).to(td)
+    B = (torch.randn((N, K) if b_k else (K, N), device="cuda") * 0.5).to(td)
+    C = torch.empty((M, N), device="cuda", dtype=td)
+    lda = A.shape[1]
+    ldb = B.shape[1]
+    g.check(g.lib().epp_kernel_gemm(M, N, K, A.data_ptr(), lda, int(a_k), B.data_ptr(), ldb, int(b_k),
+                                    C.data_ptr(), N, None, 0, 0, g.DTYPES[dtype], g.stream_ptr()))
+    torch.cuda.synchronize()
+    ref = ref_gemm(A, B, a_k, b_k, M, N, K)
+    err = (C.float() - ref).norm() / ref.norm()
+    assert err < (8e-3 if dtype == "bf16" else 1e-5), float(err)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_gemm_epilogues(dtype):
+    g = G()
+    td = torch.bfloat16 if dtype == "bf16" else torch.float32
+    M, N, K = 384, 768, 512
+    A = torch.randn((K, M), device="cuda").to(td)      # MN-major (wgrad shape)
+    B = torch.randn((K, N), device="cuda").to(td)
+    C = torch.randn((M, N), device="cuda", dtype=torch.float32)
+    C0 = C.clone()
+    g.check(g.lib().epp_kernel_gemm(M, N, K, A.data_ptr(), M, 0, B.data_ptr(), N, 0, C.data_ptr(), N,
+                                    None, 0, 1, g.DTYPES[dtype], g.stream_ptr()))
+    torch.cuda.synchronize()
+    ref = C0 + A.float().T @ B.float()
+    assert ((C - ref).norm() / ref.norm()) < (5e-3 if dtype == "bf16" else 1e-5)
+    # residual add
+    A2 = torch.randn((M, K), device="cuda").to(td)
+    B2 = torch.randn((N, K), device="cuda").to(td)
+    R = torch.randn((M, N), device="cuda").to(td)
+    C2 = torch.empty((M, N), device="cuda", dtype=td)
+    g.check(g.lib().epp_kernel_gemm(M, N, K, A2.data_ptr(), K, 1, B2.data_ptr(), K, 1, C2.data_ptr(), N,
+                                    R.data_ptr(), N, 2, g.DTYPES[dtype], g.stream_ptr()))
+    torch.cuda.synchronize()
+    ref2 = A2.float() @ B2.float().T + R.float()
+    assert ((C2.float() - ref2).norm() / ref2.norm()) < (8e-3 if dtype == "bf16" else 1e-5)
+
+
+def attn_reference(q, ks, vs, segs, scale):
+    """fp32 reference: q [T,H,hd]; ks/vs per segment [S_i, Hkv, hd]."""
+    T, H, hd = q.shape
+    out = torch.zeros(T, H, hd, device=q.device)
+    lse = torch.zeros(H, T, device=q.device)
+    for (qs, ql, ctx), k, v in zip(segs, ks, vs):
+        g = H // k.shape[1]
+        kk = k.float().repeat_interleave(g, 1)
+        vv = v.float().repeat_interleave(g, 1)
+        s = torch.einsum("thd,shd->hts", q[qs:qs + ql].float(), kk) * scale
+        qpos = torch.arange(ctx, ctx + ql, device=q.device)
+        mask = torch.arange(kk.shape[0], device=q.device)[None, :] > qpos[:, None]
+        s = s.masked_fill(mask[None], float("-inf"))
+        lse[:, qs:qs + ql] = torch.logsumexp(s, -1) / math.log(2)
+        out[qs:qs + ql] = torch.einsum("hts,shd->thd", torch.softmax(s, -1), vv)
+    return out, lse
+
+
+def run_attention(dtype, hd, H, Hkv, segs, seed=0):
+    g = G()
+    td = torch.bfloat16 if dtype == "bf16" else torch.float32
+    torch.manual_seed(seed)
+    T = sum(ql for (_, ql, _) in segs)
+    q = torch.randn(T, H, hd, device="cuda").to(td)
+    ks = [torch.randn(ctx + ql, Hkv, hd, device="cuda").to(td) for (_, ql, ctx) in segs]
+    vs = [torch.randn(ctx + ql, Hkv, hd, device="cuda").to(td) for (_, ql, ctx) in segs]
+    o = torch.empty(T, H, hd, device="cuda", dtype=td)
+    lse = torch.empty(H, T, device="cuda")
+    n = len(segs)
+    I32 = ctypes.c_int32 * n
+    VP = ctypes.c_void_p * n
+    qs_, ql_, cx_ = I32(*[s[0] for s in segs]), I32(*[s[1] for s in segs]), I32(*[s[2] for s in segs])
+    kp, vp = VP(*[k.data_ptr() for k in ks]), VP(*[v.data_ptr() for v in vs])
+    scale = 1.0 / math.sqrt(hd)
+    g.check(g.lib().epp_kernel_attention_fwd(T, H, Hkv, hd, scale, n, qs_, ql_, cx_, kp, vp, q.data_ptr(),
+                                             o.data_ptr(), lse.data_ptr(), g.DTYPES[dtype], g.stream_ptr()))
+    # backward
+    do = torch.randn(T, H, hd, device="cuda").to(td)
+    dks = [torch.zeros(k.shape, device="cuda") for k in ks]
+    dvs = [torch.zeros(v.shape, device="cuda") for v in vs]
+    dq = torch.empty(T, H, hd, device="cuda")
+    FP = ctypes.c_void_p * n
+    g.check(g.lib().epp_kernel_attention_bwd(T, H, Hkv, hd, scale, n, qs_, ql_, cx_, kp, vp,
+                                             FP(*[d.data_ptr() for d in dks]),
+                                             FP(*[d.data_ptr() for d in dvs]), q.data_ptr(), o.data_ptr(),
+                                             lse.data_ptr(), do.data_ptr(), dq.data_ptr(),
+                                             g.DTYPES[dtype], g.stream_ptr()))
+    torch.cuda.synchronize()
+    # reference with autograd
+    qr = q.float().requires_grad_()
+    kr = [k.float().requires_grad_() for k in ks]
+    vr = [v.float().requires_grad_() for v in vs]
+    ref_o, ref_lse = attn_reference(qr, kr, vr, segs, scale)
+    ref_o.backward(do.float())
+    return (o, lse, dq, dks, dvs), (ref_o.detach(), ref_lse.detach(), qr.grad, [k.grad for k in kr],
+                                   [v.grad for v in vr])
+
+
+def rel(a, b):
+    return float((a.float() - b.float()).norm() / (b.float().norm() + 1e-30))
+
+
+SEGS = {
+    "packed": [(0, 100, 0), (100, 37, 0), (137, 200, 0), (337, 1, 0)],
+    "slice_ctx": [(0, 150, 333)],
+    "hybrid": [(0, 90, 1000), (90, 64, 0), (154, 17, 0)],
+    "long": [(0, 1024, 2048)],
+}
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("hd,H,Hkv", [(64, 4, 4), (128, 4, 2), (128, 8, 8)])
+@pytest.mark.parametrize("case", list(SEGS))
+def test_attention(dtype, hd, H, Hkv, case):
+    got, ref = run_attention(dtype, hd, H, Hkv, SEGS[case])
+    tol = 2e-2 if dtype == "bf16" else 1e-4
+    o, lse, dq, dks, dvs = got
+    ro, rlse, rdq, rdks, rdvs = ref
+    assert rel(o, ro) < tol, ("o", rel(o, ro))
+    assert (lse - rlse).abs().max() < (2e-2 if dtype == "bf16" else 1e-4)
+    assert rel(dq, rdq) < 2 * tol, ("dq", rel(dq, rdq))
+    for a, b in zip(dks, rdks):
+        assert rel(a, b) < 2 * tol, ("dk", rel(a, b))
+    for a, b in zip(dvs, rdvs):
+        assert rel(a, b) < 2 * tol, ("dv", rel(a, b))
