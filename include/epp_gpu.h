@@ -140,6 +140,13 @@ int epp_kernel_attention_bwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, floa
                              const float* lse, const void* dout, float* dq, int32_t dtype,
                              void* stream);
 
+/* Opt-in per-launch timing (CUDA events on the launching stream) of kernel
+ * classes 0 = GEMM, 1 = attention forward, 2 = attention backward.
+ * profile_read synchronises on the recorded events and returns total device
+ * milliseconds, algorithmic FLOPs and launch count; reset drops the records. */
+int epp_gpu_profile(int32_t enable);
+int epp_gpu_profile_read(int32_t cls, double* ms, double* flops, int64_t* launches, int32_t reset);
+
 const char* epp_gpu_last_error(void);
 /* Kernel launches issued by this library in this process (for bench claims). */
 int64_t epp_gpu_kernel_launches(void);

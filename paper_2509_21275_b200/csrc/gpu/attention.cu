@@ -22,6 +22,7 @@
 // F32 kernels (parity mode): warp-per-row SIMT versions of the same math.
 #include "common.cuh"
 #include "kernels.h"
+#include "profile.h"
 
 namespace eppk {
 
@@ -748,6 +749,7 @@ void launch_bf16_bwd(const AttnArgs& a, cudaStream_t s) {
 void attn_fwd(const AttnArgs& a, cudaStream_t s) {
     EPP_REQUIRE(a.H % a.Hkv == 0, "attn: H must be a multiple of Hkv");
     if (a.nqwork == 0) return;
+    ProfScope prof(kProfAttnFwd, 4.0 * a.H * a.hd * a.pairs, s);
     if (a.dtype == DType::F32) {
         EPP_REQUIRE(a.hd <= 128, "attn(f32): head_dim <= 128");
         attn_fwd_f32<<<dim3(a.nqwork, a.H), 128, 0, s>>>(a);
@@ -761,6 +763,8 @@ void attn_fwd(const AttnArgs& a, cudaStream_t s) {
 
 void attn_bwd(const AttnArgs& a, cudaStream_t s) {
     EPP_REQUIRE(a.H % a.Hkv == 0, "attn: H must be a multiple of Hkv");
+    // algorithmic backward = 2x forward (dQ, dK, dV, dP matmuls)
+    ProfScope prof(kProfAttnBwd, 8.0 * a.H * a.hd * a.pairs, s);
     if (a.T > 0) {
         const long long warps = static_cast<long long>(a.T) * a.H;
         const int blocks = static_cast<int>((warps * 32 + 255) / 256);

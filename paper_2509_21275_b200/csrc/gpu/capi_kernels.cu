@@ -8,23 +8,23 @@
 #include "kernels.h"
 
 namespace eppk {
+std::string& gpu_error_slot();
 namespace {
-thread_local std::string g_kerr;
 
 template <typename F>
 int kguard(F&& f) {
-    g_kerr.clear();
+    gpu_error_slot().clear();
     try {
         f();
         return EPP_GPU_OK;
     } catch (const CudaError& e) {
-        g_kerr = e.what();
+        gpu_error_slot() = e.what();
         return EPP_GPU_ECUDA;
     } catch (const std::invalid_argument& e) {
-        g_kerr = e.what();
+        gpu_error_slot() = e.what();
         return EPP_GPU_EARG;
     } catch (const std::exception& e) {
-        g_kerr = e.what();
+        gpu_error_slot() = e.what();
         return EPP_GPU_EOTHER;
     }
 }
@@ -108,6 +108,8 @@ int epp_kernel_attention_fwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, floa
         a.T = T; a.H = H; a.Hkv = Hkv; a.hd = hd; a.layer = 0; a.scale = scale;
         a.dtype = static_cast<eppk::DType>(dtype);
         a.q = q; a.o = o; a.lse = lse;
+        for (int i = 0; i < nseg; ++i)
+            a.pairs += static_cast<double>(q_len[i]) * kv_ctx[i] + 0.5 * static_cast<double>(q_len[i]) * (q_len[i] + 1);
         eppk::attn_fwd(a, s);
     });
 }
@@ -133,6 +135,8 @@ int epp_kernel_attention_bwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, floa
         a.dtype = static_cast<eppk::DType>(dtype);
         a.q = q; a.o = const_cast<void*>(o); a.lse = const_cast<float*>(lse);
         a.dout = dout; a.delta = delta; a.dq = dq;
+        for (int i = 0; i < nseg; ++i)
+            a.pairs += static_cast<double>(q_len[i]) * kv_ctx[i] + 0.5 * static_cast<double>(q_len[i]) * (q_len[i] + 1);
         eppk::attn_bwd(a, s);
         EPP_CUDA(cudaFreeAsync(delta, s));
     });

@@ -74,6 +74,7 @@ struct AttnArgs {
     int H = 0, Hkv = 0, hd = 0;
     int layer = 0;
     float scale = 0.f;
+    double pairs = 0;     // visible (query, key) pairs, for FLOP accounting
     DType dtype = DType::BF16;
     // forward
     const void* q = nullptr;   // [T, H, hd]

@@ -1,0 +1,19 @@
+// epp-b200: launch-scoped profiling of kernel classes (see profile.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace eppk {
+enum ProfClass { kProfGemm = 0, kProfAttnFwd = 1, kProfAttnBwd = 2 };
+bool profiling();
+// Records an event pair around the launches issued during its lifetime.
+class ProfScope {
+public:
+    ProfScope(int cls, double flops, cudaStream_t s);
+    ~ProfScope();
+private:
+    int cls_;
+    double flops_;
+    cudaStream_t s_;
+    cudaEvent_t a_ = nullptr, b_ = nullptr;
+};
+}  // namespace eppk

@@ -33,9 +33,12 @@ long long& launch_counter() {
     return n;
 }
 
-namespace {
+std::string& gpu_error_slot() {
+    thread_local std::string err;
+    return err;
+}
 
-thread_local std::string g_err;
+namespace {
 
 // ----------------------------------------------------------- allocation ----
 struct Pool {
@@ -155,6 +158,7 @@ struct ChunkState {
     Buf kv_local;                  // [K|V][layer][T][Hkv*hd] rows of packed segments
     Buf dkv_local;                 // fp32 [dK|dV][T][Hkv*hd], one layer, re-zeroed per layer
     int nqwork = 0, nkwork = 0;
+    double pairs = 0;
     Buf x_in;                      // stage input (copy of act_in or embedding)
     std::vector<LayerSaved> layers;
     Buf meanf, rstdf, dxf;         // last stage: final-norm stats + d(final norm out)
@@ -470,6 +474,10 @@ private:
             for (int b = 0; b * kAttnBlock < sg.q_len; ++b) qw.push_back({i, b});
             for (int b = 0; b * kAttnBlock < sg.kv_ctx + sg.q_len; ++b) kw.push_back({i, b});
         }
+        cs.pairs = 0;
+        for (const AttnSeg& sg : cs.segs)
+            cs.pairs += static_cast<double>(sg.q_len) * sg.kv_ctx +
+                        0.5 * static_cast<double>(sg.q_len) * (sg.q_len + 1);
         cs.nqwork = static_cast<int>(qw.size());
         cs.nkwork = static_cast<int>(kw.size());
         cs.tok_seg = upload(tseg.data(), tseg.size() * sizeof(int), s);
@@ -528,6 +536,7 @@ private:
         a.layer = j;
         a.scale = 1.f / std::sqrt(static_cast<float>(hd_));
         a.dtype = dt_;
+        a.pairs = cs.pairs;
         return a;
     }
 
@@ -724,18 +733,18 @@ namespace {
 
 template <typename F>
 int guard(F&& f) {
-    eppk::g_err.clear();
+    eppk::gpu_error_slot().clear();
     try {
         f();
         return EPP_GPU_OK;
     } catch (const eppk::CudaError& e) {
-        eppk::g_err = e.what();
+        eppk::gpu_error_slot() = e.what();
         return EPP_GPU_ECUDA;
     } catch (const std::invalid_argument& e) {
-        eppk::g_err = e.what();
+        eppk::gpu_error_slot() = e.what();
         return EPP_GPU_EARG;
     } catch (const std::exception& e) {
-        eppk::g_err = e.what();
+        eppk::gpu_error_slot() = e.what();
         return EPP_GPU_EOTHER;
     }
 }
@@ -830,7 +839,7 @@ int epp_stage_memory(epp_stage* st, int64_t* live_bytes, int64_t* peak_bytes) {
     });
 }
 
-const char* epp_gpu_last_error(void) { return eppk::g_err.c_str(); }
+const char* epp_gpu_last_error(void) { return eppk::gpu_error_slot().c_str(); }
 
 int64_t epp_gpu_kernel_launches(void) { return eppk::launch_counter(); }
 

@@ -90,11 +90,14 @@ class LocalPipeline:
         self.stages = list(stages)
         self.device = device
 
-    def run_step(self, plan: Plan, tokens: Sequence[np.ndarray]) -> dict:
+    def run_step(self, plan: Plan, tokens: Sequence[np.ndarray], staged: Optional[_ChunkTokens] = None) -> dict:
+        """One global batch.  `staged`: token tensors already on the device
+        (the device-resident benchmark mode); otherwise they are copied from
+        pinned host memory here."""
         dp = len(self.stages)
         if dp != plan.pp_degree:
             raise ValueError(f"plan is for {plan.pp_degree} stages, executor has {dp}")
-        toks = _ChunkTokens(plan, tokens, self.device, True, True)
+        toks = staged or _ChunkTokens(plan, tokens, self.device, True, True)
         for unit in plan.units:
             self._run_unit(plan, unit, toks)
         return {"h2d_bytes": toks.h2d_bytes}
@@ -151,11 +154,11 @@ class DistributedPipeline:
             self.bwd_groups.append(dist.new_group([p, p + 1]))
         self.p2p_bytes = 0
 
-    def run_step(self, plan: Plan, tokens: Sequence[np.ndarray]) -> dict:
+    def run_step(self, plan: Plan, tokens: Sequence[np.ndarray], staged: Optional[_ChunkTokens] = None) -> dict:
         p, dp = self.rank, self.world
         if dp != plan.pp_degree:
             raise ValueError(f"plan is for {plan.pp_degree} stages, world size is {dp}")
-        toks = _ChunkTokens(plan, tokens, self.device, need_ids=(p == 0), need_targets=(p == dp - 1))
+        toks = staged or _ChunkTokens(plan, tokens, self.device, need_ids=(p == 0), need_targets=(p == dp - 1))
         pending = []
         for unit in plan.units:
             n = len(unit.chunks)

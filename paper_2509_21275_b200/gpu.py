@@ -70,6 +70,9 @@ def lib():
             "epp_stage_zero_grads": [vp, vp],
             "epp_stage_adamw_step": [vp, f32, f32, f32, f32, f32, i32, vp],
             "epp_stage_memory": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)],
+            "epp_gpu_profile": [i32],
+            "epp_gpu_profile_read": [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                     ctypes.POINTER(i64), i32],
             "epp_kernel_gemm": [i32, i32, i32, vp, i64, i32, vp, i64, i32, vp, i64, vp, i64, i32, i32, vp],
             "epp_kernel_attention_fwd": [i32, i32, i32, i32, f32, i32, ctypes.POINTER(i32),
                                          ctypes.POINTER(i32), ctypes.POINTER(i32),

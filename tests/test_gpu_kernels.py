@@ -21,6 +21,14 @@ def ref_gemm(A, B, a_k, b_k, M, N, K):
     return Am[:M, :K] @ Bm[:N, :K].T
 
 
+def test_gemm_rejects_unaligned_pitch():
+    g = G()
+    A = torch.zeros((64, 300), device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(g.EppGpuError, match="multiples of 8"):
+        g.check(g.lib().epp_kernel_gemm(300, 64, 64, A.data_ptr(), 300, 0, A.data_ptr(), 300, 1,
+                                        A.data_ptr(), 64, None, 0, 0, 1, g.stream_ptr()))
+
+
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("a_k,b_k", [(True, True), (True, False), (False, True), (False, False)])
 @pytest.mark.parametrize("M,N,K", [(256, 512, 256), (300, 384, 320), (1000, 256, 192), (4096, 1024, 1024)])
@@ -28,8 +36,9 @@ def test_gemm_layouts(dtype, a_k, b_k, M, N, K):
     g = G()
     td = torch.bfloat16 if dtype == "bf16" else torch.float32
     torch.manual_seed(0)
-    A = (torch.randn((M, K) if a_k else (K, M), device="cuda") * 0.5).to(td)
-    B = (torch.randn((N, K) if b_k else (K, N), device="cuda") * 0.5).to(td)
+    pad = lambda n: (n + 7) // 8 * 8   # TMA row pitch: 16-byte multiple
+    A = (torch.randn((M, pad(K)) if a_k else (K, pad(M)), device="cuda") * 0.5).to(td)
+    B = (torch.randn((N, pad(K)) if b_k else (K, pad(N)), device="cuda") * 0.5).to(td)
     C = torch.empty((M, N), device="cuda", dtype=td)
     lda = A.shape[1]
     ldb = B.shape[1]
@@ -148,7 +157,7 @@ def test_attention(dtype, hd, H, Hkv, case):
     assert rel(o, ro) < tol, ("o", rel(o, ro))
     assert (lse - rlse).abs().max() < (2e-2 if dtype == "bf16" else 1e-4)
     assert rel(dq, rdq) < 2 * tol, ("dq", rel(dq, rdq))
-    for a, b in zip(dks, rdks):
-        assert rel(a, b) < 2 * tol, ("dk", rel(a, b))
-    for a, b in zip(dvs, rdvs):
-        assert rel(a, b) < 2 * tol, ("dv", rel(a, b))
+    # a 1-token segment has exactly-zero dK: measure over all segments
+    cat = lambda xs: torch.cat([x.reshape(-1) for x in xs])
+    assert rel(cat(dks), cat(rdks)) < 2 * tol, ("dk", rel(cat(dks), cat(rdks)))
+    assert rel(cat(dvs), cat(rdvs)) < 2 * tol, ("dv", rel(cat(dvs), cat(rdvs)))

@@ -30,11 +30,19 @@ def cfg_model(arch, hd=64):
 
 def make_plan(planner, m, lengths, dp, slices, tight=False):
     cfg = M.planner_config(m, dp, mem_capacity=1e12, reserve_bytes=0)
-    if tight:
-        act = cfg["model"]["token_act_bytes"]
-        cfg["cluster"]["mem_capacity"] = max(cfg["model"]["stage_state_bytes"]) + act * 350 / dp
-    doc = planner.make_plan_document(cfg, lengths, slices, "main", 1)
-    return S.parse_plan(doc, lengths)
+    if not tight:
+        return S.parse_plan(planner.make_plan_document(cfg, lengths, slices, "main", 1), lengths)
+    # squeeze stage memory until the checkpoint ladder has to kick in
+    act = cfg["model"]["token_act_bytes"]
+    for tokens_fit in (3000, 2000, 1500, 1200, 1000, 800, 600, 500, 400):
+        cfg["cluster"]["mem_capacity"] = max(cfg["model"]["stage_state_bytes"]) + act * tokens_fit / dp
+        try:
+            plan = S.parse_plan(planner.make_plan_document(cfg, lengths, slices, "main", 1), lengths)
+        except planner.InfeasibleError:
+            break
+        if any(any(v for row in u.ckpt for v in row) for u in plan.units):
+            return plan
+    raise AssertionError("no memory budget activates the ladder")
 
 
 def run_gpu(m, params, plan, tokens, dtype):
@@ -50,7 +58,7 @@ def run_gpu(m, params, plan, tokens, dtype):
     torch.cuda.synchronize()
     grads = {}
     for st in stages:
-        grads.update({k: v.cpu() for k, v in st.grads().items()})
+        grads.update({k: v.cpu().view(params[k].shape) for k, v in st.grads().items()})
     loss_sum, cnt = stages[-1].loss()
     for st in stages:
         live, _ = st.memory()
