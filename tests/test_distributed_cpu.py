@@ -1,0 +1,84 @@
+"""World-size-2 gloo run of the one-stage-per-rank executor
+(DistributedPipeline) on CPU, with the oracle's TorchStage standing in for
+the CUDA stage: gradients equal the single-process LocalPipeline's."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from oracle import numerics as O
+from paper_2509_21275_b200 import model as M
+from paper_2509_21275_b200 import schedule as S
+from paper_2509_21275_b200.executor import DistributedPipeline, LocalPipeline, stage_layers
+
+MODEL = M.ModelConfig("t", "gpt", layers=4, hidden=64, heads=4, kv_heads=4, ffn=128, vocab=256)
+LENGTHS = [300, 37, 21, 90, 5, 64, 180]
+
+
+def spec():
+    m = MODEL
+    return O.ModelSpec(m.arch, m.layers, m.hidden, m.heads, m.kv_heads, m.head_dim, m.ffn, m.vocab)
+
+
+def plan_doc(world):
+    from paper_2509_21275_b200 import planner
+    cfg = M.planner_config(MODEL, world, mem_capacity=1e12, reserve_bytes=0)
+    return planner.make_plan_document(cfg, LENGTHS, 3, "main", 1)
+
+
+def worker(rank, world, port, doc, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
+    plan = S.parse_plan(doc, LENGTHS)
+    params = O.init_params(spec(), seed=3)
+    first, num = stage_layers(MODEL.layers, world, rank)
+    st = O.TorchStage(spec(), params, first, num, rank == 0, rank == world - 1)
+    drv = DistributedPipeline(st, rank, world, torch.device("cpu"), MODEL.hidden, torch.float32)
+    drv.run_step(plan, S.synthetic_tokens(LENGTHS, MODEL.vocab, seed=11))
+    q.put((rank, {k: v.clone() for k, v in st.grads().items()}, st.loss_sum, drv.p2p_bytes))
+    torch.distributed.barrier()
+    torch.distributed.destroy_process_group()
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_pipeline_matches_local(world):
+    doc = plan_doc(world)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, world, port, doc, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    dist_grads = {}
+    loss = None
+    for rank, g, ls, nbytes in results:
+        dist_grads.update(g)
+        if rank == world - 1:
+            loss = ls
+        if 0 < rank < world - 1:
+            assert nbytes > 0
+    plan = S.parse_plan(doc, LENGTHS)
+    params = O.init_params(spec(), seed=3)
+    stages = [O.TorchStage(spec(), params, *stage_layers(MODEL.layers, world, p), p == 0, p == world - 1)
+              for p in range(world)]
+    LocalPipeline(stages, torch.device("cpu")).run_step(plan, S.synthetic_tokens(LENGTHS, MODEL.vocab, seed=11))
+    local = {}
+    for st in stages:
+        local.update(st.grads())
+    assert abs(loss - stages[-1].loss_sum) < 1e-4
+    for k, v in local.items():
+        assert torch.allclose(dist_grads[k], v, rtol=1e-5, atol=1e-8), k
