@@ -20,6 +20,9 @@
 // The dK/dV accumulators of a split sequence persist across its chunks:
 // later slices' backwards (which run first) add into earlier slices' keys.
 // F32 kernels (parity mode): warp-per-row SIMT versions of the same math.
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "profile.h"
@@ -746,9 +749,26 @@ void launch_bf16_bwd(const AttnArgs& a, cudaStream_t s) {
 
 }  // namespace
 
+// 1 = tcgen05 kernels (default), 0 = FA2-style mma.sync kernels.  Initial
+// value from EPP_ATTN_IMPL ("fa2" selects the legacy path); switchable at
+// run time through epp_gpu_set_attention_impl for A/B tests.
+int& attention_impl() {
+    static int impl = [] {
+        const char* e = getenv("EPP_ATTN_IMPL");
+        return (e && std::string(e) == "fa2") ? 0 : 1;
+    }();
+    return impl;
+}
+
+bool use_tc_attention() { return attention_impl() == 1; }
+
 void attn_fwd(const AttnArgs& a, cudaStream_t s) {
     EPP_REQUIRE(a.H % a.Hkv == 0, "attn: H must be a multiple of Hkv");
     if (a.nqwork == 0) return;
+    if (use_tc_attention() && attn_fwd_tc_supported(a)) {
+        attn_fwd_tc(a, s);
+        return;
+    }
     ProfScope prof(kProfAttnFwd, 4.0 * a.H * a.hd * a.pairs, s);
     if (a.dtype == DType::F32) {
         EPP_REQUIRE(a.hd <= 128, "attn(f32): head_dim <= 128");
@@ -777,6 +797,10 @@ void attn_bwd(const AttnArgs& a, cudaStream_t s) {
                                                            static_cast<const bf16*>(a.o),
                                                            a.delta, a.T, a.H, a.hd);
         EPP_CHECK_LAUNCH();
+    }
+    if (use_tc_attention() && attn_bwd_tc_supported(a)) {
+        attn_bwd_tc_main(a, s);
+        return;
     }
     if (a.dtype == DType::F32) {
         if (a.nqwork > 0) {

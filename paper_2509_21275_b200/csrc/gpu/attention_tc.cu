@@ -1,0 +1,774 @@
+// epp-b200: slice-causal flash attention on tcgen05 (sm_100a).
+//
+// Same segment semantics as attention.cu (query rows of a segment sit at key
+// positions [C, C+len) of the segment's K/V rows; key j visible iff j <= pos),
+// with both matmuls on the 5th-gen tensor cores:
+//   S  = Q K^T   tcgen05.mma M=128 N=128 K=hd  -> TMEM (two S buffers)
+//   O += P V     tcgen05.mma M=128 N=hd  K=128 -> TMEM (O accumulator)
+// One CTA = one 128-row query block of one head.  Warp roles:
+//   warps 0-3  softmax: thread t owns query row t (TMEM lane t): reads S,
+//              online max with lazy O rescaling (only when the running max
+//              grows by > 8 in log2 units), writes P (bf16) to shared memory
+//              in the UMMA 128-byte-swizzled K-major layout, final O / l.
+//   warp  4    TMEM allocation + MMA issue (one lane): S(j+1) is issued
+//              before PV(j) so the tensor core works while softmax(j) runs.
+//   warps 5-7  cp.async loaders of the Q tile and a 2-stage K/V ring
+//              (zero-filled past the segment end), published to the async
+//              proxy with fence.proxy.async before the mbarrier arrive.
+#include "common.cuh"
+#include "kernels.h"
+#include "profile.h"
+#include "tc.cuh"
+
+namespace eppk {
+
+namespace {
+
+constexpr int TQ = 128;            // query rows per CTA (= TMEM lanes)
+constexpr int TK = 128;            // keys per tile
+constexpr int kThreadsTc = 256;
+constexpr int kLoadThreads = 96;   // warps 5..7
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescaleSlack = 8.f;   // log2 units: p <= 2^8 before a rescale
+
+// [128 rows x HD] bf16 tile = HD/64 column blocks of [128 rows x 128 B],
+// 16-byte chunks XOR-swizzled by (row & 7): the UMMA SWIZZLE_128B layout.
+__device__ __forceinline__ uint32_t tile_off(int row, int chunk) {
+    return static_cast<uint32_t>((chunk >> 3) * 16384 + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
+}
+
+template <int HD>
+struct FwdSmem {
+    static constexpr int kTile = TQ * HD * 2;
+    static constexpr int kQ = 0;
+    static constexpr int kK = kQ + kTile;           // 2 stages
+    static constexpr int kV = kK + 2 * kTile;       // 2 stages
+    static constexpr int kP = kV + 2 * kTile;       // 128 x 128 bf16
+    static constexpr int kBar = kP + TQ * TK * 2;
+    static constexpr int kBytes = kBar + 16 * 8 + 16;
+    static constexpr int kAlloc = kBytes + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
+    using L = FwdSmem<HD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
+    uint64_t* q_full = bar + 0;
+    uint64_t* kv_full = bar + 1;     // [2]
+    uint64_t* kv_empty = bar + 3;    // [2]
+    uint64_t* s_full = bar + 5;      // [2]
+    uint64_t* p_full = bar + 7;
+    uint64_t* o_done = bar + 8;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+
+    const AttnWork w = a.qwork128[blockIdx.x];
+    const AttnSeg sg = a.segs[w.seg];
+    const int h = blockIdx.y;
+    const int kvh = h / (a.H / a.Hkv);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q0 = w.block * TQ;
+    const int rows = min(TQ, sg.q_len - q0);
+    const int kv_end = sg.kv_ctx + q0 + rows;
+    const int nkb = (kv_end + TK - 1) / TK;
+
+    if (threadIdx.x == 0) {
+        tc::mbar_init(q_full, kLoadThreads);
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&kv_full[s], kLoadThreads);
+            tc::mbar_init(&kv_empty[s], 1);
+            tc::mbar_init(&s_full[s], 1);
+        }
+        tc::mbar_init(p_full, TQ);
+        tc::mbar_init(o_done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 4) tc::tmem_alloc(tmem_slot, 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+    constexpr uint32_t kColS = 0, kColO = 256;
+
+    if (warp >= 5) {
+        // ---------------------------------------------------------- loaders
+        const int lt = threadIdx.x - 160;
+        constexpr int kChunks = HD / 8;
+        const long long qstride = static_cast<long long>(a.H) * HD;
+        const bf16* qbase = static_cast<const bf16*>(a.q) +
+                            (static_cast<long long>(sg.q_start + q0) * a.H + h) * HD;
+        for (int i = lt; i < TQ * kChunks; i += kLoadThreads) {
+            const int r = i / kChunks, c = i % kChunks;
+            const bool ok = r < rows;
+            tc::cp_async16_zfill(smem + L::kQ + tile_off(r, c), ok ? qbase + r * qstride + c * 8 : qbase, ok);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        tc::fence_proxy_async();
+        tc::mbar_arrive(q_full);
+        const long long kvs = static_cast<long long>(a.Hkv) * HD;
+        const bf16* kb = static_cast<const bf16*>(sg.k) + a.layer * sg.kv_layer_stride + kvh * HD;
+        const bf16* vb = static_cast<const bf16*>(sg.v) + a.layer * sg.kv_layer_stride + kvh * HD;
+        for (int j = 0; j < nkb; ++j) {
+            const int s = j & 1;
+            tc::mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+            const int key0 = j * TK;
+            uint8_t* sk = smem + L::kK + s * L::kTile;
+            uint8_t* sv = smem + L::kV + s * L::kTile;
+            for (int i = lt; i < TK * kChunks; i += kLoadThreads) {
+                const int r = i / kChunks, c = i % kChunks;
+                const bool ok = key0 + r < kv_end;
+                const long long off = static_cast<long long>(key0 + r) * kvs + c * 8;
+                tc::cp_async16_zfill(sk + tile_off(r, c), ok ? kb + off : kb, ok);
+                tc::cp_async16_zfill(sv + tile_off(r, c), ok ? vb + off : vb, ok);
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            tc::fence_proxy_async();
+            tc::mbar_arrive(&kv_full[s]);
+        }
+    } else if (warp == 4) {
+        // ------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idS = tc::instr_desc_mn(TQ, TK, false, false);
+            constexpr uint32_t idO = tc::instr_desc_mn(TQ, HD, false, true);
+            const uint32_t sQ = tc::smem_u32(smem + L::kQ);
+            const uint32_t sP = tc::smem_u32(smem + L::kP);
+            auto issue_s = [&](int j) {
+                const int s = j & 1;
+                tc::mbar_wait(&kv_full[s], (j >> 1) & 1);
+                tc::fence_after();
+                const uint32_t sK = tc::smem_u32(smem + L::kK + s * L::kTile);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc::mma_bf16(tmem + kColS + s * TK, tc::smem_desc(sQ + off, 16, 1024),
+                                 tc::smem_desc(sK + off, 16, 1024), idS, kk != 0);
+                }
+                tc::commit(&s_full[s]);
+            };
+            tc::mbar_wait(q_full, 0);
+            tc::fence_after();
+            issue_s(0);
+            for (int j = 0; j < nkb; ++j) {
+                if (j + 1 < nkb) issue_s(j + 1);
+                tc::mbar_wait(p_full, j & 1);
+                tc::fence_after();
+                const int s = j & 1;
+                const uint32_t sV = tc::smem_u32(smem + L::kV + s * L::kTile);
+#pragma unroll
+                for (int kk = 0; kk < TK / 16; ++kk) {
+                    const uint32_t aoff = (kk >> 2) * 16384 + (kk & 3) * 32;   // P: K-major
+                    tc::mma_bf16(tmem + kColO, tc::smem_desc(sP + aoff, 16, 1024),
+                                 tc::smem_desc(sV + kk * 2048, 16384, 1024),  // V: MN-major
+                                 idO, (j | kk) != 0);
+                }
+                tc::commit(o_done);
+                tc::commit(&kv_empty[s]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------------------------------------------------- softmax
+        const int r = threadIdx.x;            // query row == TMEM lane
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+        const int qp = (r < rows) ? sg.kv_ctx + q0 + r : -1;
+        const float c2 = a.scale * kLog2e;
+        const int first_q = sg.kv_ctx + q0;   // smallest query position of the block
+        float m_run = -INFINITY, l = 0.f;
+        uint8_t* sP = smem + L::kP;
+        for (int j = 0; j < nkb; ++j) {
+            const int s = j & 1;
+            tc::mbar_wait(&s_full[s], (j >> 1) & 1);
+            tc::fence_after();
+            const uint32_t sb = lane_base + kColS + s * TK;
+            const int key0 = j * TK;
+            const bool need_mask = (key0 + TK - 1 > first_q) || rows < TQ;
+            float mt = -INFINITY;
+#pragma unroll 1
+            for (int c = 0; c < TK / 32; ++c) {
+                float v[32];
+                tc::tmem_ld32(sb + c * 32, v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const float x = (need_mask && key0 + c * 32 + i > qp) ? -INFINITY : v[i] * c2;
+                    mt = fmaxf(mt, x);
+                }
+            }
+            if (j > 0) {
+                tc::mbar_wait(o_done, (j - 1) & 1);   // PV(j-1) done: O stable, P free
+                tc::fence_after();
+            }
+            const bool grow = mt > m_run + kRescaleSlack || (m_run == -INFINITY && mt > -INFINITY);
+            if (__any_sync(0xffffffffu, grow) && j > 0) {
+                const float alpha = grow ? exp2f(m_run - mt) : 1.f;
+#pragma unroll 1
+                for (int c = 0; c < HD / 32; ++c) {
+                    float o[32];
+                    tc::tmem_ld32(lane_base + kColO + c * 32, o);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] *= alpha;
+                    tc::tmem_st32(lane_base + kColO + c * 32, o);
+                }
+                if (grow) l *= alpha;
+            }
+            if (grow) m_run = mt;
+            const float mu = (m_run == -INFINITY) ? 0.f : m_run;
+            uint8_t* prow = sP;
+#pragma unroll 1
+            for (int c = 0; c < TK / 32; ++c) {
+                float v[32];
+                tc::tmem_ld32(sb + c * 32, v);
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    const int k = key0 + c * 32 + i;
+                    const float p0 = (need_mask && k > qp) ? 0.f : exp2f(v[i] * c2 - mu);
+                    const float p1 = (need_mask && k + 1 > qp) ? 0.f : exp2f(v[i + 1] * c2 - mu);
+                    l += p0 + p1;
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+                    pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int chunk = c * 4 + q;       // 16-byte chunk index along keys
+                    *reinterpret_cast<uint4*>(prow + tile_off(r, chunk)) =
+                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                }
+            }
+            tc::fence_proxy_async();
+            tc::fence_before();
+            tc::mbar_arrive(p_full);
+        }
+        tc::mbar_wait(o_done, (nkb - 1) & 1);
+        tc::fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        bf16* orow = static_cast<bf16*>(a.o) + (static_cast<long long>(sg.q_start + q0 + r) * a.H + h) * HD;
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+            float o[32];
+            tc::tmem_ld32(lane_base + kColO + c * 32, o);
+            if (r < rows) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 8) {
+                    uint4 raw;
+                    __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        hh[k] = __floats2bfloat162_rn(o[i + 2 * k] * inv, o[i + 2 * k + 1] * inv);
+                    *reinterpret_cast<uint4*>(orow + c * 32 + i) = raw;
+                }
+            }
+        }
+        if (r < rows)
+            a.lse[static_cast<long long>(h) * a.T + sg.q_start + q0 + r] =
+                l > 0.f ? m_run + log2f(l) : INFINITY;
+        tc::fence_before();
+    }
+    __syncthreads();
+    if (warp == 4) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem, 512);
+    }
+}
+
+template <int HD>
+void launch_fwd_tc(const AttnArgs& a, cudaStream_t s) {
+    using L = FwdSmem<HD>;
+    static bool cfg = false;
+    if (!cfg) {
+        EPP_CUDA(cudaFuncSetAttribute(attn_fwd_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
+        cfg = true;
+    }
+    attn_fwd_tc<HD><<<dim3(a.nqwork128, a.H), kThreadsTc, L::kAlloc, s>>>(a);
+    EPP_CHECK_LAUNCH();
+}
+
+
+// ===========================================================================
+// Backward.  Two kernels, no atomics, deterministic:
+//   dq  (grid: 128-row query blocks x H):
+//        S = Q K^T, dP = dO V^T -> TMEM; dS = P (dP - delta) -> smem (bf16);
+//        dQ += dS K -> TMEM; dQ * scale -> fp32 global.
+//   dkv (grid: 128-key blocks x Hkv, GQA heads looped in the CTA):
+//        S^T = K Q^T, dP^T = V dO^T -> TMEM; P^T, dS^T -> smem (bf16);
+//        dV += P^T dO, dK += dS^T Q -> TMEM; then RMW into the fp32 dK/dV
+//        accumulators of the segment (persist across a sequence's chunks).
+// The same swizzled [rows x hd] smem tile serves as a K-major operand and,
+// with a different descriptor (LBO = 16 KB column block, +2 KB per K16 step),
+// as an MN-major operand, so Q, dO, K are loaded once per role pair.
+// ===========================================================================
+
+template <int HD>
+struct DqSmem {
+    static constexpr int kTile = 128 * HD * 2;
+    static constexpr int kQ = 0;
+    static constexpr int kO = kQ + kTile;           // dO
+    static constexpr int kK = kO + kTile;           // 2 stages
+    static constexpr int kV = kK + 2 * kTile;       // 2 stages
+    static constexpr int kS = kV + 2 * kTile;       // dS 128x128 bf16
+    static constexpr int kBar = kS + 128 * 128 * 2;
+    static constexpr int kBytes = kBar + 16 * 8 + 16;
+    static constexpr int kAlloc = kBytes + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a) {
+    using L = DqSmem<HD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
+    uint64_t* q_full = bar + 0;
+    uint64_t* kv_full = bar + 1;     // [2]
+    uint64_t* kv_empty = bar + 3;    // [2]
+    uint64_t* s_full = bar + 5;
+    uint64_t* p_full = bar + 6;
+    uint64_t* o_done = bar + 7;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+
+    const AttnWork w = a.qwork128[blockIdx.x];
+    const AttnSeg sg = a.segs[w.seg];
+    const int h = blockIdx.y;
+    const int kvh = h / (a.H / a.Hkv);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q0 = w.block * TQ;
+    const int rows = min(TQ, sg.q_len - q0);
+    const int kv_end = sg.kv_ctx + q0 + rows;
+    const int nkb = (kv_end + TK - 1) / TK;
+    const long long row0 = sg.q_start + q0;
+
+    if (threadIdx.x == 0) {
+        tc::mbar_init(q_full, kLoadThreads);
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&kv_full[s], kLoadThreads);
+            tc::mbar_init(&kv_empty[s], 1);
+        }
+        tc::mbar_init(s_full, 1);
+        tc::mbar_init(p_full, TQ);
+        tc::mbar_init(o_done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 4) tc::tmem_alloc(tmem_slot, 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+    constexpr uint32_t kColS = 0, kColP = 128, kColQ = 256;
+
+    if (warp >= 5) {
+        const int lt = threadIdx.x - 160;
+        constexpr int kChunks = HD / 8;
+        const long long qs = static_cast<long long>(a.H) * HD;
+        const bf16* qb = static_cast<const bf16*>(a.q) + (row0 * a.H + h) * HD;
+        const bf16* ob = static_cast<const bf16*>(a.dout) + (row0 * a.H + h) * HD;
+        for (int i = lt; i < TQ * kChunks; i += kLoadThreads) {
+            const int r = i / kChunks, c = i % kChunks;
+            const bool ok = r < rows;
+            tc::cp_async16_zfill(smem + L::kQ + tile_off(r, c), ok ? qb + r * qs + c * 8 : qb, ok);
+            tc::cp_async16_zfill(smem + L::kO + tile_off(r, c), ok ? ob + r * qs + c * 8 : ob, ok);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        tc::fence_proxy_async();
+        tc::mbar_arrive(q_full);
+        const long long kvs = static_cast<long long>(a.Hkv) * HD;
+        const bf16* kb = static_cast<const bf16*>(sg.k) + a.layer * sg.kv_layer_stride + kvh * HD;
+        const bf16* vb = static_cast<const bf16*>(sg.v) + a.layer * sg.kv_layer_stride + kvh * HD;
+        for (int j = 0; j < nkb; ++j) {
+            const int s = j & 1;
+            tc::mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+            const int key0 = j * TK;
+            uint8_t* sk = smem + L::kK + s * L::kTile;
+            uint8_t* sv = smem + L::kV + s * L::kTile;
+            for (int i = lt; i < TK * kChunks; i += kLoadThreads) {
+                const int r = i / kChunks, c = i % kChunks;
+                const bool ok = key0 + r < kv_end;
+                const long long off = static_cast<long long>(key0 + r) * kvs + c * 8;
+                tc::cp_async16_zfill(sk + tile_off(r, c), ok ? kb + off : kb, ok);
+                tc::cp_async16_zfill(sv + tile_off(r, c), ok ? vb + off : vb, ok);
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            tc::fence_proxy_async();
+            tc::mbar_arrive(&kv_full[s]);
+        }
+    } else if (warp == 4) {
+        if (lane == 0) {
+            constexpr uint32_t idS = tc::instr_desc_mn(TQ, TK, false, false);
+            constexpr uint32_t idQ = tc::instr_desc_mn(TQ, HD, false, true);
+            const uint32_t sQ = tc::smem_u32(smem + L::kQ);
+            const uint32_t sO = tc::smem_u32(smem + L::kO);
+            const uint32_t sS = tc::smem_u32(smem + L::kS);
+            tc::mbar_wait(q_full, 0);
+            tc::fence_after();
+            for (int j = 0; j < nkb; ++j) {
+                const int s = j & 1;
+                tc::mbar_wait(&kv_full[s], (j >> 1) & 1);
+                if (j > 0) tc::mbar_wait(p_full, (j - 1) & 1);   // S/dP of j-1 consumed
+                tc::fence_after();
+                const uint32_t sK = tc::smem_u32(smem + L::kK + s * L::kTile);
+                const uint32_t sV = tc::smem_u32(smem + L::kV + s * L::kTile);
+                if (j > 0) {
+                    // dQ += dS(j-1) K(j-1)   (K(j-1) still resident in stage s^1)
+                    const uint32_t sKp = tc::smem_u32(smem + L::kK + (s ^ 1) * L::kTile);
+#pragma unroll
+                    for (int kk = 0; kk < TK / 16; ++kk)
+                        tc::mma_bf16(tmem + kColQ, tc::smem_desc(sS + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                                     tc::smem_desc(sKp + kk * 2048, 16384, 1024), idQ, (j - 1 | kk) != 0);
+                    tc::commit(o_done);
+                    tc::commit(&kv_empty[s ^ 1]);
+                }
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc::mma_bf16(tmem + kColS, tc::smem_desc(sQ + off, 16, 1024),
+                                 tc::smem_desc(sK + off, 16, 1024), idS, kk != 0);
+                    tc::mma_bf16(tmem + kColP, tc::smem_desc(sO + off, 16, 1024),
+                                 tc::smem_desc(sV + off, 16, 1024), idS, kk != 0);
+                }
+                tc::commit(s_full);
+            }
+            tc::mbar_wait(p_full, (nkb - 1) & 1);
+            tc::fence_after();
+            const int s = (nkb - 1) & 1;
+            const uint32_t sK = tc::smem_u32(smem + L::kK + s * L::kTile);
+#pragma unroll
+            for (int kk = 0; kk < TK / 16; ++kk)
+                tc::mma_bf16(tmem + kColQ, tc::smem_desc(sS + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                             tc::smem_desc(sK + kk * 2048, 16384, 1024), idQ, (nkb - 1 | kk) != 0);
+            tc::commit(o_done);
+        }
+        __syncwarp();
+    } else {
+        const int r = threadIdx.x;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+        const int qp = (r < rows) ? sg.kv_ctx + q0 + r : -1;
+        const float c2 = a.scale * kLog2e;
+        const int first_q = sg.kv_ctx + q0;
+        const long long t = row0 + min(r, rows - 1);
+        const float lse = a.lse[static_cast<long long>(h) * a.T + t];
+        const float dlt = a.delta[static_cast<long long>(h) * a.T + t];
+        uint8_t* sS = smem + L::kS;
+        for (int j = 0; j < nkb; ++j) {
+            tc::mbar_wait(s_full, j & 1);
+            tc::fence_after();
+            if (j > 0) {
+                tc::mbar_wait(o_done, (j - 1) & 1);   // dQ(j-1) MMA done reading dS smem
+                tc::fence_after();
+            }
+            const int key0 = j * TK;
+            const bool need_mask = (key0 + TK - 1 > first_q) || rows < TQ;
+#pragma unroll 1
+            for (int c = 0; c < TK / 32; ++c) {
+                float sv[32], pv[32];
+                tc::tmem_ld32(lane_base + kColS + c * 32, sv);
+                tc::tmem_ld32(lane_base + kColP + c * 32, pv);
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    const int k = key0 + c * 32 + i;
+                    const float p0 = (need_mask && k > qp) ? 0.f : exp2f(sv[i] * c2 - lse);
+                    const float p1 = (need_mask && k + 1 > qp) ? 0.f : exp2f(sv[i + 1] * c2 - lse);
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(p0 * (pv[i] - dlt), p1 * (pv[i + 1] - dlt));
+                    pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    *reinterpret_cast<uint4*>(sS + tile_off(r, c * 4 + q)) =
+                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            }
+            tc::fence_proxy_async();
+            tc::fence_before();
+            tc::mbar_arrive(p_full);
+        }
+        tc::mbar_wait(o_done, (nkb - 1) & 1);
+        tc::fence_after();
+        float* drow = a.dq + ((row0 + r) * a.H + h) * HD;
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+            float v[32];
+            tc::tmem_ld32(lane_base + kColQ + c * 32, v);
+            if (r < rows) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4)
+                    *reinterpret_cast<float4*>(drow + c * 32 + i) =
+                        make_float4(v[i] * a.scale, v[i + 1] * a.scale, v[i + 2] * a.scale, v[i + 3] * a.scale);
+            }
+        }
+        tc::fence_before();
+    }
+    __syncthreads();
+    if (warp == 4) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem, 512);
+    }
+}
+
+template <int HD>
+struct DkvSmem {
+    static constexpr int kTile = 128 * HD * 2;
+    static constexpr int kK = 0;
+    static constexpr int kV = kK + kTile;
+    static constexpr int kQ = kV + kTile;
+    static constexpr int kO = kQ + kTile;
+    static constexpr int kP = kO + kTile;           // P^T 128x128 bf16
+    static constexpr int kS = kP + 128 * 128 * 2;   // dS^T
+    static constexpr int kLse = kS + 128 * 128 * 2; // 128 floats
+    static constexpr int kDelta = kLse + 512;
+    static constexpr int kBar = kDelta + 512;
+    static constexpr int kBytes = kBar + 16 * 8 + 16;
+    static constexpr int kAlloc = kBytes + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs a) {
+    using L = DkvSmem<HD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
+    uint64_t* kv_full = bar + 0;
+    uint64_t* qd_full = bar + 1;
+    uint64_t* qd_empty = bar + 2;
+    uint64_t* s_full = bar + 3;
+    uint64_t* p_full = bar + 4;
+    uint64_t* pd_free = bar + 5;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 6);
+    float* sLse = reinterpret_cast<float*>(smem + L::kLse);
+    float* sDelta = reinterpret_cast<float*>(smem + L::kDelta);
+
+    const AttnWork w = a.kwork128[blockIdx.x];
+    const AttnSeg sg = a.segs[w.seg];
+    const int kvh = blockIdx.y;
+    const int group = a.H / a.Hkv;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int k0 = w.block * TK;
+    const int kv_len = sg.kv_ctx + sg.q_len;
+    const int nkeys = min(TK, kv_len - k0);
+    const int qb_first = max(0, k0 - sg.kv_ctx) / TQ;
+    const int nqb = (sg.q_len + TQ - 1) / TQ;
+    const int per_head = nqb - qb_first;
+    const int iters = per_head * group;
+
+    if (threadIdx.x == 0) {
+        tc::mbar_init(kv_full, kLoadThreads);
+        tc::mbar_init(qd_full, kLoadThreads);
+        tc::mbar_init(qd_empty, 1);
+        tc::mbar_init(s_full, 1);
+        tc::mbar_init(p_full, TQ);
+        tc::mbar_init(pd_free, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 4) tc::tmem_alloc(tmem_slot, 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+    constexpr uint32_t kColS = 0, kColP = 128, kColV = 256, kColK = 384;
+
+    if (warp >= 5) {
+        const int lt = threadIdx.x - 160;
+        constexpr int kChunks = HD / 8;
+        const long long kvs = static_cast<long long>(a.Hkv) * HD;
+        const bf16* kb = static_cast<const bf16*>(sg.k) + a.layer * sg.kv_layer_stride + kvh * HD + k0 * kvs;
+        const bf16* vb = static_cast<const bf16*>(sg.v) + a.layer * sg.kv_layer_stride + kvh * HD + k0 * kvs;
+        for (int i = lt; i < TK * kChunks; i += kLoadThreads) {
+            const int r = i / kChunks, c = i % kChunks;
+            const bool ok = r < nkeys;
+            tc::cp_async16_zfill(smem + L::kK + tile_off(r, c), ok ? kb + r * kvs + c * 8 : kb, ok);
+            tc::cp_async16_zfill(smem + L::kV + tile_off(r, c), ok ? vb + r * kvs + c * 8 : vb, ok);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        tc::fence_proxy_async();
+        tc::mbar_arrive(kv_full);
+        const long long qs = static_cast<long long>(a.H) * HD;
+        for (int it = 0; it < iters; ++it) {
+            tc::mbar_wait(qd_empty, (it & 1) ^ 1);
+            const int hq = kvh * group + it / per_head;
+            const int qb = qb_first + it % per_head;
+            const int q0 = qb * TQ;
+            const int rows = min(TQ, sg.q_len - q0);
+            const long long row0 = sg.q_start + q0;
+            const bf16* qb_ = static_cast<const bf16*>(a.q) + (row0 * a.H + hq) * HD;
+            const bf16* ob_ = static_cast<const bf16*>(a.dout) + (row0 * a.H + hq) * HD;
+            for (int i = lt; i < TQ * kChunks; i += kLoadThreads) {
+                const int r = i / kChunks, c = i % kChunks;
+                const bool ok = r < rows;
+                tc::cp_async16_zfill(smem + L::kQ + tile_off(r, c), ok ? qb_ + r * qs + c * 8 : qb_, ok);
+                tc::cp_async16_zfill(smem + L::kO + tile_off(r, c), ok ? ob_ + r * qs + c * 8 : ob_, ok);
+            }
+            for (int i = lt; i < TQ; i += kLoadThreads) {
+                const bool ok = i < rows;
+                sLse[i] = ok ? a.lse[static_cast<long long>(hq) * a.T + row0 + i] : INFINITY;
+                sDelta[i] = ok ? a.delta[static_cast<long long>(hq) * a.T + row0 + i] : 0.f;
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            tc::fence_proxy_async();
+            tc::mbar_arrive(qd_full);
+        }
+    } else if (warp == 4) {
+        if (lane == 0) {
+            constexpr uint32_t idS = tc::instr_desc_mn(TK, TQ, false, false);
+            constexpr uint32_t idD = tc::instr_desc_mn(TK, HD, false, true);
+            const uint32_t sK = tc::smem_u32(smem + L::kK);
+            const uint32_t sV = tc::smem_u32(smem + L::kV);
+            const uint32_t sQ = tc::smem_u32(smem + L::kQ);
+            const uint32_t sO = tc::smem_u32(smem + L::kO);
+            const uint32_t sP = tc::smem_u32(smem + L::kP);
+            const uint32_t sS = tc::smem_u32(smem + L::kS);
+            tc::mbar_wait(kv_full, 0);
+            for (int it = 0; it < iters; ++it) {
+                tc::mbar_wait(qd_full, it & 1);
+                tc::fence_after();
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc::mma_bf16(tmem + kColS, tc::smem_desc(sK + off, 16, 1024),
+                                 tc::smem_desc(sQ + off, 16, 1024), idS, kk != 0);
+                    tc::mma_bf16(tmem + kColP, tc::smem_desc(sV + off, 16, 1024),
+                                 tc::smem_desc(sO + off, 16, 1024), idS, kk != 0);
+                }
+                tc::commit(s_full);
+                tc::mbar_wait(p_full, it & 1);                       // P^T, dS^T written
+                tc::fence_after();
+#pragma unroll
+                for (int kk = 0; kk < TQ / 16; ++kk) {
+                    const uint32_t aoff = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc::mma_bf16(tmem + kColV, tc::smem_desc(sP + aoff, 16, 1024),
+                                 tc::smem_desc(sO + kk * 2048, 16384, 1024), idD, (it | kk) != 0);
+                    tc::mma_bf16(tmem + kColK, tc::smem_desc(sS + aoff, 16, 1024),
+                                 tc::smem_desc(sQ + kk * 2048, 16384, 1024), idD, (it | kk) != 0);
+                }
+                tc::commit(qd_empty);
+                tc::commit(pd_free);
+            }
+        }
+        __syncwarp();
+    } else {
+        const int r = threadIdx.x;            // key row == TMEM lane
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+        const int kp = k0 + r;
+        const float c2 = a.scale * kLog2e;
+        uint8_t* sP = smem + L::kP;
+        uint8_t* sS = smem + L::kS;
+        for (int it = 0; it < iters; ++it) {
+            const int qb = qb_first + it % per_head;
+            const int q0 = qb * TQ;
+            const int rows = min(TQ, sg.q_len - q0);
+            tc::mbar_wait(s_full, it & 1);
+            tc::fence_after();
+            if (it > 0) {
+                tc::mbar_wait(pd_free, (it - 1) & 1);   // previous dV/dK MMAs read P^T/dS^T
+                tc::fence_after();
+            }
+            const int first_q = sg.kv_ctx + q0;
+            const bool need_mask = (k0 + TK - 1 > first_q) || rows < TQ;
+#pragma unroll 1
+            for (int c = 0; c < TQ / 32; ++c) {
+                float sv[32], dv[32];
+                tc::tmem_ld32(lane_base + kColS + c * 32, sv);
+                tc::tmem_ld32(lane_base + kColP + c * 32, dv);
+                uint32_t pk[16], dk[16];
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    float p[2], d[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int qi = c * 32 + i + e;
+                        const bool vis = !need_mask || (qi < rows && kp <= first_q + qi);
+                        p[e] = vis ? exp2f(sv[i + e] * c2 - sLse[qi]) : 0.f;
+                        d[e] = p[e] * (dv[i + e] - sDelta[qi]);
+                    }
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(p[0], p[1]);
+                    pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+                    __nv_bfloat162 d2 = __floats2bfloat162_rn(d[0], d[1]);
+                    dk[i >> 1] = *reinterpret_cast<uint32_t*>(&d2);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    *reinterpret_cast<uint4*>(sP + tile_off(r, c * 4 + q)) =
+                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                    *reinterpret_cast<uint4*>(sS + tile_off(r, c * 4 + q)) =
+                        make_uint4(dk[4 * q], dk[4 * q + 1], dk[4 * q + 2], dk[4 * q + 3]);
+                }
+            }
+            tc::fence_proxy_async();
+            tc::fence_before();
+            tc::mbar_arrive(p_full);
+        }
+        tc::mbar_wait(pd_free, (iters - 1) & 1);   // every key block has >= 1 query block
+        tc::fence_after();
+        const long long kvs = static_cast<long long>(a.Hkv) * HD;
+        float* dkr = sg.dk + a.layer * sg.dkv_layer_stride + kvh * HD + (k0 + min(r, nkeys - 1)) * kvs;
+        float* dvr = sg.dv + a.layer * sg.dkv_layer_stride + kvh * HD + (k0 + min(r, nkeys - 1)) * kvs;
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+            float kv[32], vv[32];
+            tc::tmem_ld32(lane_base + kColK + c * 32, kv);    // warp-collective: all lanes
+            tc::tmem_ld32(lane_base + kColV + c * 32, vv);
+            if (r < nkeys) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                    float4 x = *reinterpret_cast<float4*>(dkr + c * 32 + i);
+                    x.x += kv[i] * a.scale; x.y += kv[i + 1] * a.scale;
+                    x.z += kv[i + 2] * a.scale; x.w += kv[i + 3] * a.scale;
+                    *reinterpret_cast<float4*>(dkr + c * 32 + i) = x;
+                    float4 y = *reinterpret_cast<float4*>(dvr + c * 32 + i);
+                    y.x += vv[i]; y.y += vv[i + 1]; y.z += vv[i + 2]; y.w += vv[i + 3];
+                    *reinterpret_cast<float4*>(dvr + c * 32 + i) = y;
+                }
+            }
+        }
+        tc::fence_before();
+    }
+    __syncthreads();
+    if (warp == 4) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem, 512);
+    }
+}
+
+template <int HD>
+void launch_bwd_tc(const AttnArgs& a, cudaStream_t s) {
+    static bool cfg = false;
+    if (!cfg) {
+        EPP_CUDA(cudaFuncSetAttribute(attn_bwd_dq_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      DqSmem<HD>::kAlloc));
+        EPP_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      DkvSmem<HD>::kAlloc));
+        cfg = true;
+    }
+    if (a.nqwork128 > 0) {
+        attn_bwd_dq_tc<HD><<<dim3(a.nqwork128, a.H), kThreadsTc, DqSmem<HD>::kAlloc, s>>>(a);
+        EPP_CHECK_LAUNCH();
+    }
+    if (a.nkwork128 > 0) {
+        attn_bwd_dkv_tc<HD><<<dim3(a.nkwork128, a.Hkv), kThreadsTc, DkvSmem<HD>::kAlloc, s>>>(a);
+        EPP_CHECK_LAUNCH();
+    }
+}
+
+}  // namespace
+
+bool attn_fwd_tc_supported(const AttnArgs& a) {
+    return a.dtype == DType::BF16 && (a.hd == 64 || a.hd == 128) && a.qwork128 != nullptr;
+}
+
+bool attn_bwd_tc_supported(const AttnArgs& a) {
+    return a.dtype == DType::BF16 && (a.hd == 64 || a.hd == 128) && a.qwork128 != nullptr &&
+           a.kwork128 != nullptr;
+}
+
+// dq + dk/dv kernels (the delta pre-pass is issued by attn_bwd).
+void attn_bwd_tc_main(const AttnArgs& a, cudaStream_t s) {
+    if (a.hd == 64) launch_bwd_tc<64>(a, s);
+    else launch_bwd_tc<128>(a, s);
+}
+
+void attn_fwd_tc(const AttnArgs& a, cudaStream_t s) {
+    if (a.nqwork128 == 0) return;
+    ProfScope prof(kProfAttnFwd, 4.0 * a.H * a.hd * a.pairs, s);
+    if (a.hd == 64) launch_fwd_tc<64>(a, s);
+    else launch_fwd_tc<128>(a, s);
+}
+
+}  // namespace eppk

@@ -34,14 +34,16 @@ struct AttnTables {
     void* segs = nullptr;
     void* qw = nullptr;
     void* kw = nullptr;
-    int nq = 0, nk = 0;
+    void* qw128 = nullptr;
+    void* kw128 = nullptr;
+    int nq = 0, nk = 0, nq128 = 0, nk128 = 0;
     cudaStream_t s;
     AttnTables(int nseg, const int32_t* q_start, const int32_t* q_len, const int32_t* kv_ctx,
                const void* const* k, const void* const* v, float* const* dk, float* const* dv,
                cudaStream_t st)
         : s(st) {
         std::vector<AttnSeg> sg(nseg);
-        std::vector<AttnWork> q, kk;
+        std::vector<AttnWork> q, kk, q128, k128;
         for (int i = 0; i < nseg; ++i) {
             sg[i] = AttnSeg{};
             sg[i].q_start = q_start[i];
@@ -53,7 +55,15 @@ struct AttnTables {
             sg[i].dv = dv ? dv[i] : nullptr;
             for (int b = 0; b * kAttnBlock < q_len[i]; ++b) q.push_back({i, b});
             for (int b = 0; b * kAttnBlock < kv_ctx[i] + q_len[i]; ++b) kk.push_back({i, b});
+            for (int b = 0; b * 128 < q_len[i]; ++b) q128.push_back({i, b});
+            for (int b = 0; b * 128 < kv_ctx[i] + q_len[i]; ++b) k128.push_back({i, b});
         }
+        nq128 = static_cast<int>(q128.size());
+        nk128 = static_cast<int>(k128.size());
+        EPP_CUDA(cudaMalloc(&qw128, sizeof(AttnWork) * (nq128 ? nq128 : 1)));
+        EPP_CUDA(cudaMalloc(&kw128, sizeof(AttnWork) * (nk128 ? nk128 : 1)));
+        EPP_CUDA(cudaMemcpy(qw128, q128.data(), sizeof(AttnWork) * nq128, cudaMemcpyHostToDevice));
+        EPP_CUDA(cudaMemcpy(kw128, k128.data(), sizeof(AttnWork) * nk128, cudaMemcpyHostToDevice));
         nq = static_cast<int>(q.size());
         nk = static_cast<int>(kk.size());
         EPP_CUDA(cudaMalloc(&segs, sizeof(AttnSeg) * (nseg ? nseg : 1)));
@@ -68,12 +78,20 @@ struct AttnTables {
         cudaFree(segs);
         cudaFree(qw);
         cudaFree(kw);
+        cudaFree(qw128);
+        cudaFree(kw128);
     }
 };
 }  // namespace
 }  // namespace eppk
 
 extern "C" {
+
+int epp_gpu_set_attention_impl(int32_t impl) {
+    if (impl != 0 && impl != 1) return EPP_GPU_EARG;
+    eppk::attention_impl() = impl;
+    return EPP_GPU_OK;
+}
 
 int epp_kernel_gemm(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_kmajor,
                     const void* B, int64_t ldb, int32_t b_kmajor, void* C, int64_t ldc,
@@ -105,6 +123,10 @@ int epp_kernel_attention_fwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, floa
         a.nqwork = tb.nq;
         a.kwork = static_cast<const eppk::AttnWork*>(tb.kw);
         a.nkwork = tb.nk;
+        a.qwork128 = static_cast<const eppk::AttnWork*>(tb.qw128);
+        a.nqwork128 = tb.nq128;
+        a.kwork128 = static_cast<const eppk::AttnWork*>(tb.kw128);
+        a.nkwork128 = tb.nk128;
         a.T = T; a.H = H; a.Hkv = Hkv; a.hd = hd; a.layer = 0; a.scale = scale;
         a.dtype = static_cast<eppk::DType>(dtype);
         a.q = q; a.o = o; a.lse = lse;
@@ -131,6 +153,10 @@ int epp_kernel_attention_bwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, floa
         a.nqwork = tb.nq;
         a.kwork = static_cast<const eppk::AttnWork*>(tb.kw);
         a.nkwork = tb.nk;
+        a.qwork128 = static_cast<const eppk::AttnWork*>(tb.qw128);
+        a.nqwork128 = tb.nq128;
+        a.kwork128 = static_cast<const eppk::AttnWork*>(tb.kw128);
+        a.nkwork128 = tb.nk128;
         a.T = T; a.H = H; a.Hkv = Hkv; a.hd = hd; a.layer = 0; a.scale = scale;
         a.dtype = static_cast<eppk::DType>(dtype);
         a.q = q; a.o = const_cast<void*>(o); a.lse = const_cast<float*>(lse);

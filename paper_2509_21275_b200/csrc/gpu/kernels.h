@@ -70,6 +70,10 @@ struct AttnArgs {
     int nqwork = 0;
     const AttnWork* kwork = nullptr;   // key blocks (dk/dv)
     int nkwork = 0;
+    const AttnWork* qwork128 = nullptr;   // 128-row query blocks (tcgen05 kernels)
+    int nqwork128 = 0;
+    const AttnWork* kwork128 = nullptr;   // 128-key blocks (tcgen05 kernels)
+    int nkwork128 = 0;
     int T = 0;
     int H = 0, Hkv = 0, hd = 0;
     int layer = 0;
@@ -87,6 +91,13 @@ struct AttnArgs {
 };
 
 void attn_fwd(const AttnArgs& a, cudaStream_t s);
+// tcgen05 variants (attention_tc.cu); attn_fwd dispatches to them when
+// supported unless EPP_ATTN_IMPL=fa2 is set.
+int& attention_impl();
+bool attn_fwd_tc_supported(const AttnArgs& a);
+void attn_fwd_tc(const AttnArgs& a, cudaStream_t s);
+bool attn_bwd_tc_supported(const AttnArgs& a);
+void attn_bwd_tc_main(const AttnArgs& a, cudaStream_t s);
 void attn_bwd(const AttnArgs& a, cudaStream_t s);
 
 // ------------------------------------------------------- elementwise ------

@@ -15,6 +15,7 @@
 //   * the buffers are released after the sequence's first slice (context 0)
 //     finishes its backward.
 // Memory comes from the CUDA stream-ordered allocator on the stage's stream.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -154,10 +155,10 @@ struct LayerSaved {
 struct ChunkState {
     int T = 0;
     std::vector<AttnSeg> segs;     // host copy
-    Buf segs_dev, tok_seg, tok_pos, qwork, kwork;
+    Buf segs_dev, tok_seg, tok_pos, qwork, kwork, qwork128, kwork128;
     Buf kv_local;                  // [K|V][layer][T][Hkv*hd] rows of packed segments
     Buf dkv_local;                 // fp32 [dK|dV][T][Hkv*hd], one layer, re-zeroed per layer
-    int nqwork = 0, nkwork = 0;
+    int nqwork = 0, nkwork = 0, nqwork128 = 0, nkwork128 = 0;
     double pairs = 0;
     Buf x_in;                      // stage input (copy of act_in or embedding)
     std::vector<LayerSaved> layers;
@@ -464,7 +465,7 @@ private:
         }
         rope_reserve(max_pos, hd_, m_.rope_theta, s);
         std::vector<int> tseg(cs.T), tpos(cs.T);
-        std::vector<AttnWork> qw, kw;
+        std::vector<AttnWork> qw, kw, qw128, kw128;
         for (int i = 0; i < static_cast<int>(cs.segs.size()); ++i) {
             const AttnSeg& sg = cs.segs[i];
             for (int t = 0; t < sg.q_len; ++t) {
@@ -473,17 +474,45 @@ private:
             }
             for (int b = 0; b * kAttnBlock < sg.q_len; ++b) qw.push_back({i, b});
             for (int b = 0; b * kAttnBlock < sg.kv_ctx + sg.q_len; ++b) kw.push_back({i, b});
+            for (int b = 0; b * 128 < sg.q_len; ++b) qw128.push_back({i, b});
+            for (int b = 0; b * 128 < sg.kv_ctx + sg.q_len; ++b) kw128.push_back({i, b});
         }
         cs.pairs = 0;
         for (const AttnSeg& sg : cs.segs)
             cs.pairs += static_cast<double>(sg.q_len) * sg.kv_ctx +
                         0.5 * static_cast<double>(sg.q_len) * (sg.q_len + 1);
+        // Longest-processing-time first: blocks with the most keys (or the
+        // most query blocks, for the key-parallel backward) are dispatched
+        // first so long-context slices do not form the tail of the grid.
+        auto qcost = [&](const AttnWork& w, int blk) {
+            const AttnSeg& sg = cs.segs[w.seg];
+            return sg.kv_ctx + std::min(sg.q_len, (w.block + 1) * blk);
+        };
+        auto kcost = [&](const AttnWork& w, int blk) {
+            const AttnSeg& sg = cs.segs[w.seg];
+            return sg.q_len - std::max(0, w.block * blk - sg.kv_ctx);   // queries seeing the block
+        };
+        auto by = [](auto cost, int blk) {
+            return [cost, blk](const AttnWork& a, const AttnWork& b) {
+                const int ca = cost(a, blk), cb = cost(b, blk);
+                if (ca != cb) return ca > cb;
+                return a.seg != b.seg ? a.seg < b.seg : a.block < b.block;
+            };
+        };
+        std::sort(qw.begin(), qw.end(), by(qcost, kAttnBlock));
+        std::sort(kw.begin(), kw.end(), by(kcost, kAttnBlock));
+        std::sort(qw128.begin(), qw128.end(), by(qcost, 128));
+        std::sort(kw128.begin(), kw128.end(), by(kcost, 128));
         cs.nqwork = static_cast<int>(qw.size());
         cs.nkwork = static_cast<int>(kw.size());
         cs.tok_seg = upload(tseg.data(), tseg.size() * sizeof(int), s);
         cs.tok_pos = upload(tpos.data(), tpos.size() * sizeof(int), s);
         cs.qwork = upload(qw.data(), qw.size() * sizeof(AttnWork), s);
         cs.kwork = upload(kw.data(), kw.size() * sizeof(AttnWork), s);
+        cs.nqwork128 = static_cast<int>(qw128.size());
+        cs.nkwork128 = static_cast<int>(kw128.size());
+        cs.qwork128 = upload(qw128.data(), qw128.size() * sizeof(AttnWork), s);
+        cs.kwork128 = upload(kw128.data(), kw128.size() * sizeof(AttnWork), s);
         cs.segs_dev = upload(cs.segs.data(), cs.segs.size() * sizeof(AttnSeg), s);
     }
 
@@ -529,6 +558,10 @@ private:
         a.nqwork = cs.nqwork;
         a.kwork = cs.kwork.get<AttnWork>();
         a.nkwork = cs.nkwork;
+        a.qwork128 = cs.qwork128.get<AttnWork>();
+        a.nqwork128 = cs.nqwork128;
+        a.kwork128 = cs.kwork128.get<AttnWork>();
+        a.nkwork128 = cs.nkwork128;
         a.T = cs.T;
         a.H = H_;
         a.Hkv = Hkv_;

@@ -71,6 +71,7 @@ def lib():
             "epp_stage_adamw_step": [vp, f32, f32, f32, f32, f32, i32, vp],
             "epp_stage_memory": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)],
             "epp_gpu_profile": [i32],
+            "epp_gpu_set_attention_impl": [i32],
             "epp_gpu_profile_read": [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(i64), i32],
             "epp_kernel_gemm": [i32, i32, i32, vp, i64, i32, vp, i64, i32, vp, i64, vp, i64, i32, i32, vp],
@@ -95,6 +96,11 @@ def lib():
 def check(rc: int) -> None:
     if rc != 0:
         raise EppGpuError(lib().epp_gpu_last_error().decode())
+
+
+def set_attention_impl(name: str) -> None:
+    """'tc' (tcgen05, default) or 'fa2' (mma.sync) attention kernels."""
+    check(lib().epp_gpu_set_attention_impl({"fa2": 0, "tc": 1}[name]))
 
 
 def kernel_launches() -> int:

@@ -140,17 +140,22 @@ def rel(a, b):
 
 SEGS = {
     "packed": [(0, 100, 0), (100, 37, 0), (137, 200, 0), (337, 1, 0)],
+    "multi_tile": [(0, 300, 0), (300, 129, 0), (429, 257, 600)],
     "slice_ctx": [(0, 150, 333)],
     "hybrid": [(0, 90, 1000), (90, 64, 0), (154, 17, 0)],
     "long": [(0, 1024, 2048)],
 }
 
 
-@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("impl,dtype", [("tc", "bf16"), ("fa2", "bf16"), ("tc", "f32")])
 @pytest.mark.parametrize("hd,H,Hkv", [(64, 4, 4), (128, 4, 2), (128, 8, 8)])
 @pytest.mark.parametrize("case", list(SEGS))
-def test_attention(dtype, hd, H, Hkv, case):
-    got, ref = run_attention(dtype, hd, H, Hkv, SEGS[case])
+def test_attention(impl, dtype, hd, H, Hkv, case):
+    G().set_attention_impl(impl)
+    try:
+        got, ref = run_attention(dtype, hd, H, Hkv, SEGS[case])
+    finally:
+        G().set_attention_impl("tc")
     tol = 2e-2 if dtype == "bf16" else 1e-4
     o, lse, dq, dks, dvs = got
     ro, rlse, rdq, rdks, rdvs = ref

@@ -70,9 +70,12 @@ LENGTHS = [700, 37, 21, 190, 5, 64, 380, 129]
 
 
 @pytest.mark.parametrize("arch", ["gpt", "llama"])
-@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "bf16-fa2"])
 @pytest.mark.parametrize("dp,slices,tight", [(1, 3, False), (2, 3, False), (2, 4, True)])
 def test_stage_parity(planner, arch, dtype, dp, slices, tight):
+    from paper_2509_21275_b200 import gpu
+    gpu.set_attention_impl("fa2" if dtype.endswith("fa2") else "tc")
+    dtype = dtype.split("-")[0]
     m = cfg_model(arch)
     plan = make_plan(planner, m, LENGTHS, dp, slices, tight)
     if tight:
@@ -92,6 +95,7 @@ def test_stage_parity(planner, arch, dtype, dp, slices, tight):
         worst = max(worst, err)
         assert err < tol, (name, err)
     print(f"{arch} {dtype} dp={dp} worst grad rel err {worst:.2e}")
+    gpu.set_attention_impl("tc")
 
 
 def test_hd128_bf16(planner):
