@@ -31,6 +31,14 @@ constexpr int kLoadThreads = 96;   // warps 5..7
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleSlack = 8.f;   // log2 units: p <= 2^8 before a rescale
 
+// MUFU.EX2 without the denormal fix-up sequence of exp2f (inputs are
+// <= ~8 and results below 2^-126 flush to zero, which softmax tolerates).
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // [128 rows x HD] bf16 tile = HD/64 column blocks of [128 rows x 128 B],
 // 16-byte chunks XOR-swizzled by (row & 7): the UMMA SWIZZLE_128B layout.
 __device__ __forceinline__ uint32_t tile_off(int row, int chunk) {
@@ -184,24 +192,29 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
             const uint32_t sb = lane_base + kColS + s * TK;
             const int key0 = j * TK;
             const bool need_mask = (key0 + TK - 1 > first_q) || rows < TQ;
-            float mt = -INFINITY;
+            // pass 1: row max of the raw scores (scale > 0 commutes with max)
+            float mraw = -INFINITY;
 #pragma unroll 1
             for (int c = 0; c < TK / 32; ++c) {
                 float v[32];
                 tc::tmem_ld32(sb + c * 32, v);
+                if (need_mask) {
+                    const int lim = qp - (key0 + c * 32);    // keys i <= lim visible
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const float x = (need_mask && key0 + c * 32 + i > qp) ? -INFINITY : v[i] * c2;
-                    mt = fmaxf(mt, x);
+                    for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, i <= lim ? v[i] : -INFINITY);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) mraw = fmaxf(mraw, fmaxf(v[i], v[i + 1]));
                 }
             }
+            const float mt = mraw * c2;
             if (j > 0) {
                 tc::mbar_wait(o_done, (j - 1) & 1);   // PV(j-1) done: O stable, P free
                 tc::fence_after();
             }
             const bool grow = mt > m_run + kRescaleSlack || (m_run == -INFINITY && mt > -INFINITY);
             if (__any_sync(0xffffffffu, grow) && j > 0) {
-                const float alpha = grow ? exp2f(m_run - mt) : 1.f;
+                const float alpha = grow ? ex2(m_run - mt) : 1.f;
 #pragma unroll 1
                 for (int c = 0; c < HD / 32; ++c) {
                     float o[32];
@@ -220,11 +233,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
                 float v[32];
                 tc::tmem_ld32(sb + c * 32, v);
                 uint32_t pk[16];
+                const int lim = need_mask ? qp - (key0 + c * 32) : 32;
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
-                    const int k = key0 + c * 32 + i;
-                    const float p0 = (need_mask && k > qp) ? 0.f : exp2f(v[i] * c2 - mu);
-                    const float p1 = (need_mask && k + 1 > qp) ? 0.f : exp2f(v[i + 1] * c2 - mu);
+                    float p0 = ex2(fmaf(v[i], c2, -mu));
+                    float p1 = ex2(fmaf(v[i + 1], c2, -mu));
+                    if (need_mask) {
+                        p0 = i <= lim ? p0 : 0.f;
+                        p1 = i + 1 <= lim ? p1 : 0.f;
+                    }
                     l += p0 + p1;
                     __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
                     pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
@@ -287,28 +304,42 @@ void launch_fwd_tc(const AttnArgs& a, cudaStream_t s) {
 
 // ===========================================================================
 // Backward.  Two kernels, no atomics, deterministic:
-//   dq  (grid: 128-row query blocks x H):
-//        S = Q K^T, dP = dO V^T -> TMEM; dS = P (dP - delta) -> smem (bf16);
+//   dq  (grid: 128-row query blocks x H), 64-key tiles, 3-stage K/V ring:
+//        S = Q K^T, dP = dO V^T -> TMEM (double-buffered);
+//        dS = P (dP - delta) -> smem (bf16, double-buffered);
 //        dQ += dS K -> TMEM; dQ * scale -> fp32 global.
-//   dkv (grid: 128-key blocks x Hkv, GQA heads looped in the CTA):
-//        S^T = K Q^T, dP^T = V dO^T -> TMEM; P^T, dS^T -> smem (bf16);
+//   dkv (grid: 128-key blocks x Hkv, GQA heads looped in the CTA), 64-row
+//        query tiles, 2-stage Q/dO ring:
+//        S^T = K Q^T, dP^T = V dO^T -> TMEM (double-buffered);
+//        P^T, dS^T -> smem (bf16, double-buffered);
 //        dV += P^T dO, dK += dS^T Q -> TMEM; then RMW into the fp32 dK/dV
 //        accumulators of the segment (persist across a sequence's chunks).
-// The same swizzled [rows x hd] smem tile serves as a K-major operand and,
-// with a different descriptor (LBO = 16 KB column block, +2 KB per K16 step),
-// as an MN-major operand, so Q, dO, K are loaded once per role pair.
+// In both, the MMA warp issues the score MMAs of step i before the gradient
+// MMAs of step i-1, so the tensor core runs while the softmax warps work.
+// The same swizzled [rows x hd] smem tile is a K-major operand in one MMA and
+// (descriptor LBO = column-block stride, +2 KB per K16 step) an MN-major
+// operand in another, so each tile is loaded once.
 // ===========================================================================
+
+// [ROWS x HD] tile, HD/64 column blocks of ROWS x 128 B, 128B-swizzled.
+template <int ROWS>
+__device__ __forceinline__ uint32_t toff(int row, int chunk) {
+    return static_cast<uint32_t>((chunk >> 3) * (ROWS * 128) + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
+}
+
+constexpr int TB = 64;    // secondary tile (keys in dq, queries in dkv)
 
 template <int HD>
 struct DqSmem {
-    static constexpr int kTile = 128 * HD * 2;
+    static constexpr int kBig = 128 * HD * 2;       // Q / dO tiles
+    static constexpr int kSmall = TB * HD * 2;      // K / V tiles
     static constexpr int kQ = 0;
-    static constexpr int kO = kQ + kTile;           // dO
-    static constexpr int kK = kO + kTile;           // 2 stages
-    static constexpr int kV = kK + 2 * kTile;       // 2 stages
-    static constexpr int kS = kV + 2 * kTile;       // dS 128x128 bf16
-    static constexpr int kBar = kS + 128 * 128 * 2;
-    static constexpr int kBytes = kBar + 16 * 8 + 16;
+    static constexpr int kO = kQ + kBig;
+    static constexpr int kK = kO + kBig;            // 3 stages
+    static constexpr int kV = kK + 3 * kSmall;      // 3 stages
+    static constexpr int kS = kV + 3 * kSmall;      // dS [128 x 64] bf16 x 2
+    static constexpr int kBar = kS + 2 * 128 * TB * 2;
+    static constexpr int kBytes = kBar + 24 * 8 + 16;
     static constexpr int kAlloc = kBytes + 1024;
 };
 
@@ -320,12 +351,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
     uint64_t* q_full = bar + 0;
-    uint64_t* kv_full = bar + 1;     // [2]
-    uint64_t* kv_empty = bar + 3;    // [2]
-    uint64_t* s_full = bar + 5;
-    uint64_t* p_full = bar + 6;
-    uint64_t* o_done = bar + 7;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+    uint64_t* kv_full = bar + 1;     // [3]
+    uint64_t* kv_empty = bar + 4;    // [3]
+    uint64_t* s_full = bar + 7;      // [2]
+    uint64_t* p_full = bar + 9;      // [2]
+    uint64_t* dq_done = bar + 11;    // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
 
     const AttnWork w = a.qwork128[blockIdx.x];
     const AttnSeg sg = a.segs[w.seg];
@@ -335,18 +366,20 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
     const int q0 = w.block * TQ;
     const int rows = min(TQ, sg.q_len - q0);
     const int kv_end = sg.kv_ctx + q0 + rows;
-    const int nkb = (kv_end + TK - 1) / TK;
+    const int nkb = (kv_end + TB - 1) / TB;
     const long long row0 = sg.q_start + q0;
 
     if (threadIdx.x == 0) {
         tc::mbar_init(q_full, kLoadThreads);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < 3; ++s) {
             tc::mbar_init(&kv_full[s], kLoadThreads);
             tc::mbar_init(&kv_empty[s], 1);
         }
-        tc::mbar_init(s_full, 1);
-        tc::mbar_init(p_full, TQ);
-        tc::mbar_init(o_done, 1);
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&s_full[b], 1);
+            tc::mbar_init(&p_full[b], TQ);
+            tc::mbar_init(&dq_done[b], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 4) tc::tmem_alloc(tmem_slot, 512);
@@ -365,8 +398,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
         for (int i = lt; i < TQ * kChunks; i += kLoadThreads) {
             const int r = i / kChunks, c = i % kChunks;
             const bool ok = r < rows;
-            tc::cp_async16_zfill(smem + L::kQ + tile_off(r, c), ok ? qb + r * qs + c * 8 : qb, ok);
-            tc::cp_async16_zfill(smem + L::kO + tile_off(r, c), ok ? ob + r * qs + c * 8 : ob, ok);
+            tc::cp_async16_zfill(smem + L::kQ + toff<128>(r, c), ok ? qb + r * qs + c * 8 : qb, ok);
+            tc::cp_async16_zfill(smem + L::kO + toff<128>(r, c), ok ? ob + r * qs + c * 8 : ob, ok);
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
         tc::fence_proxy_async();
@@ -375,67 +408,61 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
         const bf16* kb = static_cast<const bf16*>(sg.k) + a.layer * sg.kv_layer_stride + kvh * HD;
         const bf16* vb = static_cast<const bf16*>(sg.v) + a.layer * sg.kv_layer_stride + kvh * HD;
         for (int j = 0; j < nkb; ++j) {
-            const int s = j & 1;
-            tc::mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-            const int key0 = j * TK;
-            uint8_t* sk = smem + L::kK + s * L::kTile;
-            uint8_t* sv = smem + L::kV + s * L::kTile;
-            for (int i = lt; i < TK * kChunks; i += kLoadThreads) {
+            const int st = j % 3;
+            tc::mbar_wait(&kv_empty[st], ((j / 3) & 1) ^ 1);
+            const int key0 = j * TB;
+            uint8_t* sk = smem + L::kK + st * L::kSmall;
+            uint8_t* sv = smem + L::kV + st * L::kSmall;
+            for (int i = lt; i < TB * kChunks; i += kLoadThreads) {
                 const int r = i / kChunks, c = i % kChunks;
                 const bool ok = key0 + r < kv_end;
                 const long long off = static_cast<long long>(key0 + r) * kvs + c * 8;
-                tc::cp_async16_zfill(sk + tile_off(r, c), ok ? kb + off : kb, ok);
-                tc::cp_async16_zfill(sv + tile_off(r, c), ok ? vb + off : vb, ok);
+                tc::cp_async16_zfill(sk + toff<TB>(r, c), ok ? kb + off : kb, ok);
+                tc::cp_async16_zfill(sv + toff<TB>(r, c), ok ? vb + off : vb, ok);
             }
             asm volatile("cp.async.wait_all;" ::: "memory");
             tc::fence_proxy_async();
-            tc::mbar_arrive(&kv_full[s]);
+            tc::mbar_arrive(&kv_full[st]);
         }
     } else if (warp == 4) {
         if (lane == 0) {
-            constexpr uint32_t idS = tc::instr_desc_mn(TQ, TK, false, false);
+            constexpr uint32_t idS = tc::instr_desc_mn(TQ, TB, false, false);
             constexpr uint32_t idQ = tc::instr_desc_mn(TQ, HD, false, true);
             const uint32_t sQ = tc::smem_u32(smem + L::kQ);
             const uint32_t sO = tc::smem_u32(smem + L::kO);
-            const uint32_t sS = tc::smem_u32(smem + L::kS);
-            tc::mbar_wait(q_full, 0);
-            tc::fence_after();
-            for (int j = 0; j < nkb; ++j) {
-                const int s = j & 1;
-                tc::mbar_wait(&kv_full[s], (j >> 1) & 1);
-                if (j > 0) tc::mbar_wait(p_full, (j - 1) & 1);   // S/dP of j-1 consumed
+            auto grad = [&](int j) {   // dQ += dS(j) K(j)
+                const int b = j & 1, st = j % 3;
+                tc::mbar_wait(&p_full[b], (j >> 1) & 1);
                 tc::fence_after();
-                const uint32_t sK = tc::smem_u32(smem + L::kK + s * L::kTile);
-                const uint32_t sV = tc::smem_u32(smem + L::kV + s * L::kTile);
-                if (j > 0) {
-                    // dQ += dS(j-1) K(j-1)   (K(j-1) still resident in stage s^1)
-                    const uint32_t sKp = tc::smem_u32(smem + L::kK + (s ^ 1) * L::kTile);
+                const uint32_t sS = tc::smem_u32(smem + L::kS + b * 128 * TB * 2);
+                const uint32_t sK = tc::smem_u32(smem + L::kK + st * L::kSmall);
 #pragma unroll
-                    for (int kk = 0; kk < TK / 16; ++kk)
-                        tc::mma_bf16(tmem + kColQ, tc::smem_desc(sS + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                                     tc::smem_desc(sKp + kk * 2048, 16384, 1024), idQ, (j - 1 | kk) != 0);
-                    tc::commit(o_done);
-                    tc::commit(&kv_empty[s ^ 1]);
-                }
+                for (int kk = 0; kk < TB / 16; ++kk)
+                    tc::mma_bf16(tmem + kColQ, tc::smem_desc(sS + kk * 32, 16, 1024),
+                                 tc::smem_desc(sK + kk * 2048, TB * 128, 1024), idQ, (j | kk) != 0);
+                tc::commit(&dq_done[b]);
+                tc::commit(&kv_empty[st]);
+            };
+            tc::mbar_wait(q_full, 0);
+            for (int j = 0; j < nkb; ++j) {
+                const int b = j & 1, st = j % 3;
+                tc::mbar_wait(&kv_full[st], (j / 3) & 1);
+                tc::fence_after();
+                const uint32_t sK = tc::smem_u32(smem + L::kK + st * L::kSmall);
+                const uint32_t sV = tc::smem_u32(smem + L::kV + st * L::kSmall);
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc::mma_bf16(tmem + kColS, tc::smem_desc(sQ + off, 16, 1024),
-                                 tc::smem_desc(sK + off, 16, 1024), idS, kk != 0);
-                    tc::mma_bf16(tmem + kColP, tc::smem_desc(sO + off, 16, 1024),
-                                 tc::smem_desc(sV + off, 16, 1024), idS, kk != 0);
+                    const uint32_t aoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+                    const uint32_t boff = (kk >> 2) * (TB * 128) + (kk & 3) * 32;
+                    tc::mma_bf16(tmem + kColS + b * TB, tc::smem_desc(sQ + aoff, 16, 1024),
+                                 tc::smem_desc(sK + boff, 16, 1024), idS, kk != 0);
+                    tc::mma_bf16(tmem + kColP + b * TB, tc::smem_desc(sO + aoff, 16, 1024),
+                                 tc::smem_desc(sV + boff, 16, 1024), idS, kk != 0);
                 }
-                tc::commit(s_full);
+                tc::commit(&s_full[b]);
+                if (j > 0) grad(j - 1);
             }
-            tc::mbar_wait(p_full, (nkb - 1) & 1);
-            tc::fence_after();
-            const int s = (nkb - 1) & 1;
-            const uint32_t sK = tc::smem_u32(smem + L::kK + s * L::kTile);
-#pragma unroll
-            for (int kk = 0; kk < TK / 16; ++kk)
-                tc::mma_bf16(tmem + kColQ, tc::smem_desc(sS + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                             tc::smem_desc(sK + kk * 2048, 16384, 1024), idQ, (nkb - 1 | kk) != 0);
-            tc::commit(o_done);
+            grad(nkb - 1);
         }
         __syncwarp();
     } else {
@@ -447,40 +474,43 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
         const long long t = row0 + min(r, rows - 1);
         const float lse = a.lse[static_cast<long long>(h) * a.T + t];
         const float dlt = a.delta[static_cast<long long>(h) * a.T + t];
-        uint8_t* sS = smem + L::kS;
         for (int j = 0; j < nkb; ++j) {
-            tc::mbar_wait(s_full, j & 1);
+            const int b = j & 1;
+            tc::mbar_wait(&s_full[b], (j >> 1) & 1);
             tc::fence_after();
-            if (j > 0) {
-                tc::mbar_wait(o_done, (j - 1) & 1);   // dQ(j-1) MMA done reading dS smem
-                tc::fence_after();
-            }
-            const int key0 = j * TK;
-            const bool need_mask = (key0 + TK - 1 > first_q) || rows < TQ;
-#pragma unroll 1
-            for (int c = 0; c < TK / 32; ++c) {
+            const int key0 = j * TB;
+            const bool need_mask = (key0 + TB - 1 > first_q) || rows < TQ;
+            uint32_t pk[32];
+#pragma unroll
+            for (int c = 0; c < TB / 32; ++c) {
                 float sv[32], pv[32];
-                tc::tmem_ld32(lane_base + kColS + c * 32, sv);
-                tc::tmem_ld32(lane_base + kColP + c * 32, pv);
-                uint32_t pk[16];
+                tc::tmem_ld32(lane_base + kColS + b * TB + c * 32, sv);
+                tc::tmem_ld32(lane_base + kColP + b * TB + c * 32, pv);
+                const int lim = need_mask ? qp - (key0 + c * 32) : 32;
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
-                    const int k = key0 + c * 32 + i;
-                    const float p0 = (need_mask && k > qp) ? 0.f : exp2f(sv[i] * c2 - lse);
-                    const float p1 = (need_mask && k + 1 > qp) ? 0.f : exp2f(sv[i + 1] * c2 - lse);
+                    float p0 = ex2(fmaf(sv[i], c2, -lse));
+                    float p1 = ex2(fmaf(sv[i + 1], c2, -lse));
+                    if (need_mask) {
+                        p0 = i <= lim ? p0 : 0.f;
+                        p1 = i + 1 <= lim ? p1 : 0.f;
+                    }
                     __nv_bfloat162 b2 = __floats2bfloat162_rn(p0 * (pv[i] - dlt), p1 * (pv[i + 1] - dlt));
-                    pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+                    pk[c * 16 + (i >> 1)] = *reinterpret_cast<uint32_t*>(&b2);
                 }
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    *reinterpret_cast<uint4*>(sS + tile_off(r, c * 4 + q)) =
-                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
             }
+            tc::mbar_wait(&dq_done[b], ((j >> 1) & 1) ^ 1);   // dQ(j-2) finished reading buffer b
+            tc::fence_after();
+            uint8_t* sS = smem + L::kS + b * 128 * TB * 2;
+#pragma unroll
+            for (int q = 0; q < TB / 8; ++q)
+                *reinterpret_cast<uint4*>(sS + toff<128>(r, q)) =
+                    make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
             tc::fence_proxy_async();
             tc::fence_before();
-            tc::mbar_arrive(p_full);
+            tc::mbar_arrive(&p_full[b]);
         }
-        tc::mbar_wait(o_done, (nkb - 1) & 1);
+        tc::mbar_wait(&dq_done[(nkb - 1) & 1], ((nkb - 1) >> 1) & 1);
         tc::fence_after();
         float* drow = a.dq + ((row0 + r) * a.H + h) * HD;
 #pragma unroll 1
@@ -505,17 +535,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
 
 template <int HD>
 struct DkvSmem {
-    static constexpr int kTile = 128 * HD * 2;
+    static constexpr int kBig = 128 * HD * 2;       // K / V tiles
+    static constexpr int kSmall = TB * HD * 2;      // Q / dO tiles
     static constexpr int kK = 0;
-    static constexpr int kV = kK + kTile;
-    static constexpr int kQ = kV + kTile;
-    static constexpr int kO = kQ + kTile;
-    static constexpr int kP = kO + kTile;           // P^T 128x128 bf16
-    static constexpr int kS = kP + 128 * 128 * 2;   // dS^T
-    static constexpr int kLse = kS + 128 * 128 * 2; // 128 floats
-    static constexpr int kDelta = kLse + 512;
-    static constexpr int kBar = kDelta + 512;
-    static constexpr int kBytes = kBar + 16 * 8 + 16;
+    static constexpr int kV = kK + kBig;
+    static constexpr int kQ = kV + kBig;            // 2 stages
+    static constexpr int kO = kQ + 2 * kSmall;      // 2 stages
+    static constexpr int kP = kO + 2 * kSmall;      // P^T [128 x 64] bf16 x 2
+    static constexpr int kS = kP + 2 * 128 * TB * 2;  // dS^T x 2
+    static constexpr int kLse = kS + 2 * 128 * TB * 2;   // [2][64] floats
+    static constexpr int kDelta = kLse + 2 * TB * 4;
+    static constexpr int kBar = kDelta + 2 * TB * 4;
+    static constexpr int kBytes = kBar + 24 * 8 + 16;
     static constexpr int kAlloc = kBytes + 1024;
 };
 
@@ -527,12 +558,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
     uint64_t* kv_full = bar + 0;
-    uint64_t* qd_full = bar + 1;
-    uint64_t* qd_empty = bar + 2;
-    uint64_t* s_full = bar + 3;
-    uint64_t* p_full = bar + 4;
-    uint64_t* pd_free = bar + 5;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 6);
+    uint64_t* qd_full = bar + 1;     // [2]
+    uint64_t* qd_empty = bar + 3;    // [2]
+    uint64_t* s_full = bar + 5;      // [2]
+    uint64_t* p_full = bar + 7;      // [2]
+    uint64_t* pd_free = bar + 9;     // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
     float* sLse = reinterpret_cast<float*>(smem + L::kLse);
     float* sDelta = reinterpret_cast<float*>(smem + L::kDelta);
 
@@ -544,18 +575,20 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
     const int k0 = w.block * TK;
     const int kv_len = sg.kv_ctx + sg.q_len;
     const int nkeys = min(TK, kv_len - k0);
-    const int qb_first = max(0, k0 - sg.kv_ctx) / TQ;
-    const int nqb = (sg.q_len + TQ - 1) / TQ;
+    const int qb_first = max(0, k0 - sg.kv_ctx) / TB;
+    const int nqb = (sg.q_len + TB - 1) / TB;
     const int per_head = nqb - qb_first;
-    const int iters = per_head * group;
+    const int iters = per_head * group;     // >= 1: the segment's last query sees every key
 
     if (threadIdx.x == 0) {
         tc::mbar_init(kv_full, kLoadThreads);
-        tc::mbar_init(qd_full, kLoadThreads);
-        tc::mbar_init(qd_empty, 1);
-        tc::mbar_init(s_full, 1);
-        tc::mbar_init(p_full, TQ);
-        tc::mbar_init(pd_free, 1);
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&qd_full[b], kLoadThreads);
+            tc::mbar_init(&qd_empty[b], 1);
+            tc::mbar_init(&s_full[b], 1);
+            tc::mbar_init(&p_full[b], TQ);
+            tc::mbar_init(&pd_free[b], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 4) tc::tmem_alloc(tmem_slot, 512);
@@ -563,7 +596,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = *tmem_slot;
-    constexpr uint32_t kColS = 0, kColP = 128, kColV = 256, kColK = 384;
+    constexpr uint32_t kColS = 0, kColP = 128, kColV = 256, kColK = 256 + HD;
 
     if (warp >= 5) {
         const int lt = threadIdx.x - 160;
@@ -574,73 +607,83 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
         for (int i = lt; i < TK * kChunks; i += kLoadThreads) {
             const int r = i / kChunks, c = i % kChunks;
             const bool ok = r < nkeys;
-            tc::cp_async16_zfill(smem + L::kK + tile_off(r, c), ok ? kb + r * kvs + c * 8 : kb, ok);
-            tc::cp_async16_zfill(smem + L::kV + tile_off(r, c), ok ? vb + r * kvs + c * 8 : vb, ok);
+            tc::cp_async16_zfill(smem + L::kK + toff<128>(r, c), ok ? kb + r * kvs + c * 8 : kb, ok);
+            tc::cp_async16_zfill(smem + L::kV + toff<128>(r, c), ok ? vb + r * kvs + c * 8 : vb, ok);
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
         tc::fence_proxy_async();
         tc::mbar_arrive(kv_full);
         const long long qs = static_cast<long long>(a.H) * HD;
         for (int it = 0; it < iters; ++it) {
-            tc::mbar_wait(qd_empty, (it & 1) ^ 1);
+            const int st = it & 1;
+            tc::mbar_wait(&qd_empty[st], ((it >> 1) & 1) ^ 1);
             const int hq = kvh * group + it / per_head;
-            const int qb = qb_first + it % per_head;
-            const int q0 = qb * TQ;
-            const int rows = min(TQ, sg.q_len - q0);
+            const int q0 = (qb_first + it % per_head) * TB;
+            const int rows = min(TB, sg.q_len - q0);
             const long long row0 = sg.q_start + q0;
             const bf16* qb_ = static_cast<const bf16*>(a.q) + (row0 * a.H + hq) * HD;
             const bf16* ob_ = static_cast<const bf16*>(a.dout) + (row0 * a.H + hq) * HD;
-            for (int i = lt; i < TQ * kChunks; i += kLoadThreads) {
+            uint8_t* sq = smem + L::kQ + st * L::kSmall;
+            uint8_t* so = smem + L::kO + st * L::kSmall;
+            for (int i = lt; i < TB * kChunks; i += kLoadThreads) {
                 const int r = i / kChunks, c = i % kChunks;
                 const bool ok = r < rows;
-                tc::cp_async16_zfill(smem + L::kQ + tile_off(r, c), ok ? qb_ + r * qs + c * 8 : qb_, ok);
-                tc::cp_async16_zfill(smem + L::kO + tile_off(r, c), ok ? ob_ + r * qs + c * 8 : ob_, ok);
+                tc::cp_async16_zfill(sq + toff<TB>(r, c), ok ? qb_ + r * qs + c * 8 : qb_, ok);
+                tc::cp_async16_zfill(so + toff<TB>(r, c), ok ? ob_ + r * qs + c * 8 : ob_, ok);
             }
-            for (int i = lt; i < TQ; i += kLoadThreads) {
+            for (int i = lt; i < TB; i += kLoadThreads) {
                 const bool ok = i < rows;
-                sLse[i] = ok ? a.lse[static_cast<long long>(hq) * a.T + row0 + i] : INFINITY;
-                sDelta[i] = ok ? a.delta[static_cast<long long>(hq) * a.T + row0 + i] : 0.f;
+                sLse[st * TB + i] = ok ? a.lse[static_cast<long long>(hq) * a.T + row0 + i] : INFINITY;
+                sDelta[st * TB + i] = ok ? a.delta[static_cast<long long>(hq) * a.T + row0 + i] : 0.f;
             }
             asm volatile("cp.async.wait_all;" ::: "memory");
             tc::fence_proxy_async();
-            tc::mbar_arrive(qd_full);
+            tc::mbar_arrive(&qd_full[st]);
         }
     } else if (warp == 4) {
         if (lane == 0) {
-            constexpr uint32_t idS = tc::instr_desc_mn(TK, TQ, false, false);
+            constexpr uint32_t idS = tc::instr_desc_mn(TK, TB, false, false);
             constexpr uint32_t idD = tc::instr_desc_mn(TK, HD, false, true);
             const uint32_t sK = tc::smem_u32(smem + L::kK);
             const uint32_t sV = tc::smem_u32(smem + L::kV);
-            const uint32_t sQ = tc::smem_u32(smem + L::kQ);
-            const uint32_t sO = tc::smem_u32(smem + L::kO);
-            const uint32_t sP = tc::smem_u32(smem + L::kP);
-            const uint32_t sS = tc::smem_u32(smem + L::kS);
+            auto grad = [&](int it) {   // dV += P^T dO ; dK += dS^T Q
+                const int b = it & 1;
+                tc::mbar_wait(&p_full[b], (it >> 1) & 1);
+                tc::fence_after();
+                const uint32_t sP = tc::smem_u32(smem + L::kP + b * 128 * TB * 2);
+                const uint32_t sS = tc::smem_u32(smem + L::kS + b * 128 * TB * 2);
+                const uint32_t sQ = tc::smem_u32(smem + L::kQ + b * L::kSmall);
+                const uint32_t sO = tc::smem_u32(smem + L::kO + b * L::kSmall);
+#pragma unroll
+                for (int kk = 0; kk < TB / 16; ++kk) {
+                    tc::mma_bf16(tmem + kColV, tc::smem_desc(sP + kk * 32, 16, 1024),
+                                 tc::smem_desc(sO + kk * 2048, TB * 128, 1024), idD, (it | kk) != 0);
+                    tc::mma_bf16(tmem + kColK, tc::smem_desc(sS + kk * 32, 16, 1024),
+                                 tc::smem_desc(sQ + kk * 2048, TB * 128, 1024), idD, (it | kk) != 0);
+                }
+                tc::commit(&qd_empty[b]);
+                tc::commit(&pd_free[b]);
+            };
             tc::mbar_wait(kv_full, 0);
             for (int it = 0; it < iters; ++it) {
-                tc::mbar_wait(qd_full, it & 1);
+                const int b = it & 1;
+                tc::mbar_wait(&qd_full[b], (it >> 1) & 1);
                 tc::fence_after();
+                const uint32_t sQ = tc::smem_u32(smem + L::kQ + b * L::kSmall);
+                const uint32_t sO = tc::smem_u32(smem + L::kO + b * L::kSmall);
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc::mma_bf16(tmem + kColS, tc::smem_desc(sK + off, 16, 1024),
-                                 tc::smem_desc(sQ + off, 16, 1024), idS, kk != 0);
-                    tc::mma_bf16(tmem + kColP, tc::smem_desc(sV + off, 16, 1024),
-                                 tc::smem_desc(sO + off, 16, 1024), idS, kk != 0);
+                    const uint32_t aoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+                    const uint32_t boff = (kk >> 2) * (TB * 128) + (kk & 3) * 32;
+                    tc::mma_bf16(tmem + kColS + b * TB, tc::smem_desc(sK + aoff, 16, 1024),
+                                 tc::smem_desc(sQ + boff, 16, 1024), idS, kk != 0);
+                    tc::mma_bf16(tmem + kColP + b * TB, tc::smem_desc(sV + aoff, 16, 1024),
+                                 tc::smem_desc(sO + boff, 16, 1024), idS, kk != 0);
                 }
-                tc::commit(s_full);
-                tc::mbar_wait(p_full, it & 1);                       // P^T, dS^T written
-                tc::fence_after();
-#pragma unroll
-                for (int kk = 0; kk < TQ / 16; ++kk) {
-                    const uint32_t aoff = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc::mma_bf16(tmem + kColV, tc::smem_desc(sP + aoff, 16, 1024),
-                                 tc::smem_desc(sO + kk * 2048, 16384, 1024), idD, (it | kk) != 0);
-                    tc::mma_bf16(tmem + kColK, tc::smem_desc(sS + aoff, 16, 1024),
-                                 tc::smem_desc(sQ + kk * 2048, 16384, 1024), idD, (it | kk) != 0);
-                }
-                tc::commit(qd_empty);
-                tc::commit(pd_free);
+                tc::commit(&s_full[b]);
+                if (it > 0) grad(it - 1);
             }
+            grad(iters - 1);
         }
         __syncwarp();
     } else {
@@ -648,54 +691,57 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
         const int kp = k0 + r;
         const float c2 = a.scale * kLog2e;
-        uint8_t* sP = smem + L::kP;
-        uint8_t* sS = smem + L::kS;
         for (int it = 0; it < iters; ++it) {
-            const int qb = qb_first + it % per_head;
-            const int q0 = qb * TQ;
-            const int rows = min(TQ, sg.q_len - q0);
-            tc::mbar_wait(s_full, it & 1);
-            tc::fence_after();
-            if (it > 0) {
-                tc::mbar_wait(pd_free, (it - 1) & 1);   // previous dV/dK MMAs read P^T/dS^T
-                tc::fence_after();
-            }
+            const int b = it & 1;
+            const int q0 = (qb_first + it % per_head) * TB;
+            const int rows = min(TB, sg.q_len - q0);
             const int first_q = sg.kv_ctx + q0;
-            const bool need_mask = (k0 + TK - 1 > first_q) || rows < TQ;
-#pragma unroll 1
-            for (int c = 0; c < TQ / 32; ++c) {
+            const bool need_mask = (k0 + TK - 1 > first_q) || rows < TB;
+            tc::mbar_wait(&s_full[b], (it >> 1) & 1);
+            tc::fence_after();
+            const float* lse_s = sLse + b * TB;
+            const float* dl_s = sDelta + b * TB;
+            uint32_t pk[32], dk[32];
+#pragma unroll
+            for (int c = 0; c < TB / 32; ++c) {
                 float sv[32], dv[32];
-                tc::tmem_ld32(lane_base + kColS + c * 32, sv);
-                tc::tmem_ld32(lane_base + kColP + c * 32, dv);
-                uint32_t pk[16], dk[16];
+                tc::tmem_ld32(lane_base + kColS + b * TB + c * 32, sv);
+                tc::tmem_ld32(lane_base + kColP + b * TB + c * 32, dv);
+                // query qi visible to key kp iff qi < rows && qi >= kp - first_q
+                const int qmin = kp - first_q - c * 32;
+                const int qmax = rows - c * 32;
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
                     float p[2], d[2];
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         const int qi = c * 32 + i + e;
-                        const bool vis = !need_mask || (qi < rows && kp <= first_q + qi);
-                        p[e] = vis ? exp2f(sv[i + e] * c2 - sLse[qi]) : 0.f;
-                        d[e] = p[e] * (dv[i + e] - sDelta[qi]);
+                        p[e] = ex2(fmaf(sv[i + e], c2, -lse_s[qi]));
+                        if (need_mask) p[e] = (i + e >= qmin && i + e < qmax) ? p[e] : 0.f;
+                        d[e] = p[e] * (dv[i + e] - dl_s[qi]);
                     }
                     __nv_bfloat162 b2 = __floats2bfloat162_rn(p[0], p[1]);
-                    pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+                    pk[c * 16 + (i >> 1)] = *reinterpret_cast<uint32_t*>(&b2);
                     __nv_bfloat162 d2 = __floats2bfloat162_rn(d[0], d[1]);
-                    dk[i >> 1] = *reinterpret_cast<uint32_t*>(&d2);
+                    dk[c * 16 + (i >> 1)] = *reinterpret_cast<uint32_t*>(&d2);
                 }
+            }
+            tc::mbar_wait(&pd_free[b], ((it >> 1) & 1) ^ 1);   // grad(it-2) done with buffer b
+            tc::fence_after();
+            uint8_t* sP = smem + L::kP + b * 128 * TB * 2;
+            uint8_t* sS = smem + L::kS + b * 128 * TB * 2;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    *reinterpret_cast<uint4*>(sP + tile_off(r, c * 4 + q)) =
-                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-                    *reinterpret_cast<uint4*>(sS + tile_off(r, c * 4 + q)) =
-                        make_uint4(dk[4 * q], dk[4 * q + 1], dk[4 * q + 2], dk[4 * q + 3]);
-                }
+            for (int q = 0; q < TB / 8; ++q) {
+                *reinterpret_cast<uint4*>(sP + toff<128>(r, q)) =
+                    make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                *reinterpret_cast<uint4*>(sS + toff<128>(r, q)) =
+                    make_uint4(dk[4 * q], dk[4 * q + 1], dk[4 * q + 2], dk[4 * q + 3]);
             }
             tc::fence_proxy_async();
             tc::fence_before();
-            tc::mbar_arrive(p_full);
+            tc::mbar_arrive(&p_full[b]);
         }
-        tc::mbar_wait(pd_free, (iters - 1) & 1);   // every key block has >= 1 query block
+        tc::mbar_wait(&pd_free[(iters - 1) & 1], ((iters - 1) >> 1) & 1);
         tc::fence_after();
         const long long kvs = static_cast<long long>(a.Hkv) * HD;
         float* dkr = sg.dk + a.layer * sg.dkv_layer_stride + kvh * HD + (k0 + min(r, nkeys - 1)) * kvs;
@@ -738,10 +784,12 @@ void launch_bwd_tc(const AttnArgs& a, cudaStream_t s) {
         cfg = true;
     }
     if (a.nqwork128 > 0) {
+        ProfScope prof(kProfAttnBwdDq, 6.0 * a.H * a.hd * a.pairs, s);     // executed: 3 matmuls
         attn_bwd_dq_tc<HD><<<dim3(a.nqwork128, a.H), kThreadsTc, DqSmem<HD>::kAlloc, s>>>(a);
         EPP_CHECK_LAUNCH();
     }
     if (a.nkwork128 > 0) {
+        ProfScope prof(kProfAttnBwdDkv, 8.0 * a.H * a.hd * a.pairs, s);    // executed: 4 matmuls
         attn_bwd_dkv_tc<HD><<<dim3(a.nkwork128, a.Hkv), kThreadsTc, DkvSmem<HD>::kAlloc, s>>>(a);
         EPP_CHECK_LAUNCH();
     }

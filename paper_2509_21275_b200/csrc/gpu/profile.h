@@ -3,7 +3,7 @@
 #include <cuda_runtime.h>
 
 namespace eppk {
-enum ProfClass { kProfGemm = 0, kProfAttnFwd = 1, kProfAttnBwd = 2 };
+enum ProfClass { kProfGemm = 0, kProfAttnFwd = 1, kProfAttnBwd = 2, kProfAttnBwdDq = 3, kProfAttnBwdDkv = 4 };
 bool profiling();
 // Records an event pair around the launches issued during its lifetime.
 class ProfScope {
