@@ -112,9 +112,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
             const bool ok = r < rows;
             tc::cp_async16_zfill(smem + L::kQ + tile_off(r, c), ok ? qbase + r * qstride + c * 8 : qbase, ok);
         }
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        tc::fence_proxy_async();
-        tc::mbar_arrive(q_full);
+        tc::cp_async_arrive(q_full);
         const long long kvs = static_cast<long long>(a.Hkv) * HD;
         const bf16* kb = static_cast<const bf16*>(sg.k) + a.layer * sg.kv_layer_stride + kvh * HD;
         const bf16* vb = static_cast<const bf16*>(sg.v) + a.layer * sg.kv_layer_stride + kvh * HD;
@@ -131,9 +129,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
                 tc::cp_async16_zfill(sk + tile_off(r, c), ok ? kb + off : kb, ok);
                 tc::cp_async16_zfill(sv + tile_off(r, c), ok ? vb + off : vb, ok);
             }
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            tc::fence_proxy_async();
-            tc::mbar_arrive(&kv_full[s]);
+            tc::cp_async_arrive(&kv_full[s]);
         }
     } else if (warp == 4) {
         // ------------------------------------------------------- MMA issuer
@@ -145,6 +141,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
             auto issue_s = [&](int j) {
                 const int s = j & 1;
                 tc::mbar_wait(&kv_full[s], (j >> 1) & 1);
+                tc::fence_proxy_async();   // cp.async (generic proxy) -> tcgen05 (async proxy)
                 tc::fence_after();
                 const uint32_t sK = tc::smem_u32(smem + L::kK + s * L::kTile);
 #pragma unroll
@@ -156,6 +153,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
                 tc::commit(&s_full[s]);
             };
             tc::mbar_wait(q_full, 0);
+            tc::fence_proxy_async();
             tc::fence_after();
             issue_s(0);
             for (int j = 0; j < nkb; ++j) {
@@ -328,6 +326,8 @@ __device__ __forceinline__ uint32_t toff(int row, int chunk) {
 }
 
 constexpr int TB = 64;    // secondary tile (keys in dq, queries in dkv)
+constexpr int kDqStages = 4;    // K/V ring depth of the dq kernel
+constexpr int kDkvStages = 3;   // Q/dO ring depth of the dk/dv kernel
 
 template <int HD>
 struct DqSmem {
@@ -335,9 +335,9 @@ struct DqSmem {
     static constexpr int kSmall = TB * HD * 2;      // K / V tiles
     static constexpr int kQ = 0;
     static constexpr int kO = kQ + kBig;
-    static constexpr int kK = kO + kBig;            // 3 stages
-    static constexpr int kV = kK + 3 * kSmall;      // 3 stages
-    static constexpr int kS = kV + 3 * kSmall;      // dS [128 x 64] bf16 x 2
+    static constexpr int kK = kO + kBig;                    // kDqStages stages
+    static constexpr int kV = kK + kDqStages * kSmall;
+    static constexpr int kS = kV + kDqStages * kSmall;      // dS [128 x 64] bf16 x 2
     static constexpr int kBar = kS + 2 * 128 * TB * 2;
     static constexpr int kBytes = kBar + 24 * 8 + 16;
     static constexpr int kAlloc = kBytes + 1024;
@@ -351,12 +351,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
     uint64_t* q_full = bar + 0;
-    uint64_t* kv_full = bar + 1;     // [3]
-    uint64_t* kv_empty = bar + 4;    // [3]
-    uint64_t* s_full = bar + 7;      // [2]
-    uint64_t* p_full = bar + 9;      // [2]
-    uint64_t* dq_done = bar + 11;    // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
+    uint64_t* kv_full = bar + 1;                      // [kDqStages]
+    uint64_t* kv_empty = kv_full + kDqStages;         // [kDqStages]
+    uint64_t* s_full = kv_empty + kDqStages;          // [2]
+    uint64_t* p_full = s_full + 2;                    // [2]
+    uint64_t* dq_done = p_full + 2;                   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 2);
 
     const AttnWork w = a.qwork128[blockIdx.x];
     const AttnSeg sg = a.segs[w.seg];
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
 
     if (threadIdx.x == 0) {
         tc::mbar_init(q_full, kLoadThreads);
-        for (int s = 0; s < 3; ++s) {
+        for (int s = 0; s < kDqStages; ++s) {
             tc::mbar_init(&kv_full[s], kLoadThreads);
             tc::mbar_init(&kv_empty[s], 1);
         }
@@ -401,15 +401,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
             tc::cp_async16_zfill(smem + L::kQ + toff<128>(r, c), ok ? qb + r * qs + c * 8 : qb, ok);
             tc::cp_async16_zfill(smem + L::kO + toff<128>(r, c), ok ? ob + r * qs + c * 8 : ob, ok);
         }
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        tc::fence_proxy_async();
-        tc::mbar_arrive(q_full);
+        tc::cp_async_arrive(q_full);
         const long long kvs = static_cast<long long>(a.Hkv) * HD;
         const bf16* kb = static_cast<const bf16*>(sg.k) + a.layer * sg.kv_layer_stride + kvh * HD;
         const bf16* vb = static_cast<const bf16*>(sg.v) + a.layer * sg.kv_layer_stride + kvh * HD;
         for (int j = 0; j < nkb; ++j) {
-            const int st = j % 3;
-            tc::mbar_wait(&kv_empty[st], ((j / 3) & 1) ^ 1);
+            const int st = j % kDqStages;
+            tc::mbar_wait(&kv_empty[st], ((j / kDqStages) & 1) ^ 1);
             const int key0 = j * TB;
             uint8_t* sk = smem + L::kK + st * L::kSmall;
             uint8_t* sv = smem + L::kV + st * L::kSmall;
@@ -420,9 +418,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
                 tc::cp_async16_zfill(sk + toff<TB>(r, c), ok ? kb + off : kb, ok);
                 tc::cp_async16_zfill(sv + toff<TB>(r, c), ok ? vb + off : vb, ok);
             }
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            tc::fence_proxy_async();
-            tc::mbar_arrive(&kv_full[st]);
+            tc::cp_async_arrive(&kv_full[st]);
         }
     } else if (warp == 4) {
         if (lane == 0) {
@@ -431,7 +427,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
             const uint32_t sQ = tc::smem_u32(smem + L::kQ);
             const uint32_t sO = tc::smem_u32(smem + L::kO);
             auto grad = [&](int j) {   // dQ += dS(j) K(j)
-                const int b = j & 1, st = j % 3;
+                const int b = j & 1, st = j % kDqStages;
                 tc::mbar_wait(&p_full[b], (j >> 1) & 1);
                 tc::fence_after();
                 const uint32_t sS = tc::smem_u32(smem + L::kS + b * 128 * TB * 2);
@@ -445,8 +441,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
             };
             tc::mbar_wait(q_full, 0);
             for (int j = 0; j < nkb; ++j) {
-                const int b = j & 1, st = j % 3;
-                tc::mbar_wait(&kv_full[st], (j / 3) & 1);
+                const int b = j & 1, st = j % kDqStages;
+                tc::mbar_wait(&kv_full[st], (j / kDqStages) & 1);
+                tc::fence_proxy_async();
                 tc::fence_after();
                 const uint32_t sK = tc::smem_u32(smem + L::kK + st * L::kSmall);
                 const uint32_t sV = tc::smem_u32(smem + L::kV + st * L::kSmall);
@@ -539,13 +536,13 @@ struct DkvSmem {
     static constexpr int kSmall = TB * HD * 2;      // Q / dO tiles
     static constexpr int kK = 0;
     static constexpr int kV = kK + kBig;
-    static constexpr int kQ = kV + kBig;            // 2 stages
-    static constexpr int kO = kQ + 2 * kSmall;      // 2 stages
-    static constexpr int kP = kO + 2 * kSmall;      // P^T [128 x 64] bf16 x 2
-    static constexpr int kS = kP + 2 * 128 * TB * 2;  // dS^T x 2
-    static constexpr int kLse = kS + 2 * 128 * TB * 2;   // [2][64] floats
-    static constexpr int kDelta = kLse + 2 * TB * 4;
-    static constexpr int kBar = kDelta + 2 * TB * 4;
+    static constexpr int kQ = kV + kBig;                     // kDkvStages stages
+    static constexpr int kO = kQ + kDkvStages * kSmall;
+    static constexpr int kP = kO + kDkvStages * kSmall;      // P^T [128 x 64] bf16 x 2
+    static constexpr int kS = kP + 2 * 128 * TB * 2;         // dS^T x 2
+    static constexpr int kLse = kS + 2 * 128 * TB * 2;       // [kDkvStages][64] floats
+    static constexpr int kDelta = kLse + kDkvStages * TB * 4;
+    static constexpr int kBar = kDelta + kDkvStages * TB * 4;
     static constexpr int kBytes = kBar + 24 * 8 + 16;
     static constexpr int kAlloc = kBytes + 1024;
 };
@@ -558,12 +555,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
     uint64_t* kv_full = bar + 0;
-    uint64_t* qd_full = bar + 1;     // [2]
-    uint64_t* qd_empty = bar + 3;    // [2]
-    uint64_t* s_full = bar + 5;      // [2]
-    uint64_t* p_full = bar + 7;      // [2]
-    uint64_t* pd_free = bar + 9;     // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
+    uint64_t* qd_full = bar + 1;                      // [kDkvStages]
+    uint64_t* qd_empty = qd_full + kDkvStages;        // [kDkvStages]
+    uint64_t* s_full = qd_empty + kDkvStages;         // [2]
+    uint64_t* p_full = s_full + 2;                    // [2]
+    uint64_t* pd_free = p_full + 2;                   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pd_free + 2);
     float* sLse = reinterpret_cast<float*>(smem + L::kLse);
     float* sDelta = reinterpret_cast<float*>(smem + L::kDelta);
 
@@ -582,9 +579,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
 
     if (threadIdx.x == 0) {
         tc::mbar_init(kv_full, kLoadThreads);
+        for (int st = 0; st < kDkvStages; ++st) {
+            tc::mbar_init(&qd_full[st], kLoadThreads);
+            tc::mbar_init(&qd_empty[st], 1);
+        }
         for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&qd_full[b], kLoadThreads);
-            tc::mbar_init(&qd_empty[b], 1);
             tc::mbar_init(&s_full[b], 1);
             tc::mbar_init(&p_full[b], TQ);
             tc::mbar_init(&pd_free[b], 1);
@@ -610,13 +609,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
             tc::cp_async16_zfill(smem + L::kK + toff<128>(r, c), ok ? kb + r * kvs + c * 8 : kb, ok);
             tc::cp_async16_zfill(smem + L::kV + toff<128>(r, c), ok ? vb + r * kvs + c * 8 : vb, ok);
         }
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        tc::fence_proxy_async();
-        tc::mbar_arrive(kv_full);
+        tc::cp_async_arrive(kv_full);
         const long long qs = static_cast<long long>(a.H) * HD;
         for (int it = 0; it < iters; ++it) {
-            const int st = it & 1;
-            tc::mbar_wait(&qd_empty[st], ((it >> 1) & 1) ^ 1);
+            const int st = it % kDkvStages;
+            tc::mbar_wait(&qd_empty[st], ((it / kDkvStages) & 1) ^ 1);
             const int hq = kvh * group + it / per_head;
             const int q0 = (qb_first + it % per_head) * TB;
             const int rows = min(TB, sg.q_len - q0);
@@ -631,14 +628,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
                 tc::cp_async16_zfill(sq + toff<TB>(r, c), ok ? qb_ + r * qs + c * 8 : qb_, ok);
                 tc::cp_async16_zfill(so + toff<TB>(r, c), ok ? ob_ + r * qs + c * 8 : ob_, ok);
             }
+            // lse / delta through cp.async as well, so the same async arrive
+            // publishes them (rows past the end read 0; they are masked).
+            const float* lg = a.lse + static_cast<long long>(hq) * a.T + row0;
+            const float* dg = a.delta + static_cast<long long>(hq) * a.T + row0;
             for (int i = lt; i < TB; i += kLoadThreads) {
                 const bool ok = i < rows;
-                sLse[st * TB + i] = ok ? a.lse[static_cast<long long>(hq) * a.T + row0 + i] : INFINITY;
-                sDelta[st * TB + i] = ok ? a.delta[static_cast<long long>(hq) * a.T + row0 + i] : 0.f;
+                tc::cp_async4_zfill(sLse + st * TB + i, ok ? lg + i : lg, ok);
+                tc::cp_async4_zfill(sDelta + st * TB + i, ok ? dg + i : dg, ok);
             }
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            tc::fence_proxy_async();
-            tc::mbar_arrive(&qd_full[st]);
+            tc::cp_async_arrive(&qd_full[st]);
         }
     } else if (warp == 4) {
         if (lane == 0) {
@@ -647,13 +646,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
             const uint32_t sK = tc::smem_u32(smem + L::kK);
             const uint32_t sV = tc::smem_u32(smem + L::kV);
             auto grad = [&](int it) {   // dV += P^T dO ; dK += dS^T Q
-                const int b = it & 1;
+                const int b = it & 1, st = it % kDkvStages;
                 tc::mbar_wait(&p_full[b], (it >> 1) & 1);
                 tc::fence_after();
                 const uint32_t sP = tc::smem_u32(smem + L::kP + b * 128 * TB * 2);
                 const uint32_t sS = tc::smem_u32(smem + L::kS + b * 128 * TB * 2);
-                const uint32_t sQ = tc::smem_u32(smem + L::kQ + b * L::kSmall);
-                const uint32_t sO = tc::smem_u32(smem + L::kO + b * L::kSmall);
+                const uint32_t sQ = tc::smem_u32(smem + L::kQ + st * L::kSmall);
+                const uint32_t sO = tc::smem_u32(smem + L::kO + st * L::kSmall);
 #pragma unroll
                 for (int kk = 0; kk < TB / 16; ++kk) {
                     tc::mma_bf16(tmem + kColV, tc::smem_desc(sP + kk * 32, 16, 1024),
@@ -661,16 +660,17 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
                     tc::mma_bf16(tmem + kColK, tc::smem_desc(sS + kk * 32, 16, 1024),
                                  tc::smem_desc(sQ + kk * 2048, TB * 128, 1024), idD, (it | kk) != 0);
                 }
-                tc::commit(&qd_empty[b]);
+                tc::commit(&qd_empty[st]);
                 tc::commit(&pd_free[b]);
             };
             tc::mbar_wait(kv_full, 0);
             for (int it = 0; it < iters; ++it) {
-                const int b = it & 1;
-                tc::mbar_wait(&qd_full[b], (it >> 1) & 1);
+                const int b = it & 1, st = it % kDkvStages;
+                tc::mbar_wait(&qd_full[st], (it / kDkvStages) & 1);
+                tc::fence_proxy_async();
                 tc::fence_after();
-                const uint32_t sQ = tc::smem_u32(smem + L::kQ + b * L::kSmall);
-                const uint32_t sO = tc::smem_u32(smem + L::kO + b * L::kSmall);
+                const uint32_t sQ = tc::smem_u32(smem + L::kQ + st * L::kSmall);
+                const uint32_t sO = tc::smem_u32(smem + L::kO + st * L::kSmall);
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
                     const uint32_t aoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
@@ -699,8 +699,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
             const bool need_mask = (k0 + TK - 1 > first_q) || rows < TB;
             tc::mbar_wait(&s_full[b], (it >> 1) & 1);
             tc::fence_after();
-            const float* lse_s = sLse + b * TB;
-            const float* dl_s = sDelta + b * TB;
+            const float* lse_s = sLse + (it % kDkvStages) * TB;
+            const float* dl_s = sDelta + (it % kDkvStages) * TB;
             uint32_t pk[32], dk[32];
 #pragma unroll
             for (int c = 0; c < TB / 32; ++c) {

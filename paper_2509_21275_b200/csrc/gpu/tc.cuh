@@ -155,6 +155,19 @@ __host__ __device__ constexpr uint32_t instr_desc_mn(int m, int n, bool a_mn, bo
            (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
 }
 
+// Arrive on `bar` once all of this thread's prior cp.async copies have landed
+// (the barrier's expected count includes this arrival; .noinc).
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// cp.async 4 B with zero fill when !valid.
+__device__ __forceinline__ void cp_async4_zfill(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(valid ? 4 : 0)
+                 : "memory");
+}
+
 // cp.async 16 B with zero fill when !valid.
 __device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, bool valid) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
