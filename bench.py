@@ -214,7 +214,10 @@ def run_ours(args):
     tokens = sum(sum(plans[i].lengths) for i in timed)
     flops = sum(step_flops(m, plans[i]) for i in timed)
     prof = {}
-    for cls, name in ((0, "gemm"), (1, "attn_fwd"), (2, "attn_bwd"), (3, "attn_bwd_dq"), (4, "attn_bwd_dkv")):
+    classes = ((0, "gemm"), (1, "attn_fwd"), (2, "attn_bwd"), (3, "attn_bwd_dq"), (4, "attn_bwd_dkv"),
+               (5, "norm_fwd"), (6, "norm_bwd"), (7, "rope"), (8, "act"), (9, "cross_entropy"),
+               (10, "adamw"), (11, "embed"), (12, "copy_fill"))
+    for cls, name in classes:
         a, b, c = (ctypes_double(), ctypes_double(), ctypes_i64())
         gpu.check(lib.epp_gpu_profile_read(cls, ctypes_ref(a), ctypes_ref(b), ctypes_ref(c), 1))
         prof[name] = {"ms": a.value, "flops": b.value, "launches": c.value}
@@ -307,9 +310,13 @@ def run_ours(args):
                      "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
                      "share_of_step": g["ms"] / ms if ms else None},
         "kernel_classes": {k: {"ms_per_step": v["ms"] / args.steps,
-                               "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] else 0.0,
+                               ("tflops" if k.startswith(("gemm", "attn")) else "gbs"):
+                                   ((v["flops"] / (v["ms"] / 1e3) / 1e12) if k.startswith(("gemm", "attn"))
+                                    else (v["flops"] / (v["ms"] / 1e3) / 1e9)) if v["ms"] else 0.0,
                                "launches_per_step": v["launches"] / args.steps}
                            for k, v in prof.items()},
+        "unattributed_ms_per_step": (ms - sum(v["ms"] for k, v in prof.items()
+                                               if k not in ("attn_bwd_dq", "attn_bwd_dkv"))) / args.steps,
         "clocks": clk.summary(),
         "e2e": e2e,
     }

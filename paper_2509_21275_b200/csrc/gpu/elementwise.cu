@@ -5,6 +5,7 @@
 // (16-byte accesses), one CTA per row where a row reduction is needed.
 #include "common.cuh"
 #include "kernels.h"
+#include "profile.h"
 
 namespace eppk {
 
@@ -130,71 +131,75 @@ __global__ void norm_apply_k(bool rms, const T* x, const T* w, const T* b, const
     }
 }
 
-constexpr int kNormRows = 16;     // rows per CTA in the backward (dw/db partials)
-constexpr int kNormMaxG = 8;      // vec8 groups per thread -> D <= 8192 at 128 threads
+constexpr int kNormRowBlock = 64;    // rows per dγ/dβ partial
+constexpr int kNormMaxG = 8;         // D <= 8192 (checked by the launcher)
 
+// dx = dres + rstd * (dy*w - mean(dy*w) - xhat * mean(dy*w*xhat)): one warp per
+// row, two sweeps over the row (the second re-reads from L1/L2), warp
+// shuffles only — no shared memory, no block barriers.
 template <typename T>
-__global__ void norm_bwd_k(bool rms, const T* x, const T* w, const T* dy, const float* mean,
-                           const float* rstd, const T* dres, T* dx, float* pw, float* pb,
-                           int Tn, int D) {
-    __shared__ float scratch[32];
-    float aw[kNormMaxG][8], ab[kNormMaxG][8];
+__global__ void __launch_bounds__(256) norm_bwd_dx_k(bool rms, const T* x, const T* w, const T* dy,
+                                                     const float* mean, const float* rstd,
+                                                     const T* dres, T* dx, int Tn, int D) {
+    const int lane = threadIdx.x & 31;
+    const long long row = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (row >= Tn) return;
+    const long long off = row * D;
+    const float mu = rms ? 0.f : mean[row];
+    const float rs = rstd[row];
+    float s1 = 0.f, s2 = 0.f;
+    for (int c = lane * 8; c < D; c += 256) {
+        float xv[8], wv[8], gv[8];
+        load8(x + off + c, xv);
+        load8(w + c, wv);
+        load8(dy + off + c, gv);
 #pragma unroll
-    for (int g = 0; g < kNormMaxG; ++g)
+        for (int i = 0; i < 8; ++i) {
+            const float dxh = gv[i] * wv[i];
+            s1 += dxh;
+            s2 += dxh * (xv[i] - mu) * rs;
+        }
+    }
+    const float m1 = rms ? 0.f : warp_sum(s1) / D;
+    const float m2 = warp_sum(s2) / D;
+    for (int c = lane * 8; c < D; c += 256) {
+        float xv[8], wv[8], gv[8], out[8], rv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        load8(x + off + c, xv);
+        load8(w + c, wv);
+        load8(dy + off + c, gv);
+        if (dres) load8(dres + off + c, rv);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) aw[g][i] = ab[g][i] = 0.f;
-    const int r0 = blockIdx.x * kNormRows;
-    for (int r = r0; r < min(Tn, r0 + kNormRows); ++r) {
-        const long long off = static_cast<long long>(r) * D;
+        for (int i = 0; i < 8; ++i) out[i] = rv[i] + rs * (gv[i] * wv[i] - m1 - (xv[i] - mu) * rs * m2);
+        store8(dx + off + c, out);
+    }
+}
+
+// Partial dγ/dβ over a block of kNormRowBlock rows; threads own 8
+// consecutive columns, so every load is a coalesced 16-byte access.
+template <typename T>
+__global__ void __launch_bounds__(256) norm_bwd_dw_k(bool rms, const T* x, const T* dy,
+                                                     const float* mean, const float* rstd,
+                                                     float* pw, float* pb, int Tn, int D) {
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (c >= D) return;
+    const int r0 = blockIdx.y * kNormRowBlock;
+    const int r1 = min(Tn, r0 + kNormRowBlock);
+    float aw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ab[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int r = r0; r < r1; ++r) {
+        const long long off = static_cast<long long>(r) * D + c;
         const float mu = rms ? 0.f : mean[r];
         const float rs = rstd[r];
-        float s1 = 0.f, s2 = 0.f;   // sum(dxhat), sum(dxhat * xhat)
+        float xv[8], gv[8];
+        load8(x + off, xv);
+        load8(dy + off, gv);
 #pragma unroll
-        for (int g = 0; g < kNormMaxG; ++g) {
-            const int c = (g * blockDim.x + threadIdx.x) * 8;
-            if (c >= D) break;
-            float xv[8], wv[8], gv[8];
-            load8(x + off + c, xv);
-            load8(w + c, wv);
-            load8(dy + off + c, gv);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float xh = (xv[i] - mu) * rs;
-                const float dxh = gv[i] * wv[i];
-                s1 += dxh;
-                s2 += dxh * xh;
-                aw[g][i] += gv[i] * xh;
-                ab[g][i] += gv[i];
-            }
-        }
-        const float m1 = rms ? 0.f : block_sum(s1, scratch) / D;
-        const float m2 = block_sum(s2, scratch) / D;
-#pragma unroll
-        for (int g = 0; g < kNormMaxG; ++g) {
-            const int c = (g * blockDim.x + threadIdx.x) * 8;
-            if (c >= D) break;
-            float xv[8], wv[8], gv[8], out[8], rv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            load8(x + off + c, xv);
-            load8(w + c, wv);
-            load8(dy + off + c, gv);
-            if (dres) load8(dres + off + c, rv);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float xh = (xv[i] - mu) * rs;
-                out[i] = rv[i] + rs * (gv[i] * wv[i] - m1 - xh * m2);
-            }
-            store8(dx + off + c, out);
+        for (int i = 0; i < 8; ++i) {
+            aw[i] += gv[i] * (xv[i] - mu) * rs;
+            ab[i] += gv[i];
         }
     }
-    float* prow_w = pw + static_cast<long long>(blockIdx.x) * D;
-    float* prow_b = pb ? pb + static_cast<long long>(blockIdx.x) * D : nullptr;
-#pragma unroll
-    for (int g = 0; g < kNormMaxG; ++g) {
-        const int c = (g * blockDim.x + threadIdx.x) * 8;
-        if (c >= D) break;
-        store8(prow_w + c, aw[g]);
-        if (prow_b) store8(prow_b + c, ab[g]);
-    }
+    store8(pw + static_cast<long long>(blockIdx.y) * D + c, aw);
+    if (pb) store8(pb + static_cast<long long>(blockIdx.y) * D + c, ab);
 }
 
 // dst[c] += sum_g part[g, c]  (deterministic column reduction)
@@ -226,41 +231,51 @@ __global__ void rope_table_k(float2* cs, int max_pos, int half, double theta) {
     cs[i] = make_float2(static_cast<float>(c), static_cast<float>(s));
 }
 
+// One thread = 8 consecutive rotation pairs (j .. j+7) of one head slot of
+// one token: two 16-byte loads (x1, x2 halves), 8 table entries, two
+// 16-byte stores.  Requires hd % 16 == 0.
 template <typename T>
 __global__ void rope_scatter_k(const T* qkv, T* q_out, const AttnSeg* segs, const int* tok_seg,
                                const int* tok_pos, const float2* cs, int Tn, int H, int Hkv,
                                int hd, int layer) {
     const int half = hd / 2;
+    const int per_slot = half / 8;
     const int slots = H + 2 * Hkv;
     const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= static_cast<long long>(Tn) * slots * half) return;
-    const int j = static_cast<int>(idx % half);
-    const int slot = static_cast<int>((idx / half) % slots);
-    const long long t = idx / (static_cast<long long>(half) * slots);
+    if (idx >= static_cast<long long>(Tn) * slots * per_slot) return;
+    const int j = static_cast<int>(idx % per_slot) * 8;
+    const int slot = static_cast<int>((idx / per_slot) % slots);
+    const long long t = idx / (static_cast<long long>(per_slot) * slots);
     const T* src = qkv + t * slots * hd + static_cast<long long>(slot) * hd;
     const int pos = tok_pos[t];
-    const AttnSeg& sg = segs[tok_seg[t]];
-    const long long kvrow = static_cast<long long>(pos) * Hkv * hd;
-    float x1 = to_f(src[j]), x2 = to_f(src[j + half]);
+    float x1[8], x2[8];
+    load8(src + j, x1);
+    load8(src + j + half, x2);
     if (slot < H + Hkv) {
-        const float2 c = cs[static_cast<long long>(pos) * half + j];
-        const float y1 = x1 * c.x - x2 * c.y;
-        const float y2 = x2 * c.x + x1 * c.y;
-        x1 = y1;
-        x2 = y2;
+        const float4* c4 = reinterpret_cast<const float4*>(cs + static_cast<long long>(pos) * half + j);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float4 cc = c4[k];     // (cos, sin) of pairs 2k, 2k+1
+            const float a1 = x1[2 * k] * cc.x - x2[2 * k] * cc.y;
+            const float a2 = x2[2 * k] * cc.x + x1[2 * k] * cc.y;
+            const float b1 = x1[2 * k + 1] * cc.z - x2[2 * k + 1] * cc.w;
+            const float b2 = x2[2 * k + 1] * cc.z + x1[2 * k + 1] * cc.w;
+            x1[2 * k] = a1; x2[2 * k] = a2; x1[2 * k + 1] = b1; x2[2 * k + 1] = b2;
+        }
     }
     T* dst;
     if (slot < H) {
         dst = q_out + (t * H + slot) * hd;
-    } else if (slot < H + Hkv) {
-        dst = const_cast<T*>(static_cast<const T*>(sg.k)) + layer * sg.kv_layer_stride + kvrow +
-              static_cast<long long>(slot - H) * hd;
     } else {
-        dst = const_cast<T*>(static_cast<const T*>(sg.v)) + layer * sg.kv_layer_stride + kvrow +
-              static_cast<long long>(slot - H - Hkv) * hd;
+        const AttnSeg& sg = segs[tok_seg[t]];
+        const long long kvrow = static_cast<long long>(pos) * Hkv * hd;
+        const bool is_k = slot < H + Hkv;
+        const void* base = is_k ? sg.k : sg.v;
+        dst = const_cast<T*>(static_cast<const T*>(base)) + layer * sg.kv_layer_stride + kvrow +
+              static_cast<long long>(slot - H - (is_k ? 0 : Hkv)) * hd;
     }
-    dst[j] = from_f<T>(x1);
-    dst[j + half] = from_f<T>(x2);
+    store8(dst + j, x1);
+    store8(dst + j + half, x2);
 }
 
 template <typename T>
@@ -268,34 +283,42 @@ __global__ void rope_gather_grad_k(const float* dq, const AttnSeg* segs, const i
                                    const int* tok_pos, const float2* cs, T* dqkv, int Tn, int H,
                                    int Hkv, int hd, int layer) {
     const int half = hd / 2;
+    const int per_slot = half / 8;
     const int slots = H + 2 * Hkv;
     const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= static_cast<long long>(Tn) * slots * half) return;
-    const int j = static_cast<int>(idx % half);
-    const int slot = static_cast<int>((idx / half) % slots);
-    const long long t = idx / (static_cast<long long>(half) * slots);
+    if (idx >= static_cast<long long>(Tn) * slots * per_slot) return;
+    const int j = static_cast<int>(idx % per_slot) * 8;
+    const int slot = static_cast<int>((idx / per_slot) % slots);
+    const long long t = idx / (static_cast<long long>(per_slot) * slots);
     const int pos = tok_pos[t];
-    const AttnSeg& sg = segs[tok_seg[t]];
-    const long long kvrow = static_cast<long long>(pos) * Hkv * hd;
     const float* src;
-    if (slot < H)
+    if (slot < H) {
         src = dq + (t * H + slot) * hd;
-    else if (slot < H + Hkv)
-        src = sg.dk + layer * sg.dkv_layer_stride + kvrow + static_cast<long long>(slot - H) * hd;
-    else
-        src = sg.dv + layer * sg.dkv_layer_stride + kvrow +
-              static_cast<long long>(slot - H - Hkv) * hd;
-    float g1 = src[j], g2 = src[j + half];
+    } else {
+        const AttnSeg& sg = segs[tok_seg[t]];
+        const long long kvrow = static_cast<long long>(pos) * Hkv * hd;
+        src = (slot < H + Hkv ? sg.dk + static_cast<long long>(slot - H) * hd
+                              : sg.dv + static_cast<long long>(slot - H - Hkv) * hd) +
+              layer * sg.dkv_layer_stride + kvrow;
+    }
+    float g1[8], g2[8];
+    load8(src + j, g1);
+    load8(src + j + half, g2);
     if (slot < H + Hkv) {
-        const float2 c = cs[static_cast<long long>(pos) * half + j];
-        const float y1 = g1 * c.x + g2 * c.y;
-        const float y2 = g2 * c.x - g1 * c.y;
-        g1 = y1;
-        g2 = y2;
+        const float4* c4 = reinterpret_cast<const float4*>(cs + static_cast<long long>(pos) * half + j);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float4 cc = c4[k];
+            const float a1 = g1[2 * k] * cc.x + g2[2 * k] * cc.y;
+            const float a2 = g2[2 * k] * cc.x - g1[2 * k] * cc.y;
+            const float b1 = g1[2 * k + 1] * cc.z + g2[2 * k + 1] * cc.w;
+            const float b2 = g2[2 * k + 1] * cc.z - g1[2 * k + 1] * cc.w;
+            g1[2 * k] = a1; g2[2 * k] = a2; g1[2 * k + 1] = b1; g2[2 * k + 1] = b2;
+        }
     }
     T* dst = dqkv + t * slots * hd + static_cast<long long>(slot) * hd;
-    dst[j] = from_f<T>(g1);
-    dst[j + half] = from_f<T>(g2);
+    store8(dst + j, g1);
+    store8(dst + j + half, g2);
 }
 
 // ------------------------------------------------------------ activation ---
@@ -529,6 +552,7 @@ int norm_threads(int D) {
 // =========================================================================
 void embed_fwd(DType t, const int32_t* ids, const void* table, void* out, int T, int D,
                cudaStream_t s) {
+    ProfScope prof_(kProfEmbed, 0, s);
     if (T == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
@@ -540,6 +564,7 @@ void embed_fwd(DType t, const int32_t* ids, const void* table, void* out, int T,
 
 void embed_bwd(DType t, const int32_t* ids, const void* dout, float* dtable, int T, int D,
                cudaStream_t s) {
+    ProfScope prof_(kProfEmbed, 0, s);
     if (T == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
@@ -550,6 +575,7 @@ void embed_bwd(DType t, const int32_t* ids, const void* dout, float* dtable, int
 
 void norm_fwd(DType t, bool rms, const void* x, const void* w, const void* b, void* y, float* mean,
               float* rstd, int T, int D, float eps, cudaStream_t s) {
+    ProfScope prof_(kProfNormFwd, double(T) * D * 2 * dtype_size(t), s);
     EPP_REQUIRE(D % 8 == 0, "norm: D must be a multiple of 8");
     if (T == 0) return;
     dispatch_t(t, [&](auto z) {
@@ -564,6 +590,7 @@ void norm_fwd(DType t, bool rms, const void* x, const void* w, const void* b, vo
 
 void norm_apply(DType t, bool rms, const void* x, const void* w, const void* b, const float* mean,
                 const float* rstd, void* y, int T, int D, cudaStream_t s) {
+    ProfScope prof_(kProfNormFwd, double(T) * D * 2 * dtype_size(t), s);
     if (T == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
@@ -578,20 +605,24 @@ void norm_apply(DType t, bool rms, const void* x, const void* w, const void* b, 
 void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy, const float* mean,
               const float* rstd, const void* dres, void* dx, float* dw, float* db, int T, int D,
               cudaStream_t s) {
-    EPP_REQUIRE(D % 8 == 0 && D <= 8 * 128 * kNormMaxG, "norm_bwd: unsupported D");
+    ProfScope prof_(kProfNormBwd, double(T) * D * 6 * dtype_size(t), s);
+    EPP_REQUIRE(D % 8 == 0 && D <= 8 * 256 * kNormMaxG, "norm_bwd: unsupported D");
     if (T == 0) return;
-    const int G = ceil_div(T, kNormRows);
+    const int G = ceil_div(T, kNormRowBlock);
     float* part = nullptr;
     EPP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * 2 * G * D, s));
     float* pw = part;
     float* pb = db ? part + static_cast<long long>(G) * D : nullptr;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        norm_bwd_k<E><<<G, norm_threads(D), 0, s>>>(
-            rms, static_cast<const E*>(x), static_cast<const E*>(w), static_cast<const E*>(dy),
-            mean, rstd, static_cast<const E*>(dres), static_cast<E*>(dx), pw, pb, T, D);
+        norm_bwd_dx_k<E><<<ceil_div(static_cast<long long>(T) * 32, 256), 256, 0, s>>>(
+            rms, static_cast<const E*>(x), static_cast<const E*>(w), static_cast<const E*>(dy), mean,
+            rstd, static_cast<const E*>(dres), static_cast<E*>(dx), T, D);
+        EPP_CHECK_LAUNCH();
+        norm_bwd_dw_k<E><<<dim3(ceil_div(D / 8, 256), G), 256, 0, s>>>(
+            rms, static_cast<const E*>(x), static_cast<const E*>(dy), mean, rstd, pw, pb, T, D);
+        EPP_CHECK_LAUNCH();
     });
-    EPP_CHECK_LAUNCH();
     col_reduce_add<<<ceil_div(D, 256), 256, 0, s>>>(pw, G, D, dw);
     if (db) col_reduce_add<<<ceil_div(D, 256), 256, 0, s>>>(pb, G, D, db);
     EPP_CHECK_LAUNCH();
@@ -601,11 +632,12 @@ void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy, c
 void rope_qkv_scatter(DType t, const void* qkv, void* q_out, const AttnSeg* segs_dev, int nseg,
                       const int* tok_seg, const int* tok_pos, int T, int H, int Hkv, int hd,
                       int layer, float theta, cudaStream_t s) {
+    ProfScope prof_(kProfRope, double(T) * (H + 2 * Hkv) * hd * 2 * dtype_size(t), s);
     (void)nseg;
     if (T == 0) return;
-    EPP_REQUIRE(hd % 2 == 0, "rope: head_dim must be even");
+    EPP_REQUIRE(hd % 16 == 0, "rope: head_dim must be a multiple of 16");
     const float2* cs = rope_table(0, hd, theta, s);
-    const long long n = static_cast<long long>(T) * (H + 2 * Hkv) * (hd / 2);
+    const long long n = static_cast<long long>(T) * (H + 2 * Hkv) * (hd / 16);
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
         rope_scatter_k<E><<<grid_for(n, 256), 256, 0, s>>>(static_cast<const E*>(qkv),
@@ -619,9 +651,10 @@ void rope_qkv_scatter(DType t, const void* qkv, void* q_out, const AttnSeg* segs
 void rope_qkv_gather_grad(DType t, const float* dq, const AttnSeg* segs_dev, const int* tok_seg,
                           const int* tok_pos, void* dqkv, int T, int H, int Hkv, int hd, int layer,
                           float theta, cudaStream_t s) {
+    ProfScope prof_(kProfRope, double(T) * (H + 2 * Hkv) * hd * (4 + dtype_size(t)), s);
     if (T == 0) return;
     const float2* cs = rope_table(0, hd, theta, s);
-    const long long n = static_cast<long long>(T) * (H + 2 * Hkv) * (hd / 2);
+    const long long n = static_cast<long long>(T) * (H + 2 * Hkv) * (hd / 16);
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
         rope_gather_grad_k<E><<<grid_for(n, 256), 256, 0, s>>>(dq, segs_dev, tok_seg, tok_pos, cs,
@@ -632,6 +665,7 @@ void rope_qkv_gather_grad(DType t, const float* dq, const AttnSeg* segs_dev, con
 }
 
 void act_fwd(DType t, int act, const void* h, void* a, int T, int F, cudaStream_t s) {
+    ProfScope prof_(kProfAct, double(T) * F * (act ? 3 : 2) * dtype_size(t), s);
     EPP_REQUIRE(F % 8 == 0, "act: F must be a multiple of 8");
     if (T == 0) return;
     const long long n8 = static_cast<long long>(T) * F / 8;
@@ -645,6 +679,7 @@ void act_fwd(DType t, int act, const void* h, void* a, int T, int F, cudaStream_
 
 void act_bwd(DType t, int act, const void* h, const void* da, void* dh, int T, int F,
              cudaStream_t s) {
+    ProfScope prof_(kProfAct, double(T) * F * (act ? 5 : 3) * dtype_size(t), s);
     if (T == 0) return;
     const long long n8 = static_cast<long long>(T) * F / 8;
     dispatch_t(t, [&](auto z) {
@@ -658,6 +693,7 @@ void act_bwd(DType t, int act, const void* h, const void* da, void* dh, int T, i
 
 void cross_entropy(DType t, void* logits, const int32_t* targets, float* loss_acc, int T, int V,
                    float grad_scale, cudaStream_t s) {
+    ProfScope prof_(kProfCe, double(T) * V * 2 * dtype_size(t), s);
     EPP_REQUIRE(V % 8 == 0, "ce: V must be a multiple of 8");
     if (T == 0) return;
     dispatch_t(t, [&](auto z) {
@@ -668,10 +704,12 @@ void cross_entropy(DType t, void* logits, const int32_t* targets, float* loss_ac
 }
 
 void fill_zero(void* p, size_t bytes, cudaStream_t s) {
+    ProfScope prof_(kProfCopy, double(bytes), s);
     if (bytes) EPP_CUDA(cudaMemsetAsync(p, 0, bytes, s));
 }
 
 void cast_f32_to(DType t, const float* src, void* dst, long long n, cudaStream_t s) {
+    ProfScope prof_(kProfCopy, 0, s);
     if (n == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
@@ -681,6 +719,7 @@ void cast_f32_to(DType t, const float* src, void* dst, long long n, cudaStream_t
 }
 
 void add_inplace(DType t, void* y, const void* x, long long n, cudaStream_t s) {
+    ProfScope prof_(kProfCopy, 0, s);
     if (n == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
@@ -692,6 +731,7 @@ void add_inplace(DType t, void* y, const void* x, long long n, cudaStream_t s) {
 void adamw(float* master, void* work, DType t, float* grad, float* m, float* v, long long n,
            float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
            cudaStream_t s) {
+    ProfScope prof_(kProfAdam, double(n) * (26 + dtype_size(t)), s);
     if (n == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);

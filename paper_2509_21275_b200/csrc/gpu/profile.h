@@ -3,7 +3,11 @@
 #include <cuda_runtime.h>
 
 namespace eppk {
-enum ProfClass { kProfGemm = 0, kProfAttnFwd = 1, kProfAttnBwd = 2, kProfAttnBwdDq = 3, kProfAttnBwdDkv = 4 };
+enum ProfClass {
+    kProfGemm = 0, kProfAttnFwd = 1, kProfAttnBwd = 2, kProfAttnBwdDq = 3, kProfAttnBwdDkv = 4,
+    kProfNormFwd = 5, kProfNormBwd = 6, kProfRope = 7, kProfAct = 8, kProfCe = 9, kProfAdam = 10,
+    kProfEmbed = 11, kProfCopy = 12,
+};
 bool profiling();
 // Records an event pair around the launches issued during its lifetime.
 class ProfScope {

@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "epp_gpu.h"
 #include "kernels.h"
+#include "profile.h"
 
 namespace eppk {
 
@@ -320,6 +321,7 @@ public:
                 embed_fwd(dt_, c.token_ids, work(emb_), cs.x_in.get(), cs.T, D_, s);
             } else {
                 EPP_REQUIRE(act_in != nullptr, "act_in is null");
+                ProfScope pc(kProfCopy, 2.0 * act_bytes, s);
                 EPP_CUDA(cudaMemcpyAsync(cs.x_in.get(), act_in, act_bytes, cudaMemcpyDeviceToDevice, s));
             }
             cs.layers.resize(nl_);
