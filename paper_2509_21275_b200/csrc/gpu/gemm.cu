@@ -14,6 +14,7 @@
 // conventions.
 #include <cuda.h>
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 
@@ -41,7 +42,7 @@ struct TcSmem {
     static constexpr int kBBytes = BN * kBK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kBarOffset = STAGES * kStageBytes;
-    static constexpr int kTotal = kBarOffset + (2 * STAGES + 1) * 8 + 16 + 1024;  // + align slack
+    static constexpr int kTotal = kBarOffset + (2 * STAGES + 4) * 8 + 16 + 1024;  // + align slack
 };
 
 struct TcParams {
@@ -50,6 +51,25 @@ struct TcParams {
     long long ldc;
     const bf16* R;
     long long ldr;
+};
+
+// Persistent CTAs (one per SM) walk the output tiles in a grouped raster
+// order; the TMA ring and the two TMEM accumulator buffers persist across
+// tiles, so the epilogue of tile i overlaps the mainloop of tile i+1.
+struct TileSched {
+    int tiles_m, tiles_n;
+    __device__ __forceinline__ void coords(int t, int& mb, int& nb) const {
+        // groups of 8 M-blocks: consecutive tiles share the same B column
+        // panel while sweeping a small set of A row panels (L2 reuse).
+        constexpr int G = 8;
+        const int per_group = G * tiles_n;
+        const int g = t / per_group;
+        const int first_m = g * G;
+        const int gm = min(G, tiles_m - first_m);
+        const int r = t % per_group;
+        mb = first_m + r % gm;
+        nb = r / gm;
+    }
 };
 
 template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
@@ -62,33 +82,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
     uint64_t* empty = full + STAGES;
-    uint64_t* acc_full = empty + STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+    uint64_t* acc_full = empty + STAGES;     // [2]
+    uint64_t* acc_empty = acc_full + 2;      // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * BN;
-    const int m0 = blockIdx.y * kBM;
     const int nk = (p.K + kBK - 1) / kBK;
+    const TileSched sched{(p.M + kBM - 1) / kBM, (p.N + BN - 1) / BN};
+    const int ntiles = sched.tiles_m * sched.tiles_n;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             tc::mbar_init(&full[s], 1);
             tc::mbar_init(&empty[s], 1);
         }
-        tc::mbar_init(acc_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&acc_full[b], 1);
+            tc::mbar_init(&acc_empty[b], 4);     // one arrive per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     }
-    constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         tc::smem_u32(tmem_slot)),
-                     "n"(kTmemCols)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
+    constexpr uint32_t kTmemCols = 2 * BN;     // double-buffered accumulator
+    if (warp == 1) tc::tmem_alloc(tmem_slot, kTmemCols);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
@@ -99,29 +117,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int kb = 0; kb < nk; ++kb) {
-                tc::mbar_wait(&empty[stage], phase ^ 1);
-                uint8_t* sa = smem + stage * L::kStageBytes;
-                uint8_t* sb = sa + L::kABytes;
-                tc::mbar_expect_tx(&full[stage], L::kStageBytes);
-                const int k0 = kb * kBK;
-                if (A_MN) {
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int mb, nb;
+                sched.coords(t, mb, nb);
+                const int m0 = mb * kBM, n0 = nb * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    tc::mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * L::kStageBytes;
+                    uint8_t* sb = sa + L::kABytes;
+                    tc::mbar_expect_tx(&full[stage], L::kStageBytes);
+                    const int k0 = kb * kBK;
+                    if (A_MN) {
 #pragma unroll
-                    for (int i = 0; i < kBM / 64; ++i)
-                        tc::tma_load_2d(sa + i * 8192, &map_a, &full[stage], m0 + 64 * i, k0);
-                } else {
-                    tc::tma_load_2d(sa, &map_a, &full[stage], k0, m0);
-                }
-                if (B_MN) {
+                        for (int i = 0; i < kBM / 64; ++i)
+                            tc::tma_load_2d(sa + i * 8192, &map_a, &full[stage], m0 + 64 * i, k0);
+                    } else {
+                        tc::tma_load_2d(sa, &map_a, &full[stage], k0, m0);
+                    }
+                    if (B_MN) {
 #pragma unroll
-                    for (int i = 0; i < BN / 64; ++i)
-                        tc::tma_load_2d(sb + i * 8192, &map_b, &full[stage], n0 + 64 * i, k0);
-                } else {
-                    tc::tma_load_2d(sb, &map_b, &full[stage], k0, n0);
-                }
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
+                        for (int i = 0; i < BN / 64; ++i)
+                            tc::tma_load_2d(sb + i * 8192, &map_b, &full[stage], n0 + 64 * i, k0);
+                    } else {
+                        tc::tma_load_2d(sb, &map_b, &full[stage], k0, n0);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
                 }
             }
         }
@@ -130,91 +153,107 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr uint32_t idesc = tc::instr_desc(BN, A_MN, B_MN);
         int stage = 0;
         uint32_t phase = 0;
-        for (int kb = 0; kb < nk; ++kb) {
-            tc::mbar_wait(&full[stage], phase);
+        int local = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            tc::mbar_wait(&acc_empty[acc], acc_phase ^ 1);     // epilogue drained this buffer
             tc::fence_after();
-            if (lane == 0) {
-                const uint32_t sa = tc::smem_u32(smem + stage * L::kStageBytes);
-                const uint32_t sb = sa + L::kABytes;
+            const uint32_t d = tmem + acc * BN;
+            for (int kb = 0; kb < nk; ++kb) {
+                tc::mbar_wait(&full[stage], phase);
+                tc::fence_after();
+                if (lane == 0) {
+                    const uint32_t sa = tc::smem_u32(smem + stage * L::kStageBytes);
+                    const uint32_t sb = sa + L::kABytes;
 #pragma unroll
-                for (int kk = 0; kk < kBK / 16; ++kk) {
-                    // K-major: advance 32 B inside the swizzle atom; SBO = 8 rows.
-                    // MN-major: advance 16 K-rows (2 atoms); LBO = 64-col block.
-                    const uint64_t ad = A_MN ? tc::smem_desc(sa + kk * 2048, 8192, 1024)
-                                             : tc::smem_desc(sa + kk * 32, 16, 1024);
-                    const uint64_t bd = B_MN ? tc::smem_desc(sb + kk * 2048, 8192, 1024)
-                                             : tc::smem_desc(sb + kk * 32, 16, 1024);
-                    tc::mma_bf16(tmem, ad, bd, idesc, (kb | kk) != 0);
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint64_t ad = A_MN ? tc::smem_desc(sa + kk * 2048, 8192, 1024)
+                                                 : tc::smem_desc(sa + kk * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? tc::smem_desc(sb + kk * 2048, 8192, 1024)
+                                                 : tc::smem_desc(sb + kk * 32, 16, 1024);
+                        tc::mma_bf16(d, ad, bd, idesc, (kb | kk) != 0);
+                    }
+                    tc::commit(&empty[stage]);
                 }
-                tc::commit(&empty[stage]);
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
             }
+            if (lane == 0) tc::commit(&acc_full[acc]);
             __syncwarp();
-            if (++stage == STAGES) {
-                stage = 0;
-                phase ^= 1;
-            }
         }
-        if (lane == 0) tc::commit(acc_full);
-        __syncwarp();
     } else {
         // ---------------- epilogue (warps 2..5) ----------------
         const int quarter = warp & 3;                  // TMEM lane quarter
-        const int row = m0 + quarter * 32 + lane;
-        if (nk > 0) tc::mbar_wait(acc_full, 0);
-        tc::fence_after();
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-            float v[32];
+        int local = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+            int mb, nb;
+            sched.coords(t, mb, nb);
+            const int row = mb * kBM + quarter * 32 + lane;
+            const int n0 = nb * BN;
+            const int acc = local & 1;
             if (nk > 0) {
-                tc::tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c, v);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                tc::mbar_wait(&acc_full[acc], (local >> 1) & 1);
+                tc::fence_after();
             }
-            const int col = n0 + c;
-            if (row >= p.M || col >= p.N) continue;
-            if (EPI == static_cast<int>(Epi::AccumF32) || EPI == static_cast<int>(Epi::StoreF32)) {
-                float* dst = static_cast<float*>(p.C) + static_cast<long long>(row) * p.ldc + col;
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                float v[32];
+                if (nk > 0) {
+                    tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16) + c, v);
+                } else {
 #pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                    float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                    if (EPI == static_cast<int>(Epi::AccumF32)) {
-                        const float4 old = *reinterpret_cast<const float4*>(dst + i);
-                        o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
-                    }
-                    *reinterpret_cast<float4*>(dst + i) = o;
+                    for (int i = 0; i < 32; ++i) v[i] = 0.f;
                 }
-            } else {
-                if (EPI == static_cast<int>(Epi::AddRes)) {
-                    const bf16* r = p.R + static_cast<long long>(row) * p.ldr + col;
+                const int col = n0 + c;
+                if (row >= p.M || col >= p.N) continue;
+                if (EPI == static_cast<int>(Epi::AccumF32) || EPI == static_cast<int>(Epi::StoreF32)) {
+                    float* dst = static_cast<float*>(p.C) + static_cast<long long>(row) * p.ldc + col;
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                        if (EPI == static_cast<int>(Epi::AccumF32)) {
+                            const float4 old = *reinterpret_cast<const float4*>(dst + i);
+                            o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+                        }
+                        *reinterpret_cast<float4*>(dst + i) = o;
+                    }
+                } else {
+                    if (EPI == static_cast<int>(Epi::AddRes)) {
+                        const bf16* r = p.R + static_cast<long long>(row) * p.ldr + col;
+#pragma unroll
+                        for (int i = 0; i < 32; i += 8) {
+                            const uint4 raw = *reinterpret_cast<const uint4*>(r + i);
+                            const bf16* rb = reinterpret_cast<const bf16*>(&raw);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) v[i + j] += __bfloat162float(rb[j]);
+                        }
+                    }
+                    bf16* dst = static_cast<bf16*>(p.C) + static_cast<long long>(row) * p.ldc + col;
 #pragma unroll
                     for (int i = 0; i < 32; i += 8) {
-                        const uint4 raw = *reinterpret_cast<const uint4*>(r + i);
-                        const bf16* rb = reinterpret_cast<const bf16*>(&raw);
+                        uint4 raw;
+                        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) v[i + j] += __bfloat162float(rb[j]);
+                        for (int j = 0; j < 4; ++j)
+                            h[j] = __floats2bfloat162_rn(v[i + 2 * j], v[i + 2 * j + 1]);
+                        *reinterpret_cast<uint4*>(dst + i) = raw;
                     }
                 }
-                bf16* dst = static_cast<bf16*>(p.C) + static_cast<long long>(row) * p.ldc + col;
-#pragma unroll
-                for (int i = 0; i < 32; i += 8) {
-                    uint4 raw;
-                    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        h[j] = __floats2bfloat162_rn(v[i + 2 * j], v[i + 2 * j + 1]);
-                    *reinterpret_cast<uint4*>(dst + i) = raw;
-                }
             }
+            // release the accumulator buffer to the MMA warp
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&acc_empty[acc]);
         }
-        tc::fence_before();
     }
     __syncthreads();
     if (warp == 1) {
         tc::fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                     "n"(kTmemCols)
-                     : "memory");
+        tc::tmem_dealloc(tmem, kTmemCols);
     }
 }
 
@@ -275,8 +314,14 @@ void launch_tc(const GemmArgs& g, cudaStream_t s) {
     const CUtensorMap mb = B_MN ? make_map(g.B, g.K, g.N, g.ldb, 64, kBK)
                                 : make_map(g.B, g.N, g.K, g.ldb, kBK, BN);
     TcParams p{g.M, g.N, g.K, g.C, g.ldc, static_cast<const bf16*>(g.R), g.ldr};
-    dim3 grid(ceil_div(g.N, BN), ceil_div(g.M, kBM));
-    kern<<<grid, kThreads, L::kTotal, s>>>(ma, mb, p);
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        EPP_CUDA(cudaGetDevice(&dev));
+        EPP_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int tiles = ceil_div(g.N, BN) * ceil_div(g.M, kBM);
+    kern<<<std::min(tiles, num_sms), kThreads, L::kTotal, s>>>(ma, mb, p);
     EPP_CHECK_LAUNCH();
     g_gemm_launches.fetch_add(1);
 }
