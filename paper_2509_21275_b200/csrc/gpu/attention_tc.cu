@@ -51,8 +51,8 @@ struct FwdSmem {
     static constexpr int kQ = 0;
     static constexpr int kK = kQ + kTile;           // 2 stages
     static constexpr int kV = kK + 2 * kTile;       // 2 stages
-    static constexpr int kP = kV + 2 * kTile;       // 128 x 128 bf16
-    static constexpr int kBar = kP + TQ * TK * 2;
+    static constexpr int kP = kV + 2 * kTile;       // 128 x 128 bf16, 2 buffers
+    static constexpr int kBar = kP + 2 * TQ * TK * 2;
     static constexpr int kBytes = kBar + 16 * 8 + 16;
     static constexpr int kAlloc = kBytes + 1024;
 };
@@ -69,8 +69,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
     uint64_t* kv_empty = bar + 3;    // [2]
     uint64_t* s_full = bar + 5;      // [2]
     uint64_t* p_full = bar + 7;
-    uint64_t* o_done = bar + 8;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+    uint64_t* o_done = bar + 8;      // [2]: PV of P buffer b completed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
 
     const AttnWork w = a.qwork128[blockIdx.x];
     const AttnSeg sg = a.segs[w.seg];
@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
             tc::mbar_init(&s_full[s], 1);
         }
         tc::mbar_init(p_full, TQ);
-        tc::mbar_init(o_done, 1);
+        tc::mbar_init(&o_done[0], 1);
+        tc::mbar_init(&o_done[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 4) tc::tmem_alloc(tmem_slot, 512);
@@ -137,7 +138,6 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
             constexpr uint32_t idS = tc::instr_desc_mn(TQ, TK, false, false);
             constexpr uint32_t idO = tc::instr_desc_mn(TQ, HD, false, true);
             const uint32_t sQ = tc::smem_u32(smem + L::kQ);
-            const uint32_t sP = tc::smem_u32(smem + L::kP);
             auto issue_s = [&](int j) {
                 const int s = j & 1;
                 tc::mbar_wait(&kv_full[s], (j >> 1) & 1);
@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
                 tc::fence_after();
                 const int s = j & 1;
                 const uint32_t sV = tc::smem_u32(smem + L::kV + s * L::kTile);
+                const uint32_t sP = tc::smem_u32(smem + L::kP + s * TQ * TK * 2);
 #pragma unroll
                 for (int kk = 0; kk < TK / 16; ++kk) {
                     const uint32_t aoff = (kk >> 2) * 16384 + (kk & 3) * 32;   // P: K-major
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
                                  tc::smem_desc(sV + kk * 2048, 16384, 1024),  // V: MN-major
                                  idO, (j | kk) != 0);
                 }
-                tc::commit(o_done);
+                tc::commit(&o_done[s]);
                 tc::commit(&kv_empty[s]);
             }
         }
@@ -182,7 +183,6 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
         const float c2 = a.scale * kLog2e;
         const int first_q = sg.kv_ctx + q0;   // smallest query position of the block
         float m_run = -INFINITY, l = 0.f;
-        uint8_t* sP = smem + L::kP;
         for (int j = 0; j < nkb; ++j) {
             const int s = j & 1;
             tc::mbar_wait(&s_full[s], (j >> 1) & 1);
@@ -206,12 +206,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
                 }
             }
             const float mt = mraw * c2;
-            if (j > 0) {
-                tc::mbar_wait(o_done, (j - 1) & 1);   // PV(j-1) done: O stable, P free
+            const bool grow = mt > m_run + kRescaleSlack || (m_run == -INFINITY && mt > -INFINITY);
+            const bool rescale = __any_sync(0xffffffffu, grow) && j > 0;
+            if (rescale) {
+                // O must be final up to tile j-1 before it is rescaled
+                tc::mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
                 tc::fence_after();
             }
-            const bool grow = mt > m_run + kRescaleSlack || (m_run == -INFINITY && mt > -INFINITY);
-            if (__any_sync(0xffffffffu, grow) && j > 0) {
+            // P buffer (j & 1) was last read by PV(j-2)
+            tc::mbar_wait(&o_done[j & 1], ((j >> 1) & 1) ^ 1);
+            tc::fence_after();
+            uint8_t* sP = smem + L::kP + (j & 1) * TQ * TK * 2;
+            if (rescale) {
                 const float alpha = grow ? ex2(m_run - mt) : 1.f;
 #pragma unroll 1
                 for (int c = 0; c < HD / 32; ++c) {
@@ -225,7 +231,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
             }
             if (grow) m_run = mt;
             const float mu = (m_run == -INFINITY) ? 0.f : m_run;
-            uint8_t* prow = sP;
+            uint8_t* prow = sP;   // this tile's P buffer
 #pragma unroll 1
             for (int c = 0; c < TK / 32; ++c) {
                 float v[32];
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
             tc::fence_before();
             tc::mbar_arrive(p_full);
         }
-        tc::mbar_wait(o_done, (nkb - 1) & 1);
+        tc::mbar_wait(&o_done[(nkb - 1) & 1], ((nkb - 1) >> 1) & 1);
         tc::fence_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
         bf16* orow = static_cast<bf16*>(a.o) + (static_cast<long long>(sg.q_start + q0 + r) * a.H + h) * HD;

@@ -322,16 +322,8 @@ __global__ void rope_gather_grad_k(const float* dq, const AttnSeg* segs, const i
 }
 
 // ------------------------------------------------------------ activation ---
-__device__ __forceinline__ float gelu_tanh(float x) {
-    const float k = 0.7978845608028654f;
-    return 0.5f * x * (1.f + tanhf(k * (x + 0.044715f * x * x * x)));
-}
-__device__ __forceinline__ float gelu_tanh_grad(float x) {
-    const float k = 0.7978845608028654f;
-    const float u = k * (x + 0.044715f * x * x * x);
-    const float t = tanhf(u);
-    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k * (1.f + 3.f * 0.044715f * x * x);
-}
+__device__ __forceinline__ float gelu_tanh(float x) { return gelu_tanh_f(x); }
+__device__ __forceinline__ float gelu_tanh_grad(float x) { return gelu_tanh_grad_f(x); }
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
 
 template <typename T>

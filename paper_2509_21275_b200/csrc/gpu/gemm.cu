@@ -51,6 +51,8 @@ struct TcParams {
     long long ldc;
     const bf16* R;
     long long ldr;
+    bf16* C2;
+    long long ldc2;
 };
 
 // Persistent CTAs (one per SM) walk the output tiles in a grouped raster
@@ -222,14 +224,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                         *reinterpret_cast<float4*>(dst + i) = o;
                     }
                 } else {
-                    if (EPI == static_cast<int>(Epi::AddRes)) {
+                    if (EPI == static_cast<int>(Epi::AddRes) || EPI == static_cast<int>(Epi::GeluBwd)) {
                         const bf16* r = p.R + static_cast<long long>(row) * p.ldr + col;
 #pragma unroll
                         for (int i = 0; i < 32; i += 8) {
                             const uint4 raw = *reinterpret_cast<const uint4*>(r + i);
                             const bf16* rb = reinterpret_cast<const bf16*>(&raw);
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) v[i + j] += __bfloat162float(rb[j]);
+                            for (int j = 0; j < 8; ++j) {
+                                const float rv = __bfloat162float(rb[j]);
+                                if (EPI == static_cast<int>(Epi::AddRes)) v[i + j] += rv;
+                                else v[i + j] *= gelu_tanh_grad_f(rv);
+                            }
+                        }
+                    }
+                    if (EPI == static_cast<int>(Epi::StoreGelu)) {
+                        bf16* dst2 = p.C2 + static_cast<long long>(row) * p.ldc2 + col;
+#pragma unroll
+                        for (int i = 0; i < 32; i += 8) {
+                            uint4 raw;
+                            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                h[j] = __floats2bfloat162_rn(gelu_tanh_f(v[i + 2 * j]), gelu_tanh_f(v[i + 2 * j + 1]));
+                            *reinterpret_cast<uint4*>(dst2 + i) = raw;
                         }
                     }
                     bf16* dst = static_cast<bf16*>(p.C) + static_cast<long long>(row) * p.ldc + col;
@@ -313,7 +331,8 @@ void launch_tc(const GemmArgs& g, cudaStream_t s) {
                                 : make_map(g.A, g.M, g.K, g.lda, kBK, kBM);
     const CUtensorMap mb = B_MN ? make_map(g.B, g.K, g.N, g.ldb, 64, kBK)
                                 : make_map(g.B, g.N, g.K, g.ldb, kBK, BN);
-    TcParams p{g.M, g.N, g.K, g.C, g.ldc, static_cast<const bf16*>(g.R), g.ldr};
+    TcParams p{g.M, g.N, g.K, g.C, g.ldc, static_cast<const bf16*>(g.R), g.ldr,
+               static_cast<bf16*>(g.C2), g.ldc2};
     static int num_sms = 0;
     if (!num_sms) {
         int dev = 0;
@@ -343,6 +362,8 @@ void dispatch_epi(const GemmArgs& g, cudaStream_t s) {
         case Epi::AccumF32: dispatch_major<BN, STAGES, 1>(g, s); break;
         case Epi::AddRes: dispatch_major<BN, STAGES, 2>(g, s); break;
         case Epi::StoreF32: dispatch_major<BN, STAGES, 3>(g, s); break;
+        case Epi::StoreGelu: dispatch_major<BN, STAGES, 4>(g, s); break;
+        case Epi::GeluBwd: dispatch_major<BN, STAGES, 5>(g, s); break;
     }
 }
 
@@ -410,6 +431,10 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
             } else {
                 if (g.epi == Epi::AddRes)
                     v += to_f(static_cast<const T*>(g.R)[static_cast<long long>(m) * g.ldr + n]);
+                if (g.epi == Epi::GeluBwd)
+                    v *= gelu_tanh_grad_f(to_f(static_cast<const T*>(g.R)[static_cast<long long>(m) * g.ldr + n]));
+                if (g.epi == Epi::StoreGelu)
+                    static_cast<T*>(g.C2)[static_cast<long long>(m) * g.ldc2 + n] = from_f<T>(gelu_tanh_f(v));
                 static_cast<T*>(g.C)[off] = from_f<T>(v);
             }
         }

@@ -22,6 +22,8 @@ enum class Epi : int {
     AccumF32 = 1,   // C(fp32) += acc          (weight-gradient accumulation)
     AddRes = 2,     // C = acc + R             (residual stream update)
     StoreF32 = 3,   // C(fp32) = acc
+    StoreGelu = 4,  // C = acc, C2 = gelu_tanh(acc)          (MLP up-projection)
+    GeluBwd = 5,    // C = acc * gelu_tanh'(R)               (MLP dgrad -> dh)
 };
 
 struct GemmArgs {
@@ -30,6 +32,7 @@ struct GemmArgs {
     const void* B = nullptr; long long ldb = 0; bool b_kmajor = true;
     void* C = nullptr; long long ldc = 0;
     const void* R = nullptr; long long ldr = 0;
+    void* C2 = nullptr; long long ldc2 = 0;
     Epi epi = Epi::Store;
     DType dtype = DType::BF16;
 };

@@ -621,11 +621,18 @@ private:
         norm_fwd(dt_, llama_, L.x_mid.get(), work(P.ln2_w), P.ln2_b >= 0 ? work(P.ln2_b) : nullptr,
                  xn.get(), llama_ ? nullptr : L.mean2.get<float>(), L.rstd2.get<float>(), T, D_,
                  m_.norm_eps, s);
-        gemm(mk(T, F1_, D_, xn.get(), D_, true, work(P.w1), D_, true, L.h.get(), F1_), s);
+        Buf act;
+        if (!skip_out) act = Buf(&pool_, static_cast<size_t>(T) * F_ * e, s);
+        GemmArgs up = mk(T, F1_, D_, xn.get(), D_, true, work(P.w1), D_, true, L.h.get(), F1_);
+        if (!skip_out && !llama_) {   // GELU fused into the up-projection epilogue
+            up.epi = Epi::StoreGelu;
+            up.C2 = act.get();
+            up.ldc2 = F_;
+        }
+        gemm(up, s);
         xn.release();
         if (!skip_out) {
-            Buf act(&pool_, static_cast<size_t>(T) * F_ * e, s);
-            act_fwd(dt_, llama_ ? 1 : 0, L.h.get(), act.get(), T, F_, s);
+            if (llama_) act_fwd(dt_, 1, L.h.get(), act.get(), T, F_, s);
             GemmArgs g2 = mk(T, D_, F_, act.get(), F_, true, work(P.w2), F_, true, out, D_);
             g2.epi = Epi::AddRes;
             g2.R = L.x_mid.get();
@@ -643,13 +650,21 @@ private:
         // ---- MLP ----
         Buf act(&pool_, static_cast<size_t>(T) * F_ * e, s);
         act_fwd(dt_, llama_ ? 1 : 0, L.h.get(), act.get(), T, F_, s);
-        Buf da(&pool_, static_cast<size_t>(T) * F_ * e, s);
-        gemm(mk(T, F_, D_, dy, D_, true, work(P.w2), F_, false, da.get(), F_), s);        // dA = dY W2
         wgrad(D_, F_, T, dy, D_, act.get(), F_, grad(P.w2), s);                            // dW2 += dY^T A
         act.release();
         Buf dh(&pool_, static_cast<size_t>(T) * F1_ * e, s);
-        act_bwd(dt_, llama_ ? 1 : 0, L.h.get(), da.get(), dh.get(), T, F_, s);
-        da.release();
+        if (llama_) {
+            Buf da(&pool_, static_cast<size_t>(T) * F_ * e, s);
+            gemm(mk(T, F_, D_, dy, D_, true, work(P.w2), F_, false, da.get(), F_), s);    // dA = dY W2
+            act_bwd(dt_, 1, L.h.get(), da.get(), dh.get(), T, F_, s);
+        } else {
+            // dH = (dY W2) * gelu'(H), fused into the data-gradient epilogue
+            GemmArgs g = mk(T, F_, D_, dy, D_, true, work(P.w2), F_, false, dh.get(), F_);
+            g.epi = Epi::GeluBwd;
+            g.R = L.h.get();
+            g.ldr = F_;
+            gemm(g, s);
+        }
         Buf dxn(&pool_, static_cast<size_t>(T) * D_ * e, s);
         gemm(mk(T, D_, F1_, dh.get(), F1_, true, work(P.w1), D_, false, dxn.get(), D_), s);  // dXn2
         Buf xn(&pool_, static_cast<size_t>(T) * D_ * e, s);
