@@ -26,8 +26,7 @@ namespace {
 
 constexpr int TQ = 128;            // query rows per CTA (= TMEM lanes)
 constexpr int TK = 128;            // keys per tile
-constexpr int kThreadsTc = 256;
-constexpr int kLoadThreads = 96;   // warps 5..7
+constexpr int kThreadsTc = 192;    // warps 0-3 softmax, 4 MMA, 5 TMA / loads
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleSlack = 8.f;   // log2 units: p <= 2^8 before a rescale
 
@@ -37,6 +36,36 @@ __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+// TMA tile loads: a [ROWS x HD] tile = HD/64 boxes of 64 columns, each
+// landing as ROWS x 128 B with the 128-byte swizzle (the UMMA K-major
+// SWIZZLE_128B layout).  Q/dO maps are {hd, H, T}; K/V maps {hd, Hkv, rows, L}.
+__device__ __forceinline__ void tma3(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(tc::smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(tc::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void tma4(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
+                                     int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(tc::smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(tc::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+template <int HD, int ROWS>
+__device__ __forceinline__ void load_q_tile(uint8_t* dst, const CUtensorMap* m, uint64_t* bar, int head, int row) {
+#pragma unroll
+    for (int c = 0; c < HD / 64; ++c) tma3(dst + c * ROWS * 128, m, bar, c * 64, head, row);
+}
+template <int HD, int ROWS>
+__device__ __forceinline__ void load_kv_tile(uint8_t* dst, const CUtensorMap* m, uint64_t* bar, int head, int row,
+                                             int layer) {
+#pragma unroll
+    for (int c = 0; c < HD / 64; ++c) tma4(dst + c * ROWS * 128, m, bar, c * 64, head, row, layer);
 }
 
 // [128 rows x HD] bf16 tile = HD/64 column blocks of [128 rows x 128 B],
@@ -58,7 +87,8 @@ struct FwdSmem {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
+__global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a,
+                                                             const __grid_constant__ AttnMaps mp) {
     using L = FwdSmem<HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -83,9 +113,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
     const int nkb = (kv_end + TK - 1) / TK;
 
     if (threadIdx.x == 0) {
-        tc::mbar_init(q_full, kLoadThreads);
+        tc::mbar_init(q_full, 1);
         for (int s = 0; s < 2; ++s) {
-            tc::mbar_init(&kv_full[s], kLoadThreads);
+            tc::mbar_init(&kv_full[s], 1);
             tc::mbar_init(&kv_empty[s], 1);
             tc::mbar_init(&s_full[s], 1);
         }
@@ -101,37 +131,23 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t kColS = 0, kColO = 256;
 
-    if (warp >= 5) {
-        // ---------------------------------------------------------- loaders
-        const int lt = threadIdx.x - 160;
-        constexpr int kChunks = HD / 8;
-        const long long qstride = static_cast<long long>(a.H) * HD;
-        const bf16* qbase = static_cast<const bf16*>(a.q) +
-                            (static_cast<long long>(sg.q_start + q0) * a.H + h) * HD;
-        for (int i = lt; i < TQ * kChunks; i += kLoadThreads) {
-            const int r = i / kChunks, c = i % kChunks;
-            const bool ok = r < rows;
-            tc::cp_async16_zfill(smem + L::kQ + tile_off(r, c), ok ? qbase + r * qstride + c * 8 : qbase, ok);
-        }
-        tc::cp_async_arrive(q_full);
-        const long long kvs = static_cast<long long>(a.Hkv) * HD;
-        const bf16* kb = static_cast<const bf16*>(sg.k) + a.layer * sg.kv_layer_stride + kvh * HD;
-        const bf16* vb = static_cast<const bf16*>(sg.v) + a.layer * sg.kv_layer_stride + kvh * HD;
-        for (int j = 0; j < nkb; ++j) {
-            const int s = j & 1;
-            tc::mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-            const int key0 = j * TK;
-            uint8_t* sk = smem + L::kK + s * L::kTile;
-            uint8_t* sv = smem + L::kV + s * L::kTile;
-            for (int i = lt; i < TK * kChunks; i += kLoadThreads) {
-                const int r = i / kChunks, c = i % kChunks;
-                const bool ok = key0 + r < kv_end;
-                const long long off = static_cast<long long>(key0 + r) * kvs + c * 8;
-                tc::cp_async16_zfill(sk + tile_off(r, c), ok ? kb + off : kb, ok);
-                tc::cp_async16_zfill(sv + tile_off(r, c), ok ? vb + off : vb, ok);
+    if (warp == 5) {
+        // --------------------------------------------------------- TMA loads
+        if (lane == 0) {
+            const CUtensorMap* mk = &mp.kv128[2 * sg.tma_map];
+            const CUtensorMap* mv = &mp.kv128[2 * sg.tma_map + 1];
+            tc::mbar_expect_tx(q_full, L::kTile);
+            load_q_tile<HD, TQ>(smem + L::kQ, &mp.q128, q_full, h, sg.q_start + q0);
+            for (int j = 0; j < nkb; ++j) {
+                const int s = j & 1;
+                tc::mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+                tc::mbar_expect_tx(&kv_full[s], 2 * L::kTile);
+                const int row = sg.kv_row0 + j * TK;
+                load_kv_tile<HD, TK>(smem + L::kK + s * L::kTile, mk, &kv_full[s], kvh, row, a.layer);
+                load_kv_tile<HD, TK>(smem + L::kV + s * L::kTile, mv, &kv_full[s], kvh, row, a.layer);
             }
-            tc::cp_async_arrive(&kv_full[s]);
         }
+        __syncwarp();
     } else if (warp == 4) {
         // ------------------------------------------------------- MMA issuer
         if (lane == 0) {
@@ -190,21 +206,30 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
             const uint32_t sb = lane_base + kColS + s * TK;
             const int key0 = j * TK;
             const bool need_mask = (key0 + TK - 1 > first_q) || rows < TQ;
-            // pass 1: row max of the raw scores (scale > 0 commutes with max)
-            float mraw = -INFINITY;
-#pragma unroll 1
+            // the whole 128-column score row in registers: 4 loads, one wait
+            float sv[TK / 32][32];
+#pragma unroll
+            for (int c = 0; c < TK / 32; ++c) tc::tmem_ld32_async(sb + c * 32, sv[c]);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < TK / 32; ++c) tc::reg_fence(sv[c]);
+            // pass 1: row max of the raw scores (scale > 0 commutes with max);
+            // 8 independent partial maxima so the reduction is not one long
+            // dependency chain (one softmax warp per SMSP: no TLP to hide it).
+            float mx8[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) mx8[q] = -INFINITY;
+#pragma unroll
             for (int c = 0; c < TK / 32; ++c) {
-                float v[32];
-                tc::tmem_ld32(sb + c * 32, v);
-                if (need_mask) {
-                    const int lim = qp - (key0 + c * 32);    // keys i <= lim visible
+                const int lim = need_mask ? qp - (key0 + c * 32) : 32;   // keys i <= lim visible
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, i <= lim ? v[i] : -INFINITY);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 32; i += 2) mraw = fmaxf(mraw, fmaxf(v[i], v[i + 1]));
+                for (int i = 0; i < 32; ++i) {
+                    const float x = (need_mask && i > lim) ? -INFINITY : sv[c][i];
+                    mx8[i & 7] = fmaxf(mx8[i & 7], x);
                 }
             }
+            const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                     fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
             const float mt = mraw * c2;
             const bool grow = mt > m_run + kRescaleSlack || (m_run == -INFINITY && mt > -INFINITY);
             const bool rescale = __any_sync(0xffffffffu, grow) && j > 0;
@@ -231,11 +256,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
             }
             if (grow) m_run = mt;
             const float mu = (m_run == -INFINITY) ? 0.f : m_run;
+            float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};   // independent partial sums
             uint8_t* prow = sP;   // this tile's P buffer
-#pragma unroll 1
+#pragma unroll
             for (int c = 0; c < TK / 32; ++c) {
-                float v[32];
-                tc::tmem_ld32(sb + c * 32, v);
+                const float* v = sv[c];
                 uint32_t pk[16];
                 const int lim = need_mask ? qp - (key0 + c * 32) : 32;
 #pragma unroll
@@ -246,7 +271,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
                         p0 = i <= lim ? p0 : 0.f;
                         p1 = i + 1 <= lim ? p1 : 0.f;
                     }
-                    l += p0 + p1;
+                    l8[(i >> 1) & 7] += p0 + p1;
                     __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
                     pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
                 }
@@ -257,6 +282,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a) {
                         make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
                 }
             }
+            l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
             tc::fence_proxy_async();
             tc::fence_before();
             tc::mbar_arrive(p_full);
@@ -301,7 +327,7 @@ void launch_fwd_tc(const AttnArgs& a, cudaStream_t s) {
         EPP_CUDA(cudaFuncSetAttribute(attn_fwd_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
         cfg = true;
     }
-    attn_fwd_tc<HD><<<dim3(a.nqwork128, a.H), kThreadsTc, L::kAlloc, s>>>(a);
+    attn_fwd_tc<HD><<<dim3(a.nqwork128, a.H), kThreadsTc, L::kAlloc, s>>>(a, *a.maps);
     EPP_CHECK_LAUNCH();
 }
 
@@ -350,7 +376,8 @@ struct DqSmem {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a) {
+__global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a,
+                                                                const __grid_constant__ AttnMaps mp) {
     using L = DqSmem<HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -376,9 +403,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
     const long long row0 = sg.q_start + q0;
 
     if (threadIdx.x == 0) {
-        tc::mbar_init(q_full, kLoadThreads);
+        tc::mbar_init(q_full, 1);
         for (int s = 0; s < kDqStages; ++s) {
-            tc::mbar_init(&kv_full[s], kLoadThreads);
+            tc::mbar_init(&kv_full[s], 1);
             tc::mbar_init(&kv_empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -395,37 +422,23 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t kColS = 0, kColP = 128, kColQ = 256;
 
-    if (warp >= 5) {
-        const int lt = threadIdx.x - 160;
-        constexpr int kChunks = HD / 8;
-        const long long qs = static_cast<long long>(a.H) * HD;
-        const bf16* qb = static_cast<const bf16*>(a.q) + (row0 * a.H + h) * HD;
-        const bf16* ob = static_cast<const bf16*>(a.dout) + (row0 * a.H + h) * HD;
-        for (int i = lt; i < TQ * kChunks; i += kLoadThreads) {
-            const int r = i / kChunks, c = i % kChunks;
-            const bool ok = r < rows;
-            tc::cp_async16_zfill(smem + L::kQ + toff<128>(r, c), ok ? qb + r * qs + c * 8 : qb, ok);
-            tc::cp_async16_zfill(smem + L::kO + toff<128>(r, c), ok ? ob + r * qs + c * 8 : ob, ok);
-        }
-        tc::cp_async_arrive(q_full);
-        const long long kvs = static_cast<long long>(a.Hkv) * HD;
-        const bf16* kb = static_cast<const bf16*>(sg.k) + a.layer * sg.kv_layer_stride + kvh * HD;
-        const bf16* vb = static_cast<const bf16*>(sg.v) + a.layer * sg.kv_layer_stride + kvh * HD;
-        for (int j = 0; j < nkb; ++j) {
-            const int st = j % kDqStages;
-            tc::mbar_wait(&kv_empty[st], ((j / kDqStages) & 1) ^ 1);
-            const int key0 = j * TB;
-            uint8_t* sk = smem + L::kK + st * L::kSmall;
-            uint8_t* sv = smem + L::kV + st * L::kSmall;
-            for (int i = lt; i < TB * kChunks; i += kLoadThreads) {
-                const int r = i / kChunks, c = i % kChunks;
-                const bool ok = key0 + r < kv_end;
-                const long long off = static_cast<long long>(key0 + r) * kvs + c * 8;
-                tc::cp_async16_zfill(sk + toff<TB>(r, c), ok ? kb + off : kb, ok);
-                tc::cp_async16_zfill(sv + toff<TB>(r, c), ok ? vb + off : vb, ok);
+    if (warp == 5) {
+        if (lane == 0) {
+            const CUtensorMap* mk = &mp.kv64[2 * sg.tma_map];
+            const CUtensorMap* mv = &mp.kv64[2 * sg.tma_map + 1];
+            tc::mbar_expect_tx(q_full, 2 * L::kBig);
+            load_q_tile<HD, 128>(smem + L::kQ, &mp.q128, q_full, h, static_cast<int>(row0));
+            load_q_tile<HD, 128>(smem + L::kO, &mp.do128, q_full, h, static_cast<int>(row0));
+            for (int j = 0; j < nkb; ++j) {
+                const int st = j % kDqStages;
+                tc::mbar_wait(&kv_empty[st], ((j / kDqStages) & 1) ^ 1);
+                tc::mbar_expect_tx(&kv_full[st], 2 * L::kSmall);
+                const int row = sg.kv_row0 + j * TB;
+                load_kv_tile<HD, TB>(smem + L::kK + st * L::kSmall, mk, &kv_full[st], kvh, row, a.layer);
+                load_kv_tile<HD, TB>(smem + L::kV + st * L::kSmall, mv, &kv_full[st], kvh, row, a.layer);
             }
-            tc::cp_async_arrive(&kv_full[st]);
         }
+        __syncwarp();
     } else if (warp == 4) {
         if (lane == 0) {
             constexpr uint32_t idS = tc::instr_desc_mn(TQ, TB, false, false);
@@ -484,11 +497,22 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
             const int key0 = j * TB;
             const bool need_mask = (key0 + TB - 1 > first_q) || rows < TQ;
             uint32_t pk[32];
+            float sall[TB / 32][32], pall[TB / 32][32];
 #pragma unroll
             for (int c = 0; c < TB / 32; ++c) {
-                float sv[32], pv[32];
-                tc::tmem_ld32(lane_base + kColS + b * TB + c * 32, sv);
-                tc::tmem_ld32(lane_base + kColP + b * TB + c * 32, pv);
+                tc::tmem_ld32_async(lane_base + kColS + b * TB + c * 32, sall[c]);
+                tc::tmem_ld32_async(lane_base + kColP + b * TB + c * 32, pall[c]);
+            }
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < TB / 32; ++c) {
+                tc::reg_fence(sall[c]);
+                tc::reg_fence(pall[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < TB / 32; ++c) {
+                const float* sv = sall[c];
+                const float* pv = pall[c];
                 const int lim = need_mask ? qp - (key0 + c * 32) : 32;
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
@@ -554,7 +578,8 @@ struct DkvSmem {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs a) {
+__global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs a,
+                                                                 const __grid_constant__ AttnMaps mp) {
     using L = DkvSmem<HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -584,9 +609,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
     const int iters = per_head * group;     // >= 1: the segment's last query sees every key
 
     if (threadIdx.x == 0) {
-        tc::mbar_init(kv_full, kLoadThreads);
+        tc::mbar_init(kv_full, 1);
         for (int st = 0; st < kDkvStages; ++st) {
-            tc::mbar_init(&qd_full[st], kLoadThreads);
+            tc::mbar_init(&qd_full[st], 1 + 32);      // TMA expect_tx + 32 lse/delta cp.async arrivals
             tc::mbar_init(&qd_empty[st], 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -603,20 +628,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t kColS = 0, kColP = 128, kColV = 256, kColK = 256 + HD;
 
-    if (warp >= 5) {
-        const int lt = threadIdx.x - 160;
-        constexpr int kChunks = HD / 8;
-        const long long kvs = static_cast<long long>(a.Hkv) * HD;
-        const bf16* kb = static_cast<const bf16*>(sg.k) + a.layer * sg.kv_layer_stride + kvh * HD + k0 * kvs;
-        const bf16* vb = static_cast<const bf16*>(sg.v) + a.layer * sg.kv_layer_stride + kvh * HD + k0 * kvs;
-        for (int i = lt; i < TK * kChunks; i += kLoadThreads) {
-            const int r = i / kChunks, c = i % kChunks;
-            const bool ok = r < nkeys;
-            tc::cp_async16_zfill(smem + L::kK + toff<128>(r, c), ok ? kb + r * kvs + c * 8 : kb, ok);
-            tc::cp_async16_zfill(smem + L::kV + toff<128>(r, c), ok ? vb + r * kvs + c * 8 : vb, ok);
+    if (warp == 5) {
+        const CUtensorMap* mk = &mp.kv128[2 * sg.tma_map];
+        const CUtensorMap* mv = &mp.kv128[2 * sg.tma_map + 1];
+        if (lane == 0) {
+            tc::mbar_expect_tx(kv_full, 2 * L::kBig);
+            load_kv_tile<HD, 128>(smem + L::kK, mk, kv_full, kvh, sg.kv_row0 + k0, a.layer);
+            load_kv_tile<HD, 128>(smem + L::kV, mv, kv_full, kvh, sg.kv_row0 + k0, a.layer);
         }
-        tc::cp_async_arrive(kv_full);
-        const long long qs = static_cast<long long>(a.H) * HD;
         for (int it = 0; it < iters; ++it) {
             const int st = it % kDkvStages;
             tc::mbar_wait(&qd_empty[st], ((it / kDkvStages) & 1) ^ 1);
@@ -624,21 +643,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
             const int q0 = (qb_first + it % per_head) * TB;
             const int rows = min(TB, sg.q_len - q0);
             const long long row0 = sg.q_start + q0;
-            const bf16* qb_ = static_cast<const bf16*>(a.q) + (row0 * a.H + hq) * HD;
-            const bf16* ob_ = static_cast<const bf16*>(a.dout) + (row0 * a.H + hq) * HD;
-            uint8_t* sq = smem + L::kQ + st * L::kSmall;
-            uint8_t* so = smem + L::kO + st * L::kSmall;
-            for (int i = lt; i < TB * kChunks; i += kLoadThreads) {
-                const int r = i / kChunks, c = i % kChunks;
-                const bool ok = r < rows;
-                tc::cp_async16_zfill(sq + toff<TB>(r, c), ok ? qb_ + r * qs + c * 8 : qb_, ok);
-                tc::cp_async16_zfill(so + toff<TB>(r, c), ok ? ob_ + r * qs + c * 8 : ob_, ok);
+            if (lane == 0) {
+                tc::mbar_expect_tx(&qd_full[st], 2 * L::kSmall);
+                load_q_tile<HD, TB>(smem + L::kQ + st * L::kSmall, &mp.q64, &qd_full[st], hq, static_cast<int>(row0));
+                load_q_tile<HD, TB>(smem + L::kO + st * L::kSmall, &mp.do64, &qd_full[st], hq, static_cast<int>(row0));
             }
-            // lse / delta through cp.async as well, so the same async arrive
-            // publishes them (rows past the end read 0; they are masked).
+            // lse / delta through cp.async (rows past the end read 0; they are masked)
             const float* lg = a.lse + static_cast<long long>(hq) * a.T + row0;
             const float* dg = a.delta + static_cast<long long>(hq) * a.T + row0;
-            for (int i = lt; i < TB; i += kLoadThreads) {
+            for (int i = lane; i < TB; i += 32) {
                 const bool ok = i < rows;
                 tc::cp_async4_zfill(sLse + st * TB + i, ok ? lg + i : lg, ok);
                 tc::cp_async4_zfill(sDelta + st * TB + i, ok ? dg + i : dg, ok);
@@ -708,11 +721,22 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
             const float* lse_s = sLse + (it % kDkvStages) * TB;
             const float* dl_s = sDelta + (it % kDkvStages) * TB;
             uint32_t pk[32], dk[32];
+            float sall[TB / 32][32], dall[TB / 32][32];
 #pragma unroll
             for (int c = 0; c < TB / 32; ++c) {
-                float sv[32], dv[32];
-                tc::tmem_ld32(lane_base + kColS + b * TB + c * 32, sv);
-                tc::tmem_ld32(lane_base + kColP + b * TB + c * 32, dv);
+                tc::tmem_ld32_async(lane_base + kColS + b * TB + c * 32, sall[c]);
+                tc::tmem_ld32_async(lane_base + kColP + b * TB + c * 32, dall[c]);
+            }
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < TB / 32; ++c) {
+                tc::reg_fence(sall[c]);
+                tc::reg_fence(dall[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < TB / 32; ++c) {
+                const float* sv = sall[c];
+                const float* dv = dall[c];
                 // query qi visible to key kp iff qi < rows && qi >= kp - first_q
                 const int qmin = kp - first_q - c * 32;
                 const int qmax = rows - c * 32;
@@ -791,12 +815,12 @@ void launch_bwd_tc(const AttnArgs& a, cudaStream_t s) {
     }
     if (a.nqwork128 > 0) {
         ProfScope prof(kProfAttnBwdDq, 6.0 * a.H * a.hd * a.pairs, s);     // executed: 3 matmuls
-        attn_bwd_dq_tc<HD><<<dim3(a.nqwork128, a.H), kThreadsTc, DqSmem<HD>::kAlloc, s>>>(a);
+        attn_bwd_dq_tc<HD><<<dim3(a.nqwork128, a.H), kThreadsTc, DqSmem<HD>::kAlloc, s>>>(a, *a.maps);
         EPP_CHECK_LAUNCH();
     }
     if (a.nkwork128 > 0) {
         ProfScope prof(kProfAttnBwdDkv, 8.0 * a.H * a.hd * a.pairs, s);    // executed: 4 matmuls
-        attn_bwd_dkv_tc<HD><<<dim3(a.nkwork128, a.Hkv), kThreadsTc, DkvSmem<HD>::kAlloc, s>>>(a);
+        attn_bwd_dkv_tc<HD><<<dim3(a.nkwork128, a.Hkv), kThreadsTc, DkvSmem<HD>::kAlloc, s>>>(a, *a.maps);
         EPP_CHECK_LAUNCH();
     }
 }
@@ -804,12 +828,13 @@ void launch_bwd_tc(const AttnArgs& a, cudaStream_t s) {
 }  // namespace
 
 bool attn_fwd_tc_supported(const AttnArgs& a) {
-    return a.dtype == DType::BF16 && (a.hd == 64 || a.hd == 128) && a.qwork128 != nullptr;
+    return a.dtype == DType::BF16 && (a.hd == 64 || a.hd == 128) && a.qwork128 != nullptr &&
+           a.maps != nullptr;
 }
 
 bool attn_bwd_tc_supported(const AttnArgs& a) {
     return a.dtype == DType::BF16 && (a.hd == 64 || a.hd == 128) && a.qwork128 != nullptr &&
-           a.kwork128 != nullptr;
+           a.kwork128 != nullptr && a.maps != nullptr;
 }
 
 // dq + dk/dv kernels (the delta pre-pass is issued by attn_bwd).
@@ -823,6 +848,38 @@ void attn_fwd_tc(const AttnArgs& a, cudaStream_t s) {
     ProfScope prof(kProfAttnFwd, 4.0 * a.H * a.hd * a.pairs, s);
     if (a.hd == 64) launch_fwd_tc<64>(a, s);
     else launch_fwd_tc<128>(a, s);
+}
+
+void attn_maps_q(AttnMaps& m, const void* q, const void* dout, int T, int H, int hd) {
+    const unsigned long long dims[3] = {static_cast<unsigned long long>(hd), static_cast<unsigned long long>(H),
+                                        static_cast<unsigned long long>(T)};
+    const unsigned long long st[2] = {static_cast<unsigned long long>(hd) * 2,
+                                      static_cast<unsigned long long>(H) * hd * 2};
+    const unsigned b128[3] = {64, 1, 128}, b64[3] = {64, 1, 64};
+    if (q) {
+        m.q128 = make_tma_map(q, 3, dims, st, b128);
+        m.q64 = make_tma_map(q, 3, dims, st, b64);
+    }
+    if (dout) {
+        m.do128 = make_tma_map(dout, 3, dims, st, b128);
+        m.do64 = make_tma_map(dout, 3, dims, st, b64);
+    }
+}
+
+void attn_maps_kv(AttnMaps& m, int which, const void* k, const void* v, long long rows, int layers, int Hkv,
+                  int hd) {
+    if (!k || rows <= 0) return;
+    const unsigned long long dims[4] = {static_cast<unsigned long long>(hd), static_cast<unsigned long long>(Hkv),
+                                        static_cast<unsigned long long>(rows),
+                                        static_cast<unsigned long long>(layers)};
+    const unsigned long long st[3] = {static_cast<unsigned long long>(hd) * 2,
+                                      static_cast<unsigned long long>(Hkv) * hd * 2,
+                                      static_cast<unsigned long long>(rows) * Hkv * hd * 2};
+    const unsigned b128[4] = {64, 1, 128, 1}, b64[4] = {64, 1, 64, 1};
+    m.kv128[2 * which] = make_tma_map(k, 4, dims, st, b128);
+    m.kv128[2 * which + 1] = make_tma_map(v, 4, dims, st, b128);
+    m.kv64[2 * which] = make_tma_map(k, 4, dims, st, b64);
+    m.kv64[2 * which + 1] = make_tma_map(v, 4, dims, st, b64);
 }
 
 }  // namespace eppk

@@ -31,6 +31,8 @@ int kguard(F&& f) {
 
 // Build + upload segment table and work lists for a standalone attention call.
 struct AttnTables {
+    AttnMaps maps{};
+    void* kcat = nullptr;      // all segments' K (then V) rows, concatenated (tcgen05 path)
     void* segs = nullptr;
     void* qw = nullptr;
     void* kw = nullptr;
@@ -40,9 +42,19 @@ struct AttnTables {
     cudaStream_t s;
     AttnTables(int nseg, const int32_t* q_start, const int32_t* q_len, const int32_t* kv_ctx,
                const void* const* k, const void* const* v, float* const* dk, float* const* dv,
-               cudaStream_t st)
+               cudaStream_t st, int T = 0, int H = 0, int Hkv = 0, int hd = 0, int dtype = 0,
+               const void* qptr = nullptr, const void* dout = nullptr)
         : s(st) {
         std::vector<AttnSeg> sg(nseg);
+        long long total_rows = 0;
+        for (int i = 0; i < nseg; ++i) total_rows += kv_ctx[i] + q_len[i];
+        const bool tc = dtype == static_cast<int>(DType::BF16) && total_rows > 0;
+        const size_t row_bytes = static_cast<size_t>(Hkv) * hd * 2;
+        if (tc) {
+            EPP_CUDA(cudaMalloc(&kcat, 2 * total_rows * row_bytes));
+            EPP_CUDA(cudaMemset(kcat, 0, 2 * total_rows * row_bytes));
+        }
+        long long row = 0;
         std::vector<AttnWork> q, kk, q128, k128;
         for (int i = 0; i < nseg; ++i) {
             sg[i] = AttnSeg{};
@@ -53,6 +65,15 @@ struct AttnTables {
             sg[i].v = v[i];
             sg[i].dk = dk ? dk[i] : nullptr;
             sg[i].dv = dv ? dv[i] : nullptr;
+            sg[i].tma_map = 1;
+            sg[i].kv_row0 = static_cast<int>(row);
+            if (tc) {
+                const size_t n = static_cast<size_t>(kv_ctx[i] + q_len[i]) * row_bytes;
+                EPP_CUDA(cudaMemcpy(static_cast<uint8_t*>(kcat) + row * row_bytes, k[i], n, cudaMemcpyDeviceToDevice));
+                EPP_CUDA(cudaMemcpy(static_cast<uint8_t*>(kcat) + (total_rows + row) * row_bytes, v[i], n,
+                                    cudaMemcpyDeviceToDevice));
+            }
+            row += kv_ctx[i] + q_len[i];
             for (int b = 0; b * kAttnBlock < q_len[i]; ++b) q.push_back({i, b});
             for (int b = 0; b * kAttnBlock < kv_ctx[i] + q_len[i]; ++b) kk.push_back({i, b});
             for (int b = 0; b * 128 < q_len[i]; ++b) q128.push_back({i, b});
@@ -64,6 +85,10 @@ struct AttnTables {
         EPP_CUDA(cudaMalloc(&kw128, sizeof(AttnWork) * (nk128 ? nk128 : 1)));
         EPP_CUDA(cudaMemcpy(qw128, q128.data(), sizeof(AttnWork) * nq128, cudaMemcpyHostToDevice));
         EPP_CUDA(cudaMemcpy(kw128, k128.data(), sizeof(AttnWork) * nk128, cudaMemcpyHostToDevice));
+        if (tc) {
+            attn_maps_kv(maps, 1, kcat, static_cast<uint8_t*>(kcat) + total_rows * row_bytes, total_rows, 1, Hkv, hd);
+            attn_maps_q(maps, qptr, dout, T, H, hd);
+        }
         nq = static_cast<int>(q.size());
         nk = static_cast<int>(kk.size());
         EPP_CUDA(cudaMalloc(&segs, sizeof(AttnSeg) * (nseg ? nseg : 1)));
@@ -80,6 +105,7 @@ struct AttnTables {
         cudaFree(kw);
         cudaFree(qw128);
         cudaFree(kw128);
+        if (kcat) cudaFree(kcat);
     }
 };
 }  // namespace
@@ -115,7 +141,7 @@ int epp_kernel_attention_fwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, floa
                              float* lse, int32_t dtype, void* stream) {
     return eppk::kguard([&] {
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        eppk::AttnTables tb(nseg, q_start, q_len, kv_ctx, k, v, nullptr, nullptr, s);
+        eppk::AttnTables tb(nseg, q_start, q_len, kv_ctx, k, v, nullptr, nullptr, s, T, H, Hkv, hd, dtype, q, nullptr);
         eppk::AttnArgs a;
         a.segs = static_cast<const eppk::AttnSeg*>(tb.segs);
         a.nseg = nseg;
@@ -130,6 +156,7 @@ int epp_kernel_attention_fwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, floa
         a.T = T; a.H = H; a.Hkv = Hkv; a.hd = hd; a.layer = 0; a.scale = scale;
         a.dtype = static_cast<eppk::DType>(dtype);
         a.q = q; a.o = o; a.lse = lse;
+        a.maps = tb.kcat ? &tb.maps : nullptr;
         for (int i = 0; i < nseg; ++i)
             a.pairs += static_cast<double>(q_len[i]) * kv_ctx[i] + 0.5 * static_cast<double>(q_len[i]) * (q_len[i] + 1);
         eppk::attn_fwd(a, s);
@@ -143,7 +170,7 @@ int epp_kernel_attention_bwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, floa
                              const void* dout, float* dq, int32_t dtype, void* stream) {
     return eppk::kguard([&] {
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        eppk::AttnTables tb(nseg, q_start, q_len, kv_ctx, k, v, dk, dv, s);
+        eppk::AttnTables tb(nseg, q_start, q_len, kv_ctx, k, v, dk, dv, s, T, H, Hkv, hd, dtype, q, dout);
         float* delta = nullptr;
         EPP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&delta), sizeof(float) * H * (T ? T : 1), s));
         eppk::AttnArgs a;
@@ -161,6 +188,7 @@ int epp_kernel_attention_bwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, floa
         a.dtype = static_cast<eppk::DType>(dtype);
         a.q = q; a.o = const_cast<void*>(o); a.lse = const_cast<float*>(lse);
         a.dout = dout; a.delta = delta; a.dq = dq;
+        a.maps = tb.kcat ? &tb.maps : nullptr;
         for (int i = 0; i < nseg; ++i)
             a.pairs += static_cast<double>(q_len[i]) * kv_ctx[i] + 0.5 * static_cast<double>(q_len[i]) * (q_len[i] + 1);
         eppk::attn_bwd(a, s);

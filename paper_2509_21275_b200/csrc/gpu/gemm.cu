@@ -317,6 +317,31 @@ CUtensorMap make_map(const void* base, long long rows, long long cols, long long
     return m;
 }
 
+}  // namespace
+
+// bf16 tensor map with 128-byte swizzle: dims[0] is the contiguous one,
+// strides_b[i] = byte stride of dims[i+1].
+CUtensorMap make_tma_map(const void* base, int rank, const unsigned long long* dims,
+                         const unsigned long long* strides_b, const unsigned* box) {
+    CUtensorMap m;
+    cuuint64_t d[5], st[4];
+    cuuint32_t b[5], es[5];
+    for (int i = 0; i < rank; ++i) {
+        d[i] = dims[i];
+        b[i] = box[i];
+        es[i] = 1;
+        if (i + 1 < rank) st[i] = strides_b[i];
+    }
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, st,
+                                   b, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+    return m;
+}
+
+namespace {
+
 template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 void launch_tc(const GemmArgs& g, cudaStream_t s) {
     using L = TcSmem<BN, STAGES>;

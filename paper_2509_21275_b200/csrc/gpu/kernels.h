@@ -2,6 +2,7 @@
 // All launches are stream-ordered; pointers are device pointers.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -50,6 +51,8 @@ struct AttnSeg {
     int q_start;
     int q_len;
     int kv_ctx;
+    int tma_map;     // tcgen05 kernels: 0 -> AttnMaps::kv[0..1] (sequence), 1 -> kv[2..3]
+    int kv_row0;     // row of key 0 in that map's row coordinate
     int pad_;
     const void* k;       // layer-0 base
     const void* v;
@@ -58,6 +61,23 @@ struct AttnSeg {
     long long kv_layer_stride;    // elements between layers
     long long dkv_layer_stride;
 };
+
+// TMA descriptors of one attention call (tcgen05 kernels).  Q/dO: 3-D
+// {hd, H, T}; K/V: 4-D {hd, Hkv, rows, layers}, two buffer families (a
+// sequence's KV buffer and the chunk-local one).  All bf16, 128-byte swizzle,
+// boxes of 64 hd-columns x 1 head x {64,128} rows.
+struct AttnMaps {
+    CUtensorMap q128, q64;       // Q with 128- / 64-row boxes
+    CUtensorMap do128, do64;     // dO
+    CUtensorMap kv128[4];        // k0, v0, k1, v1 with 128-row boxes
+    CUtensorMap kv64[4];         // ... 64-row boxes
+};
+// Helpers filling AttnMaps (attention_tc.cu).
+void attn_maps_q(AttnMaps& m, const void* q, const void* dout, int T, int H, int hd);
+void attn_maps_kv(AttnMaps& m, int which, const void* k, const void* v, long long rows, int layers, int Hkv,
+                  int hd);
+CUtensorMap make_tma_map(const void* base, int rank, const unsigned long long* dims,
+                         const unsigned long long* strides_b, const unsigned* box);
 
 // Work item (segment index, 64-row block index).
 struct AttnWork {
@@ -91,6 +111,7 @@ struct AttnArgs {
     const void* dout = nullptr;   // [T, H, hd]
     float* delta = nullptr;       // [H, T] scratch
     float* dq = nullptr;          // [T, H, hd] fp32 (fully written by attn_bwd)
+    const AttnMaps* maps = nullptr;   // host struct, required by the tcgen05 kernels
 };
 
 void attn_fwd(const AttnArgs& a, cudaStream_t s);

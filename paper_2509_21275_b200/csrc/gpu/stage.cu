@@ -161,6 +161,7 @@ struct ChunkState {
     Buf dkv_local;                 // fp32 [dK|dV][T][Hkv*hd], one layer, re-zeroed per layer
     int nqwork = 0, nkwork = 0, nqwork128 = 0, nkwork128 = 0;
     double pairs = 0;
+    AttnMaps maps{};               // TMA descriptors (K/V per chunk, Q/dO per layer call)
     Buf x_in;                      // stage input (copy of act_in or embedding)
     std::vector<LayerSaved> layers;
     Buf meanf, rstdf, dxf;         // last stage: final-norm stats + d(final norm out)
@@ -429,13 +430,15 @@ private:
             SeqKV& sk = seqs_[c.seq];
             if (!sk.kv) {
                 sk.len = c.seq_len;
-                sk.kv = Buf(&pool_, 2 * static_cast<size_t>(nl_) * sk.len * kvw() * esz(), s);
+                // zeroed: attention tiles may read rows of later (not yet written)
+                // slices; they are masked, and must be finite
+                sk.kv = Buf(&pool_, 2 * static_cast<size_t>(nl_) * sk.len * kvw() * esz(), s, /*zero=*/true);
             }
             EPP_REQUIRE(sk.len == c.seq_len, "seq_len changed between slices");
         } else {
             EPP_REQUIRE(c.context == 0, "context without a sequence");
         }
-        cs.kv_local = Buf(&pool_, 2 * static_cast<size_t>(nl_) * T * kvw() * esz(), s);
+        cs.kv_local = Buf(&pool_, 2 * static_cast<size_t>(nl_) * T * kvw() * esz(), s, /*zero=*/true);
         int max_pos = 0;
         long long q_start = 0;
         cs.segs.clear();
@@ -446,6 +449,8 @@ private:
             if (i == 0 && seq_chunk) {
                 SeqKV& sk = seqs_[c.seq];
                 sg.kv_ctx = static_cast<int>(c.context);
+                sg.tma_map = 0;
+                sg.kv_row0 = 0;
                 sg.k = sk.kv.get<uint8_t>();
                 sg.v = sk.kv.get<uint8_t>() + static_cast<size_t>(nl_) * sk.len * kvw() * esz();
                 sg.kv_layer_stride = sk.len * kvw();
@@ -455,6 +460,8 @@ private:
                 // strided like the sequence buffers); dK/dV in a one-layer
                 // scratch (dkv stride 0), bound at backward.
                 sg.kv_ctx = 0;
+                sg.tma_map = 1;
+                sg.kv_row0 = static_cast<int>(q_start);
                 const size_t row0 = static_cast<size_t>(q_start) * kvw();
                 sg.k = cs.kv_local.get<uint8_t>() + row0 * esz();
                 sg.v = cs.kv_local.get<uint8_t>() + (static_cast<size_t>(nl_) * T * kvw() + row0) * esz();
@@ -466,6 +473,17 @@ private:
             q_start += c.slices[i];
         }
         rope_reserve(max_pos, hd_, m_.rope_theta, s);
+        if (dt_ == DType::BF16) {
+            if (seq_chunk) {
+                const SeqKV& sk = seqs_[c.seq];
+                attn_maps_kv(cs.maps, 0, sk.kv.get(),
+                             sk.kv.get<uint8_t>() + static_cast<size_t>(nl_) * sk.len * kvw() * esz(), sk.len,
+                             nl_, Hkv_, hd_);
+            }
+            attn_maps_kv(cs.maps, 1, cs.kv_local.get(),
+                         cs.kv_local.get<uint8_t>() + static_cast<size_t>(nl_) * T * kvw() * esz(), T, nl_,
+                         Hkv_, hd_);
+        }
         std::vector<int> tseg(cs.T), tpos(cs.T);
         std::vector<AttnWork> qw, kw, qw128, kw128;
         for (int i = 0; i < static_cast<int>(cs.segs.size()); ++i) {
@@ -610,6 +628,10 @@ private:
         a.q = L.q.get();
         a.o = L.o.get();
         a.lse = L.lse.get<float>();
+        if (dt_ == DType::BF16) {
+            attn_maps_q(cs.maps, L.q.get(), nullptr, T, H_, hd_);
+            a.maps = &cs.maps;
+        }
         attn_fwd(a, s);
         // x_mid = x + o Wo^T
         GemmArgs g = mk(T, D_, H_ * hd_, L.o.get(), H_ * hd_, true, work(P.wo), H_ * hd_, true,
@@ -690,6 +712,10 @@ private:
         a.dout = dout.get();
         a.delta = delta.get<float>();
         a.dq = dq.get<float>();
+        if (dt_ == DType::BF16) {
+            attn_maps_q(cs.maps, L.q.get(), dout.get(), T, H_, hd_);
+            a.maps = &cs.maps;
+        }
         attn_bwd(a, s);
         dout.release();
         delta.release();
