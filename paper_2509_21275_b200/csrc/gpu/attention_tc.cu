@@ -2,19 +2,11 @@
 //
 // Same segment semantics as attention.cu (query rows of a segment sit at key
 // positions [C, C+len) of the segment's K/V rows; key j visible iff j <= pos),
-// with both matmuls on the 5th-gen tensor cores:
-//   S  = Q K^T   tcgen05.mma M=128 N=128 K=hd  -> TMEM (two S buffers)
-//   O += P V     tcgen05.mma M=128 N=hd  K=128 -> TMEM (O accumulator)
-// One CTA = one 128-row query block of one head.  Warp roles:
-//   warps 0-3  softmax: thread t owns query row t (TMEM lane t): reads S,
-//              online max with lazy O rescaling (only when the running max
-//              grows by > 8 in log2 units), writes P (bf16) to shared memory
-//              in the UMMA 128-byte-swizzled K-major layout, final O / l.
-//   warp  4    TMEM allocation + MMA issue (one lane): S(j+1) is issued
-//              before PV(j) so the tensor core works while softmax(j) runs.
-//   warps 5-7  cp.async loaders of the Q tile and a 2-stage K/V ring
-//              (zero-filled past the segment end), published to the async
-//              proxy with fence.proxy.async before the mbarrier arrive.
+// with every matmul on the 5th-gen tensor cores (tcgen05.mma, accumulators in
+// TMEM, operands staged by TMA in the UMMA 128-byte-swizzled layout).  The
+// forward runs two 128-row query tiles per CTA with one softmax warpgroup
+// each (see attn_fwd_tc); the backward is split into a query-parallel dQ
+// kernel and a key-parallel dK/dV kernel (see the backward section).
 #include "common.cuh"
 #include "kernels.h"
 #include "profile.h"
@@ -26,7 +18,7 @@ namespace {
 
 constexpr int TQ = 128;            // query rows per CTA (= TMEM lanes)
 constexpr int TK = 128;            // keys per tile
-constexpr int kThreadsTc = 192;    // warps 0-3 softmax, 4 MMA, 5 TMA / loads
+constexpr int kThreadsTc = 192;    // backward: warps 0-3 softmax, 4 MMA, 5 TMA / loads
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleSlack = 8.f;   // log2 units: p <= 2^8 before a rescale
 
@@ -74,246 +66,296 @@ __device__ __forceinline__ uint32_t tile_off(int row, int chunk) {
     return static_cast<uint32_t>((chunk >> 3) * 16384 + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
 }
 
+// 2^x on the FMA pipe (Cody-Waite split + degree-3 minimax, rel. err 7.5e-5,
+// far below the bf16 rounding of P): offloads part of the exponentials from
+// the MUFU unit, which a 128-wide softmax row otherwise saturates.
+__device__ __forceinline__ float ex2_fma(float x) {
+    x = fmaxf(x, -126.f);
+    const float t = x + 12582912.f;                  // 1.5 * 2^23: round to integer
+    const float f = x - (t - 12582912.f);            // f in [-0.5, 0.5]
+    float p = fmaf(fmaf(fmaf(0.05517025f, f, 0.2426079f), f, 0.6932609f), f, 0.9999283f);
+    return __int_as_float(__float_as_int(t) * (1 << 23) + __float_as_int(p));
+}
+
+__device__ __forceinline__ float max3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
+// Row maximum of a 128-wide score row (FMNMX3, 4 independent chains).
+__device__ __forceinline__ float row_max(const float (&sv)[TK / 32][32]) {
+    float m[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        m[c] = sv[c][0];
+#pragma unroll
+        for (int i = 1; i < 31; i += 2) m[c] = max3(m[c], sv[c][i], sv[c][i + 1]);
+        m[c] = fmaxf(m[c], sv[c][31]);
+    }
+    return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
+}
+
+// P = 2^(s*c2 - mu) -> bf16, stored in the UMMA K-major swizzled layout;
+// returns the fp32 row sum.  One element in four takes the FMA-pipe exp2.
+__device__ __forceinline__ float exp_pack_store(const float (&sv)[TK / 32][32], float c2, float mu,
+                                                uint8_t* prow, int r) {
+    float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int c = 0; c < TK / 32; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+            const float x0 = fmaf(sv[c][i], c2, -mu), x1 = fmaf(sv[c][i + 1], c2, -mu);
+            const bool emu = (i & 7) == 6;
+            const float p0 = emu ? ex2_fma(x0) : ex2(x0);
+            const float p1 = emu ? ex2_fma(x1) : ex2(x1);
+            l8[(i >> 1) & 7] += p0 + p1;
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+            pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<uint4*>(prow + tile_off(r, c * 4 + q)) =
+                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    }
+    return ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
+}
+
+// Forward: one CTA = 256 query rows (two 128-row tiles Q0, Q1) of one head,
+// so each K/V tile fetched into shared memory feeds two score MMAs and two PV
+// MMAs, and the two softmax warpgroups ping-pong on the tensor core:
+//   tensor queue  ... PV0(j) S0(j+1) PV1(j) S1(j+1) PV0(j+1) ...
+// while softmax group 0 works on S0(j+1) the tensor core runs PV1(j) and
+// S1(j+1), and vice versa.  S_i(j+1) is issued after PV_i(j), so the commit
+// that publishes S_i(j+1) also proves that PV_i(j) has finished reading P_i
+// and updating O_i: no separate "PV done" barrier is needed.
+// TMEM columns: S0 [0,128) S1 [128,256) O0 [256,256+HD) O1 [384,384+HD).
+// Shared memory: Q0, Q1, P0, P1 and a 3-slot ring holding K(0) V(0) K(1)
+// V(1) ... (a slot is released by the commit after its last reader).
+// Warps 0-3 softmax Q0, 4-7 softmax Q1, 8 MMA, 9 TMA, 10-11 idle: three
+// whole warpgroups, so setmaxnreg can move registers from the issue
+// warpgroup (56) to the softmax warpgroups (224; a row of S is 128 fp32).
+constexpr int kThreadsFwd = 384;
+constexpr int kFwdSlots = 3;
+
 template <int HD>
 struct FwdSmem {
-    static constexpr int kTile = TQ * HD * 2;
-    static constexpr int kQ = 0;
-    static constexpr int kK = kQ + kTile;           // 2 stages
-    static constexpr int kV = kK + 2 * kTile;       // 2 stages
-    static constexpr int kP = kV + 2 * kTile;       // 128 x 128 bf16, 2 buffers
-    static constexpr int kBar = kP + 2 * TQ * TK * 2;
+    static constexpr int kTile = TQ * HD * 2;       // one 128-row Q / K / V tile
+    static constexpr int kQ = 0;                     // Q0, Q1
+    static constexpr int kP = kQ + 2 * kTile;        // P0, P1: 128 x 128 bf16
+    static constexpr int kRing = kP + 2 * TQ * TK * 2;
+    static constexpr int kBar = kRing + kFwdSlots * kTile;
     static constexpr int kBytes = kBar + 16 * 8 + 16;
     static constexpr int kAlloc = kBytes + 1024;
 };
 
 template <int HD>
-__global__ void __launch_bounds__(kThreadsTc, 1) attn_fwd_tc(const AttnArgs a,
-                                                             const __grid_constant__ AttnMaps mp) {
+__global__ void __launch_bounds__(kThreadsFwd, 1) attn_fwd_tc(const AttnArgs a,
+                                                              const __grid_constant__ AttnMaps mp) {
     using L = FwdSmem<HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
     uint64_t* q_full = bar + 0;
-    uint64_t* kv_full = bar + 1;     // [2]
-    uint64_t* kv_empty = bar + 3;    // [2]
-    uint64_t* s_full = bar + 5;      // [2]
-    uint64_t* p_full = bar + 7;
-    uint64_t* o_done = bar + 8;      // [2]: PV of P buffer b completed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
+    uint64_t* full = bar + 1;                 // [kFwdSlots]
+    uint64_t* empty = full + kFwdSlots;       // [kFwdSlots]
+    uint64_t* s_full = empty + kFwdSlots;     // [2]
+    uint64_t* p_full = s_full + 2;            // [2]
+    uint64_t* o_full = p_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
 
-    const AttnWork w = a.qwork128[blockIdx.x];
+    const AttnWork w = a.qwork256[blockIdx.x];
     const AttnSeg sg = a.segs[w.seg];
     const int h = blockIdx.y;
     const int kvh = h / (a.H / a.Hkv);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int q0 = w.block * TQ;
-    const int rows = min(TQ, sg.q_len - q0);
-    const int kv_end = sg.kv_ctx + q0 + rows;
-    const int nkb = (kv_end + TK - 1) / TK;
+    const int q0 = w.block * 2 * TQ;
+    const int rows0 = min(TQ, sg.q_len - q0);
+    const int rows1 = max(0, min(TQ, sg.q_len - q0 - TQ));
+    const int nkb0 = (sg.kv_ctx + q0 + rows0 + TK - 1) / TK;
+    const int nkb1 = rows1 > 0 ? (sg.kv_ctx + q0 + TQ + rows1 + TK - 1) / TK : 0;
+    const int nkb = max(nkb0, nkb1);
 
     if (threadIdx.x == 0) {
         tc::mbar_init(q_full, 1);
-        for (int s = 0; s < 2; ++s) {
-            tc::mbar_init(&kv_full[s], 1);
-            tc::mbar_init(&kv_empty[s], 1);
-            tc::mbar_init(&s_full[s], 1);
+        for (int s = 0; s < kFwdSlots; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
         }
-        tc::mbar_init(p_full, TQ);
-        tc::mbar_init(&o_done[0], 1);
-        tc::mbar_init(&o_done[1], 1);
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&s_full[i], 1);
+            tc::mbar_init(&p_full[i], TQ);
+        }
+        tc::mbar_init(o_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 4) tc::tmem_alloc(tmem_slot, 512);
+    if (warp == 8) tc::tmem_alloc(tmem_slot, 512);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = *tmem_slot;
-    constexpr uint32_t kColS = 0, kColO = 256;
 
-    if (warp == 5) {
+    if (warp >= 8) tc::setmaxnreg_dec<56>();
+    if (warp == 9) {
         // --------------------------------------------------------- TMA loads
         if (lane == 0) {
             const CUtensorMap* mk = &mp.kv128[2 * sg.tma_map];
             const CUtensorMap* mv = &mp.kv128[2 * sg.tma_map + 1];
-            tc::mbar_expect_tx(q_full, L::kTile);
+            tc::mbar_expect_tx(q_full, (rows1 > 0 ? 2 : 1) * L::kTile);
             load_q_tile<HD, TQ>(smem + L::kQ, &mp.q128, q_full, h, sg.q_start + q0);
-            for (int j = 0; j < nkb; ++j) {
-                const int s = j & 1;
-                tc::mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-                tc::mbar_expect_tx(&kv_full[s], 2 * L::kTile);
-                const int row = sg.kv_row0 + j * TK;
-                load_kv_tile<HD, TK>(smem + L::kK + s * L::kTile, mk, &kv_full[s], kvh, row, a.layer);
-                load_kv_tile<HD, TK>(smem + L::kV + s * L::kTile, mv, &kv_full[s], kvh, row, a.layer);
+            if (rows1 > 0) load_q_tile<HD, TQ>(smem + L::kQ + L::kTile, &mp.q128, q_full, h, sg.q_start + q0 + TQ);
+            for (int t = 0; t < 2 * nkb; ++t) {     // t = 2j: K(j), t = 2j+1: V(j)
+                const int s = t % kFwdSlots;
+                tc::mbar_wait(&empty[s], ((t / kFwdSlots) & 1) ^ 1);
+                tc::mbar_expect_tx(&full[s], L::kTile);
+                load_kv_tile<HD, TK>(smem + L::kRing + s * L::kTile, (t & 1) ? mv : mk, &full[s], kvh,
+                                     sg.kv_row0 + (t >> 1) * TK, a.layer);
             }
         }
         __syncwarp();
-    } else if (warp == 4) {
+    } else if (warp == 8) {
         // ------------------------------------------------------- MMA issuer
         if (lane == 0) {
             constexpr uint32_t idS = tc::instr_desc_mn(TQ, TK, false, false);
             constexpr uint32_t idO = tc::instr_desc_mn(TQ, HD, false, true);
-            const uint32_t sQ = tc::smem_u32(smem + L::kQ);
-            auto issue_s = [&](int j) {
-                const int s = j & 1;
-                tc::mbar_wait(&kv_full[s], (j >> 1) & 1);
-                tc::fence_proxy_async();   // cp.async (generic proxy) -> tcgen05 (async proxy)
+            auto slot_addr = [&](int t) { return tc::smem_u32(smem + L::kRing + (t % kFwdSlots) * L::kTile); };
+            auto wait_full = [&](int t) {
+                tc::mbar_wait(&full[t % kFwdSlots], (t / kFwdSlots) & 1);
                 tc::fence_after();
-                const uint32_t sK = tc::smem_u32(smem + L::kK + s * L::kTile);
+            };
+            auto issue_s = [&](int i, int j) {       // S_i = Q_i K(j)^T
+                const uint32_t sQ = tc::smem_u32(smem + L::kQ + i * L::kTile);
+                const uint32_t sK = slot_addr(2 * j);
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
                     const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc::mma_bf16(tmem + kColS + s * TK, tc::smem_desc(sQ + off, 16, 1024),
+                    tc::mma_bf16(tmem + i * TK, tc::smem_desc(sQ + off, 16, 1024),
                                  tc::smem_desc(sK + off, 16, 1024), idS, kk != 0);
                 }
-                tc::commit(&s_full[s]);
+                tc::commit(&s_full[i]);
             };
-            tc::mbar_wait(q_full, 0);
-            tc::fence_proxy_async();
-            tc::fence_after();
-            issue_s(0);
-            for (int j = 0; j < nkb; ++j) {
-                if (j + 1 < nkb) issue_s(j + 1);
-                tc::mbar_wait(p_full, j & 1);
+            auto issue_pv = [&](int i, int j) {      // O_i += P_i V(j)
+                tc::mbar_wait(&p_full[i], j & 1);
                 tc::fence_after();
-                const int s = j & 1;
-                const uint32_t sV = tc::smem_u32(smem + L::kV + s * L::kTile);
-                const uint32_t sP = tc::smem_u32(smem + L::kP + s * TQ * TK * 2);
+                const uint32_t sP = tc::smem_u32(smem + L::kP + i * TQ * TK * 2);
+                const uint32_t sV = slot_addr(2 * j + 1);
 #pragma unroll
                 for (int kk = 0; kk < TK / 16; ++kk) {
                     const uint32_t aoff = (kk >> 2) * 16384 + (kk & 3) * 32;   // P: K-major
-                    tc::mma_bf16(tmem + kColO, tc::smem_desc(sP + aoff, 16, 1024),
+                    tc::mma_bf16(tmem + 256 + i * 128, tc::smem_desc(sP + aoff, 16, 1024),
                                  tc::smem_desc(sV + kk * 2048, 16384, 1024),  // V: MN-major
                                  idO, (j | kk) != 0);
                 }
-                tc::commit(&o_done[s]);
-                tc::commit(&kv_empty[s]);
+            };
+            tc::mbar_wait(q_full, 0);
+            tc::fence_after();
+            wait_full(0);
+            issue_s(0, 0);
+            if (nkb1 > 0) issue_s(1, 0);
+            tc::commit(&empty[0]);
+            for (int j = 0; j < nkb; ++j) {
+                wait_full(2 * j + 1);
+                if (j < nkb0) issue_pv(0, j);
+                if (j + 1 < nkb) wait_full(2 * j + 2);
+                if (j + 1 < nkb0) issue_s(0, j + 1);
+                if (j < nkb1) issue_pv(1, j);
+                tc::commit(&empty[(2 * j + 1) % kFwdSlots]);
+                if (j + 1 < nkb1) issue_s(1, j + 1);
+                if (j + 1 < nkb) tc::commit(&empty[(2 * j + 2) % kFwdSlots]);
             }
+            tc::commit(o_full);
         }
         __syncwarp();
-    } else {
+    } else if (warp < 8) {
         // ---------------------------------------------------------- softmax
-        const int r = threadIdx.x;            // query row == TMEM lane
-        const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-        const int qp = (r < rows) ? sg.kv_ctx + q0 + r : -1;
+        tc::setmaxnreg_inc<224>();
+        const int grp = warp >> 2;             // Q tile of this warpgroup
+        const int r = threadIdx.x & 127;       // query row == TMEM lane
+        const int rows = grp ? rows1 : rows0;
+        const int my_nkb = grp ? nkb1 : nkb0;
+        const int qt0 = q0 + grp * TQ;          // first query of the tile (segment-relative)
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        const uint32_t colS = grp * TK, colO = 256 + grp * 128;
+        const int qp = (r < rows) ? sg.kv_ctx + qt0 + r : -1;
         const float c2 = a.scale * kLog2e;
-        const int first_q = sg.kv_ctx + q0;   // smallest query position of the block
+        const int first_q = sg.kv_ctx + qt0;
         float m_run = -INFINITY, l = 0.f;
-        for (int j = 0; j < nkb; ++j) {
-            const int s = j & 1;
-            tc::mbar_wait(&s_full[s], (j >> 1) & 1);
+        uint8_t* prow = smem + L::kP + grp * TQ * TK * 2;
+        for (int j = 0; j < my_nkb; ++j) {
+            tc::mbar_wait(&s_full[grp], j & 1);
             tc::fence_after();
-            const uint32_t sb = lane_base + kColS + s * TK;
             const int key0 = j * TK;
             const bool need_mask = (key0 + TK - 1 > first_q) || rows < TQ;
-            // the whole 128-column score row in registers: 4 loads, one wait
             float sv[TK / 32][32];
 #pragma unroll
-            for (int c = 0; c < TK / 32; ++c) tc::tmem_ld32_async(sb + c * 32, sv[c]);
+            for (int c = 0; c < TK / 32; ++c) tc::tmem_ld32_async(lane_base + colS + c * 32, sv[c]);
             tc::tmem_wait_ld();
 #pragma unroll
             for (int c = 0; c < TK / 32; ++c) tc::reg_fence(sv[c]);
-            // pass 1: row max of the raw scores (scale > 0 commutes with max);
-            // 8 independent partial maxima so the reduction is not one long
-            // dependency chain (one softmax warp per SMSP: no TLP to hide it).
-            float mx8[8];
+            // Causal / ragged tiles (at most two per query tile) mask in
+            // place; interior tiles skip every compare and select.
+            if (need_mask) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) mx8[q] = -INFINITY;
+                for (int c = 0; c < TK / 32; ++c) {
+                    const int lim = qp - (key0 + c * 32);   // keys i <= lim visible
 #pragma unroll
-            for (int c = 0; c < TK / 32; ++c) {
-                const int lim = need_mask ? qp - (key0 + c * 32) : 32;   // keys i <= lim visible
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const float x = (need_mask && i > lim) ? -INFINITY : sv[c][i];
-                    mx8[i & 7] = fmaxf(mx8[i & 7], x);
+                    for (int i = 0; i < 32; ++i) sv[c][i] = i > lim ? -INFINITY : sv[c][i];
                 }
             }
-            const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                                     fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+            const float mraw = row_max(sv);
             const float mt = mraw * c2;
             const bool grow = mt > m_run + kRescaleSlack || (m_run == -INFINITY && mt > -INFINITY);
-            const bool rescale = __any_sync(0xffffffffu, grow) && j > 0;
-            if (rescale) {
-                // O must be final up to tile j-1 before it is rescaled
-                tc::mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-                tc::fence_after();
-            }
-            // P buffer (j & 1) was last read by PV(j-2)
-            tc::mbar_wait(&o_done[j & 1], ((j >> 1) & 1) ^ 1);
-            tc::fence_after();
-            uint8_t* sP = smem + L::kP + (j & 1) * TQ * TK * 2;
-            if (rescale) {
+            // O_i is final through tile j-1 here (S_i(j) was issued after PV_i(j-1))
+            if (__any_sync(0xffffffffu, grow) && j > 0) {
                 const float alpha = grow ? ex2(m_run - mt) : 1.f;
 #pragma unroll 1
                 for (int c = 0; c < HD / 32; ++c) {
                     float o[32];
-                    tc::tmem_ld32(lane_base + kColO + c * 32, o);
+                    tc::tmem_ld32(lane_base + colO + c * 32, o);
 #pragma unroll
                     for (int i = 0; i < 32; ++i) o[i] *= alpha;
-                    tc::tmem_st32(lane_base + kColO + c * 32, o);
+                    tc::tmem_st32(lane_base + colO + c * 32, o);
                 }
                 if (grow) l *= alpha;
             }
             if (grow) m_run = mt;
             const float mu = (m_run == -INFINITY) ? 0.f : m_run;
-            float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};   // independent partial sums
-            uint8_t* prow = sP;   // this tile's P buffer
-#pragma unroll
-            for (int c = 0; c < TK / 32; ++c) {
-                const float* v = sv[c];
-                uint32_t pk[16];
-                const int lim = need_mask ? qp - (key0 + c * 32) : 32;
-#pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    float p0 = ex2(fmaf(v[i], c2, -mu));
-                    float p1 = ex2(fmaf(v[i + 1], c2, -mu));
-                    if (need_mask) {
-                        p0 = i <= lim ? p0 : 0.f;
-                        p1 = i + 1 <= lim ? p1 : 0.f;
-                    }
-                    l8[(i >> 1) & 7] += p0 + p1;
-                    __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-                    pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int chunk = c * 4 + q;       // 16-byte chunk index along keys
-                    *reinterpret_cast<uint4*>(prow + tile_off(r, chunk)) =
-                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-                }
-            }
-            l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
+            l += exp_pack_store(sv, c2, mu, prow, r);
             tc::fence_proxy_async();
             tc::fence_before();
-            tc::mbar_arrive(p_full);
+            tc::mbar_arrive(&p_full[grp]);
         }
-        tc::mbar_wait(&o_done[(nkb - 1) & 1], ((nkb - 1) >> 1) & 1);
-        tc::fence_after();
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        bf16* orow = static_cast<bf16*>(a.o) + (static_cast<long long>(sg.q_start + q0 + r) * a.H + h) * HD;
+        if (rows > 0) {
+            tc::mbar_wait(o_full, 0);
+            tc::fence_after();
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            bf16* orow = static_cast<bf16*>(a.o) + (static_cast<long long>(sg.q_start + qt0 + r) * a.H + h) * HD;
 #pragma unroll 1
-        for (int c = 0; c < HD / 32; ++c) {
-            float o[32];
-            tc::tmem_ld32(lane_base + kColO + c * 32, o);
-            if (r < rows) {
+            for (int c = 0; c < HD / 32; ++c) {
+                float o[32];
+                tc::tmem_ld32(lane_base + colO + c * 32, o);
+                if (r < rows) {
 #pragma unroll
-                for (int i = 0; i < 32; i += 8) {
-                    uint4 raw;
-                    __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&raw);
+                    for (int i = 0; i < 32; i += 8) {
+                        uint4 raw;
+                        __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&raw);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        hh[k] = __floats2bfloat162_rn(o[i + 2 * k] * inv, o[i + 2 * k + 1] * inv);
-                    *reinterpret_cast<uint4*>(orow + c * 32 + i) = raw;
+                        for (int k = 0; k < 4; ++k)
+                            hh[k] = __floats2bfloat162_rn(o[i + 2 * k] * inv, o[i + 2 * k + 1] * inv);
+                        *reinterpret_cast<uint4*>(orow + c * 32 + i) = raw;
+                    }
                 }
             }
+            if (r < rows)
+                a.lse[static_cast<long long>(h) * a.T + sg.q_start + qt0 + r] =
+                    l > 0.f ? m_run + log2f(l) : INFINITY;
         }
-        if (r < rows)
-            a.lse[static_cast<long long>(h) * a.T + sg.q_start + q0 + r] =
-                l > 0.f ? m_run + log2f(l) : INFINITY;
         tc::fence_before();
     }
     __syncthreads();
-    if (warp == 4) {
+    if (warp == 8) {
         tc::fence_after();
         tc::tmem_dealloc(tmem, 512);
     }
@@ -327,10 +369,9 @@ void launch_fwd_tc(const AttnArgs& a, cudaStream_t s) {
         EPP_CUDA(cudaFuncSetAttribute(attn_fwd_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
         cfg = true;
     }
-    attn_fwd_tc<HD><<<dim3(a.nqwork128, a.H), kThreadsTc, L::kAlloc, s>>>(a, *a.maps);
+    attn_fwd_tc<HD><<<dim3(a.nqwork256, a.H), kThreadsFwd, L::kAlloc, s>>>(a, *a.maps);
     EPP_CHECK_LAUNCH();
 }
-
 
 // ===========================================================================
 // Backward.  Two kernels, no atomics, deterministic:
@@ -828,7 +869,7 @@ void launch_bwd_tc(const AttnArgs& a, cudaStream_t s) {
 }  // namespace
 
 bool attn_fwd_tc_supported(const AttnArgs& a) {
-    return a.dtype == DType::BF16 && (a.hd == 64 || a.hd == 128) && a.qwork128 != nullptr &&
+    return a.dtype == DType::BF16 && (a.hd == 64 || a.hd == 128) && a.qwork256 != nullptr &&
            a.maps != nullptr;
 }
 
@@ -844,7 +885,7 @@ void attn_bwd_tc_main(const AttnArgs& a, cudaStream_t s) {
 }
 
 void attn_fwd_tc(const AttnArgs& a, cudaStream_t s) {
-    if (a.nqwork128 == 0) return;
+    if (a.nqwork256 == 0) return;
     ProfScope prof(kProfAttnFwd, 4.0 * a.H * a.hd * a.pairs, s);
     if (a.hd == 64) launch_fwd_tc<64>(a, s);
     else launch_fwd_tc<128>(a, s);

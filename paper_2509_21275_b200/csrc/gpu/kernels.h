@@ -97,6 +97,8 @@ struct AttnArgs {
     int nqwork128 = 0;
     const AttnWork* kwork128 = nullptr;   // 128-key blocks (tcgen05 kernels)
     int nkwork128 = 0;
+    const AttnWork* qwork256 = nullptr;   // 256-row query blocks (tcgen05 forward: 2 tiles / CTA)
+    int nqwork256 = 0;
     int T = 0;
     int H = 0, Hkv = 0, hd = 0;
     int layer = 0;

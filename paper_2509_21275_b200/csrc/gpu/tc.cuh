@@ -200,5 +200,16 @@ __device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, boo
                  : "memory");
 }
 
+// Warpgroup-wide register budget hand-off (every warp of the warpgroup
+// executes the same instruction).
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 }  // namespace tc
 }  // namespace eppk
