@@ -66,15 +66,50 @@ __device__ __forceinline__ uint32_t tile_off(int row, int chunk) {
     return static_cast<uint32_t>((chunk >> 3) * 16384 + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
 }
 
-// 2^x on the FMA pipe (Cody-Waite split + degree-3 minimax, rel. err 7.5e-5,
-// far below the bf16 rounding of P): offloads part of the exponentials from
-// the MUFU unit, which a 128-wide softmax row otherwise saturates.
-__device__ __forceinline__ float ex2_fma(float x) {
-    x = fmaxf(x, -126.f);
-    const float t = x + 12582912.f;                  // 1.5 * 2^23: round to integer
-    const float f = x - (t - 12582912.f);            // f in [-0.5, 0.5]
-    float p = fmaf(fmaf(fmaf(0.05517025f, f, 0.2426079f), f, 0.6932609f), f, 0.9999283f);
-    return __int_as_float(__float_as_int(t) * (1 << 23) + __float_as_int(p));
+// Packed fp32x2 arithmetic (FFMA2 / FADD2 on sm_100: two lanes of work per
+// issue slot).
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// 2^x for a pair on the FMA pipe (Cody-Waite split + degree-3 minimax, rel.
+// err 7.5e-5, far below the bf16 rounding of P): offloads part of the
+// exponentials from the MUFU unit, which 128-wide softmax rows saturate.
+__device__ __forceinline__ void ex2_fma2(uint64_t x, float& p0, float& p1) {
+    float x0, x1;
+    f2unpack(x, x0, x1);
+    x = f2pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+    const uint64_t magic = f2pack(12582912.f, 12582912.f);     // 1.5 * 2^23: round to integer
+    const uint64_t t = fadd2(x, magic);
+    const uint64_t f = fsub2(x, fsub2(t, magic));              // f in [-0.5, 0.5]
+    uint64_t p = ffma2(f2pack(0.05517025f, 0.05517025f), f, f2pack(0.2426079f, 0.2426079f));
+    p = ffma2(p, f, f2pack(0.6932609f, 0.6932609f));
+    p = ffma2(p, f, f2pack(0.9999283f, 0.9999283f));
+    float t0, t1, q0, q1;
+    f2unpack(t, t0, t1);
+    f2unpack(p, q0, q1);
+    p0 = __int_as_float(__float_as_int(t0) * (1 << 23) + __float_as_int(q0));
+    p1 = __int_as_float(__float_as_int(t1) * (1 << 23) + __float_as_int(q1));
 }
 
 __device__ __forceinline__ float max3(float a, float b, float c) {
@@ -97,20 +132,27 @@ __device__ __forceinline__ float row_max(const float (&sv)[TK / 32][32]) {
 }
 
 // P = 2^(s*c2 - mu) -> bf16, stored in the UMMA K-major swizzled layout;
-// returns the fp32 row sum.  One element in four takes the FMA-pipe exp2.
+// returns the fp32 row sum.  One pair in four takes the FMA-pipe exp2.
 __device__ __forceinline__ float exp_pack_store(const float (&sv)[TK / 32][32], float c2, float mu,
                                                 uint8_t* prow, int r) {
-    float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const uint64_t c2x = f2pack(c2, c2), nmu = f2pack(-mu, -mu);
+    uint64_t l4[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int c = 0; c < TK / 32; ++c) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-            const float x0 = fmaf(sv[c][i], c2, -mu), x1 = fmaf(sv[c][i + 1], c2, -mu);
-            const bool emu = (i & 7) == 6;
-            const float p0 = emu ? ex2_fma(x0) : ex2(x0);
-            const float p1 = emu ? ex2_fma(x1) : ex2(x1);
-            l8[(i >> 1) & 7] += p0 + p1;
+            const uint64_t x = ffma2(f2pack(sv[c][i], sv[c][i + 1]), c2x, nmu);
+            float p0, p1;
+            if ((i & 7) == 6) {
+                ex2_fma2(x, p0, p1);
+            } else {
+                float x0, x1;
+                f2unpack(x, x0, x1);
+                p0 = ex2(x0);
+                p1 = ex2(x1);
+            }
+            l4[(i >> 1) & 3] = fadd2(l4[(i >> 1) & 3], f2pack(p0, p1));
             __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
             pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
         }
@@ -119,7 +161,10 @@ __device__ __forceinline__ float exp_pack_store(const float (&sv)[TK / 32][32], 
             *reinterpret_cast<uint4*>(prow + tile_off(r, c * 4 + q)) =
                 make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
     }
-    return ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
+    const uint64_t s2 = fadd2(fadd2(l4[0], l4[1]), fadd2(l4[2], l4[3]));
+    float a, b;
+    f2unpack(s2, a, b);
+    return a + b;
 }
 
 // Forward: one CTA = 256 query rows (two 128-row tiles Q0, Q1) of one head,
