@@ -18,7 +18,6 @@ namespace {
 
 constexpr int TQ = 128;            // query rows per CTA (= TMEM lanes)
 constexpr int TK = 128;            // keys per tile
-constexpr int kThreadsTc = 192;    // backward: warps 0-3 softmax, 4 MMA, 5 TMA / loads
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleSlack = 8.f;   // log2 units: p <= 2^8 before a rescale
 
@@ -420,22 +419,28 @@ void launch_fwd_tc(const AttnArgs& a, cudaStream_t s) {
 
 // ===========================================================================
 // Backward.  Two kernels, no atomics, deterministic:
-//   dq  (grid: 128-row query blocks x H), 64-key tiles, 3-stage K/V ring:
+//   dq  (grid: 128-row query blocks x H), 64-key tiles, 4-stage K/V ring:
 //        S = Q K^T, dP = dO V^T -> TMEM (double-buffered);
 //        dS = P (dP - delta) -> smem (bf16, double-buffered);
 //        dQ += dS K -> TMEM; dQ * scale -> fp32 global.
 //   dkv (grid: 128-key blocks x Hkv, GQA heads looped in the CTA), 64-row
-//        query tiles, 2-stage Q/dO ring:
+//        query tiles, 3-stage Q/dO ring:
 //        S^T = K Q^T, dP^T = V dO^T -> TMEM (double-buffered);
 //        P^T, dS^T -> smem (bf16, double-buffered);
 //        dV += P^T dO, dK += dS^T Q -> TMEM; then RMW into the fp32 dK/dV
 //        accumulators of the segment (persist across a sequence's chunks).
 // In both, the MMA warp issues the score MMAs of step i before the gradient
-// MMAs of step i-1, so the tensor core runs while the softmax warps work.
+// MMAs of step i-1, and two softmax warpgroups take alternate steps (step i
+// -> group i & 1, which owns TMEM buffer i & 1 and smem buffer i & 1), so
+// one group's elementwise work overlaps the other's and the tensor core.
 // The same swizzled [rows x hd] smem tile is a K-major operand in one MMA and
 // (descriptor LBO = column-block stride, +2 KB per K16 step) an MN-major
 // operand in another, so each tile is loaded once.
 // ===========================================================================
+
+// Warps 0-3 / 4-7 softmax groups, 8 MMA, 9 loads, 10-11 idle (whole
+// warpgroups, for setmaxnreg).
+constexpr int kThreadsBwd = 384;
 
 // [ROWS x HD] tile, HD/64 column blocks of ROWS x 128 B, 128B-swizzled.
 template <int ROWS>
@@ -443,9 +448,51 @@ __device__ __forceinline__ uint32_t toff(int row, int chunk) {
     return static_cast<uint32_t>((chunk >> 3) * (ROWS * 128) + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
 }
 
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t bf2(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
 constexpr int TB = 64;    // secondary tile (keys in dq, queries in dkv)
 constexpr int kDqStages = 4;    // K/V ring depth of the dq kernel
 constexpr int kDkvStages = 3;   // Q/dO ring depth of the dk/dv kernel
+
+// dS for one 64-key tile of a query row: dS = 2^(s*c2 - lse) * (dP - delta).
+// MASK: keys k > lim are invisible (causal diagonal / ragged block).
+template <bool MASK>
+__device__ __forceinline__ void dq_row_tile(const float (&s)[TB / 32][32], const float (&dp)[TB / 32][32],
+                                            float c2, float lse, float dlt, int lim0, uint32_t (&pk)[32]) {
+    const uint64_t c2x = f2pack(c2, c2), nl = f2pack(-lse, -lse), dl = f2pack(dlt, dlt);
+#pragma unroll
+    for (int c = 0; c < TB / 32; ++c) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+            const uint64_t x = ffma2(f2pack(s[c][i], s[c][i + 1]), c2x, nl);
+            float p0, p1;
+            if ((i & 7) == 6) {
+                ex2_fma2(x, p0, p1);
+            } else {
+                float x0, x1;
+                f2unpack(x, x0, x1);
+                p0 = ex2(x0);
+                p1 = ex2(x1);
+            }
+            float d0, d1;
+            f2unpack(fmul2(f2pack(p0, p1), fsub2(f2pack(dp[c][i], dp[c][i + 1]), dl)), d0, d1);
+            if (MASK) {
+                const int lim = lim0 - c * 32;
+                d0 = i <= lim ? d0 : 0.f;
+                d1 = i + 1 <= lim ? d1 : 0.f;
+            }
+            pk[c * 16 + (i >> 1)] = bf2(d0, d1);
+        }
+    }
+}
 
 template <int HD>
 struct DqSmem {
@@ -462,8 +509,8 @@ struct DqSmem {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a,
-                                                                const __grid_constant__ AttnMaps mp) {
+__global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs a,
+                                                                 const __grid_constant__ AttnMaps mp) {
     using L = DqSmem<HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -475,7 +522,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
     uint64_t* s_full = kv_empty + kDqStages;          // [2]
     uint64_t* p_full = s_full + 2;                    // [2]
     uint64_t* dq_done = p_full + 2;                   // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 2);
+    uint64_t* acc_full = dq_done + 2;                 // all MMAs retired (epilogue)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
     const AttnWork w = a.qwork128[blockIdx.x];
     const AttnSeg sg = a.segs[w.seg];
@@ -499,16 +547,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
             tc::mbar_init(&p_full[b], TQ);
             tc::mbar_init(&dq_done[b], 1);
         }
+        tc::mbar_init(acc_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 4) tc::tmem_alloc(tmem_slot, 512);
+    if (warp == 8) tc::tmem_alloc(tmem_slot, 512);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t kColS = 0, kColP = 128, kColQ = 256;
 
-    if (warp == 5) {
+    if (warp >= 8) tc::setmaxnreg_dec<56>();
+    if (warp == 9) {
         if (lane == 0) {
             const CUtensorMap* mk = &mp.kv64[2 * sg.tma_map];
             const CUtensorMap* mv = &mp.kv64[2 * sg.tma_map + 1];
@@ -525,7 +575,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
             }
         }
         __syncwarp();
-    } else if (warp == 4) {
+    } else if (warp == 8) {
         if (lane == 0) {
             constexpr uint32_t idS = tc::instr_desc_mn(TQ, TB, false, false);
             constexpr uint32_t idQ = tc::instr_desc_mn(TQ, HD, false, true);
@@ -548,10 +598,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
             for (int j = 0; j < nkb; ++j) {
                 const int b = j & 1, st = j % kDqStages;
                 tc::mbar_wait(&kv_full[st], (j / kDqStages) & 1);
-                tc::fence_proxy_async();
                 tc::fence_after();
                 const uint32_t sK = tc::smem_u32(smem + L::kK + st * L::kSmall);
                 const uint32_t sV = tc::smem_u32(smem + L::kV + st * L::kSmall);
+                // S/dP buffer b was last read by the softmax of step j-2,
+                // which also produced dS(j-2): grad(j-2) waited on it.
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
                     const uint32_t aoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
@@ -565,19 +616,22 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
                 if (j > 0) grad(j - 1);
             }
             grad(nkb - 1);
+            tc::commit(acc_full);
         }
         __syncwarp();
-    } else {
-        const int r = threadIdx.x;
-        const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    } else if (warp < 8) {
+        tc::setmaxnreg_inc<224>();
+        const int grp = warp >> 2;
+        const int r = threadIdx.x & 127;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
         const int qp = (r < rows) ? sg.kv_ctx + q0 + r : -1;
         const float c2 = a.scale * kLog2e;
         const int first_q = sg.kv_ctx + q0;
         const long long t = row0 + min(r, rows - 1);
         const float lse = a.lse[static_cast<long long>(h) * a.T + t];
         const float dlt = a.delta[static_cast<long long>(h) * a.T + t];
-        for (int j = 0; j < nkb; ++j) {
-            const int b = j & 1;
+        for (int j = grp; j < nkb; j += 2) {
+            const int b = grp;
             tc::mbar_wait(&s_full[b], (j >> 1) & 1);
             tc::fence_after();
             const int key0 = j * TB;
@@ -595,23 +649,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
                 tc::reg_fence(sall[c]);
                 tc::reg_fence(pall[c]);
             }
-#pragma unroll
-            for (int c = 0; c < TB / 32; ++c) {
-                const float* sv = sall[c];
-                const float* pv = pall[c];
-                const int lim = need_mask ? qp - (key0 + c * 32) : 32;
-#pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    float p0 = ex2(fmaf(sv[i], c2, -lse));
-                    float p1 = ex2(fmaf(sv[i + 1], c2, -lse));
-                    if (need_mask) {
-                        p0 = i <= lim ? p0 : 0.f;
-                        p1 = i + 1 <= lim ? p1 : 0.f;
-                    }
-                    __nv_bfloat162 b2 = __floats2bfloat162_rn(p0 * (pv[i] - dlt), p1 * (pv[i + 1] - dlt));
-                    pk[c * 16 + (i >> 1)] = *reinterpret_cast<uint32_t*>(&b2);
-                }
-            }
+            if (need_mask) dq_row_tile<true>(sall, pall, c2, lse, dlt, qp - key0, pk);
+            else dq_row_tile<false>(sall, pall, c2, lse, dlt, 0, pk);
             tc::mbar_wait(&dq_done[b], ((j >> 1) & 1) ^ 1);   // dQ(j-2) finished reading buffer b
             tc::fence_after();
             uint8_t* sS = smem + L::kS + b * 128 * TB * 2;
@@ -623,11 +662,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
             tc::fence_before();
             tc::mbar_arrive(&p_full[b]);
         }
-        tc::mbar_wait(&dq_done[(nkb - 1) & 1], ((nkb - 1) >> 1) & 1);
+        // (a group that skipped the last steps must not wait on a buffer
+        // barrier whose earlier phases it never observed: parity would alias)
+        tc::mbar_wait(acc_full, 0);
         tc::fence_after();
         float* drow = a.dq + ((row0 + r) * a.H + h) * HD;
 #pragma unroll 1
-        for (int c = 0; c < HD / 32; ++c) {
+        for (int c = grp * (HD / 64); c < (grp + 1) * (HD / 64); ++c) {   // each group: half the columns
             float v[32];
             tc::tmem_ld32(lane_base + kColQ + c * 32, v);
             if (r < rows) {
@@ -640,9 +681,50 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dq_tc(const AttnArgs a
         tc::fence_before();
     }
     __syncthreads();
-    if (warp == 4) {
+    if (warp == 8) {
         tc::fence_after();
         tc::tmem_dealloc(tmem, 512);
+    }
+}
+
+// P^T and dS^T for one 64-query tile of a key row.  MASK: query qi is
+// visible iff qmin <= qi < qmax.
+template <bool MASK>
+__device__ __forceinline__ void dkv_row_tile(const float (&s)[TB / 32][32], const float (&dp)[TB / 32][32],
+                                             float c2, const float* lse_s, const float* dl_s, int qmin,
+                                             int qmax, uint32_t (&pk)[32], uint32_t (&dk)[32]) {
+#pragma unroll
+    for (int c = 0; c < TB / 32; ++c) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            const float4 l4 = *reinterpret_cast<const float4*>(lse_s + c * 32 + i);
+            const float4 d4 = *reinterpret_cast<const float4*>(dl_s + c * 32 + i);
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+            const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+            for (int e = 0; e < 4; e += 2) {
+                const int ii = i + e;
+                const float x0 = fmaf(s[c][ii], c2, -lv[e]), x1 = fmaf(s[c][ii + 1], c2, -lv[e + 1]);
+                float p0, p1;
+                if ((ii & 7) == 6) {
+                    ex2_fma2(f2pack(x0, x1), p0, p1);
+                } else {
+                    p0 = ex2(x0);
+                    p1 = ex2(x1);
+                }
+                if (MASK) {
+                    const int q = c * 32 + ii;
+                    p0 = (q >= qmin && q < qmax) ? p0 : 0.f;
+                    p1 = (q + 1 >= qmin && q + 1 < qmax) ? p1 : 0.f;
+                }
+                float d0, d1;
+                f2unpack(fmul2(f2pack(p0, p1),
+                               fsub2(f2pack(dp[c][ii], dp[c][ii + 1]), f2pack(dv[e], dv[e + 1]))),
+                         d0, d1);
+                pk[c * 16 + (ii >> 1)] = bf2(p0, p1);
+                dk[c * 16 + (ii >> 1)] = bf2(d0, d1);
+            }
+        }
     }
 }
 
@@ -664,8 +746,8 @@ struct DkvSmem {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs a,
-                                                                 const __grid_constant__ AttnMaps mp) {
+__global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs a,
+                                                                  const __grid_constant__ AttnMaps mp) {
     using L = DkvSmem<HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -677,7 +759,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
     uint64_t* s_full = qd_empty + kDkvStages;         // [2]
     uint64_t* p_full = s_full + 2;                    // [2]
     uint64_t* pd_free = p_full + 2;                   // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pd_free + 2);
+    uint64_t* acc_full = pd_free + 2;                 // all MMAs retired (epilogue)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
     float* sLse = reinterpret_cast<float*>(smem + L::kLse);
     float* sDelta = reinterpret_cast<float*>(smem + L::kDelta);
 
@@ -705,16 +788,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
             tc::mbar_init(&p_full[b], TQ);
             tc::mbar_init(&pd_free[b], 1);
         }
+        tc::mbar_init(acc_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 4) tc::tmem_alloc(tmem_slot, 512);
+    if (warp == 8) tc::tmem_alloc(tmem_slot, 512);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t kColS = 0, kColP = 128, kColV = 256, kColK = 256 + HD;
 
-    if (warp == 5) {
+    if (warp >= 8) tc::setmaxnreg_dec<56>();
+    if (warp == 9) {
         const CUtensorMap* mk = &mp.kv128[2 * sg.tma_map];
         const CUtensorMap* mv = &mp.kv128[2 * sg.tma_map + 1];
         if (lane == 0) {
@@ -744,7 +829,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
             }
             tc::cp_async_arrive(&qd_full[st]);
         }
-    } else if (warp == 4) {
+    } else if (warp == 8) {
         if (lane == 0) {
             constexpr uint32_t idS = tc::instr_desc_mn(TK, TB, false, false);
             constexpr uint32_t idD = tc::instr_desc_mn(TK, HD, false, true);
@@ -789,15 +874,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
                 if (it > 0) grad(it - 1);
             }
             grad(iters - 1);
+            tc::commit(acc_full);
         }
         __syncwarp();
-    } else {
-        const int r = threadIdx.x;            // key row == TMEM lane
-        const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    } else if (warp < 8) {
+        tc::setmaxnreg_inc<224>();
+        const int grp = warp >> 2;
+        const int r = threadIdx.x & 127;      // key row == TMEM lane
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
         const int kp = k0 + r;
         const float c2 = a.scale * kLog2e;
-        for (int it = 0; it < iters; ++it) {
-            const int b = it & 1;
+        for (int it = grp; it < iters; it += 2) {
+            const int b = grp;
             const int q0 = (qb_first + it % per_head) * TB;
             const int rows = min(TB, sg.q_len - q0);
             const int first_q = sg.kv_ctx + q0;
@@ -819,29 +907,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
                 tc::reg_fence(sall[c]);
                 tc::reg_fence(dall[c]);
             }
-#pragma unroll
-            for (int c = 0; c < TB / 32; ++c) {
-                const float* sv = sall[c];
-                const float* dv = dall[c];
-                // query qi visible to key kp iff qi < rows && qi >= kp - first_q
-                const int qmin = kp - first_q - c * 32;
-                const int qmax = rows - c * 32;
-#pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    float p[2], d[2];
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int qi = c * 32 + i + e;
-                        p[e] = ex2(fmaf(sv[i + e], c2, -lse_s[qi]));
-                        if (need_mask) p[e] = (i + e >= qmin && i + e < qmax) ? p[e] : 0.f;
-                        d[e] = p[e] * (dv[i + e] - dl_s[qi]);
-                    }
-                    __nv_bfloat162 b2 = __floats2bfloat162_rn(p[0], p[1]);
-                    pk[c * 16 + (i >> 1)] = *reinterpret_cast<uint32_t*>(&b2);
-                    __nv_bfloat162 d2 = __floats2bfloat162_rn(d[0], d[1]);
-                    dk[c * 16 + (i >> 1)] = *reinterpret_cast<uint32_t*>(&d2);
-                }
-            }
+            // query qi visible to key kp iff kp - first_q <= qi < rows
+            if (need_mask) dkv_row_tile<true>(sall, dall, c2, lse_s, dl_s, kp - first_q, rows, pk, dk);
+            else dkv_row_tile<false>(sall, dall, c2, lse_s, dl_s, 0, TB, pk, dk);
             tc::mbar_wait(&pd_free[b], ((it >> 1) & 1) ^ 1);   // grad(it-2) done with buffer b
             tc::fence_after();
             uint8_t* sP = smem + L::kP + b * 128 * TB * 2;
@@ -857,33 +925,32 @@ __global__ void __launch_bounds__(kThreadsTc, 1) attn_bwd_dkv_tc(const AttnArgs 
             tc::fence_before();
             tc::mbar_arrive(&p_full[b]);
         }
-        tc::mbar_wait(&pd_free[(iters - 1) & 1], ((iters - 1) >> 1) & 1);
+        tc::mbar_wait(acc_full, 0);
         tc::fence_after();
+        // group 0 adds dK (scaled), group 1 adds dV into the fp32 accumulators
         const long long kvs = static_cast<long long>(a.Hkv) * HD;
-        float* dkr = sg.dk + a.layer * sg.dkv_layer_stride + kvh * HD + (k0 + min(r, nkeys - 1)) * kvs;
-        float* dvr = sg.dv + a.layer * sg.dkv_layer_stride + kvh * HD + (k0 + min(r, nkeys - 1)) * kvs;
+        float* base = grp == 0 ? sg.dk : sg.dv;
+        float* drow = base + a.layer * sg.dkv_layer_stride + kvh * HD + (k0 + min(r, nkeys - 1)) * kvs;
+        const float mul = grp == 0 ? a.scale : 1.f;
+        const uint32_t col = grp == 0 ? kColK : kColV;
 #pragma unroll 1
         for (int c = 0; c < HD / 32; ++c) {
-            float kv[32], vv[32];
-            tc::tmem_ld32(lane_base + kColK + c * 32, kv);    // warp-collective: all lanes
-            tc::tmem_ld32(lane_base + kColV + c * 32, vv);
+            float v[32];
+            tc::tmem_ld32(lane_base + col + c * 32, v);    // warp-collective: all lanes
             if (r < nkeys) {
 #pragma unroll
                 for (int i = 0; i < 32; i += 4) {
-                    float4 x = *reinterpret_cast<float4*>(dkr + c * 32 + i);
-                    x.x += kv[i] * a.scale; x.y += kv[i + 1] * a.scale;
-                    x.z += kv[i + 2] * a.scale; x.w += kv[i + 3] * a.scale;
-                    *reinterpret_cast<float4*>(dkr + c * 32 + i) = x;
-                    float4 y = *reinterpret_cast<float4*>(dvr + c * 32 + i);
-                    y.x += vv[i]; y.y += vv[i + 1]; y.z += vv[i + 2]; y.w += vv[i + 3];
-                    *reinterpret_cast<float4*>(dvr + c * 32 + i) = y;
+                    float4 x = *reinterpret_cast<float4*>(drow + c * 32 + i);
+                    x.x += v[i] * mul; x.y += v[i + 1] * mul;
+                    x.z += v[i + 2] * mul; x.w += v[i + 3] * mul;
+                    *reinterpret_cast<float4*>(drow + c * 32 + i) = x;
                 }
             }
         }
         tc::fence_before();
     }
     __syncthreads();
-    if (warp == 4) {
+    if (warp == 8) {
         tc::fence_after();
         tc::tmem_dealloc(tmem, 512);
     }
@@ -901,12 +968,12 @@ void launch_bwd_tc(const AttnArgs& a, cudaStream_t s) {
     }
     if (a.nqwork128 > 0) {
         ProfScope prof(kProfAttnBwdDq, 6.0 * a.H * a.hd * a.pairs, s);     // executed: 3 matmuls
-        attn_bwd_dq_tc<HD><<<dim3(a.nqwork128, a.H), kThreadsTc, DqSmem<HD>::kAlloc, s>>>(a, *a.maps);
+        attn_bwd_dq_tc<HD><<<dim3(a.nqwork128, a.H), kThreadsBwd, DqSmem<HD>::kAlloc, s>>>(a, *a.maps);
         EPP_CHECK_LAUNCH();
     }
     if (a.nkwork128 > 0) {
         ProfScope prof(kProfAttnBwdDkv, 8.0 * a.H * a.hd * a.pairs, s);    // executed: 4 matmuls
-        attn_bwd_dkv_tc<HD><<<dim3(a.nkwork128, a.Hkv), kThreadsTc, DkvSmem<HD>::kAlloc, s>>>(a, *a.maps);
+        attn_bwd_dkv_tc<HD><<<dim3(a.nkwork128, a.Hkv), kThreadsBwd, DkvSmem<HD>::kAlloc, s>>>(a, *a.maps);
         EPP_CHECK_LAUNCH();
     }
 }
