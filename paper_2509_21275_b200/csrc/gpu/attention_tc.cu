@@ -460,7 +460,7 @@ __device__ __forceinline__ uint32_t bf2(float a, float b) {
 
 constexpr int TB = 64;    // secondary tile (keys in dq, queries in dkv)
 constexpr int kDqStages = 4;    // K/V ring depth of the dq kernel
-constexpr int kDkvStages = 3;   // Q/dO ring depth of the dk/dv kernel
+constexpr int kDkvStages = 4;   // Q/dO ring depth of the dk/dv kernel
 
 // dS for one 64-key tile of a query row: dS = 2^(s*c2 - lse) * (dP - delta).
 // MASK: keys k > lim are invisible (causal diagonal / ragged block).
@@ -523,7 +523,8 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
     uint64_t* p_full = s_full + 2;                    // [2]
     uint64_t* dq_done = p_full + 2;                   // [2]
     uint64_t* acc_full = dq_done + 2;                 // all MMAs retired (epilogue)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+    uint64_t* s_free = acc_full + 1;                  // [2] softmax has read S/dP buffer
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + 2);
 
     const AttnWork w = a.qwork128[blockIdx.x];
     const AttnSeg sg = a.segs[w.seg];
@@ -546,6 +547,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
             tc::mbar_init(&s_full[b], 1);
             tc::mbar_init(&p_full[b], TQ);
             tc::mbar_init(&dq_done[b], 1);
+            tc::mbar_init(&s_free[b], 4);
         }
         tc::mbar_init(acc_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -594,15 +596,13 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
                 tc::commit(&dq_done[b]);
                 tc::commit(&kv_empty[st]);
             };
-            tc::mbar_wait(q_full, 0);
-            for (int j = 0; j < nkb; ++j) {
+            auto scores = [&](int j) {   // S(j) = Q K(j)^T, dP(j) = dO V(j)^T
                 const int b = j & 1, st = j % kDqStages;
                 tc::mbar_wait(&kv_full[st], (j / kDqStages) & 1);
+                if (j >= 2) tc::mbar_wait(&s_free[b], ((j - 2) >> 1) & 1);   // softmax(j-2) read buffer b
                 tc::fence_after();
                 const uint32_t sK = tc::smem_u32(smem + L::kK + st * L::kSmall);
                 const uint32_t sV = tc::smem_u32(smem + L::kV + st * L::kSmall);
-                // S/dP buffer b was last read by the softmax of step j-2,
-                // which also produced dS(j-2): grad(j-2) waited on it.
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
                     const uint32_t aoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
@@ -613,9 +613,15 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
                                  tc::smem_desc(sV + boff, 16, 1024), idS, kk != 0);
                 }
                 tc::commit(&s_full[b]);
-                if (j > 0) grad(j - 1);
+            };
+            // one step of lookahead: the scores of step j+1 run on the
+            // tensor core while the softmax group of step j works
+            tc::mbar_wait(q_full, 0);
+            scores(0);
+            for (int j = 0; j < nkb; ++j) {
+                if (j + 1 < nkb) scores(j + 1);
+                grad(j);
             }
-            grad(nkb - 1);
             tc::commit(acc_full);
         }
         __syncwarp();
@@ -644,6 +650,9 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
                 tc::tmem_ld32_async(lane_base + kColP + b * TB + c * 32, pall[c]);
             }
             tc::tmem_wait_ld();
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&s_free[b]);
 #pragma unroll
             for (int c = 0; c < TB / 32; ++c) {
                 tc::reg_fence(sall[c]);
@@ -687,45 +696,65 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
     }
 }
 
-// P^T and dS^T for one 64-query tile of a key row.  MASK: query qi is
-// visible iff qmin <= qi < qmax.
+// P^T and dS^T for one 64-query tile of a key row.  The scores arrive with
+// lse and delta already subtracted (augmented K-step, see attn_bwd_dkv_tc):
+// P^T = 2^(S'^T c2), dS^T = P^T * dP'^T.  MASK: query qi is visible iff
+// qmin <= qi < qmax.
 template <bool MASK>
 __device__ __forceinline__ void dkv_row_tile(const float (&s)[TB / 32][32], const float (&dp)[TB / 32][32],
-                                             float c2, const float* lse_s, const float* dl_s, int qmin,
-                                             int qmax, uint32_t (&pk)[32], uint32_t (&dk)[32]) {
+                                             float c2, int qmin, int qmax, uint32_t (&pk)[32], uint32_t (&dk)[32]) {
+    const uint64_t c2x = f2pack(c2, c2);
 #pragma unroll
     for (int c = 0; c < TB / 32; ++c) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-            const float4 l4 = *reinterpret_cast<const float4*>(lse_s + c * 32 + i);
-            const float4 d4 = *reinterpret_cast<const float4*>(dl_s + c * 32 + i);
-            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-            const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
-#pragma unroll
-            for (int e = 0; e < 4; e += 2) {
-                const int ii = i + e;
-                const float x0 = fmaf(s[c][ii], c2, -lv[e]), x1 = fmaf(s[c][ii + 1], c2, -lv[e + 1]);
-                float p0, p1;
-                if ((ii & 7) == 6) {
-                    ex2_fma2(f2pack(x0, x1), p0, p1);
-                } else {
-                    p0 = ex2(x0);
-                    p1 = ex2(x1);
-                }
-                if (MASK) {
-                    const int q = c * 32 + ii;
-                    p0 = (q >= qmin && q < qmax) ? p0 : 0.f;
-                    p1 = (q + 1 >= qmin && q + 1 < qmax) ? p1 : 0.f;
-                }
-                float d0, d1;
-                f2unpack(fmul2(f2pack(p0, p1),
-                               fsub2(f2pack(dp[c][ii], dp[c][ii + 1]), f2pack(dv[e], dv[e + 1]))),
-                         d0, d1);
-                pk[c * 16 + (ii >> 1)] = bf2(p0, p1);
-                dk[c * 16 + (ii >> 1)] = bf2(d0, d1);
+        for (int i = 0; i < 32; i += 2) {
+            const uint64_t x = fmul2(f2pack(s[c][i], s[c][i + 1]), c2x);
+            float p0, p1;
+            if ((i & 7) == 6) {
+                ex2_fma2(x, p0, p1);
+            } else {
+                float x0, x1;
+                f2unpack(x, x0, x1);
+                p0 = ex2(x0);
+                p1 = ex2(x1);
             }
+            if (MASK) {
+                const int q = c * 32 + i;
+                p0 = (q >= qmin && q < qmax) ? p0 : 0.f;
+                p1 = (q + 1 >= qmin && q + 1 < qmax) ? p1 : 0.f;
+            }
+            float d0, d1;
+            f2unpack(fmul2(f2pack(p0, p1), f2pack(dp[c][i], dp[c][i + 1])), d0, d1);
+            pk[c * 16 + (i >> 1)] = bf2(p0, p1);
+            dk[c * 16 + (i >> 1)] = bf2(d0, d1);
         }
     }
+}
+
+// Augmented K-step operands (UMMA K-major, 32-byte swizzle: rows of 16 bf16,
+// 8-row atoms of 256 B, 16-byte chunk c of row r stored at c ^ ((r >> 2) & 1)).
+// Only columns 0-1 are ever non-zero.
+__device__ __forceinline__ uint32_t aug_off(int row) {
+    return static_cast<uint32_t>(row * 32 + ((((row >> 2) & 1)) << 4));
+}
+// hi + lo bf16 split of x (16 mantissa bits in the sum).
+__device__ __forceinline__ uint32_t bf_hilo(float x) {
+    const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+    __nv_bfloat162 v;
+    v.x = hi;
+    v.y = lo;
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+// SWIZZLE_32B descriptor (layout type 6), SBO = one 8-row atom.
+__device__ __forceinline__ uint64_t smem_desc_sw32(uint32_t addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((addr >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>((256 >> 4) & 0x3FFFu) << 32;
+    d |= 1ull << 46;
+    d |= 6ull << 61;
+    return d;
 }
 
 template <int HD>
@@ -736,11 +765,11 @@ struct DkvSmem {
     static constexpr int kV = kK + kBig;
     static constexpr int kQ = kV + kBig;                     // kDkvStages stages
     static constexpr int kO = kQ + kDkvStages * kSmall;
-    static constexpr int kP = kO + kDkvStages * kSmall;      // P^T [128 x 64] bf16 x 2
-    static constexpr int kS = kP + 2 * 128 * TB * 2;         // dS^T x 2
-    static constexpr int kLse = kS + 2 * 128 * TB * 2;       // [kDkvStages][64] floats
-    static constexpr int kDelta = kLse + kDkvStages * TB * 4;
-    static constexpr int kBar = kDelta + kDkvStages * TB * 4;
+    static constexpr int kKa = kO + kDkvStages * kSmall;     // augmented K-step: K, V [128 x 16] (ones)
+    static constexpr int kVa = kKa + 128 * 32;
+    static constexpr int kQa = kVa + 128 * 32;               // Q, dO [64 x 16] per stage (-lse/c2, -delta)
+    static constexpr int kOa = kQa + kDkvStages * TB * 32;
+    static constexpr int kBar = kOa + kDkvStages * TB * 32;
     static constexpr int kBytes = kBar + 24 * 8 + 16;
     static constexpr int kAlloc = kBytes + 1024;
 };
@@ -758,11 +787,8 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
     uint64_t* qd_empty = qd_full + kDkvStages;        // [kDkvStages]
     uint64_t* s_full = qd_empty + kDkvStages;         // [2]
     uint64_t* p_full = s_full + 2;                    // [2]
-    uint64_t* pd_free = p_full + 2;                   // [2]
-    uint64_t* acc_full = pd_free + 2;                 // all MMAs retired (epilogue)
+    uint64_t* acc_full = p_full + 2;                  // all MMAs retired (epilogue)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
-    float* sLse = reinterpret_cast<float*>(smem + L::kLse);
-    float* sDelta = reinterpret_cast<float*>(smem + L::kDelta);
 
     const AttnWork w = a.kwork128[blockIdx.x];
     const AttnSeg sg = a.segs[w.seg];
@@ -780,18 +806,29 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
     if (threadIdx.x == 0) {
         tc::mbar_init(kv_full, 1);
         for (int st = 0; st < kDkvStages; ++st) {
-            tc::mbar_init(&qd_full[st], 1 + 32);      // TMA expect_tx + 32 lse/delta cp.async arrivals
+            tc::mbar_init(&qd_full[st], 2);      // TMA expect_tx + the augmented-column writes
             tc::mbar_init(&qd_empty[st], 1);
         }
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&s_full[b], 1);
             tc::mbar_init(&p_full[b], TQ);
-            tc::mbar_init(&pd_free[b], 1);
         }
         tc::mbar_init(acc_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 8) tc::tmem_alloc(tmem_slot, 512);
+    // Augmented K-step: S'^T = [K | 1 1] [Q | hi lo]^T = S^T - lse/c2 and
+    // dP'^T = [V | 1 1] [dO | hi lo]^T = dP^T - delta, so the softmax needs no
+    // per-query operands (they would cost 512 B of shared-memory reads per
+    // thread and step).  Zero the augmented blocks; K/V get their ones here.
+    for (int i = threadIdx.x; i < (L::kBar - L::kKa) / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem + L::kKa)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    if (threadIdx.x < 128) {
+        *reinterpret_cast<uint32_t*>(smem + L::kKa + aug_off(threadIdx.x)) = 0x3F803F80u;   // bf16 (1, 1)
+        *reinterpret_cast<uint32_t*>(smem + L::kVa + aug_off(threadIdx.x)) = 0x3F803F80u;
+    }
+    tc::fence_proxy_async();
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
@@ -807,27 +844,51 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
             load_kv_tile<HD, 128>(smem + L::kK, mk, kv_full, kvh, sg.kv_row0 + k0, a.layer);
             load_kv_tile<HD, 128>(smem + L::kV, mv, kv_full, kvh, sg.kv_row0 + k0, a.layer);
         }
-        for (int it = 0; it < iters; ++it) {
-            const int st = it % kDkvStages;
-            tc::mbar_wait(&qd_empty[st], ((it / kDkvStages) & 1) ^ 1);
+        // augmented columns: -lse/c2 (hi, lo) for Q, -delta (hi, lo) for dO
+        // (rows past the end: 0, they are masked).  The global reads of step
+        // it+1 are issued before step it's stage is awaited (latency hidden).
+        const float inv_c2 = 1.f / (a.scale * kLog2e);
+        float lv[2], dv[2];
+        auto fetch = [&](int it) {
             const int hq = kvh * group + it / per_head;
             const int q0 = (qb_first + it % per_head) * TB;
             const int rows = min(TB, sg.q_len - q0);
+            const long long base = static_cast<long long>(hq) * a.T + sg.q_start + q0;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int i = lane + 32 * u;
+                lv[u] = i < rows ? a.lse[base + i] : 0.f;
+                dv[u] = i < rows ? a.delta[base + i] : 0.f;
+            }
+        };
+        fetch(0);
+        for (int it = 0; it < iters; ++it) {
+            const int st = it % kDkvStages;
+            const int hq = kvh * group + it / per_head;
+            const int q0 = (qb_first + it % per_head) * TB;
             const long long row0 = sg.q_start + q0;
+            uint32_t qa[2], oa[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                qa[u] = bf_hilo(-lv[u] * inv_c2);
+                oa[u] = bf_hilo(-dv[u]);
+            }
+            if (it + 1 < iters) fetch(it + 1);
+            tc::mbar_wait(&qd_empty[st], ((it / kDkvStages) & 1) ^ 1);
             if (lane == 0) {
                 tc::mbar_expect_tx(&qd_full[st], 2 * L::kSmall);
                 load_q_tile<HD, TB>(smem + L::kQ + st * L::kSmall, &mp.q64, &qd_full[st], hq, static_cast<int>(row0));
                 load_q_tile<HD, TB>(smem + L::kO + st * L::kSmall, &mp.do64, &qd_full[st], hq, static_cast<int>(row0));
             }
-            // lse / delta through cp.async (rows past the end read 0; they are masked)
-            const float* lg = a.lse + static_cast<long long>(hq) * a.T + row0;
-            const float* dg = a.delta + static_cast<long long>(hq) * a.T + row0;
-            for (int i = lane; i < TB; i += 32) {
-                const bool ok = i < rows;
-                tc::cp_async4_zfill(sLse + st * TB + i, ok ? lg + i : lg, ok);
-                tc::cp_async4_zfill(sDelta + st * TB + i, ok ? dg + i : dg, ok);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int i = lane + 32 * u;
+                *reinterpret_cast<uint32_t*>(smem + L::kQa + st * TB * 32 + aug_off(i)) = qa[u];
+                *reinterpret_cast<uint32_t*>(smem + L::kOa + st * TB * 32 + aug_off(i)) = oa[u];
             }
-            tc::cp_async_arrive(&qd_full[st]);
+            tc::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&qd_full[st]);
         }
     } else if (warp == 8) {
         if (lane == 0) {
@@ -835,29 +896,29 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
             constexpr uint32_t idD = tc::instr_desc_mn(TK, HD, false, true);
             const uint32_t sK = tc::smem_u32(smem + L::kK);
             const uint32_t sV = tc::smem_u32(smem + L::kV);
-            auto grad = [&](int it) {   // dV += P^T dO ; dK += dS^T Q
+            const uint32_t sKa = tc::smem_u32(smem + L::kKa);
+            const uint32_t sVa = tc::smem_u32(smem + L::kVa);
+            auto grad = [&](int it) {   // dV += P^T dO ; dK += dS^T Q  (P^T, dS^T from TMEM)
                 const int b = it & 1, st = it % kDkvStages;
                 tc::mbar_wait(&p_full[b], (it >> 1) & 1);
                 tc::fence_after();
-                const uint32_t sP = tc::smem_u32(smem + L::kP + b * 128 * TB * 2);
-                const uint32_t sS = tc::smem_u32(smem + L::kS + b * 128 * TB * 2);
                 const uint32_t sQ = tc::smem_u32(smem + L::kQ + st * L::kSmall);
                 const uint32_t sO = tc::smem_u32(smem + L::kO + st * L::kSmall);
 #pragma unroll
                 for (int kk = 0; kk < TB / 16; ++kk) {
-                    tc::mma_bf16(tmem + kColV, tc::smem_desc(sP + kk * 32, 16, 1024),
-                                 tc::smem_desc(sO + kk * 2048, TB * 128, 1024), idD, (it | kk) != 0);
-                    tc::mma_bf16(tmem + kColK, tc::smem_desc(sS + kk * 32, 16, 1024),
-                                 tc::smem_desc(sQ + kk * 2048, TB * 128, 1024), idD, (it | kk) != 0);
+                    tc::mma_bf16_ts(tmem + kColV, tmem + kColS + b * TB + kk * 8,
+                                    tc::smem_desc(sO + kk * 2048, TB * 128, 1024), idD, (it | kk) != 0);
+                    tc::mma_bf16_ts(tmem + kColK, tmem + kColP + b * TB + kk * 8,
+                                    tc::smem_desc(sQ + kk * 2048, TB * 128, 1024), idD, (it | kk) != 0);
                 }
                 tc::commit(&qd_empty[st]);
-                tc::commit(&pd_free[b]);
             };
-            tc::mbar_wait(kv_full, 0);
-            for (int it = 0; it < iters; ++it) {
+            // Buffer b of step it is rewritten by the scores of step it+2,
+            // issued after grad(it): in-order tcgen05 execution orders the
+            // TMEM reuse, and grad(it) itself waited for the softmax of it.
+            auto scores = [&](int it) {   // S^T = K Q^T, dP^T = V dO^T
                 const int b = it & 1, st = it % kDkvStages;
                 tc::mbar_wait(&qd_full[st], (it / kDkvStages) & 1);
-                tc::fence_proxy_async();
                 tc::fence_after();
                 const uint32_t sQ = tc::smem_u32(smem + L::kQ + st * L::kSmall);
                 const uint32_t sO = tc::smem_u32(smem + L::kO + st * L::kSmall);
@@ -870,10 +931,18 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
                     tc::mma_bf16(tmem + kColP + b * TB, tc::smem_desc(sV + aoff, 16, 1024),
                                  tc::smem_desc(sO + boff, 16, 1024), idS, kk != 0);
                 }
+                tc::mma_bf16(tmem + kColS + b * TB, smem_desc_sw32(sKa),
+                             smem_desc_sw32(tc::smem_u32(smem + L::kQa + st * TB * 32)), idS, 1);
+                tc::mma_bf16(tmem + kColP + b * TB, smem_desc_sw32(sVa),
+                             smem_desc_sw32(tc::smem_u32(smem + L::kOa + st * TB * 32)), idS, 1);
                 tc::commit(&s_full[b]);
-                if (it > 0) grad(it - 1);
+            };
+            tc::mbar_wait(kv_full, 0);
+            scores(0);
+            for (int it = 0; it < iters; ++it) {
+                if (it + 1 < iters) scores(it + 1);
+                grad(it);
             }
-            grad(iters - 1);
             tc::commit(acc_full);
         }
         __syncwarp();
@@ -892,8 +961,6 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
             const bool need_mask = (k0 + TK - 1 > first_q) || rows < TB;
             tc::mbar_wait(&s_full[b], (it >> 1) & 1);
             tc::fence_after();
-            const float* lse_s = sLse + (it % kDkvStages) * TB;
-            const float* dl_s = sDelta + (it % kDkvStages) * TB;
             uint32_t pk[32], dk[32];
             float sall[TB / 32][32], dall[TB / 32][32];
 #pragma unroll
@@ -908,20 +975,13 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
                 tc::reg_fence(dall[c]);
             }
             // query qi visible to key kp iff kp - first_q <= qi < rows
-            if (need_mask) dkv_row_tile<true>(sall, dall, c2, lse_s, dl_s, kp - first_q, rows, pk, dk);
-            else dkv_row_tile<false>(sall, dall, c2, lse_s, dl_s, 0, TB, pk, dk);
-            tc::mbar_wait(&pd_free[b], ((it >> 1) & 1) ^ 1);   // grad(it-2) done with buffer b
-            tc::fence_after();
-            uint8_t* sP = smem + L::kP + b * 128 * TB * 2;
-            uint8_t* sS = smem + L::kS + b * 128 * TB * 2;
-#pragma unroll
-            for (int q = 0; q < TB / 8; ++q) {
-                *reinterpret_cast<uint4*>(sP + toff<128>(r, q)) =
-                    make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-                *reinterpret_cast<uint4*>(sS + toff<128>(r, q)) =
-                    make_uint4(dk[4 * q], dk[4 * q + 1], dk[4 * q + 2], dk[4 * q + 3]);
-            }
-            tc::fence_proxy_async();
+            if (need_mask) dkv_row_tile<true>(sall, dall, c2, kp - first_q, rows, pk, dk);
+            else dkv_row_tile<false>(sall, dall, c2, 0, TB, pk, dk);
+            // P^T / dS^T (bf16 pairs) over the first 32 columns of the S^T /
+            // dP^T buffers: the A operands of the dV / dK MMAs
+            tc::tmem_st32u(lane_base + kColS + b * TB, pk);
+            tc::tmem_st32u(lane_base + kColP + b * TB, dk);
+            tc::tmem_wait_st();
             tc::fence_before();
             tc::mbar_arrive(&p_full[b]);
         }
