@@ -201,6 +201,9 @@ __global__ void __launch_bounds__(kThreadsFwd, 1) attn_fwd_tc(const AttnArgs a,
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    // 32-bit shared-window address of the same (aligned) base: computed from
+    // the symbol directly so descriptor math stays on the uniform datapath
+    const uint32_t sbase = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
     uint64_t* q_full = bar + 0;
     uint64_t* full = bar + 1;                 // [kFwdSlots]
@@ -260,57 +263,56 @@ __global__ void __launch_bounds__(kThreadsFwd, 1) attn_fwd_tc(const AttnArgs a,
         }
         __syncwarp();
     } else if (warp == 8) {
+        // This CTA holds all 512 TMEM columns (one CTA per SM), so the
+        // allocation starts at lane 0, column 0: a compile-time base keeps the
+        // MMA operands in uniform registers.
+        if (tmem != 0) __trap();
+        constexpr uint32_t tmem_u = 0;
         // ------------------------------------------------------- MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idS = tc::instr_desc_mn(TQ, TK, false, false);
-            constexpr uint32_t idO = tc::instr_desc_mn(TQ, HD, false, true);
-            auto slot_addr = [&](int t) { return tc::smem_u32(smem + L::kRing + (t % kFwdSlots) * L::kTile); };
-            auto wait_full = [&](int t) {
-                tc::mbar_wait(&full[t % kFwdSlots], (t / kFwdSlots) & 1);
-                tc::fence_after();
-            };
-            auto issue_s = [&](int i, int j) {       // S_i = Q_i K(j)^T
-                const uint32_t sQ = tc::smem_u32(smem + L::kQ + i * L::kTile);
-                const uint32_t sK = slot_addr(2 * j);
-#pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc::mma_bf16(tmem + i * TK, tc::smem_desc(sQ + off, 16, 1024),
-                                 tc::smem_desc(sK + off, 16, 1024), idS, kk != 0);
-                }
-                tc::commit(&s_full[i]);
-            };
-            auto issue_pv = [&](int i, int j) {      // O_i += P_i V(j)
-                tc::mbar_wait(&p_full[i], j & 1);
-                tc::fence_after();
-                const uint32_t sP = tc::smem_u32(smem + L::kP + i * TQ * TK * 2);
-                const uint32_t sV = slot_addr(2 * j + 1);
-#pragma unroll
-                for (int kk = 0; kk < TK / 16; ++kk) {
-                    const uint32_t aoff = (kk >> 2) * 16384 + (kk & 3) * 32;   // P: K-major
-                    tc::mma_bf16(tmem + 256 + i * 128, tc::smem_desc(sP + aoff, 16, 1024),
-                                 tc::smem_desc(sV + kk * 2048, 16384, 1024),  // V: MN-major
-                                 idO, (j | kk) != 0);
-                }
-            };
-            tc::mbar_wait(q_full, 0);
+        constexpr uint32_t idS = tc::instr_desc_mn(TQ, TK, false, false);
+        constexpr uint32_t idO = tc::instr_desc_mn(TQ, HD, false, true);
+        auto slot_addr = [&](int t) { return (sbase + L::kRing + (t % kFwdSlots) * L::kTile); };
+        auto wait_full = [&](int t) {
+            tc::mbar_wait(&full[t % kFwdSlots], (t / kFwdSlots) & 1);
             tc::fence_after();
-            wait_full(0);
-            issue_s(0, 0);
-            if (nkb1 > 0) issue_s(1, 0);
-            tc::commit(&empty[0]);
-            for (int j = 0; j < nkb; ++j) {
-                wait_full(2 * j + 1);
-                if (j < nkb0) issue_pv(0, j);
-                if (j + 1 < nkb) wait_full(2 * j + 2);
-                if (j + 1 < nkb0) issue_s(0, j + 1);
-                if (j < nkb1) issue_pv(1, j);
-                tc::commit(&empty[(2 * j + 1) % kFwdSlots]);
-                if (j + 1 < nkb1) issue_s(1, j + 1);
-                if (j + 1 < nkb) tc::commit(&empty[(2 * j + 2) % kFwdSlots]);
-            }
-            tc::commit(o_full);
+        };
+        auto issue_s = [&](int i, int j) {       // S_i = Q_i K(j)^T
+            const uint32_t sQ = (sbase + L::kQ + i * L::kTile);
+            const uint32_t sK = slot_addr(2 * j);
+            const uint64_t dq = tc::smem_desc(sQ, 16, 1024), dk = tc::smem_desc(sK, 16, 1024);
+#pragma unroll
+            for (int cb = 0; cb < HD / 64; ++cb)   // 64-column blocks: +16 KB; K16 steps: +32 B
+                tc::mma4_ss<2, 2>(tmem_u + i * TK, dq + cb * 1024, dk + cb * 1024, idS, cb != 0);
+            tc::commit_w(&s_full[i]);
+        };
+        auto issue_pv = [&](int i, int j) {      // O_i += P_i V(j)
+            tc::mbar_wait(&p_full[i], j & 1);
+            tc::fence_after();
+            const uint32_t sP = (sbase + L::kP + i * TQ * TK * 2);
+            const uint32_t sV = slot_addr(2 * j + 1);
+            // P: K-major (+32 B per K16 step, +16 KB per 64 keys); V: MN-major (+2 KB per K16 step)
+            const uint64_t dp = tc::smem_desc(sP, 16, 1024), dv = tc::smem_desc(sV, 16384, 1024);
+#pragma unroll
+            for (int cb = 0; cb < TK / 64; ++cb)
+                tc::mma4_ss<2, 128>(tmem_u + 256 + i * 128, dp + cb * 1024, dv + cb * 512, idO, (j | cb) != 0);
+        };
+        tc::mbar_wait(q_full, 0);
+        tc::fence_after();
+        wait_full(0);
+        issue_s(0, 0);
+        if (nkb1 > 0) issue_s(1, 0);
+        tc::commit_w(&empty[0]);
+        for (int j = 0; j < nkb; ++j) {
+            wait_full(2 * j + 1);
+            if (j < nkb0) issue_pv(0, j);
+            if (j + 1 < nkb) wait_full(2 * j + 2);
+            if (j + 1 < nkb0) issue_s(0, j + 1);
+            if (j < nkb1) issue_pv(1, j);
+            tc::commit_w(&empty[(2 * j + 1) % kFwdSlots]);
+            if (j + 1 < nkb1) issue_s(1, j + 1);
+            if (j + 1 < nkb) tc::commit_w(&empty[(2 * j + 2) % kFwdSlots]);
         }
+        tc::commit_w(o_full);
         __syncwarp();
     } else if (warp < 8) {
         // ---------------------------------------------------------- softmax
@@ -515,6 +517,9 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    // 32-bit shared-window address of the same (aligned) base: computed from
+    // the symbol directly so descriptor math stays on the uniform datapath
+    const uint32_t sbase = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
     uint64_t* q_full = bar + 0;
     uint64_t* kv_full = bar + 1;                      // [kDqStages]
@@ -578,52 +583,52 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
         }
         __syncwarp();
     } else if (warp == 8) {
-        if (lane == 0) {
-            constexpr uint32_t idS = tc::instr_desc_mn(TQ, TB, false, false);
-            constexpr uint32_t idQ = tc::instr_desc_mn(TQ, HD, false, true);
-            const uint32_t sQ = tc::smem_u32(smem + L::kQ);
-            const uint32_t sO = tc::smem_u32(smem + L::kO);
-            auto grad = [&](int j) {   // dQ += dS(j) K(j)
-                const int b = j & 1, st = j % kDqStages;
-                tc::mbar_wait(&p_full[b], (j >> 1) & 1);
-                tc::fence_after();
-                const uint32_t sS = tc::smem_u32(smem + L::kS + b * 128 * TB * 2);
-                const uint32_t sK = tc::smem_u32(smem + L::kK + st * L::kSmall);
+        // This CTA holds all 512 TMEM columns (one CTA per SM), so the
+        // allocation starts at lane 0, column 0: a compile-time base keeps the
+        // MMA operands in uniform registers.
+        if (tmem != 0) __trap();
+        constexpr uint32_t tmem_u = 0;
+        constexpr uint32_t idS = tc::instr_desc_mn(TQ, TB, false, false);
+        constexpr uint32_t idQ = tc::instr_desc_mn(TQ, HD, false, true);
+        const uint32_t sQ = (sbase + L::kQ);
+        const uint32_t sO = (sbase + L::kO);
+        auto grad = [&](int j) {   // dQ += dS(j) K(j)
+            const int b = j & 1, st = j % kDqStages;
+            tc::mbar_wait(&p_full[b], (j >> 1) & 1);
+            tc::fence_after();
+            const uint32_t sS = (sbase + L::kS + b * 128 * TB * 2);
+            const uint32_t sK = (sbase + L::kK + st * L::kSmall);
+            static_assert(TB == 64, "one 4-step batch per dS tile");
+            tc::mma4_ss<2, 128>(tmem_u + kColQ, tc::smem_desc(sS, 16, 1024), tc::smem_desc(sK, TB * 128, 1024),
+                                idQ, j != 0);
+            tc::commit_w(&dq_done[b]);
+            tc::commit_w(&kv_empty[st]);
+        };
+        auto scores = [&](int j) {   // S(j) = Q K(j)^T, dP(j) = dO V(j)^T
+            const int b = j & 1, st = j % kDqStages;
+            tc::mbar_wait(&kv_full[st], (j / kDqStages) & 1);
+            if (j >= 2) tc::mbar_wait(&s_free[b], ((j - 2) >> 1) & 1);   // softmax(j-2) read buffer b
+            tc::fence_after();
+            const uint32_t sK = (sbase + L::kK + st * L::kSmall);
+            const uint32_t sV = (sbase + L::kV + st * L::kSmall);
+            const uint64_t dq = tc::smem_desc(sQ, 16, 1024), dO = tc::smem_desc(sO, 16, 1024);
+            const uint64_t dk = tc::smem_desc(sK, 16, 1024), dv = tc::smem_desc(sV, 16, 1024);
 #pragma unroll
-                for (int kk = 0; kk < TB / 16; ++kk)
-                    tc::mma_bf16(tmem + kColQ, tc::smem_desc(sS + kk * 32, 16, 1024),
-                                 tc::smem_desc(sK + kk * 2048, TB * 128, 1024), idQ, (j | kk) != 0);
-                tc::commit(&dq_done[b]);
-                tc::commit(&kv_empty[st]);
-            };
-            auto scores = [&](int j) {   // S(j) = Q K(j)^T, dP(j) = dO V(j)^T
-                const int b = j & 1, st = j % kDqStages;
-                tc::mbar_wait(&kv_full[st], (j / kDqStages) & 1);
-                if (j >= 2) tc::mbar_wait(&s_free[b], ((j - 2) >> 1) & 1);   // softmax(j-2) read buffer b
-                tc::fence_after();
-                const uint32_t sK = tc::smem_u32(smem + L::kK + st * L::kSmall);
-                const uint32_t sV = tc::smem_u32(smem + L::kV + st * L::kSmall);
-#pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {
-                    const uint32_t aoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-                    const uint32_t boff = (kk >> 2) * (TB * 128) + (kk & 3) * 32;
-                    tc::mma_bf16(tmem + kColS + b * TB, tc::smem_desc(sQ + aoff, 16, 1024),
-                                 tc::smem_desc(sK + boff, 16, 1024), idS, kk != 0);
-                    tc::mma_bf16(tmem + kColP + b * TB, tc::smem_desc(sO + aoff, 16, 1024),
-                                 tc::smem_desc(sV + boff, 16, 1024), idS, kk != 0);
-                }
-                tc::commit(&s_full[b]);
-            };
-            // one step of lookahead: the scores of step j+1 run on the
-            // tensor core while the softmax group of step j works
-            tc::mbar_wait(q_full, 0);
-            scores(0);
-            for (int j = 0; j < nkb; ++j) {
-                if (j + 1 < nkb) scores(j + 1);
-                grad(j);
+            for (int cb = 0; cb < HD / 64; ++cb) {   // 64-column blocks: +16 KB (Q, dO), +8 KB (K, V)
+                tc::mma4_ss<2, 2>(tmem_u + kColS + b * TB, dq + cb * 1024, dk + cb * 512, idS, cb != 0);
+                tc::mma4_ss<2, 2>(tmem_u + kColP + b * TB, dO + cb * 1024, dv + cb * 512, idS, cb != 0);
             }
-            tc::commit(acc_full);
+            tc::commit_w(&s_full[b]);
+        };
+        // one step of lookahead: the scores of step j+1 run on the
+        // tensor core while the softmax group of step j works
+        tc::mbar_wait(q_full, 0);
+        scores(0);
+        for (int j = 0; j < nkb; ++j) {
+            if (j + 1 < nkb) scores(j + 1);
+            grad(j);
         }
+        tc::commit_w(acc_full);
         __syncwarp();
     } else if (warp < 8) {
         tc::setmaxnreg_inc<224>();
@@ -781,6 +786,9 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    // 32-bit shared-window address of the same (aligned) base: computed from
+    // the symbol directly so descriptor math stays on the uniform datapath
+    const uint32_t sbase = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
     uint64_t* kv_full = bar + 0;
     uint64_t* qd_full = bar + 1;                      // [kDkvStages]
@@ -891,60 +899,58 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
             if (lane == 0) tc::mbar_arrive(&qd_full[st]);
         }
     } else if (warp == 8) {
-        if (lane == 0) {
-            constexpr uint32_t idS = tc::instr_desc_mn(TK, TB, false, false);
-            constexpr uint32_t idD = tc::instr_desc_mn(TK, HD, false, true);
-            const uint32_t sK = tc::smem_u32(smem + L::kK);
-            const uint32_t sV = tc::smem_u32(smem + L::kV);
-            const uint32_t sKa = tc::smem_u32(smem + L::kKa);
-            const uint32_t sVa = tc::smem_u32(smem + L::kVa);
-            auto grad = [&](int it) {   // dV += P^T dO ; dK += dS^T Q  (P^T, dS^T from TMEM)
-                const int b = it & 1, st = it % kDkvStages;
-                tc::mbar_wait(&p_full[b], (it >> 1) & 1);
-                tc::fence_after();
-                const uint32_t sQ = tc::smem_u32(smem + L::kQ + st * L::kSmall);
-                const uint32_t sO = tc::smem_u32(smem + L::kO + st * L::kSmall);
+        // This CTA holds all 512 TMEM columns (one CTA per SM), so the
+        // allocation starts at lane 0, column 0: a compile-time base keeps the
+        // MMA operands in uniform registers.
+        if (tmem != 0) __trap();
+        constexpr uint32_t tmem_u = 0;
+        constexpr uint32_t idS = tc::instr_desc_mn(TK, TB, false, false);
+        constexpr uint32_t idD = tc::instr_desc_mn(TK, HD, false, true);
+        const uint32_t sK = (sbase + L::kK);
+        const uint32_t sV = (sbase + L::kV);
+        const uint32_t sKa = (sbase + L::kKa);
+        const uint32_t sVa = (sbase + L::kVa);
+        const uint64_t dK = tc::smem_desc(sK, 16, 1024), dV = tc::smem_desc(sV, 16, 1024);
+        auto grad = [&](int it) {   // dV += P^T dO ; dK += dS^T Q  (P^T, dS^T from TMEM)
+            const int b = it & 1, st = it % kDkvStages;
+            tc::mbar_wait(&p_full[b], (it >> 1) & 1);
+            tc::fence_after();
+            const uint32_t sQ = (sbase + L::kQ + st * L::kSmall);
+            const uint32_t sO = (sbase + L::kO + st * L::kSmall);
+            tc::mma4_ts<8, 128>(tmem_u + kColV, tmem_u + kColS + b * TB, tc::smem_desc(sO, TB * 128, 1024), idD,
+                                it != 0);
+            tc::mma4_ts<8, 128>(tmem_u + kColK, tmem_u + kColP + b * TB, tc::smem_desc(sQ, TB * 128, 1024), idD,
+                                it != 0);
+            tc::commit_w(&qd_empty[st]);
+        };
+        // Buffer b of step it is rewritten by the scores of step it+2,
+        // issued after grad(it): in-order tcgen05 execution orders the
+        // TMEM reuse, and grad(it) itself waited for the softmax of it.
+        auto scores = [&](int it) {   // S^T = K Q^T, dP^T = V dO^T
+            const int b = it & 1, st = it % kDkvStages;
+            tc::mbar_wait(&qd_full[st], (it / kDkvStages) & 1);
+            tc::fence_after();
+            const uint32_t sQ = (sbase + L::kQ + st * L::kSmall);
+            const uint32_t sO = (sbase + L::kO + st * L::kSmall);
+            const uint64_t dq = tc::smem_desc(sQ, 16, 1024), dO = tc::smem_desc(sO, 16, 1024);
 #pragma unroll
-                for (int kk = 0; kk < TB / 16; ++kk) {
-                    tc::mma_bf16_ts(tmem + kColV, tmem + kColS + b * TB + kk * 8,
-                                    tc::smem_desc(sO + kk * 2048, TB * 128, 1024), idD, (it | kk) != 0);
-                    tc::mma_bf16_ts(tmem + kColK, tmem + kColP + b * TB + kk * 8,
-                                    tc::smem_desc(sQ + kk * 2048, TB * 128, 1024), idD, (it | kk) != 0);
-                }
-                tc::commit(&qd_empty[st]);
-            };
-            // Buffer b of step it is rewritten by the scores of step it+2,
-            // issued after grad(it): in-order tcgen05 execution orders the
-            // TMEM reuse, and grad(it) itself waited for the softmax of it.
-            auto scores = [&](int it) {   // S^T = K Q^T, dP^T = V dO^T
-                const int b = it & 1, st = it % kDkvStages;
-                tc::mbar_wait(&qd_full[st], (it / kDkvStages) & 1);
-                tc::fence_after();
-                const uint32_t sQ = tc::smem_u32(smem + L::kQ + st * L::kSmall);
-                const uint32_t sO = tc::smem_u32(smem + L::kO + st * L::kSmall);
-#pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {
-                    const uint32_t aoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-                    const uint32_t boff = (kk >> 2) * (TB * 128) + (kk & 3) * 32;
-                    tc::mma_bf16(tmem + kColS + b * TB, tc::smem_desc(sK + aoff, 16, 1024),
-                                 tc::smem_desc(sQ + boff, 16, 1024), idS, kk != 0);
-                    tc::mma_bf16(tmem + kColP + b * TB, tc::smem_desc(sV + aoff, 16, 1024),
-                                 tc::smem_desc(sO + boff, 16, 1024), idS, kk != 0);
-                }
-                tc::mma_bf16(tmem + kColS + b * TB, smem_desc_sw32(sKa),
-                             smem_desc_sw32(tc::smem_u32(smem + L::kQa + st * TB * 32)), idS, 1);
-                tc::mma_bf16(tmem + kColP + b * TB, smem_desc_sw32(sVa),
-                             smem_desc_sw32(tc::smem_u32(smem + L::kOa + st * TB * 32)), idS, 1);
-                tc::commit(&s_full[b]);
-            };
-            tc::mbar_wait(kv_full, 0);
-            scores(0);
-            for (int it = 0; it < iters; ++it) {
-                if (it + 1 < iters) scores(it + 1);
-                grad(it);
+            for (int cb = 0; cb < HD / 64; ++cb) {   // 64-column blocks: +16 KB (K, V), +8 KB (Q, dO)
+                tc::mma4_ss<2, 2>(tmem_u + kColS + b * TB, dK + cb * 1024, dq + cb * 512, idS, cb != 0);
+                tc::mma4_ss<2, 2>(tmem_u + kColP + b * TB, dV + cb * 1024, dO + cb * 512, idS, cb != 0);
             }
-            tc::commit(acc_full);
+            tc::mma_bf16_w(tmem_u + kColS + b * TB, smem_desc_sw32(sKa),
+                         smem_desc_sw32((sbase + L::kQa + st * TB * 32)), idS, 1);
+            tc::mma_bf16_w(tmem_u + kColP + b * TB, smem_desc_sw32(sVa),
+                         smem_desc_sw32((sbase + L::kOa + st * TB * 32)), idS, 1);
+            tc::commit_w(&s_full[b]);
+        };
+        tc::mbar_wait(kv_full, 0);
+        scores(0);
+        for (int it = 0; it < iters; ++it) {
+            if (it + 1 < iters) scores(it + 1);
+            grad(it);
         }
+        tc::commit_w(acc_full);
         __syncwarp();
     } else if (warp < 8) {
         tc::setmaxnreg_inc<224>();
