@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const uint32_t sbase = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
     uint64_t* empty = full + STAGES;
     uint64_t* acc_full = empty + STAGES;     // [2]
@@ -165,27 +166,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kb = 0; kb < nk; ++kb) {
                 tc::mbar_wait(&full[stage], phase);
                 tc::fence_after();
-                if (lane == 0) {
-                    const uint32_t sa = tc::smem_u32(smem + stage * L::kStageBytes);
-                    const uint32_t sb = sa + L::kABytes;
-#pragma unroll
-                    for (int kk = 0; kk < kBK / 16; ++kk) {
-                        const uint64_t ad = A_MN ? tc::smem_desc(sa + kk * 2048, 8192, 1024)
-                                                 : tc::smem_desc(sa + kk * 32, 16, 1024);
-                        const uint64_t bd = B_MN ? tc::smem_desc(sb + kk * 2048, 8192, 1024)
-                                                 : tc::smem_desc(sb + kk * 32, 16, 1024);
-                        tc::mma_bf16(d, ad, bd, idesc, (kb | kk) != 0);
-                    }
-                    tc::commit(&empty[stage]);
-                }
-                __syncwarp();
+                // whole warp, one elected lane issues the 4 K16 steps of the
+                // stage (K-major: +32 B per step; MN-major: +2 KB per step)
+                const uint32_t sa = sbase + stage * L::kStageBytes;
+                const uint32_t sb = sa + L::kABytes;
+                const uint64_t ad = A_MN ? tc::smem_desc(sa, 8192, 1024) : tc::smem_desc(sa, 16, 1024);
+                const uint64_t bd = B_MN ? tc::smem_desc(sb, 8192, 1024) : tc::smem_desc(sb, 16, 1024);
+                static_assert(kBK == 64, "one 4-step batch per stage");
+                tc::mma4_ss<A_MN ? 128 : 2, B_MN ? 128 : 2>(d, ad, bd, idesc, kb != 0);
+                tc::commit_w(&empty[stage]);
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            if (lane == 0) tc::commit(&acc_full[acc]);
-            __syncwarp();
+            tc::commit_w(&acc_full[acc]);
         }
     } else {
         // ---------------- epilogue (warps 2..5) ----------------

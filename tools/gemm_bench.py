@@ -1,0 +1,60 @@
+"""GEMM microbenchmark (GPU): the tcgen05 GEMM on the stage executor's
+shapes (GPT-1.3B, T tokens per chunk): forward X W^T, data-gradient dY W and
+weight-gradient dY^T X, timed by the library's per-launch CUDA events.
+
+    python tools/gemm_bench.py [--T 16384] [--reps 10]
+"""
+import argparse
+import ctypes
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2509_21275_b200 import gpu  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--T", type=int, default=16384)
+    ap.add_argument("--D", type=int, default=2048)
+    ap.add_argument("--F", type=int, default=8192)
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--lib", default=None, help="alternative libepp_gpu.so (A/B runs)")
+    args = ap.parse_args()
+    if args.lib:
+        gpu._LIB_PATH = Path(args.lib)
+    torch.cuda.set_device(0)
+    lib = gpu.lib()
+    T, D, F = args.T, args.D, args.F
+    bf = torch.bfloat16
+    out = {}
+    # (name, M, N, K, a_kmajor, b_kmajor, epi): A is [M,K] (K-major) or [K,M]; B is [N,K] or [K,N]
+    cases = [("fwd_qkv", T, 3 * D, D, 1, 1, 0), ("fwd_up", T, F, D, 1, 1, 0), ("fwd_down", T, D, F, 1, 1, 0),
+             ("dgrad_up", T, D, F, 1, 0, 0), ("wgrad_up", F, D, T, 0, 0, 1), ("wgrad_down", D, F, T, 0, 0, 1)]
+    for name, M, N, K, ak, bk, epi in cases:
+        A = torch.randn((M, K) if ak else (K, M), device="cuda").to(bf)
+        B = torch.randn((N, K) if bk else (K, N), device="cuda").to(bf)
+        C = torch.zeros((M, N), device="cuda", dtype=torch.float32 if epi == 1 else bf)
+
+        def once():
+            gpu.check(lib.epp_kernel_gemm(M, N, K, A.data_ptr(), A.shape[1], ak, B.data_ptr(), B.shape[1], bk,
+                                          C.data_ptr(), N, None, 0, epi, 1, gpu.stream_ptr()))
+
+        once()
+        torch.cuda.synchronize()
+        lib.epp_gpu_profile(1)
+        for _ in range(args.reps):
+            once()
+        torch.cuda.synchronize()
+        lib.epp_gpu_profile(0)
+        a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        gpu.check(lib.epp_gpu_profile_read(0, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), 1))
+        out[name] = {"ms": round(a.value / c.value, 4), "tflops": round(b.value / a.value / 1e9, 1)}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
