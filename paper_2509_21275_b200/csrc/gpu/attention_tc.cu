@@ -130,10 +130,10 @@ __device__ __forceinline__ float row_max(const float (&sv)[TK / 32][32]) {
     return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
 }
 
-// P = 2^(s*c2 - mu) -> bf16, stored in the UMMA K-major swizzled layout;
-// returns the fp32 row sum.  One pair in four takes the FMA-pipe exp2.
-__device__ __forceinline__ float exp_pack_store(const float (&sv)[TK / 32][32], float c2, float mu,
-                                                uint8_t* prow, int r) {
+// P = 2^(s*c2 - mu) -> bf16 pairs written over the first 64 columns of the
+// row's S buffer in TMEM (the A operand of the PV MMA); returns the fp32 row
+// sum.  One pair in four takes the FMA-pipe exp2.
+__device__ __forceinline__ float exp_pack_tmem(const float (&sv)[TK / 32][32], float c2, float mu, uint32_t taddr) {
     const uint64_t c2x = f2pack(c2, c2), nmu = f2pack(-mu, -mu);
     uint64_t l4[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -155,11 +155,9 @@ __device__ __forceinline__ float exp_pack_store(const float (&sv)[TK / 32][32], 
             __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
             pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<uint4*>(prow + tile_off(r, c * 4 + q)) =
-                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        tc::tmem_st16u(taddr + c * 16, pk);
     }
+    tc::tmem_wait_st();
     const uint64_t s2 = fadd2(fadd2(l4[0], l4[1]), fadd2(l4[2], l4[3]));
     float a, b;
     f2unpack(s2, a, b);
@@ -174,21 +172,22 @@ __device__ __forceinline__ float exp_pack_store(const float (&sv)[TK / 32][32], 
 // S1(j+1), and vice versa.  S_i(j+1) is issued after PV_i(j), so the commit
 // that publishes S_i(j+1) also proves that PV_i(j) has finished reading P_i
 // and updating O_i: no separate "PV done" barrier is needed.
-// TMEM columns: S0 [0,128) S1 [128,256) O0 [256,256+HD) O1 [384,384+HD).
-// Shared memory: Q0, Q1, P0, P1 and a 3-slot ring holding K(0) V(0) K(1)
-// V(1) ... (a slot is released by the commit after its last reader).
+// TMEM columns: S0 [0,128) S1 [128,256) O0 [256,256+HD) O1 [384,384+HD);
+// P_i (bf16 pairs) overwrites the first 64 columns of S_i and feeds the PV
+// MMA straight from TMEM (A operand), so P costs no shared memory traffic.
+// Shared memory: Q0, Q1 and a 4-slot ring holding K(0) V(0) K(1) V(1) ...
+// (a slot is released by the commit after its last reader).
 // Warps 0-3 softmax Q0, 4-7 softmax Q1, 8 MMA, 9 TMA, 10-11 idle: three
 // whole warpgroups, so setmaxnreg can move registers from the issue
 // warpgroup (56) to the softmax warpgroups (224; a row of S is 128 fp32).
 constexpr int kThreadsFwd = 384;
-constexpr int kFwdSlots = 3;
+constexpr int kFwdSlots = 4;
 
 template <int HD>
 struct FwdSmem {
     static constexpr int kTile = TQ * HD * 2;       // one 128-row Q / K / V tile
     static constexpr int kQ = 0;                     // Q0, Q1
-    static constexpr int kP = kQ + 2 * kTile;        // P0, P1: 128 x 128 bf16
-    static constexpr int kRing = kP + 2 * TQ * TK * 2;
+    static constexpr int kRing = kQ + 2 * kTile;
     static constexpr int kBar = kRing + kFwdSlots * kTile;
     static constexpr int kBytes = kBar + 16 * 8 + 16;
     static constexpr int kAlloc = kBytes + 1024;
@@ -288,13 +287,13 @@ __global__ void __launch_bounds__(kThreadsFwd, 1) attn_fwd_tc(const AttnArgs a,
         auto issue_pv = [&](int i, int j) {      // O_i += P_i V(j)
             tc::mbar_wait(&p_full[i], j & 1);
             tc::fence_after();
-            const uint32_t sP = (sbase + L::kP + i * TQ * TK * 2);
             const uint32_t sV = slot_addr(2 * j + 1);
-            // P: K-major (+32 B per K16 step, +16 KB per 64 keys); V: MN-major (+2 KB per K16 step)
-            const uint64_t dp = tc::smem_desc(sP, 16, 1024), dv = tc::smem_desc(sV, 16384, 1024);
+            // P from TMEM (bf16 pairs over S_i: 8 columns per K16 step); V: MN-major (+2 KB per K16 step)
+            const uint64_t dv = tc::smem_desc(sV, 16384, 1024);
 #pragma unroll
             for (int cb = 0; cb < TK / 64; ++cb)
-                tc::mma4_ss<2, 128>(tmem_u + 256 + i * 128, dp + cb * 1024, dv + cb * 512, idO, (j | cb) != 0);
+                tc::mma4_ts<8, 128>(tmem_u + 256 + i * 128, tmem_u + i * TK + cb * 32, dv + cb * 512, idO,
+                                    (j | cb) != 0);
         };
         tc::mbar_wait(q_full, 0);
         tc::fence_after();
@@ -328,7 +327,6 @@ __global__ void __launch_bounds__(kThreadsFwd, 1) attn_fwd_tc(const AttnArgs a,
         const float c2 = a.scale * kLog2e;
         const int first_q = sg.kv_ctx + qt0;
         float m_run = -INFINITY, l = 0.f;
-        uint8_t* prow = smem + L::kP + grp * TQ * TK * 2;
         for (int j = 0; j < my_nkb; ++j) {
             tc::mbar_wait(&s_full[grp], j & 1);
             tc::fence_after();
@@ -368,8 +366,7 @@ __global__ void __launch_bounds__(kThreadsFwd, 1) attn_fwd_tc(const AttnArgs a,
             }
             if (grow) m_run = mt;
             const float mu = (m_run == -INFINITY) ? 0.f : m_run;
-            l += exp_pack_store(sv, c2, mu, prow, r);
-            tc::fence_proxy_async();
+            l += exp_pack_tmem(sv, c2, mu, lane_base + colS);
             tc::fence_before();
             tc::mbar_arrive(&p_full[grp]);
         }
@@ -423,12 +420,12 @@ void launch_fwd_tc(const AttnArgs& a, cudaStream_t s) {
 // Backward.  Two kernels, no atomics, deterministic:
 //   dq  (grid: 128-row query blocks x H), 64-key tiles, 4-stage K/V ring:
 //        S = Q K^T, dP = dO V^T -> TMEM (double-buffered);
-//        dS = P (dP - delta) -> smem (bf16, double-buffered);
+//        dS = P (dP - delta) -> TMEM over S (bf16), the A operand of
 //        dQ += dS K -> TMEM; dQ * scale -> fp32 global.
 //   dkv (grid: 128-key blocks x Hkv, GQA heads looped in the CTA), 64-row
 //        query tiles, 3-stage Q/dO ring:
 //        S^T = K Q^T, dP^T = V dO^T -> TMEM (double-buffered);
-//        P^T, dS^T -> smem (bf16, double-buffered);
+//        P^T, dS^T -> TMEM over S^T / dP^T (bf16), the A operands of
 //        dV += P^T dO, dK += dS^T Q -> TMEM; then RMW into the fp32 dK/dV
 //        accumulators of the segment (persist across a sequence's chunks).
 // In both, the MMA warp issues the score MMAs of step i before the gradient
@@ -444,11 +441,6 @@ void launch_fwd_tc(const AttnArgs& a, cudaStream_t s) {
 // warpgroups, for setmaxnreg).
 constexpr int kThreadsBwd = 384;
 
-// [ROWS x HD] tile, HD/64 column blocks of ROWS x 128 B, 128B-swizzled.
-template <int ROWS>
-__device__ __forceinline__ uint32_t toff(int row, int chunk) {
-    return static_cast<uint32_t>((chunk >> 3) * (ROWS * 128) + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
-}
 
 __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
     uint64_t d;
@@ -461,7 +453,7 @@ __device__ __forceinline__ uint32_t bf2(float a, float b) {
 }
 
 constexpr int TB = 64;    // secondary tile (keys in dq, queries in dkv)
-constexpr int kDqStages = 4;    // K/V ring depth of the dq kernel
+constexpr int kDqStages = 5;    // K/V ring depth of the dq kernel
 constexpr int kDkvStages = 4;   // Q/dO ring depth of the dk/dv kernel
 
 // dS for one 64-key tile of a query row: dS = 2^(s*c2 - lse) * (dP - delta).
@@ -504,8 +496,7 @@ struct DqSmem {
     static constexpr int kO = kQ + kBig;
     static constexpr int kK = kO + kBig;                    // kDqStages stages
     static constexpr int kV = kK + kDqStages * kSmall;
-    static constexpr int kS = kV + kDqStages * kSmall;      // dS [128 x 64] bf16 x 2
-    static constexpr int kBar = kS + 2 * 128 * TB * 2;
+    static constexpr int kBar = kV + kDqStages * kSmall;
     static constexpr int kBytes = kBar + 24 * 8 + 16;
     static constexpr int kAlloc = kBytes + 1024;
 };
@@ -526,10 +517,8 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
     uint64_t* kv_empty = kv_full + kDqStages;         // [kDqStages]
     uint64_t* s_full = kv_empty + kDqStages;          // [2]
     uint64_t* p_full = s_full + 2;                    // [2]
-    uint64_t* dq_done = p_full + 2;                   // [2]
-    uint64_t* acc_full = dq_done + 2;                 // all MMAs retired (epilogue)
-    uint64_t* s_free = acc_full + 1;                  // [2] softmax has read S/dP buffer
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + 2);
+    uint64_t* acc_full = p_full + 2;                  // all MMAs retired (epilogue)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
     const AttnWork w = a.qwork128[blockIdx.x];
     const AttnSeg sg = a.segs[w.seg];
@@ -551,8 +540,6 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&s_full[b], 1);
             tc::mbar_init(&p_full[b], TQ);
-            tc::mbar_init(&dq_done[b], 1);
-            tc::mbar_init(&s_free[b], 4);
         }
         tc::mbar_init(acc_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -592,22 +579,22 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
         constexpr uint32_t idQ = tc::instr_desc_mn(TQ, HD, false, true);
         const uint32_t sQ = (sbase + L::kQ);
         const uint32_t sO = (sbase + L::kO);
-        auto grad = [&](int j) {   // dQ += dS(j) K(j)
+        // Buffer b of step j is rewritten by the scores of step j+2, issued
+        // after grad(j) (which waited for the softmax of j): in-order tcgen05
+        // execution orders every TMEM reuse, no extra barriers.
+        auto grad = [&](int j) {   // dQ += dS(j) K(j), dS from TMEM (bf16 pairs over S buffer b)
             const int b = j & 1, st = j % kDqStages;
             tc::mbar_wait(&p_full[b], (j >> 1) & 1);
             tc::fence_after();
-            const uint32_t sS = (sbase + L::kS + b * 128 * TB * 2);
             const uint32_t sK = (sbase + L::kK + st * L::kSmall);
             static_assert(TB == 64, "one 4-step batch per dS tile");
-            tc::mma4_ss<2, 128>(tmem_u + kColQ, tc::smem_desc(sS, 16, 1024), tc::smem_desc(sK, TB * 128, 1024),
-                                idQ, j != 0);
-            tc::commit_w(&dq_done[b]);
+            tc::mma4_ts<8, 128>(tmem_u + kColQ, tmem_u + kColS + b * TB, tc::smem_desc(sK, TB * 128, 1024), idQ,
+                                j != 0);
             tc::commit_w(&kv_empty[st]);
         };
         auto scores = [&](int j) {   // S(j) = Q K(j)^T, dP(j) = dO V(j)^T
             const int b = j & 1, st = j % kDqStages;
             tc::mbar_wait(&kv_full[st], (j / kDqStages) & 1);
-            if (j >= 2) tc::mbar_wait(&s_free[b], ((j - 2) >> 1) & 1);   // softmax(j-2) read buffer b
             tc::fence_after();
             const uint32_t sK = (sbase + L::kK + st * L::kSmall);
             const uint32_t sV = (sbase + L::kV + st * L::kSmall);
@@ -655,9 +642,6 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
                 tc::tmem_ld32_async(lane_base + kColP + b * TB + c * 32, pall[c]);
             }
             tc::tmem_wait_ld();
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&s_free[b]);
 #pragma unroll
             for (int c = 0; c < TB / 32; ++c) {
                 tc::reg_fence(sall[c]);
@@ -665,14 +649,10 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
             }
             if (need_mask) dq_row_tile<true>(sall, pall, c2, lse, dlt, qp - key0, pk);
             else dq_row_tile<false>(sall, pall, c2, lse, dlt, 0, pk);
-            tc::mbar_wait(&dq_done[b], ((j >> 1) & 1) ^ 1);   // dQ(j-2) finished reading buffer b
-            tc::fence_after();
-            uint8_t* sS = smem + L::kS + b * 128 * TB * 2;
-#pragma unroll
-            for (int q = 0; q < TB / 8; ++q)
-                *reinterpret_cast<uint4*>(sS + toff<128>(r, q)) =
-                    make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-            tc::fence_proxy_async();
+            // dS (bf16 pairs) over the first 32 columns of S buffer b: the A
+            // operand of the dQ MMA
+            tc::tmem_st32u(lane_base + kColS + b * TB, pk);
+            tc::tmem_wait_st();
             tc::fence_before();
             tc::mbar_arrive(&p_full[b]);
         }
