@@ -109,6 +109,9 @@ int epp_seq_release(epp_stage* st, int32_t seq);
 /* Last stage: accumulated (sum of token losses, #targets) since the last
  * reset.  Synchronises `stream`. */
 int epp_stage_loss(epp_stage* st, double out[2], int32_t reset, void* stream);
+/* Same, stream-ordered and non-blocking: copies the two fp32 accumulators to
+ * out2 (pinned host or device memory) when `stream` reaches this point. */
+int epp_stage_loss_async(epp_stage* st, float* out2, int32_t reset, void* stream);
 int epp_stage_zero_grads(epp_stage* st, void* stream);
 /* AdamW on fp32 masters (bias-corrected, step >= 1); zeroes the grads. */
 int epp_stage_adamw_step(epp_stage* st, float lr, float beta1, float beta2, float eps,

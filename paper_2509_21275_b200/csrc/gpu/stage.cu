@@ -305,6 +305,13 @@ public:
         if (reset) EPP_CUDA(cudaMemsetAsync(loss_acc_, 0, sizeof(float) * 2, s));
     }
 
+    // Stream-ordered copy of the accumulator into caller memory (pinned host
+    // or device), optional reset; no synchronisation.
+    void loss_async(float* out2, bool reset, cudaStream_t s) {
+        EPP_CUDA(cudaMemcpyAsync(out2, loss_acc_, sizeof(float) * 2, cudaMemcpyDefault, s));
+        if (reset) EPP_CUDA(cudaMemsetAsync(loss_acc_, 0, sizeof(float) * 2, s));
+    }
+
     void release_seq(int seq) { seqs_.erase(seq); }
 
     // ------------------------------------------------------------------
@@ -903,6 +910,13 @@ int epp_seq_release(epp_stage* st, int32_t seq) {
 
 int epp_stage_loss(epp_stage* st, double out[2], int32_t reset, void* stream) {
     return guard([&] { st->impl->loss(out, reset != 0, S(stream)); });
+}
+
+int epp_stage_loss_async(epp_stage* st, float* out2, int32_t reset, void* stream) {
+    return guard([&] {
+        EPP_REQUIRE(out2 != nullptr, "out2 is null");
+        st->impl->loss_async(out2, reset != 0, S(stream));
+    });
 }
 
 int epp_stage_zero_grads(epp_stage* st, void* stream) {

@@ -67,6 +67,7 @@ def lib():
             "epp_stage_backward": [vp, ctypes.POINTER(ChunkDesc), vp, vp, vp],
             "epp_seq_release": [vp, i32],
             "epp_stage_loss": [vp, ctypes.POINTER(ctypes.c_double), i32, vp],
+            "epp_stage_loss_async": [vp, vp, i32, vp],
             "epp_stage_zero_grads": [vp, vp],
             "epp_stage_adamw_step": [vp, f32, f32, f32, f32, f32, i32, vp],
             "epp_stage_memory": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)],
@@ -185,6 +186,11 @@ class CudaStage:
         out = (ctypes.c_double * 2)()
         check(lib().epp_stage_loss(self.h, out, int(reset), stream_ptr()))
         return out[0], out[1]
+
+    def loss_async(self, out2: torch.Tensor, reset: bool = False):
+        """Enqueue a copy of (loss sum, #targets) into `out2` (2 fp32, pinned
+        host or device) on the current stream; the caller synchronises."""
+        check(lib().epp_stage_loss_async(self.h, ctypes.c_void_p(out2.data_ptr()), int(reset), stream_ptr()))
 
     def memory(self):
         live, peak = ctypes.c_int64(), ctypes.c_int64()
