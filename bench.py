@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--seqs-per-gpu", type=int, default=64)
     ap.add_argument("--cap", type=int, default=32768)
     ap.add_argument("--preset", default="github_like")
+    ap.add_argument("--slices", type=int, default=0, help="fixed slice count N (0 = planner auto-N)")
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -158,7 +159,7 @@ def run_ours(args):
     t0 = time.perf_counter()
     plans = []
     for lengths, _ in batches[: args.warmup + args.steps]:
-        plans.append(schedule.parse_plan(planner.make_plan_document(cfg, lengths, None, "main", jobs),
+        plans.append(schedule.parse_plan(planner.make_plan_document(cfg, lengths, args.slices or None, "main", jobs),
                                          lengths))
     planner_s = (time.perf_counter() - t0) / len(plans)
 
@@ -232,7 +233,7 @@ def run_ours(args):
 
         def solve(k):
             lengths = e2e_batches[k][0]
-            ahead[k] = schedule.parse_plan(planner.make_plan_document(cfg, lengths, None, "main", jobs),
+            ahead[k] = schedule.parse_plan(planner.make_plan_document(cfg, lengths, args.slices or None, "main", jobs),
                                            lengths)
 
         solve(0)    # batch 0's plan is solved during the (untimed) previous step
@@ -310,6 +311,7 @@ def run_ours(args):
                                f"{args.seqs_per_gpu} seqs/GPU/step, d_p={dp}",
                    "model": args.model, "global_batch_seqs": args.seqs_per_gpu * world,
                    "tokens_per_step": tokens / args.steps, "seq_len_cap": args.cap,
+                   "slices": args.slices or "auto",
                    "parallelism": f"pp{dp}", "l2": "inputs larger than L2 (activations GBs/step)"},
         "mfu": flops / (sec * world * tf_burst * 1e12),
         "mfu_vs_sustained": flops / (sec * world * tf_sus * 1e12),
