@@ -131,7 +131,6 @@ __global__ void norm_apply_k(bool rms, const T* x, const T* w, const T* b, const
     }
 }
 
-constexpr int kNormRowBlock = 64;    // rows per dγ/dβ partial
 constexpr int kNormMaxG = 8;         // D <= 8192 (checked by the launcher)
 
 // dx = dres + rstd * (dy*w - mean(dy*w) - xhat * mean(dy*w*xhat)): one warp per
@@ -174,16 +173,17 @@ __global__ void __launch_bounds__(256) norm_bwd_dx_k(bool rms, const T* x, const
     }
 }
 
-// Partial dγ/dβ over a block of kNormRowBlock rows; threads own 8
-// consecutive columns, so every load is a coalesced 16-byte access.
+// Partial dγ/dβ over a block of `rows_per` rows; threads own 8 consecutive
+// columns, so every load is a coalesced 16-byte access.  The launcher sizes
+// rows_per so the grid covers the SMs several times even for short chunks.
 template <typename T>
 __global__ void __launch_bounds__(256) norm_bwd_dw_k(bool rms, const T* x, const T* dy,
                                                      const float* mean, const float* rstd,
-                                                     float* pw, float* pb, int Tn, int D) {
+                                                     float* pw, float* pb, int Tn, int D, int rows_per) {
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
     if (c >= D) return;
-    const int r0 = blockIdx.y * kNormRowBlock;
-    const int r1 = min(Tn, r0 + kNormRowBlock);
+    const int r0 = blockIdx.y * rows_per;
+    const int r1 = min(Tn, r0 + rows_per);
     float aw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ab[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int r = r0; r < r1; ++r) {
         const long long off = static_cast<long long>(r) * D + c;
@@ -202,13 +202,26 @@ __global__ void __launch_bounds__(256) norm_bwd_dw_k(bool rms, const T* x, const
     if (pb) store8(pb + static_cast<long long>(blockIdx.y) * D + c, ab);
 }
 
-// dst[c] += sum_g part[g, c]  (deterministic column reduction)
-__global__ void col_reduce_add(const float* part, int G, int D, float* dst) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= D) return;
+// dst[c] += sum_g part[g, c]  (deterministic column reduction).  A CTA owns
+// 32 columns; its 8 warps stride over g with coalesced 128-byte row reads,
+// then combine in shared memory in a fixed order.
+__global__ void __launch_bounds__(256) col_reduce_add(const float* part, int G, int D, float* dst) {
+    __shared__ float red[8][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int c = blockIdx.x * 32 + tx;
     float s = 0.f;
-    for (int g = 0; g < G; ++g) s += part[static_cast<long long>(g) * D + c];
-    dst[c] += s;
+    if (c < D) {
+#pragma unroll 4
+        for (int g = ty; g < G; g += 8) s += part[static_cast<long long>(g) * D + c];
+    }
+    red[ty][tx] = s;
+    __syncthreads();
+    if (ty == 0 && c < D) {
+        float t = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t += red[i][tx];
+        dst[c] += t;
+    }
 }
 
 // ----------------------------------------------------------------- RoPE ---
@@ -600,7 +613,10 @@ void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy, c
     ProfScope prof_(kProfNormBwd, double(T) * D * 6 * dtype_size(t), s);
     EPP_REQUIRE(D % 8 == 0 && D <= 8 * 256 * kNormMaxG, "norm_bwd: unsupported D");
     if (T == 0) return;
-    const int G = ceil_div(T, kNormRowBlock);
+    // ~4 waves of 148 SMs for the partial-sum kernel, rows per block >= 8
+    const int col_blocks = ceil_div(D / 8, 256);
+    const int rows_per = std::max(8, ceil_div(T, std::max(1, 592 / col_blocks)));
+    const int G = ceil_div(T, rows_per);
     float* part = nullptr;
     EPP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * 2 * G * D, s));
     float* pw = part;
@@ -611,12 +627,12 @@ void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy, c
             rms, static_cast<const E*>(x), static_cast<const E*>(w), static_cast<const E*>(dy), mean,
             rstd, static_cast<const E*>(dres), static_cast<E*>(dx), T, D);
         EPP_CHECK_LAUNCH();
-        norm_bwd_dw_k<E><<<dim3(ceil_div(D / 8, 256), G), 256, 0, s>>>(
-            rms, static_cast<const E*>(x), static_cast<const E*>(dy), mean, rstd, pw, pb, T, D);
+        norm_bwd_dw_k<E><<<dim3(col_blocks, G), 256, 0, s>>>(
+            rms, static_cast<const E*>(x), static_cast<const E*>(dy), mean, rstd, pw, pb, T, D, rows_per);
         EPP_CHECK_LAUNCH();
     });
-    col_reduce_add<<<ceil_div(D, 256), 256, 0, s>>>(pw, G, D, dw);
-    if (db) col_reduce_add<<<ceil_div(D, 256), 256, 0, s>>>(pb, G, D, db);
+    col_reduce_add<<<ceil_div(D, 32), 256, 0, s>>>(pw, G, D, dw);
+    if (db) col_reduce_add<<<ceil_div(D, 32), 256, 0, s>>>(pb, G, D, db);
     EPP_CHECK_LAUNCH();
     EPP_CUDA(cudaFreeAsync(part, s));
 }
