@@ -15,6 +15,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <mutex>
 
@@ -27,6 +28,15 @@ namespace eppk {
 
 static std::atomic<long long> g_gemm_launches{0};
 long long gemm_launch_count() { return g_gemm_launches.load(); }
+
+// CTA-pair GEMM on by default; EPP_GEMM_PAIR=0 selects the single-CTA kernel (A/B runs).
+static bool gemm_pair_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("EPP_GEMM_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 
 // =========================================================================
@@ -73,6 +83,75 @@ struct TileSched {
         nb = r / gm;
     }
 };
+
+// Epilogue of one accumulator row slice: this thread's output row `row`,
+// columns [n0, n0 + BN), read 32 columns at a time from TMEM (taddr = the
+// warp's lane quarter), fused epilogue, 16-byte stores.  The tcgen05.ld is
+// warp-collective, so every lane runs the loop even past the matrix edge.
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t taddr, int row, int n0, bool have_acc) {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        if (have_acc) {
+            tc::tmem_ld32(taddr + c, v);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        const int col = n0 + c;
+        if (row >= p.M || col >= p.N) continue;
+        if (EPI == static_cast<int>(Epi::AccumF32) || EPI == static_cast<int>(Epi::StoreF32)) {
+            float* dst = static_cast<float*>(p.C) + static_cast<long long>(row) * p.ldc + col;
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                if (EPI == static_cast<int>(Epi::AccumF32)) {
+                    const float4 old = *reinterpret_cast<const float4*>(dst + i);
+                    o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+                }
+                *reinterpret_cast<float4*>(dst + i) = o;
+            }
+        } else {
+            if (EPI == static_cast<int>(Epi::AddRes) || EPI == static_cast<int>(Epi::GeluBwd)) {
+                const bf16* r = p.R + static_cast<long long>(row) * p.ldr + col;
+#pragma unroll
+                for (int i = 0; i < 32; i += 8) {
+                    const uint4 raw = *reinterpret_cast<const uint4*>(r + i);
+                    const bf16* rb = reinterpret_cast<const bf16*>(&raw);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float rv = __bfloat162float(rb[j]);
+                        if (EPI == static_cast<int>(Epi::AddRes)) v[i + j] += rv;
+                        else v[i + j] *= gelu_tanh_grad_f(rv);
+                    }
+                }
+            }
+            if (EPI == static_cast<int>(Epi::StoreGelu)) {
+                bf16* dst2 = p.C2 + static_cast<long long>(row) * p.ldc2 + col;
+#pragma unroll
+                for (int i = 0; i < 32; i += 8) {
+                    uint4 raw;
+                    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        h[j] = __floats2bfloat162_rn(gelu_tanh_f(v[i + 2 * j]), gelu_tanh_f(v[i + 2 * j + 1]));
+                    *reinterpret_cast<uint4*>(dst2 + i) = raw;
+                }
+            }
+            bf16* dst = static_cast<bf16*>(p.C) + static_cast<long long>(row) * p.ldc + col;
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+                uint4 raw;
+                __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    h[j] = __floats2bfloat162_rn(v[i + 2 * j], v[i + 2 * j + 1]);
+                *reinterpret_cast<uint4*>(dst + i) = raw;
+            }
+        }
+    }
+}
 
 template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -196,67 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::mbar_wait(&acc_full[acc], (local >> 1) & 1);
                 tc::fence_after();
             }
-#pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
-                float v[32];
-                if (nk > 0) {
-                    tc::tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16) + c, v);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] = 0.f;
-                }
-                const int col = n0 + c;
-                if (row >= p.M || col >= p.N) continue;
-                if (EPI == static_cast<int>(Epi::AccumF32) || EPI == static_cast<int>(Epi::StoreF32)) {
-                    float* dst = static_cast<float*>(p.C) + static_cast<long long>(row) * p.ldc + col;
-#pragma unroll
-                    for (int i = 0; i < 32; i += 4) {
-                        float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                        if (EPI == static_cast<int>(Epi::AccumF32)) {
-                            const float4 old = *reinterpret_cast<const float4*>(dst + i);
-                            o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
-                        }
-                        *reinterpret_cast<float4*>(dst + i) = o;
-                    }
-                } else {
-                    if (EPI == static_cast<int>(Epi::AddRes) || EPI == static_cast<int>(Epi::GeluBwd)) {
-                        const bf16* r = p.R + static_cast<long long>(row) * p.ldr + col;
-#pragma unroll
-                        for (int i = 0; i < 32; i += 8) {
-                            const uint4 raw = *reinterpret_cast<const uint4*>(r + i);
-                            const bf16* rb = reinterpret_cast<const bf16*>(&raw);
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                const float rv = __bfloat162float(rb[j]);
-                                if (EPI == static_cast<int>(Epi::AddRes)) v[i + j] += rv;
-                                else v[i + j] *= gelu_tanh_grad_f(rv);
-                            }
-                        }
-                    }
-                    if (EPI == static_cast<int>(Epi::StoreGelu)) {
-                        bf16* dst2 = p.C2 + static_cast<long long>(row) * p.ldc2 + col;
-#pragma unroll
-                        for (int i = 0; i < 32; i += 8) {
-                            uint4 raw;
-                            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
-#pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                h[j] = __floats2bfloat162_rn(gelu_tanh_f(v[i + 2 * j]), gelu_tanh_f(v[i + 2 * j + 1]));
-                            *reinterpret_cast<uint4*>(dst2 + i) = raw;
-                        }
-                    }
-                    bf16* dst = static_cast<bf16*>(p.C) + static_cast<long long>(row) * p.ldc + col;
-#pragma unroll
-                    for (int i = 0; i < 32; i += 8) {
-                        uint4 raw;
-                        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
-#pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            h[j] = __floats2bfloat162_rn(v[i + 2 * j], v[i + 2 * j + 1]);
-                        *reinterpret_cast<uint4*>(dst + i) = raw;
-                    }
-                }
-            }
+            epilogue_rows<BN, EPI>(p, tmem + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16), row, n0, nk > 0);
             // release the accumulator buffer to the MMA warp
             tc::fence_before();
             __syncwarp();
@@ -267,6 +286,220 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) {
         tc::fence_after();
         tc::tmem_dealloc(tmem, kTmemCols);
+    }
+}
+
+
+// =========================================================================
+// CTA-pair kernel (cta_group::2): a cluster of two CTAs on one TPC computes
+// a 256 x BN tile with M=256 MMAs issued by the leader CTA.  Each CTA stages
+// its own 128 rows of A and BN/2 rows of B (the MMA reads the peer's halves
+// through the pair's shared-memory path), so per SM the TMA and tensor-core
+// shared-memory traffic per FLOP is 2/3 of the single-CTA 128 x 256 tile and
+// the issuing warp runs at half the rate.  Barriers:
+//   full[s]      leader only: its producer arms 2 x stage bytes, both CTAs'
+//                TMA loads complete_tx on it (peer bit cleared in the address)
+//   empty[s]     both CTAs: the leader's MMA commit multicasts to the pair
+//   acc_full[b]  both CTAs: multicast commit after a tile's last MMA
+//   acc_empty[b] leader only: 4 epilogue warps x 2 CTAs arrive (peer: remote)
+// =========================================================================
+template <int BN, int STAGES>
+struct Tc2Smem {
+    static constexpr int kABytes = kBM * kBK * 2;            // this CTA's 128 rows of A
+    static constexpr int kBBytes = (BN / 2) * kBK * 2;       // this CTA's BN/2 rows of B
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kBarOffset = STAGES * kStageBytes;
+    static constexpr int kTotal = kBarOffset + (2 * STAGES + 4) * 8 + 16 + 1024;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA 2-D load whose completion is counted on the LEADER CTA's barrier.
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                 int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+// Four K16 MMAs, cta_group::2 (see tc::mma4_ss).
+template <int A_STEP, int B_STEP>
+__device__ __forceinline__ void mma4_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 a, b;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "mov.b64 a, %1;\n\tmov.b64 b, %2;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, p;\n\t"
+        "add.s64 a, a, %5;\n\tadd.s64 b, b, %6;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+        "add.s64 a, a, %5;\n\tadd.s64 b, b, %6;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+        "add.s64 a, a, %5;\n\tadd.s64 b, b, %6;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc0), "n"(A_STEP), "n"(B_STEP)
+        : "memory");
+}
+__device__ __forceinline__ void commit_pair(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            tc::smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a,
+                    const __grid_constant__ CUtensorMap map_b, const TcParams p) {
+    using L = Tc2Smem<BN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const uint32_t sbase = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+    uint64_t* empty = full + STAGES;
+    uint64_t* acc_full = empty + STAGES;     // [2]
+    uint64_t* acc_empty = acc_full + 2;      // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int nk = (p.K + kBK - 1) / kBK;
+    const TileSched sched{(p.M + 2 * kBM - 1) / (2 * kBM), (p.N + BN - 1) / BN};
+    const int ntiles = sched.tiles_m * sched.tiles_n;
+    const int cluster_id = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&acc_full[b], 1);
+            tc::mbar_init(&acc_empty[b], 8);     // 4 epilogue warps x 2 CTAs (leader's copy)
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+    }
+    constexpr uint32_t kTmemCols = 2 * BN;     // double-buffered accumulator (this CTA's 128 rows)
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(tmem_slot)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc::fence_before();
+    cluster_sync_all();      // barrier inits and the TMEM allocation visible to the pair
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer (both CTAs) ----------------
+        if (lane == 0) {
+            const uint32_t leader_full0 = tc::smem_u32(full) & 0xFEFFFFFFu;   // peer bit cleared
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = cluster_id; t < ntiles; t += nclusters) {
+                int mb, nb;
+                sched.coords(t, mb, nb);
+                const int m0 = mb * 2 * kBM + rank * kBM, n0 = nb * BN + rank * (BN / 2);
+                for (int kb = 0; kb < nk; ++kb) {
+                    tc::mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) tc::mbar_expect_tx(&full[stage], 2 * L::kStageBytes);
+                    const uint32_t sa = sbase + stage * L::kStageBytes;
+                    const uint32_t sb = sa + L::kABytes;
+                    const uint32_t fb = leader_full0 + stage * 8;
+                    const int k0 = kb * kBK;
+                    if (A_MN) {
+#pragma unroll
+                        for (int i = 0; i < kBM / 64; ++i) tma_load_2d_pair(sa + i * 8192, &map_a, fb, m0 + 64 * i, k0);
+                    } else {
+                        tma_load_2d_pair(sa, &map_a, fb, k0, m0);
+                    }
+                    if (B_MN) {
+#pragma unroll
+                        for (int i = 0; i < BN / 128; ++i) tma_load_2d_pair(sb + i * 8192, &map_b, fb, n0 + 64 * i, k0);
+                    } else {
+                        tma_load_2d_pair(sb, &map_b, fb, k0, n0);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (leader CTA only) ----------------
+        if (leader) {
+            constexpr uint32_t idesc = tc::instr_desc_mn(2 * kBM, BN, A_MN, B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int local = 0;
+            for (int t = cluster_id; t < ntiles; t += nclusters, ++local) {
+                const int acc = local & 1;
+                tc::mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);   // both CTAs drained this buffer
+                tc::fence_after();
+                const uint32_t d = tmem + acc * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    tc::mbar_wait(&full[stage], phase);
+                    tc::fence_after();
+                    const uint32_t sa = sbase + stage * L::kStageBytes;
+                    const uint32_t sb = sa + L::kABytes;
+                    const uint64_t ad = A_MN ? tc::smem_desc(sa, 8192, 1024) : tc::smem_desc(sa, 16, 1024);
+                    const uint64_t bd = B_MN ? tc::smem_desc(sb, 8192, 1024) : tc::smem_desc(sb, 16, 1024);
+                    mma4_pair<A_MN ? 128 : 2, B_MN ? 128 : 2>(d, ad, bd, idesc, kb != 0);
+                    commit_pair(&empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                commit_pair(&acc_full[acc]);
+            }
+        }
+    } else {
+        // ---------------- epilogue (warps 2..5, both CTAs) ----------------
+        const int quarter = warp & 3;
+        uint32_t leader_acc_empty0;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_acc_empty0) : "r"(tc::smem_u32(acc_empty)));
+        int local = 0;
+        for (int t = cluster_id; t < ntiles; t += nclusters, ++local) {
+            int mb, nb;
+            sched.coords(t, mb, nb);
+            const int row = mb * 2 * kBM + rank * kBM + quarter * 32 + lane;
+            const int n0 = nb * BN;
+            const int acc = local & 1;
+            tc::mbar_wait(&acc_full[acc], (local >> 1) & 1);
+            tc::fence_after();
+            epilogue_rows<BN, EPI>(p, tmem + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16), row, n0, true);
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                                 leader_acc_empty0 + acc * 8)
+                             : "memory");
+        }
+    }
+    tc::fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc::fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
     }
 }
 
@@ -387,6 +620,56 @@ void dispatch_epi(const GemmArgs& g, cudaStream_t s) {
     }
 }
 
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
+void launch_tc2(const GemmArgs& g, cudaStream_t s) {
+    using L = Tc2Smem<BN, STAGES>;
+    auto kern = gemm_tc2_kernel<BN, STAGES, A_MN, B_MN, EPI>;
+    static bool configured = false;   // per instantiation
+    if (!configured) {
+        EPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
+        configured = true;
+    }
+    // per CTA: A box = 128 rows (or 64-col MN boxes), B box = BN/2 rows
+    const CUtensorMap ma = A_MN ? make_map(g.A, g.K, g.M, g.lda, 64, kBK)
+                                : make_map(g.A, g.M, g.K, g.lda, kBK, kBM);
+    const CUtensorMap mb = B_MN ? make_map(g.B, g.K, g.N, g.ldb, 64, kBK)
+                                : make_map(g.B, g.N, g.K, g.ldb, kBK, BN / 2);
+    TcParams p{g.M, g.N, g.K, g.C, g.ldc, static_cast<const bf16*>(g.R), g.ldr,
+               static_cast<bf16*>(g.C2), g.ldc2};
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        EPP_CUDA(cudaGetDevice(&dev));
+        EPP_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int tiles = ceil_div(g.N, BN) * ceil_div(g.M, 2 * kBM);
+    const int clusters = std::min(tiles, num_sms / 2);
+    kern<<<2 * clusters, kThreads, L::kTotal, s>>>(ma, mb, p);
+    EPP_CHECK_LAUNCH();
+    g_gemm_launches.fetch_add(1);
+}
+
+template <int BN, int STAGES, int EPI>
+void dispatch_major2(const GemmArgs& g, cudaStream_t s) {
+    const bool a_mn = !g.a_kmajor, b_mn = !g.b_kmajor;
+    if (!a_mn && !b_mn) launch_tc2<BN, STAGES, false, false, EPI>(g, s);
+    else if (!a_mn && b_mn) launch_tc2<BN, STAGES, false, true, EPI>(g, s);
+    else if (a_mn && !b_mn) launch_tc2<BN, STAGES, true, false, EPI>(g, s);
+    else launch_tc2<BN, STAGES, true, true, EPI>(g, s);
+}
+
+template <int BN, int STAGES>
+void dispatch_epi2(const GemmArgs& g, cudaStream_t s) {
+    switch (g.epi) {
+        case Epi::Store: dispatch_major2<BN, STAGES, 0>(g, s); break;
+        case Epi::AccumF32: dispatch_major2<BN, STAGES, 1>(g, s); break;
+        case Epi::AddRes: dispatch_major2<BN, STAGES, 2>(g, s); break;
+        case Epi::StoreF32: dispatch_major2<BN, STAGES, 3>(g, s); break;
+        case Epi::StoreGelu: dispatch_major2<BN, STAGES, 4>(g, s); break;
+        case Epi::GeluBwd: dispatch_major2<BN, STAGES, 5>(g, s); break;
+    }
+}
+
 // ---------------------------------------------------------------- SIMT f32
 template <typename T>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
@@ -487,7 +770,10 @@ void gemm(const GemmArgs& g, cudaStream_t s) {
     // Wide tiles keep the tensor pipe fed (128x256 per MMA); narrow problems
     // use 128-wide tiles to expose more CTAs.
     const long long tiles256 = static_cast<long long>(ceil_div(g.N, 256)) * ceil_div(g.M, kBM);
-    if (g.N % 256 == 0 && tiles256 >= 120)
+    const long long pair_tiles = static_cast<long long>(ceil_div(g.N, 256)) * ceil_div(g.M, 2 * kBM);
+    if (g.K > 0 && g.N % 256 == 0 && pair_tiles >= 60 && gemm_pair_enabled())
+        dispatch_epi2<256, 6>(g, s);      // CTA pairs: 256 x 256 tiles
+    else if (g.N % 256 == 0 && tiles256 >= 120)
         dispatch_epi<256, 4>(g, s);
     else
         dispatch_epi<128, 6>(g, s);

@@ -31,7 +31,8 @@ def test_gemm_rejects_unaligned_pitch():
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("a_k,b_k", [(True, True), (True, False), (False, True), (False, False)])
-@pytest.mark.parametrize("M,N,K", [(256, 512, 256), (300, 384, 320), (1000, 256, 192), (4096, 1024, 1024)])
+@pytest.mark.parametrize("M,N,K", [(256, 512, 256), (300, 384, 320), (1000, 256, 192), (4096, 1024, 1024),
+                                   (2312, 4096, 576)])   # the last two take the CTA-pair (cta_group::2) kernel
 def test_gemm_layouts(dtype, a_k, b_k, M, N, K):
     g = G()
     td = torch.bfloat16 if dtype == "bf16" else torch.float32
@@ -74,6 +75,35 @@ def test_gemm_epilogues(dtype):
     torch.cuda.synchronize()
     ref2 = A2.float() @ B2.float().T + R.float()
     assert ((C2.float() - ref2).norm() / ref2.norm()) < (8e-3 if dtype == "bf16" else 1e-5)
+
+
+@pytest.mark.parametrize("epi", [1, 2])
+def test_gemm_pair_epilogues(epi):
+    """CTA-pair kernel (M >= 256 tiles, N % 256 == 0): fp32 accumulate (wgrad,
+    MN-major operands) and residual add, with a ragged M edge."""
+    g = G()
+    torch.manual_seed(1)
+    M, N, K = 2200, 2048, 768
+    if epi == 1:
+        A = torch.randn((K, M), device="cuda").bfloat16()
+        B = torch.randn((K, N), device="cuda").bfloat16()
+        C = torch.randn((M, N), device="cuda")
+        C0 = C.clone()
+        g.check(g.lib().epp_kernel_gemm(M, N, K, A.data_ptr(), M, 0, B.data_ptr(), N, 0, C.data_ptr(), N,
+                                        None, 0, 1, g.DTYPES["bf16"], g.stream_ptr()))
+        torch.cuda.synchronize()
+        ref = C0 + A.float().T @ B.float()
+        assert ((C - ref).norm() / ref.norm()) < 5e-3
+    else:
+        A = torch.randn((M, K), device="cuda").bfloat16()
+        B = torch.randn((N, K), device="cuda").bfloat16()
+        R = torch.randn((M, N), device="cuda").bfloat16()
+        C = torch.empty((M, N), device="cuda", dtype=torch.bfloat16)
+        g.check(g.lib().epp_kernel_gemm(M, N, K, A.data_ptr(), K, 1, B.data_ptr(), K, 1, C.data_ptr(), N,
+                                        R.data_ptr(), N, 2, g.DTYPES["bf16"], g.stream_ptr()))
+        torch.cuda.synchronize()
+        ref = A.float() @ B.float().T + R.float()
+        assert ((C.float() - ref).norm() / ref.norm()) < 8e-3
 
 
 def attn_reference(q, ks, vs, segs, scale):
