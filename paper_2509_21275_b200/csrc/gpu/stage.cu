@@ -48,6 +48,21 @@ struct Pool {
     long long peak = 0;
 };
 
+// Activations come from the device's default stream-ordered pool
+// (cudaMallocAsync).  With the default release threshold (0) the driver hands
+// freed memory back to the OS at every stream/event synchronisation and must
+// re-map it on the next step, which shows up as 100s of ms of idle GPU in
+// steps whose chunks are larger than the previous step's; a stage keeps its
+// high-water mark reserved instead.
+inline void keep_pool_reserved() {
+    int dev = 0;
+    EPP_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t mp;
+    EPP_CUDA(cudaDeviceGetDefaultMemPool(&mp, dev));
+    uint64_t thr = ~0ull;
+    EPP_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
+}
+
 // Stream-ordered device buffer.
 class Buf {
 public:
@@ -188,6 +203,7 @@ public:
                     "hidden/ffn/vocab must be multiples of 64");
         EPP_REQUIRE(dt == DType::F32 || m.head_dim == 64 || m.head_dim == 128,
                     "bf16 attention supports head_dim 64 or 128");
+        keep_pool_reserved();
         D_ = m.hidden;
         H_ = m.heads;
         Hkv_ = m.kv_heads;
