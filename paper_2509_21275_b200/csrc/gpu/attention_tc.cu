@@ -59,12 +59,6 @@ __device__ __forceinline__ void load_kv_tile(uint8_t* dst, const CUtensorMap* m,
     for (int c = 0; c < HD / 64; ++c) tma4(dst + c * ROWS * 128, m, bar, c * 64, head, row, layer);
 }
 
-// [128 rows x HD] bf16 tile = HD/64 column blocks of [128 rows x 128 B],
-// 16-byte chunks XOR-swizzled by (row & 7): the UMMA SWIZZLE_128B layout.
-__device__ __forceinline__ uint32_t tile_off(int row, int chunk) {
-    return static_cast<uint32_t>((chunk >> 3) * 16384 + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
-}
-
 // Packed fp32x2 arithmetic (FFMA2 / FADD2 on sm_100: two lanes of work per
 // issue slot).
 __device__ __forceinline__ uint64_t f2pack(float a, float b) {
@@ -89,6 +83,20 @@ __device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
     uint64_t d;
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
     return d;
+}
+
+// Share of exponentials (in eighths of the pairs) computed on the FMA pipe
+// instead of MUFU.EX2; tuned with tools/attn_bench.py.
+#ifndef EPP_FWD_EMU
+#define EPP_FWD_EMU 3
+#endif
+#ifndef EPP_BWD_EMU
+#define EPP_BWD_EMU 0
+#endif
+constexpr int kEmuFwd = EPP_FWD_EMU, kEmuBwd = EPP_BWD_EMU;
+template <int E>
+__device__ __forceinline__ constexpr bool emu_pair(int q) {   // q: pair index within a 32-column chunk
+    return (q & 7) >= 8 - E;
 }
 
 // 2^x for a pair on the FMA pipe (Cody-Waite split + degree-3 minimax, rel.
@@ -143,7 +151,7 @@ __device__ __forceinline__ float exp_pack_tmem(const float (&sv)[TK / 32][32], f
         for (int i = 0; i < 32; i += 2) {
             const uint64_t x = ffma2(f2pack(sv[c][i], sv[c][i + 1]), c2x, nmu);
             float p0, p1;
-            if ((i & 7) == 6) {
+            if (emu_pair<kEmuFwd>(i >> 1)) {
                 ex2_fma2(x, p0, p1);
             } else {
                 float x0, x1;
@@ -163,6 +171,21 @@ __device__ __forceinline__ float exp_pack_tmem(const float (&sv)[TK / 32][32], f
     f2unpack(s2, a, b);
     return a + b;
 }
+
+// Launch order.  The block scheduler dispatches in linear block order and
+// the work lists are sorted longest-first.  Large launches run head-major
+// (grid (work, head)): a wave covers one or two heads, whose K/V (16 MB per
+// head at 32K) then stays in L2.  Launches of a few waves run head-fastest
+// (grid (head, work)), so every head's most expensive item starts in the
+// first wave instead of forming the tail.  The kernels read the order from
+// AttnArgs::hfast, set by the launcher.
+constexpr int kAttnFewWaves = 4 * 148;
+inline bool attn_hfast(int heads, int nwork) { return static_cast<long long>(heads) * nwork <= kAttnFewWaves; }
+inline dim3 attn_grid(int heads, int nwork) {
+    return attn_hfast(heads, nwork) ? dim3(heads, nwork) : dim3(nwork, heads);
+}
+#define EPP_WORK_INDEX (a.hfast ? blockIdx.y : blockIdx.x)
+#define EPP_HEAD_INDEX (a.hfast ? blockIdx.x : blockIdx.y)
 
 // Forward: one CTA = 256 query rows (two 128-row tiles Q0, Q1) of one head,
 // so each K/V tile fetched into shared memory feeds two score MMAs and two PV
@@ -212,9 +235,9 @@ __global__ void __launch_bounds__(kThreadsFwd, 1) attn_fwd_tc(const AttnArgs a,
     uint64_t* o_full = p_full + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
 
-    const AttnWork w = a.qwork256[blockIdx.x];
+    const AttnWork w = a.qwork256[EPP_WORK_INDEX];
     const AttnSeg sg = a.segs[w.seg];
-    const int h = blockIdx.y;
+    const int h = EPP_HEAD_INDEX;
     const int kvh = h / (a.H / a.Hkv);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q0 = w.block * 2 * TQ;
@@ -348,6 +371,21 @@ __global__ void __launch_bounds__(kThreadsFwd, 1) attn_fwd_tc(const AttnArgs a,
                     for (int i = 0; i < 32; ++i) sv[c][i] = i > lim ? -INFINITY : sv[c][i];
                 }
             }
+#ifdef EPP_FWD_FAKE_SOFTMAX   // pipeline-bound experiment: no max, no exp (wrong results)
+            {
+                uint32_t pk[16];
+#pragma unroll
+                for (int c = 0; c < TK / 32; ++c) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) pk[i] = __float_as_uint(sv[c][2 * i]);
+                    tc::tmem_st16u(lane_base + colS + c * 16, pk);
+                }
+                tc::tmem_wait_st();
+                tc::fence_before();
+                tc::mbar_arrive(&p_full[grp]);
+                continue;
+            }
+#endif
             const float mraw = row_max(sv);
             const float mt = mraw * c2;
             const bool grow = mt > m_run + kRescaleSlack || (m_run == -INFINITY && mt > -INFINITY);
@@ -412,7 +450,9 @@ void launch_fwd_tc(const AttnArgs& a, cudaStream_t s) {
         EPP_CUDA(cudaFuncSetAttribute(attn_fwd_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
         cfg = true;
     }
-    attn_fwd_tc<HD><<<dim3(a.nqwork256, a.H), kThreadsFwd, L::kAlloc, s>>>(a, *a.maps);
+    AttnArgs b = a;
+    b.hfast = attn_hfast(a.H, a.nqwork256);
+    attn_fwd_tc<HD><<<attn_grid(a.H, a.nqwork256), kThreadsFwd, L::kAlloc, s>>>(b, *a.maps);
     EPP_CHECK_LAUNCH();
 }
 
@@ -468,7 +508,7 @@ __device__ __forceinline__ void dq_row_tile(const float (&s)[TB / 32][32], const
         for (int i = 0; i < 32; i += 2) {
             const uint64_t x = ffma2(f2pack(s[c][i], s[c][i + 1]), c2x, nl);
             float p0, p1;
-            if ((i & 7) == 6) {
+            if (emu_pair<kEmuBwd>(i >> 1)) {
                 ex2_fma2(x, p0, p1);
             } else {
                 float x0, x1;
@@ -520,9 +560,9 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
     uint64_t* acc_full = p_full + 2;                  // all MMAs retired (epilogue)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
-    const AttnWork w = a.qwork128[blockIdx.x];
+    const AttnWork w = a.qwork128[EPP_WORK_INDEX];
     const AttnSeg sg = a.segs[w.seg];
-    const int h = blockIdx.y;
+    const int h = EPP_HEAD_INDEX;
     const int kvh = h / (a.H / a.Hkv);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q0 = w.block * TQ;
@@ -695,7 +735,7 @@ __device__ __forceinline__ void dkv_row_tile(const float (&s)[TB / 32][32], cons
         for (int i = 0; i < 32; i += 2) {
             const uint64_t x = fmul2(f2pack(s[c][i], s[c][i + 1]), c2x);
             float p0, p1;
-            if ((i & 7) == 6) {
+            if (emu_pair<kEmuBwd>(i >> 1)) {
                 ex2_fma2(x, p0, p1);
             } else {
                 float x0, x1;
@@ -778,9 +818,9 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
     uint64_t* acc_full = p_full + 2;                  // all MMAs retired (epilogue)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
-    const AttnWork w = a.kwork128[blockIdx.x];
+    const AttnWork w = a.kwork128[EPP_WORK_INDEX];
     const AttnSeg sg = a.segs[w.seg];
-    const int kvh = blockIdx.y;
+    const int kvh = EPP_HEAD_INDEX;
     const int group = a.H / a.Hkv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int k0 = w.block * TK;
@@ -1014,12 +1054,16 @@ void launch_bwd_tc(const AttnArgs& a, cudaStream_t s) {
     }
     if (a.nqwork128 > 0) {
         ProfScope prof(kProfAttnBwdDq, 6.0 * a.H * a.hd * a.pairs, s);     // executed: 3 matmuls
-        attn_bwd_dq_tc<HD><<<dim3(a.nqwork128, a.H), kThreadsBwd, DqSmem<HD>::kAlloc, s>>>(a, *a.maps);
+        AttnArgs b = a;
+        b.hfast = attn_hfast(a.H, a.nqwork128);
+        attn_bwd_dq_tc<HD><<<attn_grid(a.H, a.nqwork128), kThreadsBwd, DqSmem<HD>::kAlloc, s>>>(b, *a.maps);
         EPP_CHECK_LAUNCH();
     }
     if (a.nkwork128 > 0) {
         ProfScope prof(kProfAttnBwdDkv, 8.0 * a.H * a.hd * a.pairs, s);    // executed: 4 matmuls
-        attn_bwd_dkv_tc<HD><<<dim3(a.nkwork128, a.Hkv), kThreadsBwd, DkvSmem<HD>::kAlloc, s>>>(a, *a.maps);
+        AttnArgs b = a;
+        b.hfast = attn_hfast(a.Hkv, a.nkwork128);
+        attn_bwd_dkv_tc<HD><<<attn_grid(a.Hkv, a.nkwork128), kThreadsBwd, DkvSmem<HD>::kAlloc, s>>>(b, *a.maps);
         EPP_CHECK_LAUNCH();
     }
 }

@@ -99,6 +99,7 @@ struct AttnArgs {
     int nkwork128 = 0;
     const AttnWork* qwork256 = nullptr;   // 256-row query blocks (tcgen05 forward: 2 tiles / CTA)
     int nqwork256 = 0;
+    int hfast = 0;                        // launch order: grid (head, work) instead of (work, head)
     int T = 0;
     int H = 0, Hkv = 0, hd = 0;
     int layer = 0;

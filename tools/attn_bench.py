@@ -22,6 +22,10 @@ CASES = {
     "ctx12k+4k": dict(H=16, Hkv=16, hd=128, segs=[(0, 4096, 12288)]),
     "packed": dict(H=16, Hkv=16, hd=128, segs=None),
     "gqa8k": dict(H=32, Hkv=8, hd=128, segs=[(0, 8192, 0)]),
+    "long32k": dict(H=16, Hkv=16, hd=128, segs=[(0, 32768, 0)]),
+    "seq4k": dict(H=16, Hkv=16, hd=128, segs=[(0, 4096, 0)]),
+    "seq2k": dict(H=16, Hkv=16, hd=128, segs=[(0, 2048, 0)]),
+    "seq1k_x8": dict(H=16, Hkv=16, hd=128, segs=[(i * 1024, 1024, 0) for i in range(8)]),
 }
 
 
@@ -86,7 +90,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--cases", default=",".join(CASES))
+    ap.add_argument("--lib", default=None, help="alternative libepp_gpu.so (A/B runs)")
     args = ap.parse_args()
+    if args.lib:
+        gpu._LIB_PATH = Path(args.lib)
     torch.cuda.set_device(0)
     res = {k: run(CASES[k], args.reps) for k in args.cases.split(",")}
     print(json.dumps(res))
