@@ -183,6 +183,11 @@ def run_ours(args):
         stage.adamw_step(1e-4, step_no[0])
 
     # ---- warmup -------------------------------------------------------------
+    # Reserve the activation pool up front (all but 6 GB of what is free after
+    # the stage's weights and optimizer state): steps whose chunks are larger
+    # than any earlier step's then never wait for the driver to map memory.
+    free_b, _ = torch.cuda.mem_get_info()
+    gpu.pool_reserve(free_b - int(6e9))
     for i in range(args.warmup):
         driver.run_step(plans[i], batches[i][1])
         optimizer()

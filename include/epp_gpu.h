@@ -113,6 +113,10 @@ int epp_stage_loss(epp_stage* st, double out[2], int32_t reset, void* stream);
  * out2 (pinned host or device memory) when `stream` reaches this point. */
 int epp_stage_loss_async(epp_stage* st, float* out2, int32_t reset, void* stream);
 int epp_stage_zero_grads(epp_stage* st, void* stream);
+/* Pre-reserve `bytes` in the device's stream-ordered pool that backs all
+ * stage activations (kept reserved: later steps never wait on the driver to
+ * map memory).  Synchronises `stream`. */
+int epp_gpu_pool_reserve(uint64_t bytes, void* stream);
 /* AdamW on fp32 masters (bias-corrected, step >= 1); zeroes the grads. */
 int epp_stage_adamw_step(epp_stage* st, float lr, float beta1, float beta2, float eps,
                          float weight_decay, int32_t step, void* stream);

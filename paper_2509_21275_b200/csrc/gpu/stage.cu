@@ -935,6 +935,18 @@ int epp_stage_loss_async(epp_stage* st, float* out2, int32_t reset, void* stream
     });
 }
 
+int epp_gpu_pool_reserve(uint64_t bytes, void* stream) {
+    return guard([&] {
+        eppk::keep_pool_reserved();
+        if (bytes == 0) return;
+        cudaStream_t s = S(stream);
+        void* p = nullptr;
+        EPP_CUDA(cudaMallocAsync(&p, bytes, s));
+        EPP_CUDA(cudaFreeAsync(p, s));
+        EPP_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 int epp_stage_zero_grads(epp_stage* st, void* stream) {
     return guard([&] { st->impl->zero_grads(S(stream)); });
 }

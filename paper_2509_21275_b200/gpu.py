@@ -68,6 +68,7 @@ def lib():
             "epp_seq_release": [vp, i32],
             "epp_stage_loss": [vp, ctypes.POINTER(ctypes.c_double), i32, vp],
             "epp_stage_loss_async": [vp, vp, i32, vp],
+            "epp_gpu_pool_reserve": [ctypes.c_uint64, vp],
             "epp_stage_zero_grads": [vp, vp],
             "epp_stage_adamw_step": [vp, f32, f32, f32, f32, f32, i32, vp],
             "epp_stage_memory": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)],
@@ -102,6 +103,11 @@ def check(rc: int) -> None:
 def set_attention_impl(name: str) -> None:
     """'tc' (tcgen05, default) or 'fa2' (mma.sync) attention kernels."""
     check(lib().epp_gpu_set_attention_impl({"fa2": 0, "tc": 1}[name]))
+
+
+def pool_reserve(nbytes: int) -> None:
+    """Pre-reserve device memory for stage activations (see epp_gpu.h)."""
+    check(lib().epp_gpu_pool_reserve(int(max(0, nbytes)), stream_ptr()))
 
 
 def kernel_launches() -> int:
