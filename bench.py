@@ -145,8 +145,12 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        dist.init_process_group("nccl")
+        # EPP_BENCH_BACKEND=gloo runs the multi-rank code path with several
+        # ranks sharing one GPU (messages staged through host memory): a
+        # functional check only, never a reported number
+        dist.init_process_group(os.environ.get("EPP_BENCH_BACKEND", "nccl"))
         assert dist.get_world_size() == world
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     m = M.MODELS[args.model]
@@ -186,8 +190,9 @@ def run_ours(args):
     # Reserve the activation pool up front (all but 6 GB of what is free after
     # the stage's weights and optimizer state): steps whose chunks are larger
     # than any earlier step's then never wait for the driver to map memory.
-    free_b, _ = torch.cuda.mem_get_info()
-    gpu.pool_reserve(free_b - int(6e9))
+    if os.environ.get("EPP_BENCH_BACKEND", "nccl") == "nccl":   # (ranks own their GPU)
+        free_b, _ = torch.cuda.mem_get_info()
+        gpu.pool_reserve(free_b - int(6e9))
     for i in range(args.warmup):
         driver.run_step(plans[i], batches[i][1])
         optimizer()
@@ -273,9 +278,14 @@ def run_ours(args):
         sync_all()
         e_s = time.perf_counter() - e0
         if world > 1:
+            # slowest rank's wall time; H2D (stage 0) and D2H (last stage)
+            # bytes are counted where they happen and summed over ranks
             t = torch.tensor([e_s], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_s = float(t.item())
+            b = torch.tensor([float(h2d), float(d2h)], device=dev)
+            dist.all_reduce(b, op=dist.ReduceOp.SUM)
+            h2d, d2h = int(b[0].item()), int(b[1].item())
         e_tokens = sum(sum(b[0]) for b in e2e_batches)
         nb = len(e2e_batches)
         e2e = {"value": e_tokens / e_s, "unit": "tokens/s", "h2d_bytes_per_step": h2d // nb,

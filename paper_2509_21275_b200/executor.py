@@ -138,7 +138,11 @@ class LocalPipeline:
 
 
 class DistributedPipeline:
-    """One stage per rank of the default process group (rank = stage)."""
+    """One stage per rank of the default process group (rank = stage).
+
+    Transport: device tensors go straight to NCCL (B200s: NVLink P2P);
+    with a gloo group and CUDA stages (the multi-process test that shares one
+    GPU) messages are staged through host memory instead."""
 
     def __init__(self, stage, rank: int, world: int, device: torch.device, hidden: int,
                  act_dtype: torch.dtype):
@@ -146,6 +150,7 @@ class DistributedPipeline:
         self.dist = dist
         self.stage, self.rank, self.world = stage, rank, world
         self.device, self.hidden, self.act_dtype = device, hidden, act_dtype
+        self.via_host = device.type == "cuda" and dist.get_backend() == "gloo"
         # One group per adjacent pair and direction; every rank creates all of
         # them in the same order (new_group is collective).
         self.fwd_groups, self.bwd_groups = [], []
@@ -153,6 +158,18 @@ class DistributedPipeline:
             self.fwd_groups.append(dist.new_group([p, p + 1]))
             self.bwd_groups.append(dist.new_group([p, p + 1]))
         self.p2p_bytes = 0
+
+    def _recv(self, T: int, src: int, group) -> torch.Tensor:
+        dev = torch.device("cpu") if self.via_host else self.device
+        buf = torch.empty((T, self.hidden), dtype=self.act_dtype, device=dev)
+        self.dist.irecv(buf, src=src, group=group).wait()
+        return buf.to(self.device) if self.via_host else buf
+
+    def _send(self, t: torch.Tensor, dst: int, group, pending: list):
+        if self.via_host:
+            t = t.cpu()
+        pending.append((self.dist.isend(t, dst=dst, group=group), t))
+        self.p2p_bytes += t.numel() * t.element_size()
 
     def run_step(self, plan: Plan, tokens: Sequence[np.ndarray], staged: Optional[_ChunkTokens] = None) -> dict:
         p, dp = self.rank, self.world
@@ -166,23 +183,15 @@ class DistributedPipeline:
                 T = plan.chunks[unit.chunks[pos]].tokens
                 op = _op(plan, unit, pos, p, toks)
                 if kind == "F":
-                    act_in = None
-                    if p > 0:
-                        act_in = torch.empty((T, self.hidden), dtype=self.act_dtype, device=self.device)
-                        self.dist.irecv(act_in, src=p - 1, group=self.fwd_groups[p - 1]).wait()
+                    act_in = self._recv(T, p - 1, self.fwd_groups[p - 1]) if p > 0 else None
                     out = self.stage.forward(op, act_in)
                     if p + 1 < dp:
-                        pending.append((self.dist.isend(out, dst=p + 1, group=self.fwd_groups[p]), out))
-                        self.p2p_bytes += out.numel() * out.element_size()
+                        self._send(out, p + 1, self.fwd_groups[p], pending)
                 else:
-                    g_in = None
-                    if p + 1 < dp:
-                        g_in = torch.empty((T, self.hidden), dtype=self.act_dtype, device=self.device)
-                        self.dist.irecv(g_in, src=p + 1, group=self.bwd_groups[p]).wait()
+                    g_in = self._recv(T, p + 1, self.bwd_groups[p]) if p + 1 < dp else None
                     g_out = self.stage.backward(op, g_in)
                     if p > 0:
-                        pending.append((self.dist.isend(g_out, dst=p - 1, group=self.bwd_groups[p - 1]), g_out))
-                        self.p2p_bytes += g_out.numel() * g_out.element_size()
+                        self._send(g_out, p - 1, self.bwd_groups[p - 1], pending)
             for w, _ in pending:
                 w.wait()
             pending.clear()
