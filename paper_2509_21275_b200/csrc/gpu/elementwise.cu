@@ -3,6 +3,8 @@
 // into the per-segment KV rows and its inverse gather, GELU / SwiGLU, fused
 // softmax cross-entropy, AdamW and initialisation.  All are vectorised
 // (16-byte accesses), one CTA per row where a row reduction is needed.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "profile.h"
@@ -106,6 +108,72 @@ __global__ void norm_fwd_k(bool rms, const T* x, const T* w, const T* b, T* y, f
     for (int c = threadIdx.x * 8; c < D; c += blockDim.x * 8) {
         float v[8], wv[8], bv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         load8(xr + c, v);
+        load8(w + c, wv);
+        if (b) load8(b + c, bv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = (v[i] - mu) * rs * wv[i] + bv[i];
+        store8(y + row * D + c, v);
+    }
+}
+
+// Warp-per-row variant (bf16, D = 256 * NC, the model widths): the row stays
+// in registers as packed bf16 between the mean, variance and normalise passes
+// (one HBM read), reductions are warp shuffles only.
+template <int NC>
+__global__ void __launch_bounds__(256) norm_fwd_warp_k(bool rms, const bf16* x, const bf16* w, const bf16* b,
+                                                       bf16* y, float* mean, float* rstd, int Tn, float eps) {
+    constexpr int D = 256 * NC;
+    const int lane = threadIdx.x & 31;
+    const long long row = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (row >= Tn) return;
+    const bf16* xr = x + row * D;
+    uint4 raw[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) raw[k] = *reinterpret_cast<const uint4*>(xr + k * 256 + lane * 8);
+    auto unpack = [](const uint4& r, float (&v)[8]) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(h[i]);
+            v[2 * i] = f.x;
+            v[2 * i + 1] = f.y;
+        }
+    };
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        float v[8];
+        unpack(raw[k], v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += v[i];
+    }
+    // keep the row packed between passes (re-expanding is cheaper than 8 NC
+    // live fp32 registers per lane)
+    auto pin = [&]() {
+#pragma unroll
+        for (int k = 0; k < NC; ++k) asm volatile("" : "+r"(raw[k].x), "+r"(raw[k].y), "+r"(raw[k].z), "+r"(raw[k].w));
+    };
+    pin();
+    const float mu = rms ? 0.f : warp_sum(s) / D;
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        float v[8];
+        unpack(raw[k], v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) q += (v[i] - mu) * (v[i] - mu);
+    }
+    pin();
+    const float rs = rsqrtf(warp_sum(q) / D + eps);
+    if (lane == 0) {
+        if (mean) mean[row] = mu;
+        rstd[row] = rs;
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        const int c = k * 256 + lane * 8;
+        float v[8], wv[8], bv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        unpack(raw[k], v);
         load8(w + c, wv);
         if (b) load8(b + c, bv);
 #pragma unroll
@@ -335,9 +403,22 @@ __global__ void rope_gather_grad_k(const float* dq, const AttnSeg* segs, const i
 }
 
 // ------------------------------------------------------------ activation ---
-__device__ __forceinline__ float gelu_tanh(float x) { return gelu_tanh_f(x); }
-__device__ __forceinline__ float gelu_tanh_grad(float x) { return gelu_tanh_grad_f(x); }
-__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+// fp32 (parity) path: exact tanhf / division; bf16 path: MUFU forms.
+template <typename T>
+__device__ __forceinline__ float gelu_tanh(float x) {
+    if constexpr (std::is_same<T, float>::value) return gelu_tanh_f(x);
+    else return gelu_tanh_fast_f(x);
+}
+template <typename T>
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+    if constexpr (std::is_same<T, float>::value) return gelu_tanh_grad_f(x);
+    else return gelu_tanh_grad_fast_f(x);
+}
+template <typename T>
+__device__ __forceinline__ float sigmoidf_(float x) {
+    if constexpr (std::is_same<T, float>::value) return 1.f / (1.f + expf(-x));
+    else return __fdividef(1.f, 1.f + __expf(-x));
+}
 
 template <typename T>
 __global__ void act_fwd_k(int act, const T* h, T* out, long long Tn, int F) {
@@ -349,7 +430,7 @@ __global__ void act_fwd_k(int act, const T* h, T* out, long long Tn, int F) {
         if (act == 0) {
             load8(h + e, v);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = gelu_tanh(v[k]);
+            for (int k = 0; k < 8; ++k) v[k] = gelu_tanh<T>(v[k]);
         } else {
             const long long t = e / F;
             const int c = static_cast<int>(e % F);
@@ -357,7 +438,7 @@ __global__ void act_fwd_k(int act, const T* h, T* out, long long Tn, int F) {
             load8(h + t * 2 * F + c, g);
             load8(h + t * 2 * F + F + c, u);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = g[k] * sigmoidf_(g[k]) * u[k];
+            for (int k = 0; k < 8; ++k) v[k] = g[k] * sigmoidf_<T>(g[k]) * u[k];
         }
         store8(out + e, v);
     }
@@ -375,7 +456,7 @@ __global__ void act_bwd_k(int act, const T* h, const T* da, T* dh, long long Tn,
             float x[8];
             load8(h + e, x);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) d[k] *= gelu_tanh_grad(x[k]);
+            for (int k = 0; k < 8; ++k) d[k] *= gelu_tanh_grad<T>(x[k]);
             store8(dh + e, d);
         } else {
             const long long t = e / F;
@@ -385,7 +466,7 @@ __global__ void act_bwd_k(int act, const T* h, const T* da, T* dh, long long Tn,
             load8(h + t * 2 * F + F + c, u);
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                const float sg = sigmoidf_(g[k]);
+                const float sg = sigmoidf_<T>(g[k]);
                 const float si = g[k] * sg;
                 du[k] = d[k] * si;
                 dg[k] = d[k] * u[k] * sg * (1.f + g[k] * (1.f - sg));
@@ -483,15 +564,45 @@ __global__ void add_k(T* y, const T* x, long long n) {
 template <typename T>
 __global__ void adamw_k(float* master, T* work, float* grad, float* m, float* v, long long n,
                         float lr, float b1, float b2, float eps, float wd, float bc1, float bc2) {
-    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+    // 4 parameters per thread and iteration (16-byte fp32 accesses); tensors
+    // are allocated 256-byte aligned, n need not be a multiple of 4
+    const long long n4 = n / 4;
+    const float ib1 = 1.f / bc1, ib2 = 1.f / bc2;
+    auto one = [&](float& p, float& mi, float& vi, float g) {
+        mi = b1 * mi + (1.f - b1) * g;
+        vi = b2 * vi + (1.f - b2) * g * g;
+        p -= lr * (wd * p + (mi * ib1) / (sqrtf(vi * ib2) + eps));
+    };
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const float g = grad[i];
-        const float mi = b1 * m[i] + (1.f - b1) * g;
-        const float vi = b2 * v[i] + (1.f - b2) * g * g;
+        float4 g = reinterpret_cast<const float4*>(grad)[i];
+        float4 mm = reinterpret_cast<const float4*>(m)[i];
+        float4 vv = reinterpret_cast<const float4*>(v)[i];
+        float4 p = reinterpret_cast<const float4*>(master)[i];
+        one(p.x, mm.x, vv.x, g.x);
+        one(p.y, mm.y, vv.y, g.y);
+        one(p.z, mm.z, vv.z, g.z);
+        one(p.w, mm.w, vv.w, g.w);
+        reinterpret_cast<float4*>(m)[i] = mm;
+        reinterpret_cast<float4*>(v)[i] = vv;
+        reinterpret_cast<float4*>(master)[i] = p;
+        reinterpret_cast<float4*>(grad)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if constexpr (std::is_same<T, float>::value) {
+            reinterpret_cast<float4*>(work)[i] = p;
+        } else {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(p.x, p.y), hi = __floats2bfloat162_rn(p.z, p.w);
+            uint2 raw;
+            raw.x = *reinterpret_cast<uint32_t*>(&lo);
+            raw.y = *reinterpret_cast<uint32_t*>(&hi);
+            reinterpret_cast<uint2*>(work)[i] = raw;
+        }
+    }
+    for (long long i = 4 * n4 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        float p = master[i], mi = m[i], vi = v[i];
+        one(p, mi, vi, grad[i]);
         m[i] = mi;
         v[i] = vi;
-        float p = master[i];
-        p -= lr * (wd * p + (mi / bc1) / (sqrtf(vi / bc2) + eps));
         master[i] = p;
         work[i] = from_f<T>(p);
         grad[i] = 0.f;
@@ -585,6 +696,20 @@ void norm_fwd(DType t, bool rms, const void* x, const void* w, const void* b, vo
     if (T == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
+        const int blocks = ceil_div(static_cast<long long>(T) * 32, 256);
+        auto warp_kernel = [&](auto nc) {
+            constexpr int NC = decltype(nc)::value;
+            norm_fwd_warp_k<NC><<<blocks, 256, 0, s>>>(rms, static_cast<const bf16*>(x), static_cast<const bf16*>(w),
+                                                       static_cast<const bf16*>(b), static_cast<bf16*>(y), mean, rstd,
+                                                       T, eps);
+        };
+        if constexpr (std::is_same<E, bf16>::value) {
+            if (D == 256) return warp_kernel(std::integral_constant<int, 1>{});
+            if (D == 512) return warp_kernel(std::integral_constant<int, 2>{});
+            if (D == 1024) return warp_kernel(std::integral_constant<int, 4>{});
+            if (D == 2048) return warp_kernel(std::integral_constant<int, 8>{});
+            if (D == 4096) return warp_kernel(std::integral_constant<int, 16>{});
+        }
         norm_fwd_k<E><<<T, norm_threads(D), 0, s>>>(rms, static_cast<const E*>(x),
                                                     static_cast<const E*>(w),
                                                     static_cast<const E*>(b), static_cast<E*>(y),
@@ -743,7 +868,7 @@ void adamw(float* master, void* work, DType t, float* grad, float* m, float* v, 
     if (n == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        adamw_k<E><<<grid_for(n, 256), 256, 0, s>>>(master, static_cast<E*>(work), grad, m, v, n,
+        adamw_k<E><<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(master, static_cast<E*>(work), grad, m, v, n,
                                                      lr, b1, b2, eps, wd, bc1, bc2);
     });
     EPP_CHECK_LAUNCH();

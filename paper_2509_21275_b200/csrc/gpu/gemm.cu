@@ -123,7 +123,7 @@ __device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t taddr,
                     for (int j = 0; j < 8; ++j) {
                         const float rv = __bfloat162float(rb[j]);
                         if (EPI == static_cast<int>(Epi::AddRes)) v[i + j] += rv;
-                        else v[i + j] *= gelu_tanh_grad_f(rv);
+                        else v[i + j] *= gelu_tanh_grad_fast_f(rv);
                     }
                 }
             }
@@ -135,7 +135,7 @@ __device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t taddr,
                     __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        h[j] = __floats2bfloat162_rn(gelu_tanh_f(v[i + 2 * j]), gelu_tanh_f(v[i + 2 * j + 1]));
+                        h[j] = __floats2bfloat162_rn(gelu_tanh_fast_f(v[i + 2 * j]), gelu_tanh_fast_f(v[i + 2 * j + 1]));
                     *reinterpret_cast<uint4*>(dst2 + i) = raw;
                 }
             }
