@@ -1026,9 +1026,11 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
             if (r < nkeys) {
 #pragma unroll
                 for (int i = 0; i < 32; i += 4) {
-                    float4 x = *reinterpret_cast<float4*>(drow + c * 32 + i);
-                    x.x += v[i] * mul; x.y += v[i + 1] * mul;
-                    x.z += v[i + 2] * mul; x.w += v[i + 3] * mul;
+                    float4 x = make_float4(v[i] * mul, v[i + 1] * mul, v[i + 2] * mul, v[i + 3] * mul);
+                    if (sg.dkv_accum) {   // later slices' contributions are already there
+                        const float4 o = *reinterpret_cast<const float4*>(drow + c * 32 + i);
+                        x.x += o.x; x.y += o.y; x.z += o.z; x.w += o.w;
+                    }
                     *reinterpret_cast<float4*>(drow + c * 32 + i) = x;
                 }
             }

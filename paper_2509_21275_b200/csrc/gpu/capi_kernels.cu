@@ -59,6 +59,7 @@ struct AttnTables {
         std::vector<AttnWork> q, kk, q128, k128, q256;
         for (int i = 0; i < nseg; ++i) {
             sg[i] = AttnSeg{};
+            sg[i].dkv_accum = 1;   // kernel-level ABI: dK/dV accumulate into the caller's buffers
             sg[i].q_start = q_start[i];
             sg[i].q_len = q_len[i];
             sg[i].kv_ctx = kv_ctx[i];

@@ -53,7 +53,8 @@ struct AttnSeg {
     int kv_ctx;
     int tma_map;     // tcgen05 kernels: 0 -> AttnMaps::kv[0..1] (sequence), 1 -> kv[2..3]
     int kv_row0;     // row of key 0 in that map's row coordinate
-    int pad_;
+    int dkv_accum;   // 1: dK/dV accumulate into a persistent (sequence) buffer;
+                     // 0: chunk-local scratch, written once (tcgen05 backward)
     const void* k;       // layer-0 base
     const void* v;
     float* dk;           // fp32 gradient accumulators (backward), may be null in fwd

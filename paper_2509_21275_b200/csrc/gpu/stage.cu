@@ -478,6 +478,7 @@ private:
                 sg.v = sk.kv.get<uint8_t>() + static_cast<size_t>(nl_) * sk.len * kvw() * esz();
                 sg.kv_layer_stride = sk.len * kvw();
                 sg.dkv_layer_stride = sk.len * kvw();
+                sg.dkv_accum = 1;
             } else {
                 // Packed document: K/V rows in the chunk-local buffer (layer
                 // strided like the sequence buffers); dK/dV in a one-layer
@@ -490,6 +491,7 @@ private:
                 sg.v = cs.kv_local.get<uint8_t>() + (static_cast<size_t>(nl_) * T * kvw() + row0) * esz();
                 sg.kv_layer_stride = T * kvw();
                 sg.dkv_layer_stride = 0;
+                sg.dkv_accum = 0;
             }
             max_pos = std::max(max_pos, sg.kv_ctx + sg.q_len);
             cs.segs.push_back(sg);
@@ -733,8 +735,11 @@ private:
         wgrad(D_, Dq, T, dxm.get(), D_, L.o.get(), Dq, grad(P.wo), s);                       // dWo
         Buf dq(&pool_, sizeof(float) * static_cast<size_t>(T) * Dq, s);
         Buf delta(&pool_, sizeof(float) * static_cast<size_t>(H_) * T, s);
-        fill_zero(cs.dkv_local.get(), 2 * static_cast<size_t>(T) * kvw() * sizeof(float), s);
         AttnArgs a = attn_args(cs, j);
+        // the tcgen05 dK/dV kernel writes every key row of a packed segment
+        // exactly once (dkv_accum = 0); the other kernels accumulate
+        if (!(dt_ == DType::BF16 && attention_impl() == 1))
+            fill_zero(cs.dkv_local.get(), 2 * static_cast<size_t>(T) * kvw() * sizeof(float), s);
         a.q = L.q.get();
         a.o = L.o.get();
         a.lse = L.lse.get<float>();
