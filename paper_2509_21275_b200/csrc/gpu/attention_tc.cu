@@ -493,7 +493,7 @@ __device__ __forceinline__ uint32_t bf2(float a, float b) {
 }
 
 constexpr int TB = 64;    // secondary tile (keys in dq, queries in dkv)
-constexpr int kDqStages = 5;    // K/V ring depth of the dq kernel
+constexpr int kDqStages = 7;    // K/V ring depth of the dq kernel
 constexpr int kDkvStages = 4;   // Q/dO ring depth of the dk/dv kernel
 
 // dS for one 64-key tile of a query row: dS = 2^(s*c2 - lse) * (dP - delta).
@@ -530,11 +530,8 @@ __device__ __forceinline__ void dq_row_tile(const float (&s)[TB / 32][32], const
 
 template <int HD>
 struct DqSmem {
-    static constexpr int kBig = 128 * HD * 2;       // Q / dO tiles
     static constexpr int kSmall = TB * HD * 2;      // K / V tiles
-    static constexpr int kQ = 0;
-    static constexpr int kO = kQ + kBig;
-    static constexpr int kK = kO + kBig;                    // kDqStages stages
+    static constexpr int kK = 0;                            // kDqStages stages
     static constexpr int kV = kK + kDqStages * kSmall;
     static constexpr int kBar = kV + kDqStages * kSmall;
     static constexpr int kBytes = kBar + 24 * 8 + 16;
@@ -572,7 +569,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
     const long long row0 = sg.q_start + q0;
 
     if (threadIdx.x == 0) {
-        tc::mbar_init(q_full, 1);
+        tc::mbar_init(q_full, 2 * TQ);      // both softmax groups stage Q / dO rows into TMEM
         for (int s = 0; s < kDqStages; ++s) {
             tc::mbar_init(&kv_full[s], 1);
             tc::mbar_init(&kv_empty[s], 1);
@@ -589,16 +586,17 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = *tmem_slot;
-    constexpr uint32_t kColS = 0, kColP = 128, kColQ = 256;
+    // TMEM: Q and dO (bf16 pairs, the A operands of the score MMAs: the
+    // CTA's fixed operands cost no shared-memory bandwidth), S and dP
+    // (double-buffered), the dQ accumulator.
+    constexpr uint32_t kColQin = 0, kColOin = HD / 2, kColS = HD, kColP = HD + 2 * TB, kColQ = HD + 4 * TB;
+    static_assert(HD + 4 * TB + HD <= 512, "TMEM budget");
 
     if (warp >= 8) tc::setmaxnreg_dec<56>();
     if (warp == 9) {
         if (lane == 0) {
             const CUtensorMap* mk = &mp.kv64[2 * sg.tma_map];
             const CUtensorMap* mv = &mp.kv64[2 * sg.tma_map + 1];
-            tc::mbar_expect_tx(q_full, 2 * L::kBig);
-            load_q_tile<HD, 128>(smem + L::kQ, &mp.q128, q_full, h, static_cast<int>(row0));
-            load_q_tile<HD, 128>(smem + L::kO, &mp.do128, q_full, h, static_cast<int>(row0));
             for (int j = 0; j < nkb; ++j) {
                 const int st = j % kDqStages;
                 tc::mbar_wait(&kv_empty[st], ((j / kDqStages) & 1) ^ 1);
@@ -617,8 +615,6 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
         constexpr uint32_t tmem_u = 0;
         constexpr uint32_t idS = tc::instr_desc_mn(TQ, TB, false, false);
         constexpr uint32_t idQ = tc::instr_desc_mn(TQ, HD, false, true);
-        const uint32_t sQ = (sbase + L::kQ);
-        const uint32_t sO = (sbase + L::kO);
         // Buffer b of step j is rewritten by the scores of step j+2, issued
         // after grad(j) (which waited for the softmax of j): in-order tcgen05
         // execution orders every TMEM reuse, no extra barriers.
@@ -638,18 +634,18 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
             tc::fence_after();
             const uint32_t sK = (sbase + L::kK + st * L::kSmall);
             const uint32_t sV = (sbase + L::kV + st * L::kSmall);
-            const uint64_t dq = tc::smem_desc(sQ, 16, 1024), dO = tc::smem_desc(sO, 16, 1024);
             const uint64_t dk = tc::smem_desc(sK, 16, 1024), dv = tc::smem_desc(sV, 16, 1024);
 #pragma unroll
-            for (int cb = 0; cb < HD / 64; ++cb) {   // 64-column blocks: +16 KB (Q, dO), +8 KB (K, V)
-                tc::mma4_ss<2, 2>(tmem_u + kColS + b * TB, dq + cb * 1024, dk + cb * 512, idS, cb != 0);
-                tc::mma4_ss<2, 2>(tmem_u + kColP + b * TB, dO + cb * 1024, dv + cb * 512, idS, cb != 0);
+            for (int cb = 0; cb < HD / 64; ++cb) {   // 64 hd per block: A +32 TMEM columns, B +8 KB
+                tc::mma4_ts<8, 2>(tmem_u + kColS + b * TB, tmem_u + kColQin + cb * 32, dk + cb * 512, idS, cb != 0);
+                tc::mma4_ts<8, 2>(tmem_u + kColP + b * TB, tmem_u + kColOin + cb * 32, dv + cb * 512, idS, cb != 0);
             }
             tc::commit_w(&s_full[b]);
         };
         // one step of lookahead: the scores of step j+1 run on the
         // tensor core while the softmax group of step j works
         tc::mbar_wait(q_full, 0);
+        tc::fence_after();
         scores(0);
         for (int j = 0; j < nkb; ++j) {
             if (j + 1 < nkb) scores(j + 1);
@@ -668,6 +664,25 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
         const long long t = row0 + min(r, rows - 1);
         const float lse = a.lse[static_cast<long long>(h) * a.T + t];
         const float dlt = a.delta[static_cast<long long>(h) * a.T + t];
+        {   // stage this row of Q (group 0) / dO (group 1) into TMEM
+            const bf16* src = static_cast<const bf16*>(grp ? a.dout : a.q) + (t * a.H + h) * HD;
+#pragma unroll
+            for (int c = 0; c < HD / 64; ++c) {
+                uint32_t wv[32];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const uint4 u = *reinterpret_cast<const uint4*>(src + c * 64 + i * 8);
+                    wv[4 * i] = u.x;
+                    wv[4 * i + 1] = u.y;
+                    wv[4 * i + 2] = u.z;
+                    wv[4 * i + 3] = u.w;
+                }
+                tc::tmem_st32u(lane_base + (grp ? kColOin : kColQin) + c * 32, wv);
+            }
+            tc::tmem_wait_st();
+            tc::fence_before();
+            tc::mbar_arrive(q_full);
+        }
         for (int j = grp; j < nkb; j += 2) {
             const int b = grp;
             tc::mbar_wait(&s_full[b], (j >> 1) & 1);
@@ -687,8 +702,13 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
                 tc::reg_fence(sall[c]);
                 tc::reg_fence(pall[c]);
             }
+#ifdef EPP_BWD_FAKE_SOFTMAX   // pipeline-bound experiment (wrong results)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) pk[i] = __float_as_uint(sall[i >> 4][(i & 15) * 2] + pall[i >> 4][(i & 15) * 2]);
+#else
             if (need_mask) dq_row_tile<true>(sall, pall, c2, lse, dlt, qp - key0, pk);
             else dq_row_tile<false>(sall, pall, c2, lse, dlt, 0, pk);
+#endif
             // dS (bf16 pairs) over the first 32 columns of S buffer b: the A
             // operand of the dQ MMA
             tc::tmem_st32u(lane_base + kColS + b * TB, pk);
@@ -1001,8 +1021,16 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
                 tc::reg_fence(dall[c]);
             }
             // query qi visible to key kp iff kp - first_q <= qi < rows
+#ifdef EPP_BWD_FAKE_SOFTMAX
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                pk[i] = __float_as_uint(sall[i >> 4][(i & 15) * 2]);
+                dk[i] = __float_as_uint(dall[i >> 4][(i & 15) * 2]);
+            }
+#else
             if (need_mask) dkv_row_tile<true>(sall, dall, c2, kp - first_q, rows, pk, dk);
             else dkv_row_tile<false>(sall, dall, c2, 0, TB, pk, dk);
+#endif
             // P^T / dS^T (bf16 pairs) over the first 32 columns of the S^T /
             // dP^T buffers: the A operands of the dV / dK MMAs
             tc::tmem_st32u(lane_base + kColS + b * TB, pk);
