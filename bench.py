@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--cap", type=int, default=32768)
     ap.add_argument("--preset", default="github_like")
     ap.add_argument("--slices", type=int, default=0, help="fixed slice count N (0 = planner auto-N)")
+    ap.add_argument("--uniform-min", type=int, default=1, help="preset=uniform: shortest length")
+    ap.add_argument("--uniform-max", type=int, default=0, help="preset=uniform: longest length")
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -130,7 +132,8 @@ def make_batches(args, n_batches, world, vocab):
     from paper_2509_21275_b200 import planner, schedule
     out = []
     for i in range(n_batches):
-        lengths = planner.generate_workload(args.preset, args.seqs_per_gpu * world, 1000 + i, args.cap)
+        lengths = planner.generate_workload(args.preset, args.seqs_per_gpu * world, 1000 + i, args.cap,
+                                            args.uniform_min, args.uniform_max)
         out.append((lengths, schedule.synthetic_tokens(lengths, vocab, seed=1000 + i)))
     return out
 

@@ -126,7 +126,12 @@ def planner_config(m: ModelConfig, pp_degree: int, mem_capacity: float = 180e9,
         "cluster": {"num_gpus": pp_degree, "pp_degree": pp_degree, "sp_degree": 1,
                     "mem_capacity": float(mem_capacity),
                     "all2all_bandwidth": {}, "all2all_latency": {}},
-        "model": {"layers": L, "hidden_dim": m.hidden, "elem_bytes": 2.0,
+        # elem_bytes = 4: Eq. 10 charges the dK/dV accumulators of non-tail
+        # chunks as 2 * e * D per token per layer, and the executor keeps them
+        # in fp32 (bf16 would lose the cross-slice accumulation); the
+        # checkpointed-layer term (3 - 2I) e D l is then charged at 2x the
+        # bf16 bytes it keeps, i.e. conservatively.
+        "model": {"layers": L, "hidden_dim": m.hidden, "elem_bytes": 4.0,
                   "token_act_bytes": float(activation_bytes_per_token(m) * L),
                   "stage_state_bytes": [float(x) for x in states]},
         "cost": cost,
