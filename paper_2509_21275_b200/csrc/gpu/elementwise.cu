@@ -241,33 +241,50 @@ __global__ void __launch_bounds__(256) norm_bwd_dx_k(bool rms, const T* x, const
     }
 }
 
-// Partial dγ/dβ over a block of `rows_per` rows; threads own 8 consecutive
-// columns, so every load is a coalesced 16-byte access.  The launcher sizes
-// rows_per so the grid covers the SMs several times even for short chunks.
+// Partial dγ/dβ, one partial row per CTA: 32 column groups (8 columns each)
+// x 8 row groups; the row groups are combined in shared memory.
 template <typename T>
-__global__ void __launch_bounds__(256) norm_bwd_dw_k(bool rms, const T* x, const T* dy,
-                                                     const float* mean, const float* rstd,
-                                                     float* pw, float* pb, int Tn, int D, int rows_per) {
-    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
-    if (c >= D) return;
-    const int r0 = blockIdx.y * rows_per;
-    const int r1 = min(Tn, r0 + rows_per);
+__global__ void __launch_bounds__(256) norm_bwd_dw2_k(bool rms, const T* x, const T* dy, const float* mean,
+                                                      const float* rstd, float* pw, float* pb, int Tn, int D,
+                                                      int rows_per) {
+    __shared__ float red[2][8][256 + 8];
+    const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
+    const int c = blockIdx.x * 256 + cx * 8;
+    const int r0 = blockIdx.y * rows_per, r1 = min(Tn, r0 + rows_per);
     float aw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ab[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int r = r0; r < r1; ++r) {
-        const long long off = static_cast<long long>(r) * D + c;
-        const float mu = rms ? 0.f : mean[r];
-        const float rs = rstd[r];
-        float xv[8], gv[8];
-        load8(x + off, xv);
-        load8(dy + off, gv);
+    if (c < D) {
+        for (int r = r0 + ry; r < r1; r += 8) {
+            const long long o = static_cast<long long>(r) * D + c;
+            const float mu = rms ? 0.f : mean[r];
+            const float rs = rstd[r];
+            float xv[8], gv[8];
+            load8(x + o, xv);
+            load8(dy + o, gv);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            aw[i] += gv[i] * (xv[i] - mu) * rs;
-            ab[i] += gv[i];
+            for (int i = 0; i < 8; ++i) {
+                aw[i] += gv[i] * (xv[i] - mu) * rs;
+                ab[i] += gv[i];
+            }
         }
     }
-    store8(pw + static_cast<long long>(blockIdx.y) * D + c, aw);
-    if (pb) store8(pb + static_cast<long long>(blockIdx.y) * D + c, ab);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        red[0][ry][cx * 8 + i] = aw[i];
+        red[1][ry][cx * 8 + i] = ab[i];
+    }
+    __syncthreads();
+    // 256 threads: thread t reduces column t of the CTA's 256 columns
+    const int col = blockIdx.x * 256 + threadIdx.x;
+    if (col < D) {
+        float sw = 0.f, sb = 0.f;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            sw += red[0][g][threadIdx.x];
+            sb += red[1][g][threadIdx.x];
+        }
+        pw[static_cast<long long>(blockIdx.y) * D + col] = sw;
+        if (pb) pb[static_cast<long long>(blockIdx.y) * D + col] = sb;
+    }
 }
 
 // dst[c] += sum_g part[g, c]  (deterministic column reduction).  A CTA owns
@@ -738,10 +755,10 @@ void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy, c
     ProfScope prof_(kProfNormBwd, double(T) * D * 6 * dtype_size(t), s);
     EPP_REQUIRE(D % 8 == 0 && D <= 8 * 256 * kNormMaxG, "norm_bwd: unsupported D");
     if (T == 0) return;
-    // ~4 waves of 148 SMs for the partial-sum kernel, rows per block >= 8
-    const int col_blocks = ceil_div(D / 8, 256);
-    const int rows_per = std::max(8, ceil_div(T, std::max(1, 592 / col_blocks)));
-    const int G = ceil_div(T, rows_per);
+    // ~4 waves of 148 SMs for the partial-sum kernel (256 columns per CTA)
+    const int col_blocks = ceil_div(D, 256);
+    const int G = std::max(1, std::min(ceil_div(T, 8), 592 / col_blocks));
+    const int rows_per = ceil_div(T, G);
     float* part = nullptr;
     EPP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * 2 * G * D, s));
     float* pw = part;
@@ -752,7 +769,7 @@ void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy, c
             rms, static_cast<const E*>(x), static_cast<const E*>(w), static_cast<const E*>(dy), mean,
             rstd, static_cast<const E*>(dres), static_cast<E*>(dx), T, D);
         EPP_CHECK_LAUNCH();
-        norm_bwd_dw_k<E><<<dim3(col_blocks, G), 256, 0, s>>>(
+        norm_bwd_dw2_k<E><<<dim3(col_blocks, G), 256, 0, s>>>(
             rms, static_cast<const E*>(x), static_cast<const E*>(dy), mean, rstd, pw, pb, T, D, rows_per);
         EPP_CHECK_LAUNCH();
     });
