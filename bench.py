@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--cap", type=int, default=32768)
     ap.add_argument("--preset", default="github_like")
     ap.add_argument("--slices", type=int, default=0, help="fixed slice count N (0 = planner auto-N)")
+    ap.add_argument("--no-calibrate", action="store_true",
+                    help="keep the analytic Eq. 1 coefficients (default: fit them on warmup step 0)")
     ap.add_argument("--uniform-min", type=int, default=1, help="preset=uniform: shortest length")
     ap.add_argument("--uniform-max", type=int, default=0, help="preset=uniform: longest length")
     ap.add_argument("--dtype", default="bf16")
@@ -141,7 +143,7 @@ def make_batches(args, n_batches, world, vocab):
 def run_ours(args):
     import torch.distributed as dist
 
-    from paper_2509_21275_b200 import gpu, model as M, planner, schedule
+    from paper_2509_21275_b200 import calibrate, gpu, model as M, planner, schedule
     from paper_2509_21275_b200.executor import DistributedPipeline, LocalPipeline, _ChunkTokens, stage_layers
 
     world = args.gpus
@@ -163,20 +165,27 @@ def run_ours(args):
     jobs = os.cpu_count() or 8
 
     batches = make_batches(args, args.warmup + args.steps, world, m.vocab)
-    t0 = time.perf_counter()
-    plans = []
-    for lengths, _ in batches[: args.warmup + args.steps]:
-        plans.append(schedule.parse_plan(planner.make_plan_document(cfg, lengths, args.slices or None, "main", jobs),
-                                         lengths))
-    planner_s = (time.perf_counter() - t0) / len(plans)
+
+    def plan_all(config, first):
+        out, t = [], time.perf_counter()
+        for lengths, _ in batches[first:]:
+            out.append(schedule.parse_plan(planner.make_plan_document(config, lengths, args.slices or None, "main",
+                                                                      jobs), lengths))
+        return out, (time.perf_counter() - t) / max(1, len(out))
+
+    plans, planner_s = plan_all(cfg, 0)
 
     first, num = stage_layers(m.layers, dp, rank)
     stage = gpu.CudaStage(m, first, num, rank == 0, rank == dp - 1, dtype=args.dtype, device=local)
     stage.init_weights(1234)
-    if world > 1:
-        driver = DistributedPipeline(stage, rank, world, dev, m.hidden, gpu.TORCH_DTYPES[args.dtype])
-    else:
-        driver = LocalPipeline([stage], dev)
+    timed_stage = calibrate.TimedStage(stage)
+
+    def make_driver(st):
+        if world > 1:
+            return DistributedPipeline(st, rank, world, dev, m.hidden, gpu.TORCH_DTYPES[args.dtype])
+        return LocalPipeline([st], dev)
+
+    driver = make_driver(stage)
 
     def sync_all():
         torch.cuda.synchronize()
@@ -196,7 +205,31 @@ def run_ours(args):
     if os.environ.get("EPP_BENCH_BACKEND", "nccl") == "nccl":   # (ranks own their GPU)
         free_b, _ = torch.cuda.mem_get_info()
         gpu.pool_reserve(free_b - int(6e9))
+    cost_report = {"source": "analytic (model.default_cost)"}
     for i in range(args.warmup):
+        if i == 0 and not args.no_calibrate:
+            # closed loop: time every stage op of warmup step 0, fit Eq. 1 to
+            # it (all ranks' samples, so every rank plans identically) and
+            # re-plan the remaining batches with the fitted coefficients
+            make_driver(timed_stage).run_step(plans[0], batches[0][1])
+            optimizer()
+            sync_all()
+            samples = timed_stage.samples()
+            if world > 1:
+                gathered = [None] * world
+                dist.all_gather_object(gathered, samples)
+                samples = [x for part in gathered for x in part]
+            try:
+                fitted = calibrate.calibrated_config(cfg, samples)
+                cfg = calibrate.planner_config_only(fitted)
+                rest, planner_s = plan_all(cfg, 1)
+                plans = plans[:1] + rest
+                cost_report = {"source": f"fitted on warmup step 0 ({fitted['_fit']['samples']} stage-op samples)",
+                               "fwd_residual": fitted["_fit"]["fwd_residual"],
+                               "bwd_residual": fitted["_fit"]["bwd_residual"], "cost": cfg["cost"]}
+            except planner.Error as e:
+                cost_report = {"source": "analytic (fit failed: %s)" % e}
+            continue
         driver.run_step(plans[i], batches[i][1])
         optimizer()
     sync_all()
@@ -300,6 +333,10 @@ def run_ours(args):
             dist.destroy_process_group()
         return
     hbm, tf_burst, tf_sus, peak_src = peaks()
+    # the planner's simulated makespan of the timed plans vs the measured step
+    predicted = sum(calibrate.predicted_seconds(plans[i].doc) for i in timed) / len(timed)
+    cost_model = dict(cost_report, predicted_step_s=predicted, measured_step_s=ms / 1e3 / args.steps,
+                      measured_over_predicted=(ms / 1e3 / args.steps) / predicted if predicted > 0 else None)
     # dominant kernel class by device time in the timed region
     names = {"gemm": "gemm_tc_kernel (tcgen05 BF16 GEMM, fwd/dgrad/wgrad)",
              "attn_fwd": "attn_fwd (slice-causal flash attention forward)",
@@ -336,6 +373,7 @@ def run_ours(args):
         "model_tflops_per_gpu": flops / sec / world / 1e12,
         "loss": (loss_sum / loss_cnt) if loss_cnt else None,
         "planner_seconds_per_batch": planner_s,
+        "cost_model": cost_model,
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "kernel": names[dom],
                      "achieved": achieved, "peak": tf_sus, "unit": "TFLOP/s",

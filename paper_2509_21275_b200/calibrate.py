@@ -1,0 +1,84 @@
+"""Closed-loop cost model: measured stage times -> Eq. 1 coefficients.
+
+The planner prices every chunk with Eq. 1 (proj/src/cost_model.cpp:12-25),
+whose coefficients the paper obtains by offline profiling.
+This module measures them on the GPU executor itself:
+
+  1. `TimedStage` wraps a stage (gpu.CudaStage) and records CUDA events
+     around every forward / backward call of a step;
+  2. `samples()` turns those into fit samples {context, slices, phase,
+     seconds} (backward ops that re-ran checkpointed layers are skipped:
+     Eq. 1 prices recompute separately, via layer_fwd_seconds);
+  3. `calibrated_config()` feeds them to fit_cost_params
+     (proj/src/cost_model.cpp:143-223, the planner library's C ABI) and returns
+     the planner configuration with the fitted coefficients;
+  4. `predicted_seconds()` is the planner's simulated makespan of a plan
+     (plan_simulated_seconds, planner.cpp:489-493), to compare with the
+     measured step time.
+"""
+from __future__ import annotations
+
+import copy
+import json
+from typing import Dict, List
+
+import torch
+
+from . import planner
+
+
+class TimedStage:
+    """Delegates to `stage`, timing each forward/backward on the current
+    stream (CUDA events; read after the step has been synchronised)."""
+
+    def __init__(self, stage):
+        self.stage = stage
+        self.records = []   # (op, phase, start event, end event)
+
+    def __getattr__(self, name):
+        return getattr(self.stage, name)
+
+    def _timed(self, phase, fn, op, x):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = fn(op, x)
+        b.record()
+        self.records.append((op, phase, a, b))
+        return out
+
+    def forward(self, op, act_in):
+        return self._timed("forward", self.stage.forward, op, act_in)
+
+    def backward(self, op, grad_in):
+        return self._timed("backward", self.stage.backward, op, grad_in)
+
+    def samples(self) -> List[Dict]:
+        out = []
+        for op, phase, a, b in self.records:
+            if phase == "backward" and op.ckpt_layers > 0:
+                continue
+            out.append({"context": int(op.context), "slices": [int(s) for s in op.slices], "phase": phase,
+                        "seconds": a.elapsed_time(b) / 1e3})
+        return out
+
+
+def calibrated_config(cfg: Dict, samples: List[Dict]) -> Dict:
+    """`cfg` with Eq. 1 coefficients fitted to `samples` (needs >= 4 samples
+    per phase over >= 2 distinct chunk sizes)."""
+    fit = planner.fit_cost_params(cfg, samples)
+    out = copy.deepcopy(cfg)
+    out["cost"].update({k: float(v) for k, v in fit["cost"].items()})
+    out["_fit"] = {"fwd_residual": fit["fwd_residual"], "bwd_residual": fit["bwd_residual"],
+                   "samples": len(samples)}
+    return out
+
+
+def planner_config_only(cfg: Dict) -> Dict:
+    """Drop bookkeeping keys before handing a config to the planner."""
+    return {k: v for k, v in cfg.items() if not k.startswith("_")}
+
+
+def predicted_seconds(plan_doc) -> float:
+    """Simulated makespan summed over the plan's units (seconds)."""
+    _, total = planner.simulate_plan_document(plan_doc if isinstance(plan_doc, str) else json.dumps(plan_doc))
+    return total

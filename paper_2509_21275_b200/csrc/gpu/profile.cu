@@ -17,10 +17,40 @@ struct Rec {
 };
 std::mutex g_mu;
 bool g_on = false;
-std::vector<Rec> g_recs;
+std::vector<Rec> g_recs;       // oldest first
+size_t g_head = 0;             // first record not yet harvested
 std::vector<cudaEvent_t> g_free;
+struct Acc {
+    double ms = 0, flops = 0;
+    int64_t n = 0;
+};
+Acc g_acc[32];                 // harvested totals per class
+
+// Fold completed records (oldest first) into the per-class totals and
+// recycle their events, so a long timed region keeps a bounded event pool
+// instead of creating two events per launch.
+void harvest() {
+    while (g_head < g_recs.size()) {
+        const Rec& r = g_recs[g_head];
+        if (cudaEventQuery(r.b) != cudaSuccess) break;
+        float e = 0;
+        if (cudaEventElapsedTime(&e, r.a, r.b) != cudaSuccess) break;
+        Acc& a = g_acc[r.cls];
+        a.ms += e;
+        a.flops += r.flops;
+        ++a.n;
+        g_free.push_back(r.a);
+        g_free.push_back(r.b);
+        ++g_head;
+    }
+    if (g_head > 4096 && g_head * 2 > g_recs.size()) {
+        g_recs.erase(g_recs.begin(), g_recs.begin() + static_cast<long>(g_head));
+        g_head = 0;
+    }
+}
 
 cudaEvent_t take() {
+    if (g_free.empty()) harvest();
     if (!g_free.empty()) {
         cudaEvent_t e = g_free.back();
         g_free.pop_back();
@@ -59,31 +89,15 @@ int epp_gpu_profile(int32_t enable) {
 
 int epp_gpu_profile_read(int32_t cls, double* ms, double* flops, int64_t* launches, int32_t reset) {
     std::lock_guard<std::mutex> lk(eppk::g_mu);
-    double t = 0, f = 0;
-    int64_t n = 0;
-    std::vector<eppk::Rec> keep;
-    for (auto& r : eppk::g_recs) {
-        if (r.cls != cls) {
-            keep.push_back(r);
-            continue;
-        }
-        float e = 0;
-        if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&e, r.a, r.b) != cudaSuccess)
-            return EPP_GPU_ECUDA;
-        t += e;
-        f += r.flops;
-        ++n;
-        if (reset) {
-            eppk::g_free.push_back(r.a);
-            eppk::g_free.push_back(r.b);
-        } else {
-            keep.push_back(r);
-        }
-    }
-    eppk::g_recs.swap(keep);
-    if (ms) *ms = t;
-    if (flops) *flops = f;
-    if (launches) *launches = n;
+    if (cls < 0 || cls >= 32) return EPP_GPU_EARG;
+    for (size_t i = eppk::g_head; i < eppk::g_recs.size(); ++i)
+        if (cudaEventSynchronize(eppk::g_recs[i].b) != cudaSuccess) return EPP_GPU_ECUDA;
+    eppk::harvest();
+    const eppk::Acc a = eppk::g_acc[cls];
+    if (reset) eppk::g_acc[cls] = eppk::Acc{};
+    if (ms) *ms = a.ms;
+    if (flops) *flops = a.flops;
+    if (launches) *launches = a.n;
     return 0;
 }
 }
