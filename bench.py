@@ -221,8 +221,9 @@ def run_ours(args):
                 samples = [x for part in gathered for x in part]
             try:
                 fitted = calibrate.calibrated_config(cfg, samples)
-                cfg = calibrate.planner_config_only(fitted)
-                rest, planner_s = plan_all(cfg, 1)
+                cfg_fit = calibrate.planner_config_only(fitted)
+                rest, planner_s = plan_all(cfg_fit, 1)
+                cfg = cfg_fit
                 plans = plans[:1] + rest
                 cost_report = {"source": f"fitted on warmup step 0 ({fitted['_fit']['samples']} stage-op samples)",
                                "fwd_residual": fitted["_fit"]["fwd_residual"],

@@ -67,7 +67,10 @@ def calibrated_config(cfg: Dict, samples: List[Dict]) -> Dict:
     per phase over >= 2 distinct chunk sizes)."""
     fit = planner.fit_cost_params(cfg, samples)
     out = copy.deepcopy(cfg)
-    out["cost"].update({k: float(v) for k, v in fit["cost"].items()})
+    # the least-squares fit is unconstrained; a coefficient that comes out
+    # negative (noise around ~0, e.g. a tiny fixed cost) is clamped to 0, the
+    # planner's config contract (config.cpp validate: non-negative costs)
+    out["cost"].update({k: max(0.0, float(v)) for k, v in fit["cost"].items()})
     out["_fit"] = {"fwd_residual": fit["fwd_residual"], "bwd_residual": fit["bwd_residual"],
                    "samples": len(samples)}
     return out
