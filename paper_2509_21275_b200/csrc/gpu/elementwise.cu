@@ -903,6 +903,8 @@ void init_const(float* dst, long long n, float v, cudaStream_t s) {
     EPP_CHECK_LAUNCH();
 }
 
+const float2* rope_table_ptr(int hd, float theta, cudaStream_t s) { return rope_table(0, hd, theta, s); }
+
 void rope_reserve(int max_pos, int hd, float theta, cudaStream_t s) {
     rope_table(max_pos, hd, theta, s);
 }

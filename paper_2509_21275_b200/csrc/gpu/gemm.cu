@@ -63,6 +63,7 @@ struct TcParams {
     long long ldr;
     bf16* C2;
     long long ldc2;
+    RopeScatterArgs rope;
 };
 
 // Persistent CTAs (one per SM) walk the output tiles in a grouped raster
@@ -88,8 +89,80 @@ struct TileSched {
 // columns [n0, n0 + BN), read 32 columns at a time from TMEM (taddr = the
 // warp's lane quarter), fused epilogue, 16-byte stores.  The tcgen05.ld is
 // warp-collective, so every lane runs the loop even past the matrix edge.
+// Fused QKV epilogue (Epi::RopeScatter): rotate-half RoPE on the q and k
+// heads of the tile (column d pairs with d + hd/2 of the same head, so the
+// two 32-column chunks are read together), one bf16 rounding, and direct
+// stores to q [T, H, hd] and to the segment's K / V rows of this layer —
+// the separate rope_qkv_scatter pass and the [T, (H+2Hkv) hd] round trip
+// through HBM disappear.
+template <int BN>
+__device__ __forceinline__ void epilogue_rope(const TcParams& p, uint32_t taddr, int row, int n0) {
+    const RopeScatterArgs& rp = p.rope;
+    const int hd = rp.hd, half = hd / 2;
+    const bool valid = row < p.M;
+    const int pos = valid ? rp.tok_pos[row] : 0;
+    const AttnSeg* sg = valid ? rp.segs + rp.tok_seg[row] : nullptr;
+#pragma unroll 1
+    for (int hs = 0; hs < BN; hs += hd) {
+        const int slot = (n0 + hs) / hd;
+#pragma unroll 1
+        for (int cc = 0; cc < half; cc += 32) {
+            float a[32], b[32];
+            tc::tmem_ld32(taddr + hs + cc, a);          // warp-collective: every lane
+            tc::tmem_ld32(taddr + hs + half + cc, b);
+            if (!valid || n0 + hs >= p.N) continue;
+            if (slot < rp.H + rp.Hkv) {
+                const float4* c4 = reinterpret_cast<const float4*>(rp.cs + static_cast<long long>(pos) * half + cc);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const float4 cs2 = c4[k];          // (cos, sin) of d = cc + 2k, cc + 2k + 1
+                    const float a0 = a[2 * k] * cs2.x - b[2 * k] * cs2.y;
+                    const float b0 = b[2 * k] * cs2.x + a[2 * k] * cs2.y;
+                    const float a1 = a[2 * k + 1] * cs2.z - b[2 * k + 1] * cs2.w;
+                    const float b1 = b[2 * k + 1] * cs2.z + a[2 * k + 1] * cs2.w;
+                    a[2 * k] = a0; b[2 * k] = b0; a[2 * k + 1] = a1; b[2 * k + 1] = b1;
+                }
+            }
+            bf16* dst;
+            if (slot < rp.H) {
+                dst = static_cast<bf16*>(rp.q_out) + (static_cast<long long>(row) * rp.H + slot) * hd;
+            } else {
+                const bool is_k = slot < rp.H + rp.Hkv;
+                const int kvh = slot - rp.H - (is_k ? 0 : rp.Hkv);
+                dst = static_cast<bf16*>(const_cast<void*>(is_k ? sg->k : sg->v)) + rp.layer * sg->kv_layer_stride +
+                      static_cast<long long>(pos) * rp.Hkv * hd + static_cast<long long>(kvh) * hd;
+            }
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+                uint4 ra, rb;
+                __nv_bfloat162* ha = reinterpret_cast<__nv_bfloat162*>(&ra);
+                __nv_bfloat162* hb = reinterpret_cast<__nv_bfloat162*>(&rb);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    ha[j] = __floats2bfloat162_rn(a[i + 2 * j], a[i + 2 * j + 1]);
+                    hb[j] = __floats2bfloat162_rn(b[i + 2 * j], b[i + 2 * j + 1]);
+                }
+                *reinterpret_cast<uint4*>(dst + cc + i) = ra;
+                *reinterpret_cast<uint4*>(dst + half + cc + i) = rb;
+            }
+        }
+    }
+}
+
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_plain(const TcParams& p, uint32_t taddr, int row, int n0, bool have_acc);
+
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t taddr, int row, int n0, bool have_acc) {
+    if constexpr (EPI == static_cast<int>(Epi::RopeScatter)) {
+        epilogue_rope<BN>(p, taddr, row, n0);
+    } else {
+        epilogue_plain<BN, EPI>(p, taddr, row, n0, have_acc);
+    }
+}
+
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_plain(const TcParams& p, uint32_t taddr, int row, int n0, bool have_acc) {
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
         float v[32];
@@ -585,7 +658,7 @@ void launch_tc(const GemmArgs& g, cudaStream_t s) {
     const CUtensorMap mb = B_MN ? make_map(g.B, g.K, g.N, g.ldb, 64, kBK)
                                 : make_map(g.B, g.N, g.K, g.ldb, kBK, BN);
     TcParams p{g.M, g.N, g.K, g.C, g.ldc, static_cast<const bf16*>(g.R), g.ldr,
-               static_cast<bf16*>(g.C2), g.ldc2};
+               static_cast<bf16*>(g.C2), g.ldc2, g.rope ? *g.rope : RopeScatterArgs{}};
     static int num_sms = 0;
     if (!num_sms) {
         int dev = 0;
@@ -617,6 +690,10 @@ void dispatch_epi(const GemmArgs& g, cudaStream_t s) {
         case Epi::StoreF32: dispatch_major<BN, STAGES, 3>(g, s); break;
         case Epi::StoreGelu: dispatch_major<BN, STAGES, 4>(g, s); break;
         case Epi::GeluBwd: dispatch_major<BN, STAGES, 5>(g, s); break;
+        case Epi::RopeScatter:
+            EPP_REQUIRE(g.a_kmajor && g.b_kmajor && g.rope, "RopeScatter: K-major operands and rope args");
+            launch_tc<BN, STAGES, false, false, 6>(g, s);
+            break;
     }
 }
 
@@ -635,7 +712,7 @@ void launch_tc2(const GemmArgs& g, cudaStream_t s) {
     const CUtensorMap mb = B_MN ? make_map(g.B, g.K, g.N, g.ldb, 64, kBK)
                                 : make_map(g.B, g.N, g.K, g.ldb, kBK, BN / 2);
     TcParams p{g.M, g.N, g.K, g.C, g.ldc, static_cast<const bf16*>(g.R), g.ldr,
-               static_cast<bf16*>(g.C2), g.ldc2};
+               static_cast<bf16*>(g.C2), g.ldc2, g.rope ? *g.rope : RopeScatterArgs{}};
     static int num_sms = 0;
     if (!num_sms) {
         int dev = 0;
@@ -667,6 +744,10 @@ void dispatch_epi2(const GemmArgs& g, cudaStream_t s) {
         case Epi::StoreF32: dispatch_major2<BN, STAGES, 3>(g, s); break;
         case Epi::StoreGelu: dispatch_major2<BN, STAGES, 4>(g, s); break;
         case Epi::GeluBwd: dispatch_major2<BN, STAGES, 5>(g, s); break;
+        case Epi::RopeScatter:
+            EPP_REQUIRE(g.a_kmajor && g.b_kmajor && g.rope, "RopeScatter: K-major operands and rope args");
+            launch_tc2<BN, STAGES, false, false, 6>(g, s);
+            break;
     }
 }
 

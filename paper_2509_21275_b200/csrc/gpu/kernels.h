@@ -25,6 +25,20 @@ enum class Epi : int {
     StoreF32 = 3,   // C(fp32) = acc
     StoreGelu = 4,  // C = acc, C2 = gelu_tanh(acc)          (MLP up-projection)
     GeluBwd = 5,    // C = acc * gelu_tanh'(R)               (MLP dgrad -> dh)
+    RopeScatter = 6,  // QKV projection: RoPE on q/k, q -> [T,H,hd], k/v -> the segments' KV rows
+};
+
+struct AttnSeg;
+// Destination of the fused QKV epilogue (Epi::RopeScatter), the same mapping
+// as rope_qkv_scatter: token t of the chunk sits at position tok_pos[t] of
+// segment tok_seg[t]; cs is the (cos, sin) table [pos][hd/2].
+struct RopeScatterArgs {
+    void* q_out = nullptr;
+    const AttnSeg* segs = nullptr;
+    const int* tok_seg = nullptr;
+    const int* tok_pos = nullptr;
+    const float2* cs = nullptr;
+    int H = 0, Hkv = 0, hd = 0, layer = 0;
 };
 
 struct GemmArgs {
@@ -34,6 +48,7 @@ struct GemmArgs {
     void* C = nullptr; long long ldc = 0;
     const void* R = nullptr; long long ldr = 0;
     void* C2 = nullptr; long long ldc2 = 0;
+    const RopeScatterArgs* rope = nullptr;   // Epi::RopeScatter
     Epi epi = Epi::Store;
     DType dtype = DType::BF16;
 };
@@ -146,6 +161,8 @@ void norm_apply(DType t, bool rms, const void* x, const void* w, const void* b,
 
 // Ensure the RoPE cos/sin table covers positions [0, max_pos).
 void rope_reserve(int max_pos, int hd, float theta, cudaStream_t s);
+// The (cos, sin) table for head_dim hd (after rope_reserve).
+const float2* rope_table_ptr(int hd, float theta, cudaStream_t s);
 // RoPE + scatter of a packed [T, (H+2Hkv)*hd] QKV row block: q -> q_out [T,H,hd],
 // k/v -> each segment's key/value rows for `layer`.
 void rope_qkv_scatter(DType t, const void* qkv, void* q_out, const AttnSeg* segs_dev, int nseg,

@@ -649,12 +649,29 @@ private:
         norm_fwd(dt_, llama_, x, work(P.ln1_w), P.ln1_b >= 0 ? work(P.ln1_b) : nullptr, xn.get(),
                  llama_ ? nullptr : L.mean1.get<float>(), L.rstd1.get<float>(), T, D_,
                  m_.norm_eps, s);
-        Buf qkv(&pool_, static_cast<size_t>(T) * Nqkv_ * e, s);
-        gemm(mk(T, Nqkv_, D_, xn.get(), D_, true, work(P.wqkv), D_, true, qkv.get(), Nqkv_), s);
-        rope_qkv_scatter(dt_, qkv.get(), L.q.get(), cs.segs_dev.get<AttnSeg>(),
-                         static_cast<int>(cs.segs.size()), cs.tok_seg.get<int>(),
-                         cs.tok_pos.get<int>(), T, H_, Hkv_, hd_, j, m_.rope_theta, s);
-        qkv.release();
+        if (dt_ == DType::BF16) {
+            // QKV projection with RoPE and the q / K / V scatter in its epilogue
+            RopeScatterArgs ra;
+            ra.q_out = L.q.get();
+            ra.segs = cs.segs_dev.get<AttnSeg>();
+            ra.tok_seg = cs.tok_seg.get<int>();
+            ra.tok_pos = cs.tok_pos.get<int>();
+            ra.cs = rope_table_ptr(hd_, m_.rope_theta, s);
+            ra.H = H_;
+            ra.Hkv = Hkv_;
+            ra.hd = hd_;
+            ra.layer = j;
+            GemmArgs g = mk(T, Nqkv_, D_, xn.get(), D_, true, work(P.wqkv), D_, true, nullptr, Nqkv_);
+            g.epi = Epi::RopeScatter;
+            g.rope = &ra;
+            gemm(g, s);
+        } else {
+            Buf qkv(&pool_, static_cast<size_t>(T) * Nqkv_ * e, s);
+            gemm(mk(T, Nqkv_, D_, xn.get(), D_, true, work(P.wqkv), D_, true, qkv.get(), Nqkv_), s);
+            rope_qkv_scatter(dt_, qkv.get(), L.q.get(), cs.segs_dev.get<AttnSeg>(),
+                             static_cast<int>(cs.segs.size()), cs.tok_seg.get<int>(),
+                             cs.tok_pos.get<int>(), T, H_, Hkv_, hd_, j, m_.rope_theta, s);
+        }
         AttnArgs a = attn_args(cs, j);
         a.q = L.q.get();
         a.o = L.o.get();
