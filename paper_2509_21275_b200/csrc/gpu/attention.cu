@@ -802,6 +802,7 @@ void attn_bwd(const AttnArgs& a, cudaStream_t s) {
         attn_bwd_tc_main(a, s);
         return;
     }
+    EPP_REQUIRE(a.dqkv_out == nullptr, "attn_bwd: dqkv_out needs the tcgen05 kernels");
     if (a.dtype == DType::F32) {
         if (a.nqwork > 0) {
             attn_bwd_dq_f32<<<dim3(a.nqwork, a.H), 128, 0, s>>>(a);

@@ -720,16 +720,57 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
         // barrier whose earlier phases it never observed: parity would alias)
         tc::mbar_wait(acc_full, 0);
         tc::fence_after();
-        float* drow = a.dq + ((row0 + r) * a.H + h) * HD;
+        if (a.dqkv_out) {
+            // dQ straight into the q columns of dqkv (bf16) with RoPE undone:
+            // group g takes the column pairs (d, d + HD/2) for d in chunk g
+            constexpr int HALF = HD / 2;
+            const long long t_out = row0 + r;
+            const int pos = r < rows ? a.tok_pos[t_out] : 0;
+            bf16* drow = static_cast<bf16*>(a.dqkv_out) + t_out * (a.H + 2 * a.Hkv) * HD + h * HD;
 #pragma unroll 1
-        for (int c = grp * (HD / 64); c < (grp + 1) * (HD / 64); ++c) {   // each group: half the columns
-            float v[32];
-            tc::tmem_ld32(lane_base + kColQ + c * 32, v);
-            if (r < rows) {
+            for (int cc = grp * 32; cc < HALF; cc += 64) {
+                float g1[32], g2[32];
+                tc::tmem_ld32(lane_base + kColQ + cc, g1);
+                tc::tmem_ld32(lane_base + kColQ + HALF + cc, g2);
+                if (r < rows) {
+                    const float4* c4 = reinterpret_cast<const float4*>(a.rope_cs + static_cast<long long>(pos) * HALF + cc);
 #pragma unroll
-                for (int i = 0; i < 32; i += 4)
-                    *reinterpret_cast<float4*>(drow + c * 32 + i) =
-                        make_float4(v[i] * a.scale, v[i + 1] * a.scale, v[i + 2] * a.scale, v[i + 3] * a.scale);
+                    for (int k = 0; k < 16; ++k) {
+                        const float4 cs = c4[k];
+                        const float x0 = g1[2 * k] * a.scale, y0 = g2[2 * k] * a.scale;
+                        const float x1 = g1[2 * k + 1] * a.scale, y1 = g2[2 * k + 1] * a.scale;
+                        g1[2 * k] = x0 * cs.x + y0 * cs.y;
+                        g2[2 * k] = y0 * cs.x - x0 * cs.y;
+                        g1[2 * k + 1] = x1 * cs.z + y1 * cs.w;
+                        g2[2 * k + 1] = y1 * cs.z - x1 * cs.w;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 32; i += 8) {
+                        uint4 ra, rb;
+                        __nv_bfloat162* ha = reinterpret_cast<__nv_bfloat162*>(&ra);
+                        __nv_bfloat162* hb = reinterpret_cast<__nv_bfloat162*>(&rb);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            ha[j] = __floats2bfloat162_rn(g1[i + 2 * j], g1[i + 2 * j + 1]);
+                            hb[j] = __floats2bfloat162_rn(g2[i + 2 * j], g2[i + 2 * j + 1]);
+                        }
+                        *reinterpret_cast<uint4*>(drow + cc + i) = ra;
+                        *reinterpret_cast<uint4*>(drow + HALF + cc + i) = rb;
+                    }
+                }
+            }
+        } else {
+            float* drow = a.dq + ((row0 + r) * a.H + h) * HD;
+#pragma unroll 1
+            for (int c = grp * (HD / 64); c < (grp + 1) * (HD / 64); ++c) {   // each group: half the columns
+                float v[32];
+                tc::tmem_ld32(lane_base + kColQ + c * 32, v);
+                if (r < rows) {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4)
+                        *reinterpret_cast<float4*>(drow + c * 32 + i) =
+                            make_float4(v[i] * a.scale, v[i + 1] * a.scale, v[i + 2] * a.scale, v[i + 3] * a.scale);
+                }
             }
         }
         tc::fence_before();

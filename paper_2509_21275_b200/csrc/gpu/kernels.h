@@ -130,6 +130,12 @@ struct AttnArgs {
     const void* dout = nullptr;   // [T, H, hd]
     float* delta = nullptr;       // [H, T] scratch
     float* dq = nullptr;          // [T, H, hd] fp32 (fully written by attn_bwd)
+    // tcgen05 dQ kernel: when set, dQ is written instead as bf16 into the q
+    // columns of dqkv [T, (H+2Hkv) hd] with RoPE undone (rope_cs = the
+    // (cos, sin) table, tok_pos = each query's position); dq is then unused
+    void* dqkv_out = nullptr;
+    const int* tok_pos = nullptr;
+    const float2* rope_cs = nullptr;
     const AttnMaps* maps = nullptr;   // host struct, required by the tcgen05 kernels
 };
 
@@ -172,7 +178,7 @@ void rope_qkv_scatter(DType t, const void* qkv, void* q_out, const AttnSeg* segs
 // un-rotating dq/dk.
 void rope_qkv_gather_grad(DType t, const float* dq, const AttnSeg* segs_dev, const int* tok_seg,
                           const int* tok_pos, void* dqkv, int T, int H, int Hkv, int hd,
-                          int layer, float theta, cudaStream_t s);
+                          int layer, float theta, cudaStream_t s, bool kv_only = false);
 
 // act: 0 = GELU(tanh), 1 = SwiGLU (input [T,2F] gate|up -> [T,F])
 void act_fwd(DType t, int act, const void* h, void* a, int T, int F, cudaStream_t s);

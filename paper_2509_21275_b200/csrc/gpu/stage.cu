@@ -750,19 +750,29 @@ private:
         Buf dout(&pool_, static_cast<size_t>(T) * Dq * e, s);
         gemm(mk(T, Dq, D_, dxm.get(), D_, true, work(P.wo), Dq, false, dout.get(), Dq), s);  // dO
         wgrad(D_, Dq, T, dxm.get(), D_, L.o.get(), Dq, grad(P.wo), s);                       // dWo
-        Buf dq(&pool_, sizeof(float) * static_cast<size_t>(T) * Dq, s);
         Buf delta(&pool_, sizeof(float) * static_cast<size_t>(H_) * T, s);
+        Buf dqkv(&pool_, static_cast<size_t>(T) * Nqkv_ * e, s);
         AttnArgs a = attn_args(cs, j);
-        // the tcgen05 dK/dV kernel writes every key row of a packed segment
-        // exactly once (dkv_accum = 0); the other kernels accumulate
-        if (!(dt_ == DType::BF16 && attention_impl() == 1))
-            fill_zero(cs.dkv_local.get(), 2 * static_cast<size_t>(T) * kvw() * sizeof(float), s);
+        // tcgen05 backward: the dK/dV kernel writes every key row of a packed
+        // segment exactly once (dkv_accum = 0) and the dQ kernel writes the
+        // un-rotated bf16 dQ straight into dqkv; the other kernels accumulate
+        // into zeroed buffers and leave dQ in fp32 for the gather pass
+        const bool tc_bwd = dt_ == DType::BF16 && attention_impl() == 1;
+        if (!tc_bwd) fill_zero(cs.dkv_local.get(), 2 * static_cast<size_t>(T) * kvw() * sizeof(float), s);
         a.q = L.q.get();
         a.o = L.o.get();
         a.lse = L.lse.get<float>();
         a.dout = dout.get();
         a.delta = delta.get<float>();
-        a.dq = dq.get<float>();
+        Buf dq;
+        if (tc_bwd) {
+            a.dqkv_out = dqkv.get();
+            a.tok_pos = cs.tok_pos.get<int>();
+            a.rope_cs = rope_table_ptr(hd_, m_.rope_theta, s);
+        } else {
+            dq = Buf(&pool_, sizeof(float) * static_cast<size_t>(T) * Dq, s);
+            a.dq = dq.get<float>();
+        }
         if (dt_ == DType::BF16) {
             attn_maps_q(cs.maps, L.q.get(), dout.get(), T, H_, hd_);
             a.maps = &cs.maps;
@@ -770,9 +780,9 @@ private:
         attn_bwd(a, s);
         dout.release();
         delta.release();
-        Buf dqkv(&pool_, static_cast<size_t>(T) * Nqkv_ * e, s);
         rope_qkv_gather_grad(dt_, dq.get<float>(), cs.segs_dev.get<AttnSeg>(), cs.tok_seg.get<int>(),
-                             cs.tok_pos.get<int>(), dqkv.get(), T, H_, Hkv_, hd_, j, m_.rope_theta, s);
+                             cs.tok_pos.get<int>(), dqkv.get(), T, H_, Hkv_, hd_, j, m_.rope_theta, s,
+                             /*kv_only=*/tc_bwd);
         dq.release();
         gemm(mk(T, D_, Nqkv_, dqkv.get(), Nqkv_, true, work(P.wqkv), D_, false, dxn.get(), D_), s);
         norm_apply(dt_, llama_, x, work(P.ln1_w), P.ln1_b >= 0 ? work(P.ln1_b) : nullptr,
