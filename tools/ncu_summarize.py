@@ -17,7 +17,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 OUT = ROOT / "gpurun_out"
 PROF = ROOT / "profiles"
-CLASS = {"gemm_tc_kernel": "gemm", "attn_fwd_tc": "attn_fwd", "attn_bwd_dq_tc": "attn_bwd_dq",
+CLASS = {"gemm_tc2_kernel": "gemm", "attn_fwd_tc": "attn_fwd", "attn_bwd_dq_tc": "attn_bwd_dq",
          "attn_bwd_dkv_tc": "attn_bwd_dkv", "norm_bwd_dx_k": "norm_bwd", "rope_gather_grad_k": "rope"}
 KEYS = {"duration": "gpu__time_duration.sum",
         "dram_read_bytes": "dram__bytes_read.sum", "dram_write_bytes": "dram__bytes_write.sum",
