@@ -785,6 +785,10 @@ void attn_bwd(const AttnArgs& a, cudaStream_t s) {
     EPP_REQUIRE(a.H % a.Hkv == 0, "attn: H must be a multiple of Hkv");
     // algorithmic backward = 2x forward (dQ, dK, dV, dP matmuls)
     ProfScope prof(kProfAttnBwd, 8.0 * a.H * a.hd * a.pairs, s);
+    if (use_tc_attention() && attn_bwd_tc_supported(a)) {
+        attn_bwd_tc_main(a, s);      // the dQ kernel forms delta itself
+        return;
+    }
     if (a.T > 0) {
         const long long warps = static_cast<long long>(a.T) * a.H;
         const int blocks = static_cast<int>((warps * 32 + 255) / 256);
@@ -797,10 +801,6 @@ void attn_bwd(const AttnArgs& a, cudaStream_t s) {
                                                            static_cast<const bf16*>(a.o),
                                                            a.delta, a.T, a.H, a.hd);
         EPP_CHECK_LAUNCH();
-    }
-    if (use_tc_attention() && attn_bwd_tc_supported(a)) {
-        attn_bwd_tc_main(a, s);
-        return;
     }
     EPP_REQUIRE(a.dqkv_out == nullptr, "attn_bwd: dqkv_out needs the tcgen05 kernels");
     if (a.dtype == DType::F32) {

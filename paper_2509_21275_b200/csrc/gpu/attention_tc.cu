@@ -533,7 +533,8 @@ struct DqSmem {
     static constexpr int kSmall = TB * HD * 2;      // K / V tiles
     static constexpr int kK = 0;                            // kDqStages stages
     static constexpr int kV = kK + kDqStages * kSmall;
-    static constexpr int kBar = kV + kDqStages * kSmall;
+    static constexpr int kDelta = kV + kDqStages * kSmall;  // [128] fp32 per-row delta
+    static constexpr int kBar = kDelta + 128 * 4;
     static constexpr int kBytes = kBar + 24 * 8 + 16;
     static constexpr int kAlloc = kBytes + 1024;
 };
@@ -663,9 +664,14 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
         const int first_q = sg.kv_ctx + q0;
         const long long t = row0 + min(r, rows - 1);
         const float lse = a.lse[static_cast<long long>(h) * a.T + t];
-        const float dlt = a.delta[static_cast<long long>(h) * a.T + t];
-        {   // stage this row of Q (group 0) / dO (group 1) into TMEM
+        float* sDelta = reinterpret_cast<float*>(smem + L::kDelta);
+        {   // stage this row of Q (group 0) / dO (group 1) into TMEM; group 1
+            // also forms delta = rowsum(dO * O) (the separate delta pass of
+            // the other backends), shares it through shared memory and
+            // writes it for the dK/dV kernel that runs next
             const bf16* src = static_cast<const bf16*>(grp ? a.dout : a.q) + (t * a.H + h) * HD;
+            const bf16* orow = static_cast<const bf16*>(a.o) + (t * a.H + h) * HD;
+            float dsum = 0.f;
 #pragma unroll
             for (int c = 0; c < HD / 64; ++c) {
                 uint32_t wv[32];
@@ -676,13 +682,29 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
                     wv[4 * i + 1] = u.y;
                     wv[4 * i + 2] = u.z;
                     wv[4 * i + 3] = u.w;
+                    if (grp) {
+                        const uint4 ov = *reinterpret_cast<const uint4*>(orow + c * 64 + i * 8);
+                        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+                        const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float2 gf = __bfloat1622float2(g2[k]), of = __bfloat1622float2(o2[k]);
+                            dsum = fmaf(gf.x, of.x, fmaf(gf.y, of.y, dsum));
+                        }
+                    }
                 }
                 tc::tmem_st32u(lane_base + (grp ? kColOin : kColQin) + c * 32, wv);
+            }
+            if (grp) {
+                sDelta[r] = dsum;
+                if (r < rows) a.delta[static_cast<long long>(h) * a.T + row0 + r] = dsum;
             }
             tc::tmem_wait_st();
             tc::fence_before();
             tc::mbar_arrive(q_full);
         }
+        tc::mbar_wait(q_full, 0);   // both groups: operands staged, delta shared
+        const float dlt = sDelta[r];
         for (int j = grp; j < nkb; j += 2) {
             const int b = grp;
             tc::mbar_wait(&s_full[b], (j >> 1) & 1);
@@ -1151,7 +1173,7 @@ bool attn_bwd_tc_supported(const AttnArgs& a) {
            a.kwork128 != nullptr && a.maps != nullptr;
 }
 
-// dq + dk/dv kernels (the delta pre-pass is issued by attn_bwd).
+// dq + dk/dv kernels; the dq kernel also forms delta = rowsum(dO * O) for the dk/dv kernel.
 void attn_bwd_tc_main(const AttnArgs& a, cudaStream_t s) {
     if (a.hd == 64) launch_bwd_tc<64>(a, s);
     else launch_bwd_tc<128>(a, s);
