@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--cap", type=int, default=32768)
     ap.add_argument("--preset", default="github_like")
     ap.add_argument("--slices", type=int, default=0, help="fixed slice count N (0 = planner auto-N)")
+    ap.add_argument("--pp", type=int, default=0,
+                    help="pipeline degree d_p (default: --gpus); --gpus / d_p data-parallel replicas")
     ap.add_argument("--no-calibrate", action="store_true",
                     help="keep the analytic Eq. 1 coefficients (default: fit them on warmup step 0)")
     ap.add_argument("--uniform-min", type=int, default=1, help="preset=uniform: shortest length")
@@ -130,13 +132,16 @@ def step_flops(m, plan):
     return total
 
 
-def make_batches(args, n_batches, world, vocab):
+def make_batches(args, n_batches, world, vocab, replica=0):
+    """Synthetic batches of `seqs_per_gpu * world` sequences (world = the
+    pipeline's GPUs); data-parallel replicas draw from disjoint seeds."""
     from paper_2509_21275_b200 import planner, schedule
     out = []
     for i in range(n_batches):
-        lengths = planner.generate_workload(args.preset, args.seqs_per_gpu * world, 1000 + i, args.cap,
+        seed = 1000 + i + 100003 * replica
+        lengths = planner.generate_workload(args.preset, args.seqs_per_gpu * world, seed, args.cap,
                                             args.uniform_min, args.uniform_max)
-        out.append((lengths, schedule.synthetic_tokens(lengths, vocab, seed=1000 + i)))
+        out.append((lengths, schedule.synthetic_tokens(lengths, vocab, seed=seed)))
     return out
 
 
@@ -144,7 +149,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2509_21275_b200 import calibrate, gpu, model as M, planner, schedule
-    from paper_2509_21275_b200.executor import DistributedPipeline, LocalPipeline, _ChunkTokens, stage_layers
+    from paper_2509_21275_b200.executor import (DistributedPipeline, LocalPipeline, _ChunkTokens, allreduce_grads,
+                                                pipeline_groups, stage_layers)
 
     world = args.gpus
     rank = int(os.environ.get("RANK", "0"))
@@ -159,12 +165,16 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     m = M.MODELS[args.model]
-    dp = world
+    dp = args.pp or world                    # pipeline degree d_p
+    assert world % dp == 0, "--gpus must be a multiple of --pp"
+    replicas = world // dp
+    replica, prank = rank // dp, rank % dp   # data-parallel replica, stage index
+    pipes, dp_groups = pipeline_groups(dp, replicas) if world > 1 else ([None], [None])
     free, total_mem = torch.cuda.mem_get_info()
     cfg = M.planner_config(m, dp, mem_capacity=float(total_mem) - 2e9, cost=M.default_cost(m))
     jobs = os.cpu_count() or 8
 
-    batches = make_batches(args, args.warmup + args.steps, world, m.vocab)
+    batches = make_batches(args, args.warmup + args.steps, dp, m.vocab, replica)
 
     def plan_all(config, first):
         out, t = [], time.perf_counter()
@@ -175,14 +185,15 @@ def run_ours(args):
 
     plans, planner_s = plan_all(cfg, 0)
 
-    first, num = stage_layers(m.layers, dp, rank)
-    stage = gpu.CudaStage(m, first, num, rank == 0, rank == dp - 1, dtype=args.dtype, device=local)
+    first, num = stage_layers(m.layers, dp, prank)
+    stage = gpu.CudaStage(m, first, num, prank == 0, prank == dp - 1, dtype=args.dtype, device=local)
     stage.init_weights(1234)
     timed_stage = calibrate.TimedStage(stage)
 
     def make_driver(st):
-        if world > 1:
-            return DistributedPipeline(st, rank, world, dev, m.hidden, gpu.TORCH_DTYPES[args.dtype])
+        if dp > 1:
+            return DistributedPipeline(st, prank, dp, dev, m.hidden, gpu.TORCH_DTYPES[args.dtype],
+                                       pipe=pipes[replica])
         return LocalPipeline([st], dev)
 
     driver = make_driver(stage)
@@ -196,6 +207,7 @@ def run_ours(args):
 
     def optimizer():
         step_no[0] += 1
+        allreduce_grads(stage, dp_groups[prank], replicas)   # data-parallel replicas (NCCL all-reduce)
         stage.adamw_step(1e-4, step_no[0])
 
     # ---- warmup -------------------------------------------------------------
@@ -238,7 +250,7 @@ def run_ours(args):
 
     # ---- device-resident timed region (value) -------------------------------
     timed = list(range(args.warmup, args.warmup + args.steps))
-    pre = [_ChunkTokens(plans[i], batches[i][1], dev, rank == 0, rank == dp - 1) for i in timed]
+    pre = [_ChunkTokens(plans[i], batches[i][1], dev, prank == 0, prank == dp - 1) for i in timed]
     sync_all()
     launches0 = gpu.kernel_launches()
     lib = gpu.lib()
@@ -261,6 +273,11 @@ def run_ours(args):
         ms = float(t.item())
     tokens = sum(sum(plans[i].lengths) for i in timed)
     flops = sum(step_flops(m, plans[i]) for i in timed)
+    if replicas > 1:   # every replica's tokens and FLOPs (each counted once, by its stage 0)
+        t = torch.tensor([float(tokens) if prank == 0 else 0.0, flops if prank == 0 else 0.0], device=dev,
+                         dtype=torch.float64)
+        dist.all_reduce(t)
+        tokens, flops = int(t[0].item()), float(t[1].item())
     prof = {}
     classes = ((0, "gemm"), (1, "attn_fwd"), (2, "attn_bwd"), (3, "attn_bwd_dq"), (4, "attn_bwd_dkv"),
                (5, "norm_fwd"), (6, "norm_bwd"), (7, "rope"), (8, "act"), (9, "cross_entropy"),
@@ -269,7 +286,7 @@ def run_ours(args):
         a, b, c = (ctypes_double(), ctypes_double(), ctypes_i64())
         gpu.check(lib.epp_gpu_profile_read(cls, ctypes_ref(a), ctypes_ref(b), ctypes_ref(c), 1))
         prof[name] = {"ms": a.value, "flops": b.value, "launches": c.value}
-    loss_sum, loss_cnt = (stage.loss(reset=True) if rank == dp - 1 else (0.0, 0.0))
+    loss_sum, loss_cnt = (stage.loss(reset=True) if prank == dp - 1 else (0.0, 0.0))
 
     # ---- end-to-end timed region (e2e) ---------------------------------------
     e2e = None
@@ -300,7 +317,7 @@ def run_ours(args):
             st = driver.run_step(ahead.pop(k), e2e_batches[k][1])
             h2d += st["h2d_bytes"]
             optimizer()
-            if rank == dp - 1:
+            if prank == dp - 1:
                 stage.loss_async(loss_host[k], reset=True)
                 loss_ev[k].record()
                 d2h += 8
@@ -309,7 +326,7 @@ def run_ours(args):
                     losses.append(float(loss_host[k - 1, 0] / max(1.0, float(loss_host[k - 1, 1]))))
             if th:
                 th.join()
-        if rank == dp - 1:
+        if prank == dp - 1:
             loss_ev[-1].synchronize()
             losses.append(float(loss_host[-1, 0] / max(1.0, float(loss_host[-1, 1]))))
         sync_all()
@@ -324,6 +341,10 @@ def run_ours(args):
             dist.all_reduce(b, op=dist.ReduceOp.SUM)
             h2d, d2h = int(b[0].item()), int(b[1].item())
         e_tokens = sum(sum(b[0]) for b in e2e_batches)
+        if replicas > 1:
+            t = torch.tensor([float(e_tokens) if prank == 0 else 0.0], device=dev, dtype=torch.float64)
+            dist.all_reduce(t)
+            e_tokens = int(t.item())
         nb = len(e2e_batches)
         e2e = {"value": e_tokens / e_s, "unit": "tokens/s", "h2d_bytes_per_step": h2d // nb,
                "d2h_bytes_per_step": d2h // nb}
@@ -368,7 +389,7 @@ def run_ours(args):
                    "model": args.model, "global_batch_seqs": args.seqs_per_gpu * world,
                    "tokens_per_step": tokens / args.steps, "seq_len_cap": args.cap,
                    "slices": args.slices or "auto",
-                   "parallelism": f"pp{dp}", "l2": "inputs larger than L2 (activations GBs/step)"},
+                   "parallelism": f"pp{dp}" + (f"xdp{replicas}" if replicas > 1 else ""), "l2": "inputs larger than L2 (activations GBs/step)"},
         "mfu": flops / (sec * world * tf_burst * 1e12),
         "mfu_vs_sustained": flops / (sec * world * tf_sus * 1e12),
         "model_tflops_per_gpu": flops / sec / world / 1e12,

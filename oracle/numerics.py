@@ -259,6 +259,12 @@ class TorchStage:
         return {n: (p.grad.detach().clone() if p.grad is not None else torch.zeros_like(p))
                 for n, p in self.params.items()}
 
+    def grad_views(self):
+        for p in self.params.values():
+            if p.grad is None:
+                p.grad = torch.zeros_like(p)
+        return {n: p.grad for n, p in self.params.items()}
+
     def forward(self, c: ChunkIO, act_in: Optional[torch.Tensor]):
         spec, P = self.spec, self.params
         T = sum(c.slices)

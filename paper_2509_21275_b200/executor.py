@@ -137,26 +137,58 @@ class LocalPipeline:
                 raise RuntimeError("pipeline op lists deadlocked (plan/op-list mismatch)")
 
 
+def pipeline_groups(pp: int, replicas: int = 1):
+    """Process groups of `replicas` data-parallel copies of a `pp`-stage
+    pipeline (global rank = replica * pp + stage).  Collective: every rank
+    calls it with the same arguments (torch's new_group is).
+
+    Returns (pipes, dp_groups): pipes[q] = (ranks, fwd_groups, bwd_groups) of
+    replica q, one group per adjacent stage pair and direction; dp_groups[p]
+    = the group of stage p across replicas (None without replicas)."""
+    import torch.distributed as dist
+    pipes = []
+    for q in range(replicas):
+        ranks = [q * pp + p for p in range(pp)]
+        fwd, bwd = [], []
+        for p in range(pp - 1):
+            fwd.append(dist.new_group([ranks[p], ranks[p + 1]]))
+            bwd.append(dist.new_group([ranks[p], ranks[p + 1]]))
+        pipes.append((ranks, fwd, bwd))
+    dp_groups = [dist.new_group([q * pp + p for q in range(replicas)]) if replicas > 1 else None
+                 for p in range(pp)]
+    return pipes, dp_groups
+
+
+def allreduce_grads(stage, group, replicas: int) -> None:
+    """Data-parallel gradient average of one stage over its replicas (NCCL
+    all-reduce on B200s), in place on the stage's accumulated gradients."""
+    if group is None or replicas <= 1:
+        return
+    import torch.distributed as dist
+    for t in stage.grad_views().values():
+        dist.all_reduce(t, group=group)
+        t.mul_(1.0 / replicas)
+
+
 class DistributedPipeline:
-    """One stage per rank of the default process group (rank = stage).
+    """One stage per rank (rank = stage) of a pipeline.
 
     Transport: device tensors go straight to NCCL (B200s: NVLink P2P);
     with a gloo group and CUDA stages (the multi-process test that shares one
-    GPU) messages are staged through host memory instead."""
+    GPU) messages are staged through host memory instead.  `pipe` =
+    (global ranks of the stages, fwd groups, bwd groups) from
+    pipeline_groups(); by default the whole world is one pipeline."""
 
     def __init__(self, stage, rank: int, world: int, device: torch.device, hidden: int,
-                 act_dtype: torch.dtype):
+                 act_dtype: torch.dtype, pipe=None):
         import torch.distributed as dist
         self.dist = dist
         self.stage, self.rank, self.world = stage, rank, world
         self.device, self.hidden, self.act_dtype = device, hidden, act_dtype
         self.via_host = device.type == "cuda" and dist.get_backend() == "gloo"
-        # One group per adjacent pair and direction; every rank creates all of
-        # them in the same order (new_group is collective).
-        self.fwd_groups, self.bwd_groups = [], []
-        for p in range(world - 1):
-            self.fwd_groups.append(dist.new_group([p, p + 1]))
-            self.bwd_groups.append(dist.new_group([p, p + 1]))
+        if pipe is None:
+            (pipe,), _ = pipeline_groups(world, 1)
+        self.ranks, self.fwd_groups, self.bwd_groups = pipe
         self.p2p_bytes = 0
 
     def _recv(self, T: int, src: int, group) -> torch.Tensor:
@@ -183,15 +215,15 @@ class DistributedPipeline:
                 T = plan.chunks[unit.chunks[pos]].tokens
                 op = _op(plan, unit, pos, p, toks)
                 if kind == "F":
-                    act_in = self._recv(T, p - 1, self.fwd_groups[p - 1]) if p > 0 else None
+                    act_in = self._recv(T, self.ranks[p - 1], self.fwd_groups[p - 1]) if p > 0 else None
                     out = self.stage.forward(op, act_in)
                     if p + 1 < dp:
-                        self._send(out, p + 1, self.fwd_groups[p], pending)
+                        self._send(out, self.ranks[p + 1], self.fwd_groups[p], pending)
                 else:
-                    g_in = self._recv(T, p + 1, self.bwd_groups[p]) if p + 1 < dp else None
+                    g_in = self._recv(T, self.ranks[p + 1], self.bwd_groups[p]) if p + 1 < dp else None
                     g_out = self.stage.backward(op, g_in)
                     if p > 0:
-                        self._send(g_out, p - 1, self.bwd_groups[p - 1], pending)
+                        self._send(g_out, self.ranks[p - 1], self.bwd_groups[p - 1], pending)
             for w, _ in pending:
                 w.wait()
             pending.clear()

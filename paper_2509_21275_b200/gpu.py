@@ -182,6 +182,12 @@ class CudaStage:
         return {name: _wrap_ptr(p["grad"], p["numel"], torch.float32, self.device).clone()
                 for name, p in self.params().items()}
 
+    def grad_views(self) -> Dict[str, torch.Tensor]:
+        """Zero-copy fp32 views of the accumulated gradients (in-place
+        collectives, e.g. the data-parallel all-reduce)."""
+        return {name: _wrap_ptr(p["grad"], p["numel"], torch.float32, self.device)
+                for name, p in self.params().items()}
+
     def zero_grads(self):
         check(lib().epp_stage_zero_grads(self.h, stream_ptr()))
 

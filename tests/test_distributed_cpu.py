@@ -82,3 +82,65 @@ def test_gloo_pipeline_matches_local(world):
     assert abs(loss - stages[-1].loss_sum) < 1e-4
     for k, v in local.items():
         assert torch.allclose(dist_grads[k], v, rtol=1e-5, atol=1e-8), k
+
+
+LENGTHS_B = [120, 260, 33, 75, 9, 140]
+
+
+def dp_worker(rank, world, pp, port, docs, q):
+    from paper_2509_21275_b200.executor import allreduce_grads, pipeline_groups
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
+    replicas = world // pp
+    pipes, dp_groups = pipeline_groups(pp, replicas)
+    replica, p = rank // pp, rank % pp
+    lengths = (LENGTHS, LENGTHS_B)[replica]
+    plan = S.parse_plan(docs[replica], lengths)
+    params = O.init_params(spec(), seed=3)
+    first, num = stage_layers(MODEL.layers, pp, p)
+    st = O.TorchStage(spec(), params, first, num, p == 0, p == pp - 1)
+    drv = DistributedPipeline(st, p, pp, torch.device("cpu"), MODEL.hidden, torch.float32, pipe=pipes[replica])
+    drv.run_step(plan, S.synthetic_tokens(lengths, MODEL.vocab, seed=11 + replica))
+    allreduce_grads(st, dp_groups[p], replicas)
+    q.put((rank, {k: v.numpy().copy() for k, v in st.grads().items()}))   # by value: the worker exits
+    torch.distributed.barrier()
+    torch.distributed.destroy_process_group()
+
+
+def test_gloo_pipeline_data_parallel_replicas():
+    """pp 2 x dp 2: each replica pipelines its own batch, then the stage
+    gradients are averaged across replicas (allreduce_grads)."""
+    from paper_2509_21275_b200 import planner
+    pp, world = 2, 4
+    cfg = M.planner_config(MODEL, pp, mem_capacity=1e12, reserve_bytes=0)
+    docs = [planner.make_plan_document(cfg, LENGTHS, 3, "main", 1),
+            planner.make_plan_document(cfg, LENGTHS_B, 3, "main", 1)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=dp_worker, args=(r, world, pp, port, docs, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = {r: {k: torch.from_numpy(v) for k, v in g.items()} for r, g in (q.get(timeout=300) for _ in range(world))}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # reference: each replica's batch through a local pipeline, grads averaged
+    ref = {}
+    for replica, lengths in enumerate((LENGTHS, LENGTHS_B)):
+        params = O.init_params(spec(), seed=3)
+        stages = [O.TorchStage(spec(), params, *stage_layers(MODEL.layers, pp, p), p == 0, p == pp - 1)
+                  for p in range(pp)]
+        LocalPipeline(stages, torch.device("cpu")).run_step(S.parse_plan(docs[replica], lengths),
+                                                           S.synthetic_tokens(lengths, MODEL.vocab, seed=11 + replica))
+        for st in stages:
+            for k, v in st.grads().items():
+                ref[k] = ref.get(k, 0) + v / 2
+    for rank in range(world):
+        p = rank % pp
+        for k, v in results[rank].items():
+            assert torch.allclose(v, ref[k], rtol=1e-5, atol=1e-8), (rank, k)
+    # both replicas of a stage hold identical averaged gradients
+    for p in range(pp):
+        for k in results[p]:
+            assert torch.equal(results[p][k], results[pp + p][k])
