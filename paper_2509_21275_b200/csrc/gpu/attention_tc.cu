@@ -353,6 +353,11 @@ __global__ void __launch_bounds__(kThreadsFwd, 1) attn_fwd_tc(const AttnArgs a,
         for (int j = 0; j < my_nkb; ++j) {
             tc::mbar_wait(&s_full[grp], j & 1);
             tc::fence_after();
+#ifdef EPP_FWD_MMA_ONLY   // pipeline experiment: no softmax work at all (wrong results)
+            tc::fence_before();
+            tc::mbar_arrive(&p_full[grp]);
+            continue;
+#endif
             const int key0 = j * TK;
             const bool need_mask = (key0 + TK - 1 > first_q) || rows < TQ;
             float sv[TK / 32][32];
