@@ -218,12 +218,13 @@ def run_ours(args):
         free_b, _ = torch.cuda.mem_get_info()
         gpu.pool_reserve(free_b - int(6e9))
     cost_report = {"source": "analytic (model.default_cost)"}
+    cal_step = args.warmup - 1          # calibrate on the last (warm) warmup step
     for i in range(args.warmup):
-        if i == 0 and not args.no_calibrate:
-            # closed loop: time every stage op of warmup step 0, fit Eq. 1 to
-            # it (all ranks' samples, so every rank plans identically) and
-            # re-plan the remaining batches with the fitted coefficients
-            make_driver(timed_stage).run_step(plans[0], batches[0][1])
+        if i == cal_step and not args.no_calibrate:
+            # closed loop: time every stage op of the last warmup step, fit
+            # Eq. 1 to it (all ranks' samples, so every rank plans
+            # identically) and re-plan the timed batches with the fit
+            make_driver(timed_stage).run_step(plans[i], batches[i][1])
             optimizer()
             sync_all()
             samples = timed_stage.samples()
@@ -234,10 +235,10 @@ def run_ours(args):
             try:
                 fitted = calibrate.calibrated_config(cfg, samples)
                 cfg_fit = calibrate.planner_config_only(fitted)
-                rest, planner_s = plan_all(cfg_fit, 1)
+                rest, planner_s = plan_all(cfg_fit, args.warmup)
                 cfg = cfg_fit
-                plans = plans[:1] + rest
-                cost_report = {"source": f"fitted on warmup step 0 ({fitted['_fit']['samples']} stage-op samples)",
+                plans = plans[:args.warmup] + rest
+                cost_report = {"source": f"fitted on warmup step {i} ({fitted['_fit']['samples']} stage-op samples)",
                                "fwd_residual": fitted["_fit"]["fwd_residual"],
                                "bwd_residual": fitted["_fit"]["bwd_residual"], "cost": cfg["cost"]}
             except planner.Error as e:

@@ -7,8 +7,9 @@ This module measures them on the GPU executor itself:
   1. `TimedStage` wraps a stage (gpu.CudaStage) and records CUDA events
      around every forward / backward call of a step;
   2. `samples()` turns those into fit samples {context, slices, phase,
-     seconds} (backward ops that re-ran checkpointed layers are skipped:
-     Eq. 1 prices recompute separately, via layer_fwd_seconds);
+     seconds} (a backward that re-ran checkpointed layers is charged the
+     recompute estimated from its forward: Eq. 1 prices recompute
+     separately);
   3. `calibrated_config()` feeds them to fit_cost_params
      (proj/src/cost_model.cpp:143-223, the planner library's C ABI) and returns
      the planner configuration with the fitted coefficients;
@@ -53,12 +54,24 @@ class TimedStage:
         return self._timed("backward", self.stage.backward, op, grad_in)
 
     def samples(self) -> List[Dict]:
+        """Fit samples.  A backward that first re-ran `ckpt_layers` of the
+        stage's `num` layers is charged its recompute, estimated from the same
+        chunk's measured forward (ckpt_layers / num of it), which Eq. 1
+        prices separately (recompute_time, cost_model.cpp:68-78)."""
+        fwd = {}
+        for op, phase, a, b in self.records:
+            if phase == "forward":
+                fwd[op.id] = a.elapsed_time(b) / 1e3
+        layers = max(1, int(getattr(self.stage, "num", 1)))
         out = []
         for op, phase, a, b in self.records:
+            sec = a.elapsed_time(b) / 1e3
             if phase == "backward" and op.ckpt_layers > 0:
-                continue
+                if op.id not in fwd:
+                    continue
+                sec -= fwd[op.id] * op.ckpt_layers / layers
             out.append({"context": int(op.context), "slices": [int(s) for s in op.slices], "phase": phase,
-                        "seconds": a.elapsed_time(b) / 1e3})
+                        "seconds": sec})
         return out
 
 
