@@ -182,6 +182,125 @@ __global__ void __launch_bounds__(256) norm_fwd_warp_k(bool rms, const bf16* x, 
     }
 }
 
+// CTA-per-row variants (bf16, D = 1024 * NPT): 128 threads, each holding
+// NPT packed 16-byte chunks of the row in registers (one HBM read), a
+// 4-warp shuffle + shared-memory reduction.  Small register footprint, so
+// many rows are in flight per SM even for short chunks.
+__device__ __forceinline__ void unpack8(const uint4& r, float (&v)[8]) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(h[i]);
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+    }
+}
+__device__ __forceinline__ float sum128(float v, float* red) {   // 4-warp CTA sum
+    v = warp_sum(v);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    return (red[0] + red[1]) + (red[2] + red[3]);
+}
+
+template <int NPT>
+__global__ void __launch_bounds__(128) norm_fwd_row_k(bool rms, const bf16* x, const bf16* w, const bf16* b, bf16* y,
+                                                      float* mean, float* rstd, float eps) {
+    constexpr int D = 1024 * NPT;
+    __shared__ float red[4];
+    const long long row = blockIdx.x;
+    const bf16* xr = x + row * D;
+    uint4 raw[NPT];
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) raw[k] = *reinterpret_cast<const uint4*>(xr + k * 1024 + threadIdx.x * 8);
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+        float v[8];
+        unpack8(raw[k], v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += v[i];
+    }
+    const float mu = rms ? 0.f : sum128(s, red) / D;
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+        float v[8];
+        unpack8(raw[k], v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) q += (v[i] - mu) * (v[i] - mu);
+    }
+    const float rs = rsqrtf(sum128(q, red) / D + eps);
+    if (threadIdx.x == 0) {
+        if (mean) mean[row] = mu;
+        rstd[row] = rs;
+    }
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+        const int c = k * 1024 + threadIdx.x * 8;
+        float v[8], wv[8], bv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        unpack8(raw[k], v);
+        load8(w + c, wv);
+        if (b) load8(b + c, bv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = (v[i] - mu) * rs * wv[i] + bv[i];
+        store8(y + row * D + c, v);
+    }
+}
+
+template <int NPT>
+__global__ void __launch_bounds__(128) norm_bwd_dx_row_k(bool rms, const bf16* x, const bf16* w, const bf16* dy,
+                                                         const float* mean, const float* rstd, const bf16* dres,
+                                                         bf16* dx) {
+    constexpr int D = 1024 * NPT;
+    __shared__ float red[2][4];
+    const long long row = blockIdx.x;
+    const long long off = row * D;
+    uint4 rx[NPT], rg[NPT];
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+        rx[k] = *reinterpret_cast<const uint4*>(x + off + k * 1024 + threadIdx.x * 8);
+        rg[k] = *reinterpret_cast<const uint4*>(dy + off + k * 1024 + threadIdx.x * 8);
+    }
+    const float mu = rms ? 0.f : mean[row];
+    const float rs = rstd[row];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+        float xv[8], gv[8], wv[8];
+        unpack8(rx[k], xv);
+        unpack8(rg[k], gv);
+        load8(w + k * 1024 + threadIdx.x * 8, wv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float dxh = gv[i] * wv[i];
+            s1 += dxh;
+            s2 += dxh * (xv[i] - mu) * rs;
+        }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = s1;
+        red[1][threadIdx.x >> 5] = s2;
+    }
+    __syncthreads();
+    const float m1 = rms ? 0.f : ((red[0][0] + red[0][1]) + (red[0][2] + red[0][3])) / D;
+    const float m2 = ((red[1][0] + red[1][1]) + (red[1][2] + red[1][3])) / D;
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+        const int c = k * 1024 + threadIdx.x * 8;
+        float xv[8], gv[8], wv[8], out[8], rv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        unpack8(rx[k], xv);
+        unpack8(rg[k], gv);
+        load8(w + c, wv);
+        if (dres) load8(dres + off + c, rv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) out[i] = rv[i] + rs * (gv[i] * wv[i] - m1 - (xv[i] - mu) * rs * m2);
+        store8(dx + off + c, out);
+    }
+}
+
 template <typename T>
 __global__ void norm_apply_k(bool rms, const T* x, const T* w, const T* b, const float* mean,
                              const float* rstd, T* y, int D) {
@@ -722,11 +841,18 @@ void norm_fwd(DType t, bool rms, const void* x, const void* w, const void* b, vo
                                                        T, eps);
         };
         if constexpr (std::is_same<E, bf16>::value) {
+            auto row_kernel = [&](auto npt) {
+                constexpr int NPT = decltype(npt)::value;
+                norm_fwd_row_k<NPT><<<T, 128, 0, s>>>(rms, static_cast<const bf16*>(x), static_cast<const bf16*>(w),
+                                                      static_cast<const bf16*>(b), static_cast<bf16*>(y), mean, rstd,
+                                                      eps);
+            };
             if (D == 256) return warp_kernel(std::integral_constant<int, 1>{});
             if (D == 512) return warp_kernel(std::integral_constant<int, 2>{});
-            if (D == 1024) return warp_kernel(std::integral_constant<int, 4>{});
-            if (D == 2048) return warp_kernel(std::integral_constant<int, 8>{});
-            if (D == 4096) return warp_kernel(std::integral_constant<int, 16>{});
+            if (D == 1024) return row_kernel(std::integral_constant<int, 1>{});
+            if (D == 2048) return row_kernel(std::integral_constant<int, 2>{});
+            if (D == 4096) return row_kernel(std::integral_constant<int, 4>{});
+            if (D == 8192) return row_kernel(std::integral_constant<int, 8>{});
         }
         norm_fwd_k<E><<<T, norm_threads(D), 0, s>>>(rms, static_cast<const E*>(x),
                                                     static_cast<const E*>(w),
@@ -766,9 +892,24 @@ void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy, c
     float* pb = db ? part + static_cast<long long>(G) * D : nullptr;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        norm_bwd_dx_k<E><<<ceil_div(static_cast<long long>(T) * 32, 256), 256, 0, s>>>(
-            rms, static_cast<const E*>(x), static_cast<const E*>(w), static_cast<const E*>(dy), mean,
-            rstd, static_cast<const E*>(dres), static_cast<E*>(dx), T, D);
+        bool done = false;
+        if constexpr (std::is_same<E, bf16>::value) {
+            auto row_kernel = [&](auto npt) {
+                constexpr int NPT = decltype(npt)::value;
+                norm_bwd_dx_row_k<NPT><<<T, 128, 0, s>>>(rms, static_cast<const bf16*>(x), static_cast<const bf16*>(w),
+                                                         static_cast<const bf16*>(dy), mean, rstd,
+                                                         static_cast<const bf16*>(dres), static_cast<bf16*>(dx));
+                done = true;
+            };
+            if (D == 1024) row_kernel(std::integral_constant<int, 1>{});
+            else if (D == 2048) row_kernel(std::integral_constant<int, 2>{});
+            else if (D == 4096) row_kernel(std::integral_constant<int, 4>{});
+            else if (D == 8192) row_kernel(std::integral_constant<int, 8>{});
+        }
+        if (!done)
+            norm_bwd_dx_k<E><<<ceil_div(static_cast<long long>(T) * 32, 256), 256, 0, s>>>(
+                rms, static_cast<const E*>(x), static_cast<const E*>(w), static_cast<const E*>(dy), mean,
+                rstd, static_cast<const E*>(dres), static_cast<E*>(dx), T, D);
         EPP_CHECK_LAUNCH();
         norm_bwd_dw2_k<E><<<dim3(col_blocks, G), 256, 0, s>>>(
             rms, static_cast<const E*>(x), static_cast<const E*>(dy), mean, rstd, pw, pb, T, D, rows_per);
