@@ -37,7 +37,8 @@ def worker(rank, world, port, doc, q):
     st = O.TorchStage(spec(), params, first, num, rank == 0, rank == world - 1)
     drv = DistributedPipeline(st, rank, world, torch.device("cpu"), MODEL.hidden, torch.float32)
     drv.run_step(plan, S.synthetic_tokens(LENGTHS, MODEL.vocab, seed=11))
-    q.put((rank, {k: v.clone() for k, v in st.grads().items()}, st.loss_sum, drv.p2p_bytes))
+    # by value (numpy): shared-memory tensors would vanish with the exiting worker
+    q.put((rank, {k: v.numpy().copy() for k, v in st.grads().items()}, float(st.loss_sum), drv.p2p_bytes))
     torch.distributed.barrier()
     torch.distributed.destroy_process_group()
 
@@ -66,7 +67,7 @@ def test_gloo_pipeline_matches_local(world):
     dist_grads = {}
     loss = None
     for rank, g, ls, nbytes in results:
-        dist_grads.update(g)
+        dist_grads.update({k: torch.from_numpy(v) for k, v in g.items()})
         if rank == world - 1:
             loss = ls
         if 0 < rank < world - 1:

@@ -45,7 +45,7 @@ def worker(rank, world, port, doc, q):
     drv = DistributedPipeline(st, rank, world, torch.device("cuda"), MODEL.hidden, torch.float32)
     drv.run_step(plan, S.synthetic_tokens(LENGTHS, MODEL.vocab, seed=13))
     torch.cuda.synchronize()
-    grads = {k: v.cpu().clone() for k, v in st.grads().items()}
+    grads = {k: v.cpu().numpy().copy() for k, v in st.grads().items()}   # by value
     loss = st.loss()[0] if rank == world - 1 else None
     q.put((rank, grads, loss, drv.p2p_bytes))
     torch.distributed.barrier()
@@ -76,7 +76,7 @@ def test_two_rank_cuda_pipeline_matches_local():
         assert p.exitcode == 0
     dist_grads, loss = {}, None
     for rank, g, ls, nbytes in results:
-        dist_grads.update(g)
+        dist_grads.update({k: torch.from_numpy(v) for k, v in g.items()})
         assert nbytes > 0
         if rank == world - 1:
             loss = ls
