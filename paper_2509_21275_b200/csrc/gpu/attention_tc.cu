@@ -561,7 +561,8 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
     uint64_t* s_full = kv_empty + kDqStages;          // [2]
     uint64_t* p_full = s_full + 2;                    // [2]
     uint64_t* acc_full = p_full + 2;                  // all MMAs retired (epilogue)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+    uint64_t* d_full = acc_full + 1;                  // per-row delta in shared memory
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + 1);
 
     const AttnWork w = a.qwork128[EPP_WORK_INDEX];
     const AttnSeg sg = a.segs[w.seg];
@@ -576,6 +577,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
 
     if (threadIdx.x == 0) {
         tc::mbar_init(q_full, 2 * TQ);      // both softmax groups stage Q / dO rows into TMEM
+        tc::mbar_init(d_full, TQ);          // group 1 publishes delta
         for (int s = 0; s < kDqStages; ++s) {
             tc::mbar_init(&kv_full[s], 1);
             tc::mbar_init(&kv_empty[s], 1);
@@ -670,45 +672,50 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
         const long long t = row0 + min(r, rows - 1);
         const float lse = a.lse[static_cast<long long>(h) * a.T + t];
         float* sDelta = reinterpret_cast<float*>(smem + L::kDelta);
-        {   // stage this row of Q (group 0) / dO (group 1) into TMEM; group 1
-            // also forms delta = rowsum(dO * O) (the separate delta pass of
-            // the other backends), shares it through shared memory and
-            // writes it for the dK/dV kernel that runs next
+        {   // stage this row of Q (group 0) / dO (group 1) into TMEM, release
+            // the MMA warp, then group 1 forms delta = rowsum(dO * O) (the
+            // separate delta pass of the other backends) off the MMA's
+            // critical path, shares it through shared memory and writes it for
+            // the dK/dV kernel that runs next
             const bf16* src = static_cast<const bf16*>(grp ? a.dout : a.q) + (t * a.H + h) * HD;
-            const bf16* orow = static_cast<const bf16*>(a.o) + (t * a.H + h) * HD;
-            float dsum = 0.f;
+            uint4 keep[HD / 8];
 #pragma unroll
             for (int c = 0; c < HD / 64; ++c) {
                 uint32_t wv[32];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const uint4 u = *reinterpret_cast<const uint4*>(src + c * 64 + i * 8);
+                    keep[c * 8 + i] = u;
                     wv[4 * i] = u.x;
                     wv[4 * i + 1] = u.y;
                     wv[4 * i + 2] = u.z;
                     wv[4 * i + 3] = u.w;
-                    if (grp) {
-                        const uint4 ov = *reinterpret_cast<const uint4*>(orow + c * 64 + i * 8);
-                        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-                        const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const float2 gf = __bfloat1622float2(g2[k]), of = __bfloat1622float2(o2[k]);
-                            dsum = fmaf(gf.x, of.x, fmaf(gf.y, of.y, dsum));
-                        }
-                    }
                 }
                 tc::tmem_st32u(lane_base + (grp ? kColOin : kColQin) + c * 32, wv);
-            }
-            if (grp) {
-                sDelta[r] = dsum;
-                if (r < rows) a.delta[static_cast<long long>(h) * a.T + row0 + r] = dsum;
             }
             tc::tmem_wait_st();
             tc::fence_before();
             tc::mbar_arrive(q_full);
+            if (grp) {
+                const bf16* orow = static_cast<const bf16*>(a.o) + (t * a.H + h) * HD;
+                float dsum = 0.f;
+#pragma unroll
+                for (int i = 0; i < HD / 8; ++i) {
+                    const uint4 ov = *reinterpret_cast<const uint4*>(orow + i * 8);
+                    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&keep[i]);
+                    const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float2 gf = __bfloat1622float2(g2[k]), of = __bfloat1622float2(o2[k]);
+                        dsum = fmaf(gf.x, of.x, fmaf(gf.y, of.y, dsum));
+                    }
+                }
+                sDelta[r] = dsum;
+                if (r < rows) a.delta[static_cast<long long>(h) * a.T + row0 + r] = dsum;
+                tc::mbar_arrive(d_full);
+            }
         }
-        tc::mbar_wait(q_full, 0);   // both groups: operands staged, delta shared
+        tc::mbar_wait(d_full, 0);
         const float dlt = sDelta[r];
         for (int j = grp; j < nkb; j += 2) {
             const int b = grp;
