@@ -150,7 +150,7 @@ def run_ours(args):
 
     from paper_2509_21275_b200 import calibrate, gpu, model as M, planner, schedule
     from paper_2509_21275_b200.executor import (DistributedPipeline, LocalPipeline, _ChunkTokens, allreduce_grads,
-                                                pipeline_groups, stage_layers)
+                                                balanced_stage_counts, pipeline_groups, stage_layers)
 
     world = args.gpus
     rank = int(os.environ.get("RANK", "0"))
@@ -171,7 +171,10 @@ def run_ours(args):
     replica, prank = rank // dp, rank % dp   # data-parallel replica, stage index
     pipes, dp_groups = pipeline_groups(dp, replicas) if world > 1 else ([None], [None])
     free, total_mem = torch.cuda.mem_get_info()
-    cfg = M.planner_config(m, dp, mem_capacity=float(total_mem) - 2e9, cost=M.default_cost(m))
+    # the last stage also runs the LM head: give it fewer layers when that
+    # lowers the bottleneck stage (GPT-1.3B at d_p 8: 4,3,3,3,3,3,3,2)
+    counts = balanced_stage_counts(m.layers, dp, M.head_layer_equivalents(m))
+    cfg = M.planner_config(m, dp, mem_capacity=float(total_mem) - 2e9, cost=M.default_cost(m), stage_counts=counts)
     jobs = os.cpu_count() or 8
 
     batches = make_batches(args, args.warmup + args.steps, dp, m.vocab, replica)
@@ -185,7 +188,7 @@ def run_ours(args):
 
     plans, planner_s = plan_all(cfg, 0)
 
-    first, num = stage_layers(m.layers, dp, prank)
+    first, num = stage_layers(m.layers, dp, prank, counts)
     stage = gpu.CudaStage(m, first, num, prank == 0, prank == dp - 1, dtype=args.dtype, device=local)
     stage.init_weights(1234)
     timed_stage = calibrate.TimedStage(stage)
@@ -389,7 +392,7 @@ def run_ours(args):
                                f"{args.seqs_per_gpu} seqs/GPU/step, d_p={dp}",
                    "model": args.model, "global_batch_seqs": args.seqs_per_gpu * world,
                    "tokens_per_step": tokens / args.steps, "seq_len_cap": args.cap,
-                   "slices": args.slices or "auto",
+                   "slices": args.slices or "auto", "stage_layers": counts,
                    "parallelism": f"pp{dp}" + (f"xdp{replicas}" if replicas > 1 else ""), "l2": "inputs larger than L2 (activations GBs/step)"},
         "mfu": flops / (sec * world * tf_burst * 1e12),
         "mfu_vs_sustained": flops / (sec * world * tf_sus * 1e12),

@@ -45,11 +45,38 @@ class ChunkOp:
     target_ids: Optional[torch.Tensor]
 
 
-def stage_layers(layers: int, pp_degree: int, stage: int):
-    """(first layer, count) of 0-based `stage` — contiguous L/d_p blocks
-    (proj/src/config.cpp:25-26 requires L % d_p == 0)."""
-    per = layers // pp_degree
-    return stage * per, per
+def stage_layers(layers: int, pp_degree: int, stage: int, counts: Optional[Sequence[int]] = None):
+    """(first layer, count) of 0-based `stage`: contiguous blocks, L/d_p each
+    (proj/src/config.cpp:25-26 requires L % d_p == 0) unless explicit
+    per-stage `counts` (balanced_stage_counts) are given."""
+    if counts is None:
+        per = layers // pp_degree
+        return stage * per, per
+    assert len(counts) == pp_degree and sum(counts) == layers
+    return sum(counts[:stage]), counts[stage]
+
+
+def balanced_stage_counts(layers: int, pp_degree: int, head_layers: float) -> List[int]:
+    """Layers per stage when the last stage also runs the LM head and
+    cross-entropy, worth `head_layers` transformer layers of work: start from
+    the uniform split and move single layers from the most to the least
+    loaded stage while that lowers the pipeline's bottleneck stage.  The
+    planner still prices uniform stages (its contract); the executor's memory
+    model is made conservative for the largest stage (model.planner_config)."""
+    counts = [layers // pp_degree] * pp_degree
+    if pp_degree == 1:
+        return counts
+
+    def load(i):
+        return counts[i] + (head_layers if i == pp_degree - 1 else 0.0)
+
+    while True:
+        hi = max(range(pp_degree), key=load)
+        lo = min(range(pp_degree), key=load)
+        if counts[hi] <= 1 or load(lo) + 1 >= load(hi):
+            return counts
+        counts[hi] -= 1
+        counts[lo] += 1
 
 
 class _ChunkTokens:

@@ -213,8 +213,11 @@ class CudaStage:
     def _desc(self, c) -> ChunkDesc:
         slices = (ctypes.c_int64 * len(c.slices))(*c.slices)
         self._keep[c.id] = slices
+        # the ladder counts layers of a uniform L/d_p stage; a head-balanced
+        # split can give this stage fewer layers than that
+        ckpt = min(int(c.ckpt_layers), self.num)
         return ChunkDesc(c.id, c.seq, c.kind, int(c.tail), c.context, c.seq_len, len(c.slices),
-                         slices, c.ckpt_layers, c.loss_scale, _ptr(c.token_ids), _ptr(c.target_ids))
+                         slices, ckpt, c.loss_scale, _ptr(c.token_ids), _ptr(c.target_ids))
 
     def forward(self, c, act_in: Optional[torch.Tensor]) -> Optional[torch.Tensor]:
         T = sum(c.slices)

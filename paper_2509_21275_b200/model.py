@@ -10,7 +10,7 @@ memory rows describe the real executor.
 from __future__ import annotations
 
 from dataclasses import asdict, dataclass
-from typing import Dict, Optional
+from typing import List, Dict, Optional
 
 
 @dataclass(frozen=True)
@@ -96,6 +96,15 @@ def activation_bytes_per_token(m: ModelConfig, elem_bytes: int = 2) -> float:
     return elems * elem_bytes + 4 * 4 + 4 * m.heads
 
 
+def head_layer_equivalents(m: "ModelConfig", pairs_per_token: float = 2048.0) -> float:
+    """LM head + cross-entropy work of the last stage in units of one
+    transformer layer's (matmul FLOPs, attention at `pairs_per_token` visible
+    keys per query)."""
+    head = 2.0 * m.hidden * m.vocab
+    layer = m.linear_flops_per_token_layer() + m.attn_flops_per_pair_layer() * pairs_per_token
+    return head / layer
+
+
 def state_bytes_per_param(dtype: str = "bf16") -> float:
     """fp32 master + fp32 grad + fp32 Adam m, v (+ bf16 working copy)."""
     return 16.0 + (2.0 if dtype == "bf16" else 0.0)
@@ -103,7 +112,7 @@ def state_bytes_per_param(dtype: str = "bf16") -> float:
 
 def planner_config(m: ModelConfig, pp_degree: int, mem_capacity: float = 180e9,
                    cost: Optional[Dict[str, float]] = None, reserve_bytes: float = 12e9,
-                   dtype: str = "bf16") -> Dict:
+                   dtype: str = "bf16", stage_counts: Optional[List[int]] = None) -> Dict:
     """SystemConfig document for the planner (proj/src/config.cpp:76-113).
 
     token_act_bytes: whole-model, unsharded activation bytes per token;
@@ -112,11 +121,12 @@ def planner_config(m: ModelConfig, pp_degree: int, mem_capacity: float = 180e9,
     """
     L = m.layers
     assert L % pp_degree == 0, "layers must divide by pp_degree"
+    counts = list(stage_counts) if stage_counts else [L // pp_degree] * pp_degree
     per_layer = m.params_per_layer()
     sbp = state_bytes_per_param(dtype)
     states = []
     for p in range(pp_degree):
-        n = per_layer * (L // pp_degree)
+        n = per_layer * counts[p]
         if p == 0:
             n += m.vocab * m.hidden
         if p == pp_degree - 1:
@@ -133,7 +143,9 @@ def planner_config(m: ModelConfig, pp_degree: int, mem_capacity: float = 180e9,
         # checkpointed-layer term (3 - 2I) e D l is then charged at 2x the
         # bf16 bytes it keeps, i.e. conservatively.
         "model": {"layers": L, "hidden_dim": m.hidden, "elem_bytes": 4.0,
-                  "token_act_bytes": float(activation_bytes_per_token(m) * L),
+                  # Eq. 10 charges L/d_p layers per stage; with a head-balanced
+                  # split the largest stage holds max(counts), so scale up
+                  "token_act_bytes": float(activation_bytes_per_token(m) * L * max(counts) * pp_degree / L),
                   "stage_state_bytes": [float(x) for x in states]},
         "cost": cost,
     }

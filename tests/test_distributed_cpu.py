@@ -28,12 +28,17 @@ def plan_doc(world):
     return planner.make_plan_document(cfg, LENGTHS, 3, "main", 1)
 
 
+def counts_for(world):
+    # head-balanced (non-uniform) split for world 2: the last stage gets fewer layers
+    return [3, 1] if world == 2 else None
+
+
 def worker(rank, world, port, doc, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
     plan = S.parse_plan(doc, LENGTHS)
     params = O.init_params(spec(), seed=3)
-    first, num = stage_layers(MODEL.layers, world, rank)
+    first, num = stage_layers(MODEL.layers, world, rank, counts_for(world))
     st = O.TorchStage(spec(), params, first, num, rank == 0, rank == world - 1)
     drv = DistributedPipeline(st, rank, world, torch.device("cpu"), MODEL.hidden, torch.float32)
     drv.run_step(plan, S.synthetic_tokens(LENGTHS, MODEL.vocab, seed=11))
@@ -74,7 +79,8 @@ def test_gloo_pipeline_matches_local(world):
             assert nbytes > 0
     plan = S.parse_plan(doc, LENGTHS)
     params = O.init_params(spec(), seed=3)
-    stages = [O.TorchStage(spec(), params, *stage_layers(MODEL.layers, world, p), p == 0, p == world - 1)
+    stages = [O.TorchStage(spec(), params, *stage_layers(MODEL.layers, world, p, counts_for(world)), p == 0,
+                           p == world - 1)
               for p in range(world)]
     LocalPipeline(stages, torch.device("cpu")).run_step(plan, S.synthetic_tokens(LENGTHS, MODEL.vocab, seed=11))
     local = {}

@@ -18,6 +18,7 @@ pytestmark = pytest.mark.gpu
 
 MODEL = M.ModelConfig("t", "llama", layers=4, hidden=256, heads=4, kv_heads=2, ffn=384, vocab=512)
 LENGTHS = [900, 37, 210, 90, 5, 64, 380, 1500]
+COUNTS = [3, 1]     # head-balanced (non-uniform) stage split
 
 
 def spec():
@@ -39,7 +40,7 @@ def worker(rank, world, port, doc, q):
     torch.cuda.set_device(0)
     plan = S.parse_plan(doc, LENGTHS)
     params = O.init_params(spec(), seed=5)
-    first, num = stage_layers(MODEL.layers, world, rank)
+    first, num = stage_layers(MODEL.layers, world, rank, COUNTS)
     st = CudaStage(MODEL, first, num, rank == 0, rank == world - 1, dtype="f32")
     st.load_weights(params)
     drv = DistributedPipeline(st, rank, world, torch.device("cuda"), MODEL.hidden, torch.float32)
@@ -84,7 +85,7 @@ def test_two_rank_cuda_pipeline_matches_local():
     params = O.init_params(spec(), seed=5)
     stages = []
     for p in range(world):
-        st = CudaStage(MODEL, *stage_layers(MODEL.layers, world, p), p == 0, p == world - 1, dtype="f32")
+        st = CudaStage(MODEL, *stage_layers(MODEL.layers, world, p, COUNTS), p == 0, p == world - 1, dtype="f32")
         st.load_weights(params)
         stages.append(st)
     LocalPipeline(stages, torch.device("cuda")).run_step(plan, S.synthetic_tokens(LENGTHS, MODEL.vocab, seed=13))
