@@ -154,7 +154,8 @@ int epp_kernel_attention_bwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, floa
 int epp_gpu_profile(int32_t enable);
 int epp_gpu_profile_read(int32_t cls, double* ms, double* flops, int64_t* launches, int32_t reset);
 
-/* Attention kernel family: 1 = tcgen05 (default), 0 = mma.sync FA2-style. */
+/* Attention kernel family: 1 = tcgen05 (default), 2 = tcgen05 with the fused
+ * dK/dV/dQ backward (hd 128), 0 = mma.sync FA2-style. */
 int epp_gpu_set_attention_impl(int32_t impl);
 
 const char* epp_gpu_last_error(void);

@@ -749,18 +749,34 @@ void launch_bf16_bwd(const AttnArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-// 1 = tcgen05 kernels (default), 0 = FA2-style mma.sync kernels.  Initial
-// value from EPP_ATTN_IMPL ("fa2" selects the legacy path); switchable at
-// run time through epp_gpu_set_attention_impl for A/B tests.
+// 1 = tcgen05 kernels (default), 2 = tcgen05 with the fused dK/dV/dQ
+// backward, 0 = FA2-style mma.sync kernels.  Initial value from
+// EPP_ATTN_IMPL ("fa2", "fused"); switchable at run time through
+// epp_gpu_set_attention_impl for A/B tests.
 int& attention_impl() {
     static int impl = [] {
         const char* e = getenv("EPP_ATTN_IMPL");
-        return (e && std::string(e) == "fa2") ? 0 : 1;
+        if (e && std::string(e) == "fa2") return 0;
+        if (e && std::string(e) == "fused") return 2;
+        return 1;
     }();
     return impl;
 }
 
-bool use_tc_attention() { return attention_impl() == 1; }
+bool use_tc_attention() { return attention_impl() >= 1; }
+
+void attn_delta(const AttnArgs& a, cudaStream_t s) {
+    if (a.T <= 0) return;
+    const long long warps = static_cast<long long>(a.T) * a.H;
+    const int blocks = static_cast<int>((warps * 32 + 255) / 256);
+    if (a.dtype == DType::F32)
+        attn_delta_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(a.dout),
+                                                        static_cast<const float*>(a.o), a.delta, a.T, a.H, a.hd);
+    else
+        attn_delta_kernel<bf16><<<blocks, 256, 0, s>>>(static_cast<const bf16*>(a.dout),
+                                                       static_cast<const bf16*>(a.o), a.delta, a.T, a.H, a.hd);
+    EPP_CHECK_LAUNCH();
+}
 
 void attn_fwd(const AttnArgs& a, cudaStream_t s) {
     EPP_REQUIRE(a.H % a.Hkv == 0, "attn: H must be a multiple of Hkv");
@@ -786,22 +802,10 @@ void attn_bwd(const AttnArgs& a, cudaStream_t s) {
     // algorithmic backward = 2x forward (dQ, dK, dV, dP matmuls)
     ProfScope prof(kProfAttnBwd, 8.0 * a.H * a.hd * a.pairs, s);
     if (use_tc_attention() && attn_bwd_tc_supported(a)) {
-        attn_bwd_tc_main(a, s);      // the dQ kernel forms delta itself
+        attn_bwd_tc_main(a, s);      // the dQ kernel (or the fused path) forms delta
         return;
     }
-    if (a.T > 0) {
-        const long long warps = static_cast<long long>(a.T) * a.H;
-        const int blocks = static_cast<int>((warps * 32 + 255) / 256);
-        if (a.dtype == DType::F32)
-            attn_delta_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(a.dout),
-                                                            static_cast<const float*>(a.o),
-                                                            a.delta, a.T, a.H, a.hd);
-        else
-            attn_delta_kernel<bf16><<<blocks, 256, 0, s>>>(static_cast<const bf16*>(a.dout),
-                                                           static_cast<const bf16*>(a.o),
-                                                           a.delta, a.T, a.H, a.hd);
-        EPP_CHECK_LAUNCH();
-    }
+    attn_delta(a, s);
     EPP_REQUIRE(a.dqkv_out == nullptr, "attn_bwd: dqkv_out needs the tcgen05 kernels");
     if (a.dtype == DType::F32) {
         if (a.nqwork > 0) {

@@ -121,7 +121,7 @@ struct AttnTables {
 extern "C" {
 
 int epp_gpu_set_attention_impl(int32_t impl) {
-    if (impl != 0 && impl != 1) return EPP_GPU_EARG;
+    if (impl < 0 || impl > 2) return EPP_GPU_EARG;
     eppk::attention_impl() = impl;
     return EPP_GPU_OK;
 }

@@ -146,6 +146,10 @@ int& attention_impl();
 bool attn_fwd_tc_supported(const AttnArgs& a);
 void attn_fwd_tc(const AttnArgs& a, cudaStream_t s);
 bool attn_bwd_tc_supported(const AttnArgs& a);
+// attention_impl() == 2 (hd 128, fp32 a.dq output): one fused tcgen05 kernel
+// forms dK, dV and dQ (reduced into a.dq) after a separate delta pass.
+bool attn_bwd_fused(const AttnArgs& a);
+void attn_delta(const AttnArgs& a, cudaStream_t s);   // delta = rowsum(dO * O)
 void attn_bwd_tc_main(const AttnArgs& a, cudaStream_t s);
 void attn_bwd(const AttnArgs& a, cudaStream_t s);
 

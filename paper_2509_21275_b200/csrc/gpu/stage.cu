@@ -757,7 +757,9 @@ private:
         // segment exactly once (dkv_accum = 0) and the dQ kernel writes the
         // un-rotated bf16 dQ straight into dqkv; the other kernels accumulate
         // into zeroed buffers and leave dQ in fp32 for the gather pass
-        const bool tc_bwd = dt_ == DType::BF16 && attention_impl() == 1;
+        // (fused: one kernel forms dK/dV and reduces dQ into fp32 dq)
+        const bool fused = dt_ == DType::BF16 && attention_impl() == 2 && hd_ == 128;
+        const bool tc_bwd = dt_ == DType::BF16 && attention_impl() >= 1;
         if (!tc_bwd) fill_zero(cs.dkv_local.get(), 2 * static_cast<size_t>(T) * kvw() * sizeof(float), s);
         a.q = L.q.get();
         a.o = L.o.get();
@@ -765,7 +767,7 @@ private:
         a.dout = dout.get();
         a.delta = delta.get<float>();
         Buf dq;
-        if (tc_bwd) {
+        if (tc_bwd && !fused) {
             a.dqkv_out = dqkv.get();
             a.tok_pos = cs.tok_pos.get<int>();
             a.rope_cs = rope_table_ptr(hd_, m_.rope_theta, s);
@@ -782,7 +784,7 @@ private:
         delta.release();
         rope_qkv_gather_grad(dt_, dq.get<float>(), cs.segs_dev.get<AttnSeg>(), cs.tok_seg.get<int>(),
                              cs.tok_pos.get<int>(), dqkv.get(), T, H_, Hkv_, hd_, j, m_.rope_theta, s,
-                             /*kv_only=*/tc_bwd);
+                             /*kv_only=*/tc_bwd && !fused);
         dq.release();
         gemm(mk(T, D_, Nqkv_, dqkv.get(), Nqkv_, true, work(P.wqkv), D_, false, dxn.get(), D_), s);
         norm_apply(dt_, llama_, x, work(P.ln1_w), P.ln1_b >= 0 ? work(P.ln1_b) : nullptr,

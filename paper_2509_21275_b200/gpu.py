@@ -101,8 +101,9 @@ def check(rc: int) -> None:
 
 
 def set_attention_impl(name: str) -> None:
-    """'tc' (tcgen05, default) or 'fa2' (mma.sync) attention kernels."""
-    check(lib().epp_gpu_set_attention_impl({"fa2": 0, "tc": 1}[name]))
+    """'tc' (tcgen05, default), 'fused' (tcgen05, single-pass dK/dV/dQ
+    backward for hd 128) or 'fa2' (mma.sync) attention kernels."""
+    check(lib().epp_gpu_set_attention_impl({"fa2": 0, "tc": 1, "fused": 2}[name]))
 
 
 def pool_reserve(nbytes: int) -> None:

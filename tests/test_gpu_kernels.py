@@ -177,7 +177,7 @@ SEGS = {
 }
 
 
-@pytest.mark.parametrize("impl,dtype", [("tc", "bf16"), ("fa2", "bf16"), ("tc", "f32")])
+@pytest.mark.parametrize("impl,dtype", [("tc", "bf16"), ("fused", "bf16"), ("fa2", "bf16"), ("tc", "f32")])
 @pytest.mark.parametrize("hd,H,Hkv", [(64, 4, 4), (128, 4, 2), (128, 8, 8)])
 @pytest.mark.parametrize("case", list(SEGS))
 def test_attention(impl, dtype, hd, H, Hkv, case):

@@ -98,12 +98,18 @@ def test_stage_parity(planner, arch, dtype, dp, slices, tight):
     gpu.set_attention_impl("tc")
 
 
-def test_hd128_bf16(planner):
+@pytest.mark.parametrize("impl", ["tc", "fused"])
+def test_hd128_bf16(planner, impl):
+    from paper_2509_21275_b200 import gpu
     m = M.ModelConfig("g128", "gpt", layers=2, hidden=256, heads=2, kv_heads=2, ffn=512, vocab=512)
     plan = make_plan(planner, m, [300, 90, 40, 513], 1, 2)
     params = O.init_params(spec_of(m), seed=1)
     tokens = S.synthetic_tokens([300, 90, 40, 513], m.vocab, seed=3)
-    loss_sum, cnt, grads = run_gpu(m, params, plan, tokens, "bf16")
+    gpu.set_attention_impl(impl)
+    try:
+        loss_sum, cnt, grads = run_gpu(m, params, plan, tokens, "bf16")
+    finally:
+        gpu.set_attention_impl("tc")
     ref_loss, ref_grads, _ = O.whole_batch_grads(spec_of(m), params,
                                                  [torch.from_numpy(t).long() for t in tokens])
     assert abs(loss_sum / cnt - ref_loss.item()) / ref_loss.item() < 5e-3
