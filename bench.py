@@ -260,6 +260,12 @@ def run_ours(args):
     lib = gpu.lib()
     lib.epp_gpu_profile(1)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    trace = os.environ.get("EPP_BENCH_TRACE")   # diagnostics only: a profiler-perturbed run
+    tracer = None
+    if trace:
+        tracer = torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA,
+                                                    torch.profiler.ProfilerActivity.CPU])
+        tracer.__enter__()
     with ClockSampler(local) as clk:
         sync_all()
         ev0.record()
@@ -268,6 +274,9 @@ def run_ours(args):
             optimizer()
         ev1.record()
         sync_all()
+    if tracer is not None:
+        tracer.__exit__(None, None, None)
+        tracer.export_chrome_trace(trace)
     lib.epp_gpu_profile(0)
     launches = gpu.kernel_launches() - launches0
     ms = ev0.elapsed_time(ev1)

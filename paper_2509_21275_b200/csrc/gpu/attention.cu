@@ -121,6 +121,8 @@ __device__ __forceinline__ void load_tile(bf16* tile, const bf16* base, long lon
 // ------------------------------------------------------------ forward ----
 template <int HD>
 __global__ void __launch_bounds__(128) attn_fwd_bf16(const AttnArgs a) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(128) uint8_t smem_raw[];
     bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
     bf16* sK = sQ + BM * HD;          // 2 buffers
@@ -275,6 +277,8 @@ __global__ void __launch_bounds__(128) attn_fwd_bf16(const AttnArgs a) {
 // ------------------------------------------------------- backward: dQ ----
 template <int HD>
 __global__ void __launch_bounds__(128) attn_bwd_dq_bf16(const AttnArgs a) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(128) uint8_t smem_raw[];
     bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
     bf16* sO = sQ + BM * HD;           // dO
@@ -401,6 +405,8 @@ __global__ void __launch_bounds__(128) attn_bwd_dq_bf16(const AttnArgs a) {
 // --------------------------------------------------- backward: dK, dV ----
 template <int HD>
 __global__ void __launch_bounds__(128) attn_bwd_dkv_bf16(const AttnArgs a) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(128) uint8_t smem_raw[];
     bf16* sK = reinterpret_cast<bf16*>(smem_raw);
     bf16* sV = sK + BN * HD;
@@ -560,6 +566,8 @@ __global__ void __launch_bounds__(128) attn_bwd_dkv_bf16(const AttnArgs a) {
 template <typename T>
 __global__ void attn_delta_kernel(const T* dout, const T* out, float* delta, int Tn, int H,
                                   int hd) {
+    pdl_wait();
+    pdl_trigger();
     const long long wid = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (wid >= static_cast<long long>(Tn) * H) return;
@@ -576,6 +584,8 @@ __global__ void attn_delta_kernel(const T* dout, const T* out, float* delta, int
 // ------------------------------------------------------- F32 (parity) ----
 // One warp per query row; lanes split the head dimension.
 __global__ void attn_fwd_f32(const AttnArgs a) {
+    pdl_wait();
+    pdl_trigger();
     const AttnWork w = a.qwork[blockIdx.x];
     const AttnSeg sg = a.segs[w.seg];
     const int h = blockIdx.y, kvh = h / (a.H / a.Hkv);
@@ -614,6 +624,8 @@ __global__ void attn_fwd_f32(const AttnArgs a) {
 }
 
 __global__ void attn_bwd_dq_f32(const AttnArgs a) {
+    pdl_wait();
+    pdl_trigger();
     const AttnWork w = a.qwork[blockIdx.x];
     const AttnSeg sg = a.segs[w.seg];
     const int h = blockIdx.y, kvh = h / (a.H / a.Hkv);
@@ -658,6 +670,8 @@ __global__ void attn_bwd_dq_f32(const AttnArgs a) {
 }
 
 __global__ void attn_bwd_dkv_f32(const AttnArgs a) {
+    pdl_wait();
+    pdl_trigger();
     const AttnWork w = a.kwork[blockIdx.x];
     const AttnSeg sg = a.segs[w.seg];
     const int kvh = blockIdx.y, group = a.H / a.Hkv;
@@ -723,7 +737,7 @@ void launch_bf16_fwd(const AttnArgs& a, cudaStream_t s) {
                                       fwd_smem<HD>()));
         cfg = true;
     }
-    attn_fwd_bf16<HD><<<dim3(a.nqwork, a.H), 128, fwd_smem<HD>(), s>>>(a);
+    launch_k(attn_fwd_bf16<HD>, dim3(a.nqwork, a.H), 128, fwd_smem<HD>(), s, a);
     EPP_CHECK_LAUNCH();
 }
 
@@ -738,11 +752,11 @@ void launch_bf16_bwd(const AttnArgs& a, cudaStream_t s) {
         cfg = true;
     }
     if (a.nqwork > 0) {
-        attn_bwd_dq_bf16<HD><<<dim3(a.nqwork, a.H), 128, dq_smem<HD>(), s>>>(a);
+        launch_k(attn_bwd_dq_bf16<HD>, dim3(a.nqwork, a.H), 128, dq_smem<HD>(), s, a);
         EPP_CHECK_LAUNCH();
     }
     if (a.nkwork > 0) {
-        attn_bwd_dkv_bf16<HD><<<dim3(a.nkwork, a.Hkv), 128, dkv_smem<HD>(), s>>>(a);
+        launch_k(attn_bwd_dkv_bf16<HD>, dim3(a.nkwork, a.Hkv), 128, dkv_smem<HD>(), s, a);
         EPP_CHECK_LAUNCH();
     }
 }
@@ -770,10 +784,10 @@ void attn_delta(const AttnArgs& a, cudaStream_t s) {
     const long long warps = static_cast<long long>(a.T) * a.H;
     const int blocks = static_cast<int>((warps * 32 + 255) / 256);
     if (a.dtype == DType::F32)
-        attn_delta_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(a.dout),
+        launch_k(attn_delta_kernel<float>, blocks, 256, 0, s, static_cast<const float*>(a.dout),
                                                         static_cast<const float*>(a.o), a.delta, a.T, a.H, a.hd);
     else
-        attn_delta_kernel<bf16><<<blocks, 256, 0, s>>>(static_cast<const bf16*>(a.dout),
+        launch_k(attn_delta_kernel<bf16>, blocks, 256, 0, s, static_cast<const bf16*>(a.dout),
                                                        static_cast<const bf16*>(a.o), a.delta, a.T, a.H, a.hd);
     EPP_CHECK_LAUNCH();
 }
@@ -788,7 +802,7 @@ void attn_fwd(const AttnArgs& a, cudaStream_t s) {
     ProfScope prof(kProfAttnFwd, 4.0 * a.H * a.hd * a.pairs, s);
     if (a.dtype == DType::F32) {
         EPP_REQUIRE(a.hd <= 128, "attn(f32): head_dim <= 128");
-        attn_fwd_f32<<<dim3(a.nqwork, a.H), 128, 0, s>>>(a);
+        launch_k(attn_fwd_f32, dim3(a.nqwork, a.H), 128, 0, s, a);
         EPP_CHECK_LAUNCH();
         return;
     }
@@ -809,11 +823,11 @@ void attn_bwd(const AttnArgs& a, cudaStream_t s) {
     EPP_REQUIRE(a.dqkv_out == nullptr, "attn_bwd: dqkv_out needs the tcgen05 kernels");
     if (a.dtype == DType::F32) {
         if (a.nqwork > 0) {
-            attn_bwd_dq_f32<<<dim3(a.nqwork, a.H), 128, 0, s>>>(a);
+            launch_k(attn_bwd_dq_f32, dim3(a.nqwork, a.H), 128, 0, s, a);
             EPP_CHECK_LAUNCH();
         }
         if (a.nkwork > 0) {
-            attn_bwd_dkv_f32<<<dim3(a.nkwork, a.Hkv), 128, 0, s>>>(a);
+            launch_k(attn_bwd_dkv_f32, dim3(a.nkwork, a.Hkv), 128, 0, s, a);
             EPP_CHECK_LAUNCH();
         }
         return;

@@ -219,6 +219,8 @@ struct FwdSmem {
 template <int HD>
 __global__ void __launch_bounds__(kThreadsFwd, 1) attn_fwd_tc(const AttnArgs a,
                                                               const __grid_constant__ AttnMaps mp) {
+    pdl_wait();
+    pdl_trigger();
     using L = FwdSmem<HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -457,7 +459,7 @@ void launch_fwd_tc(const AttnArgs& a, cudaStream_t s) {
     }
     AttnArgs b = a;
     b.hfast = attn_hfast(a.H, a.nqwork256);
-    attn_fwd_tc<HD><<<attn_grid(a.H, a.nqwork256), kThreadsFwd, L::kAlloc, s>>>(b, *a.maps);
+    launch_k(attn_fwd_tc<HD>, attn_grid(a.H, a.nqwork256), kThreadsFwd, L::kAlloc, s, b, *a.maps);
     EPP_CHECK_LAUNCH();
 }
 
@@ -547,6 +549,8 @@ struct DqSmem {
 template <int HD>
 __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs a,
                                                                  const __grid_constant__ AttnMaps mp) {
+    pdl_wait();
+    pdl_trigger();
     using L = DqSmem<HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -914,6 +918,8 @@ struct DkvSmem {
 template <int HD, bool FUSED>
 __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs a,
                                                                   const __grid_constant__ AttnMaps mp) {
+    pdl_wait();
+    pdl_trigger();
     using L = DkvSmem<HD, FUSED>;
     constexpr int kDkvStages = L::kStages;
     static_assert(!FUSED || HD == 128, "fused dQ^T needs M = hd = 128");
@@ -1270,8 +1276,8 @@ void launch_bwd_tc(const AttnArgs& a, cudaStream_t s) {
                 ProfScope prof(kProfAttnBwdDkv, 10.0 * a.H * a.hd * a.pairs, s);    // executed: 5 matmuls
                 AttnArgs b = a;
                 b.hfast = attn_hfast(a.Hkv, a.nkwork128);
-                attn_bwd_dkv_tc<HD, true><<<attn_grid(a.Hkv, a.nkwork128), kThreadsBwd, DkvSmem<HD, true>::kAlloc,
-                                            s>>>(b, *a.maps);
+                launch_k(attn_bwd_dkv_tc<HD, true>, attn_grid(a.Hkv, a.nkwork128), kThreadsBwd, DkvSmem<HD, true>::kAlloc,
+                                            s, b, *a.maps);
                 EPP_CHECK_LAUNCH();
             }
             return;
@@ -1281,15 +1287,15 @@ void launch_bwd_tc(const AttnArgs& a, cudaStream_t s) {
         ProfScope prof(kProfAttnBwdDq, 6.0 * a.H * a.hd * a.pairs, s);     // executed: 3 matmuls
         AttnArgs b = a;
         b.hfast = attn_hfast(a.H, a.nqwork128);
-        attn_bwd_dq_tc<HD><<<attn_grid(a.H, a.nqwork128), kThreadsBwd, DqSmem<HD>::kAlloc, s>>>(b, *a.maps);
+        launch_k(attn_bwd_dq_tc<HD>, attn_grid(a.H, a.nqwork128), kThreadsBwd, DqSmem<HD>::kAlloc, s, b, *a.maps);
         EPP_CHECK_LAUNCH();
     }
     if (a.nkwork128 > 0) {
         ProfScope prof(kProfAttnBwdDkv, 8.0 * a.H * a.hd * a.pairs, s);    // executed: 4 matmuls
         AttnArgs b = a;
         b.hfast = attn_hfast(a.Hkv, a.nkwork128);
-        attn_bwd_dkv_tc<HD, false><<<attn_grid(a.Hkv, a.nkwork128), kThreadsBwd, DkvSmem<HD, false>::kAlloc,
-                                     s>>>(b, *a.maps);
+        launch_k(attn_bwd_dkv_tc<HD, false>, attn_grid(a.Hkv, a.nkwork128), kThreadsBwd, DkvSmem<HD, false>::kAlloc,
+                                     s, b, *a.maps);
         EPP_CHECK_LAUNCH();
     }
 }

@@ -7,6 +7,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 namespace eppk {
 
@@ -33,6 +34,32 @@ long long& launch_counter();
         EPP_CUDA(cudaGetLastError());                                                    \
         ++::eppk::launch_counter();                                                      \
     } while (0)
+
+// Programmatic dependent launch.  Every kernel starts with pdl_wait() (the
+// previous grid in the stream has completed and its writes are visible) and
+// then pdl_trigger() (the next grid may be scheduled), and is launched with
+// launch_k(), which sets programmatic stream serialisation: the next
+// kernel's launch and CTA rasterisation overlap the tail of the current one
+// instead of following its completion (~8 us per transition between the
+// large tcgen05 kernels).  EPP_PDL=0 launches conventionally.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    EPP_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 #define EPP_REQUIRE(cond, msg)                                                           \
     do {                                                                                 \

@@ -55,6 +55,8 @@ int grid_for(long long n, int threads) {
 // ------------------------------------------------------------ embedding ---
 template <typename T>
 __global__ void embed_fwd_k(const int32_t* ids, const T* table, T* out, int Tn, int D) {
+    pdl_wait();
+    pdl_trigger();
     const int t = blockIdx.x;
     const T* src = table + static_cast<long long>(ids[t]) * D;
     T* dst = out + static_cast<long long>(t) * D;
@@ -66,6 +68,8 @@ __global__ void embed_fwd_k(const int32_t* ids, const T* table, T* out, int Tn, 
 }
 template <typename T>
 __global__ void embed_bwd_k(const int32_t* ids, const T* dout, float* dtable, int Tn, int D) {
+    pdl_wait();
+    pdl_trigger();
     const int t = blockIdx.x;
     float* dst = dtable + static_cast<long long>(ids[t]) * D;
     const T* src = dout + static_cast<long long>(t) * D;
@@ -82,6 +86,8 @@ __global__ void embed_bwd_k(const int32_t* ids, const T* dout, float* dtable, in
 template <typename T>
 __global__ void norm_fwd_k(bool rms, const T* x, const T* w, const T* b, T* y, float* mean,
                            float* rstd, int D, float eps) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float scratch[32];
     const long long row = blockIdx.x;
     const T* xr = x + row * D;
@@ -122,6 +128,8 @@ __global__ void norm_fwd_k(bool rms, const T* x, const T* w, const T* b, T* y, f
 template <int NC>
 __global__ void __launch_bounds__(256) norm_fwd_warp_k(bool rms, const bf16* x, const bf16* w, const bf16* b,
                                                        bf16* y, float* mean, float* rstd, int Tn, float eps) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int D = 256 * NC;
     const int lane = threadIdx.x & 31;
     const long long row = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -206,6 +214,8 @@ __device__ __forceinline__ float sum128(float v, float* red) {   // 4-warp CTA s
 template <int NPT>
 __global__ void __launch_bounds__(128) norm_fwd_row_k(bool rms, const bf16* x, const bf16* w, const bf16* b, bf16* y,
                                                       float* mean, float* rstd, float eps) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int D = 1024 * NPT;
     __shared__ float red[4];
     const long long row = blockIdx.x;
@@ -252,6 +262,8 @@ template <int NPT>
 __global__ void __launch_bounds__(128) norm_bwd_dx_row_k(bool rms, const bf16* x, const bf16* w, const bf16* dy,
                                                          const float* mean, const float* rstd, const bf16* dres,
                                                          bf16* dx) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int D = 1024 * NPT;
     __shared__ float red[2][4];
     const long long row = blockIdx.x;
@@ -304,6 +316,8 @@ __global__ void __launch_bounds__(128) norm_bwd_dx_row_k(bool rms, const bf16* x
 template <typename T>
 __global__ void norm_apply_k(bool rms, const T* x, const T* w, const T* b, const float* mean,
                              const float* rstd, T* y, int D) {
+    pdl_wait();
+    pdl_trigger();
     const long long row = blockIdx.x;
     const float mu = rms ? 0.f : mean[row];
     const float rs = rstd[row];
@@ -327,6 +341,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) norm_bwd_dx_k(bool rms, const T* x, const T* w, const T* dy,
                                                      const float* mean, const float* rstd,
                                                      const T* dres, T* dx, int Tn, int D) {
+    pdl_wait();
+    pdl_trigger();
     const int lane = threadIdx.x & 31;
     const long long row = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (row >= Tn) return;
@@ -366,6 +382,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) norm_bwd_dw2_k(bool rms, const T* x, const T* dy, const float* mean,
                                                       const float* rstd, float* pw, float* pb, int Tn, int D,
                                                       int rows_per) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float red[2][8][256 + 8];
     const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
     const int c = blockIdx.x * 256 + cx * 8;
@@ -410,6 +428,8 @@ __global__ void __launch_bounds__(256) norm_bwd_dw2_k(bool rms, const T* x, cons
 // 32 columns; its 8 warps stride over g with coalesced 128-byte row reads,
 // then combine in shared memory in a fixed order.
 __global__ void __launch_bounds__(256) col_reduce_add(const float* part, int G, int D, float* dst) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float red[8][33];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int c = blockIdx.x * 32 + tx;
@@ -439,6 +459,8 @@ struct RopeTable {
 };
 
 __global__ void rope_table_k(float2* cs, int max_pos, int half, double theta) {
+    pdl_wait();
+    pdl_trigger();
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= static_cast<long long>(max_pos) * half) return;
     const int pos = static_cast<int>(i / half), j = static_cast<int>(i % half);
@@ -455,6 +477,8 @@ template <typename T>
 __global__ void rope_scatter_k(const T* qkv, T* q_out, const AttnSeg* segs, const int* tok_seg,
                                const int* tok_pos, const float2* cs, int Tn, int H, int Hkv,
                                int hd, int layer) {
+    pdl_wait();
+    pdl_trigger();
     const int half = hd / 2;
     const int per_slot = half / 8;
     const int slots = H + 2 * Hkv;
@@ -499,6 +523,8 @@ template <typename T>
 __global__ void rope_gather_grad_k(const float* dq, const AttnSeg* segs, const int* tok_seg,
                                    const int* tok_pos, const float2* cs, T* dqkv, int Tn, int H,
                                    int Hkv, int hd, int layer, int slot0) {
+    pdl_wait();
+    pdl_trigger();
     const int half = hd / 2;
     const int per_slot = half / 8;
     const int slots = H + 2 * Hkv;
@@ -559,6 +585,8 @@ __device__ __forceinline__ float sigmoidf_(float x) {
 
 template <typename T>
 __global__ void act_fwd_k(int act, const T* h, T* out, long long Tn, int F) {
+    pdl_wait();
+    pdl_trigger();
     const long long n8 = Tn * F / 8;
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n8;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -583,6 +611,8 @@ __global__ void act_fwd_k(int act, const T* h, T* out, long long Tn, int F) {
 
 template <typename T>
 __global__ void act_bwd_k(int act, const T* h, const T* da, T* dh, long long Tn, int F) {
+    pdl_wait();
+    pdl_trigger();
     const long long n8 = Tn * F / 8;
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n8;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -618,6 +648,8 @@ __global__ void act_bwd_k(int act, const T* h, const T* da, T* dh, long long Tn,
 // One CTA per row; logits overwritten with grad_scale * (softmax - onehot).
 template <typename T>
 __global__ void ce_k(T* logits, const int32_t* targets, float* loss_acc, int V, float gscale) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float scratch[32];
     __shared__ float red_m[32], red_s[32];
     const long long row = blockIdx.x;
@@ -686,6 +718,8 @@ __global__ void ce_k(T* logits, const int32_t* targets, float* loss_acc, int V, 
 // ---------------------------------------------------------------- misc ----
 template <typename T>
 __global__ void cast_k(const float* src, T* dst, long long n) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x)
         dst[i] = from_f<T>(src[i]);
@@ -693,6 +727,8 @@ __global__ void cast_k(const float* src, T* dst, long long n) {
 
 template <typename T>
 __global__ void add_k(T* y, const T* x, long long n) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x)
         y[i] = from_f<T>(to_f(y[i]) + to_f(x[i]));
@@ -701,6 +737,8 @@ __global__ void add_k(T* y, const T* x, long long n) {
 template <typename T>
 __global__ void adamw_k(float* master, T* work, float* grad, float* m, float* v, long long n,
                         float lr, float b1, float b2, float eps, float wd, float bc1, float bc2) {
+    pdl_wait();
+    pdl_trigger();
     // 4 parameters per thread and iteration (16-byte fp32 accesses); tensors
     // are allocated 256-byte aligned, n need not be a multiple of 4
     const long long n4 = n / 4;
@@ -754,6 +792,8 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
 }
 
 __global__ void init_normal_k(float* dst, long long n, float std, unsigned long long seed) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const unsigned long long r = mix64(seed ^ mix64(static_cast<unsigned long long>(i)));
@@ -764,6 +804,8 @@ __global__ void init_normal_k(float* dst, long long n, float std, unsigned long 
 }
 
 __global__ void init_const_k(float* dst, long long n, float v) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x)
         dst[i] = v;
@@ -785,7 +827,7 @@ const float2* rope_table(int max_pos, int hd, float theta, cudaStream_t s) {
     }
     EPP_CUDA(cudaMalloc(&g_rope.cs, sizeof(float2) * want * half));
     const long long n = static_cast<long long>(want) * half;
-    rope_table_k<<<grid_for(n, 256), 256, 0, s>>>(g_rope.cs, want, half, theta);
+    launch_k(rope_table_k, grid_for(n, 256), 256, 0, s, g_rope.cs, want, half, theta);
     EPP_CHECK_LAUNCH();
     g_rope.max_pos = want;
     g_rope.half = half;
@@ -809,7 +851,7 @@ void embed_fwd(DType t, const int32_t* ids, const void* table, void* out, int T,
     if (T == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        embed_fwd_k<E><<<T, norm_threads(D), 0, s>>>(ids, static_cast<const E*>(table),
+        launch_k(embed_fwd_k<E>, T, norm_threads(D), 0, s, ids, static_cast<const E*>(table),
                                                      static_cast<E*>(out), T, D);
     });
     EPP_CHECK_LAUNCH();
@@ -821,7 +863,7 @@ void embed_bwd(DType t, const int32_t* ids, const void* dout, float* dtable, int
     if (T == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        embed_bwd_k<E><<<T, norm_threads(D), 0, s>>>(ids, static_cast<const E*>(dout), dtable, T, D);
+        launch_k(embed_bwd_k<E>, T, norm_threads(D), 0, s, ids, static_cast<const E*>(dout), dtable, T, D);
     });
     EPP_CHECK_LAUNCH();
 }
@@ -836,14 +878,14 @@ void norm_fwd(DType t, bool rms, const void* x, const void* w, const void* b, vo
         const int blocks = ceil_div(static_cast<long long>(T) * 32, 256);
         auto warp_kernel = [&](auto nc) {
             constexpr int NC = decltype(nc)::value;
-            norm_fwd_warp_k<NC><<<blocks, 256, 0, s>>>(rms, static_cast<const bf16*>(x), static_cast<const bf16*>(w),
+            launch_k(norm_fwd_warp_k<NC>, blocks, 256, 0, s, rms, static_cast<const bf16*>(x), static_cast<const bf16*>(w),
                                                        static_cast<const bf16*>(b), static_cast<bf16*>(y), mean, rstd,
                                                        T, eps);
         };
         if constexpr (std::is_same<E, bf16>::value) {
             auto row_kernel = [&](auto npt) {
                 constexpr int NPT = decltype(npt)::value;
-                norm_fwd_row_k<NPT><<<T, 128, 0, s>>>(rms, static_cast<const bf16*>(x), static_cast<const bf16*>(w),
+                launch_k(norm_fwd_row_k<NPT>, T, 128, 0, s, rms, static_cast<const bf16*>(x), static_cast<const bf16*>(w),
                                                       static_cast<const bf16*>(b), static_cast<bf16*>(y), mean, rstd,
                                                       eps);
             };
@@ -854,7 +896,7 @@ void norm_fwd(DType t, bool rms, const void* x, const void* w, const void* b, vo
             if (D == 4096) return row_kernel(std::integral_constant<int, 4>{});
             if (D == 8192) return row_kernel(std::integral_constant<int, 8>{});
         }
-        norm_fwd_k<E><<<T, norm_threads(D), 0, s>>>(rms, static_cast<const E*>(x),
+        launch_k(norm_fwd_k<E>, T, norm_threads(D), 0, s, rms, static_cast<const E*>(x),
                                                     static_cast<const E*>(w),
                                                     static_cast<const E*>(b), static_cast<E*>(y),
                                                     mean, rstd, D, eps);
@@ -868,7 +910,7 @@ void norm_apply(DType t, bool rms, const void* x, const void* w, const void* b, 
     if (T == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        norm_apply_k<E><<<T, norm_threads(D), 0, s>>>(rms, static_cast<const E*>(x),
+        launch_k(norm_apply_k<E>, T, norm_threads(D), 0, s, rms, static_cast<const E*>(x),
                                                       static_cast<const E*>(w),
                                                       static_cast<const E*>(b), mean, rstd,
                                                       static_cast<E*>(y), D);
@@ -896,7 +938,7 @@ void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy, c
         if constexpr (std::is_same<E, bf16>::value) {
             auto row_kernel = [&](auto npt) {
                 constexpr int NPT = decltype(npt)::value;
-                norm_bwd_dx_row_k<NPT><<<T, 128, 0, s>>>(rms, static_cast<const bf16*>(x), static_cast<const bf16*>(w),
+                launch_k(norm_bwd_dx_row_k<NPT>, T, 128, 0, s, rms, static_cast<const bf16*>(x), static_cast<const bf16*>(w),
                                                          static_cast<const bf16*>(dy), mean, rstd,
                                                          static_cast<const bf16*>(dres), static_cast<bf16*>(dx));
                 done = true;
@@ -907,16 +949,16 @@ void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy, c
             else if (D == 8192) row_kernel(std::integral_constant<int, 8>{});
         }
         if (!done)
-            norm_bwd_dx_k<E><<<ceil_div(static_cast<long long>(T) * 32, 256), 256, 0, s>>>(
+            launch_k(norm_bwd_dx_k<E>, ceil_div(static_cast<long long>(T) * 32, 256), 256, 0, s, 
                 rms, static_cast<const E*>(x), static_cast<const E*>(w), static_cast<const E*>(dy), mean,
                 rstd, static_cast<const E*>(dres), static_cast<E*>(dx), T, D);
         EPP_CHECK_LAUNCH();
-        norm_bwd_dw2_k<E><<<dim3(col_blocks, G), 256, 0, s>>>(
+        launch_k(norm_bwd_dw2_k<E>, dim3(col_blocks, G), 256, 0, s, 
             rms, static_cast<const E*>(x), static_cast<const E*>(dy), mean, rstd, pw, pb, T, D, rows_per);
         EPP_CHECK_LAUNCH();
     });
-    col_reduce_add<<<ceil_div(D, 32), 256, 0, s>>>(pw, G, D, dw);
-    if (db) col_reduce_add<<<ceil_div(D, 32), 256, 0, s>>>(pb, G, D, db);
+    launch_k(col_reduce_add, ceil_div(D, 32), 256, 0, s, pw, G, D, dw);
+    if (db) launch_k(col_reduce_add, ceil_div(D, 32), 256, 0, s, pb, G, D, db);
     EPP_CHECK_LAUNCH();
     EPP_CUDA(cudaFreeAsync(part, s));
 }
@@ -932,7 +974,7 @@ void rope_qkv_scatter(DType t, const void* qkv, void* q_out, const AttnSeg* segs
     const long long n = static_cast<long long>(T) * (H + 2 * Hkv) * (hd / 16);
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        rope_scatter_k<E><<<grid_for(n, 256), 256, 0, s>>>(static_cast<const E*>(qkv),
+        launch_k(rope_scatter_k<E>, grid_for(n, 256), 256, 0, s, static_cast<const E*>(qkv),
                                                            static_cast<E*>(q_out), segs_dev,
                                                            tok_seg, tok_pos, cs, T, H, Hkv, hd,
                                                            layer);
@@ -950,7 +992,7 @@ void rope_qkv_gather_grad(DType t, const float* dq, const AttnSeg* segs_dev, con
     const long long n = static_cast<long long>(T) * (H + 2 * Hkv - slot0) * (hd / 16);
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        rope_gather_grad_k<E><<<grid_for(n, 256), 256, 0, s>>>(dq, segs_dev, tok_seg, tok_pos, cs,
+        launch_k(rope_gather_grad_k<E>, grid_for(n, 256), 256, 0, s, dq, segs_dev, tok_seg, tok_pos, cs,
                                                                static_cast<E*>(dqkv), T, H, Hkv,
                                                                hd, layer, slot0);
     });
@@ -964,7 +1006,7 @@ void act_fwd(DType t, int act, const void* h, void* a, int T, int F, cudaStream_
     const long long n8 = static_cast<long long>(T) * F / 8;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        act_fwd_k<E><<<grid_for(n8, 256), 256, 0, s>>>(act, static_cast<const E*>(h),
+        launch_k(act_fwd_k<E>, grid_for(n8, 256), 256, 0, s, act, static_cast<const E*>(h),
                                                        static_cast<E*>(a), T, F);
     });
     EPP_CHECK_LAUNCH();
@@ -977,7 +1019,7 @@ void act_bwd(DType t, int act, const void* h, const void* da, void* dh, int T, i
     const long long n8 = static_cast<long long>(T) * F / 8;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        act_bwd_k<E><<<grid_for(n8, 256), 256, 0, s>>>(act, static_cast<const E*>(h),
+        launch_k(act_bwd_k<E>, grid_for(n8, 256), 256, 0, s, act, static_cast<const E*>(h),
                                                        static_cast<const E*>(da),
                                                        static_cast<E*>(dh), T, F);
     });
@@ -991,7 +1033,7 @@ void cross_entropy(DType t, void* logits, const int32_t* targets, float* loss_ac
     if (T == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        ce_k<E><<<T, 256, 0, s>>>(static_cast<E*>(logits), targets, loss_acc, V, grad_scale);
+        launch_k(ce_k<E>, T, 256, 0, s, static_cast<E*>(logits), targets, loss_acc, V, grad_scale);
     });
     EPP_CHECK_LAUNCH();
 }
@@ -1006,7 +1048,7 @@ void cast_f32_to(DType t, const float* src, void* dst, long long n, cudaStream_t
     if (n == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        cast_k<E><<<grid_for(n, 256), 256, 0, s>>>(src, static_cast<E*>(dst), n);
+        launch_k(cast_k<E>, grid_for(n, 256), 256, 0, s, src, static_cast<E*>(dst), n);
     });
     EPP_CHECK_LAUNCH();
 }
@@ -1016,7 +1058,7 @@ void add_inplace(DType t, void* y, const void* x, long long n, cudaStream_t s) {
     if (n == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        add_k<E><<<grid_for(n, 256), 256, 0, s>>>(static_cast<E*>(y), static_cast<const E*>(x), n);
+        launch_k(add_k<E>, grid_for(n, 256), 256, 0, s, static_cast<E*>(y), static_cast<const E*>(x), n);
     });
     EPP_CHECK_LAUNCH();
 }
@@ -1028,7 +1070,7 @@ void adamw(float* master, void* work, DType t, float* grad, float* m, float* v, 
     if (n == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        adamw_k<E><<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(master, static_cast<E*>(work), grad, m, v, n,
+        launch_k(adamw_k<E>, grid_for((n + 3) / 4, 256), 256, 0, s, master, static_cast<E*>(work), grad, m, v, n,
                                                      lr, b1, b2, eps, wd, bc1, bc2);
     });
     EPP_CHECK_LAUNCH();
@@ -1036,13 +1078,13 @@ void adamw(float* master, void* work, DType t, float* grad, float* m, float* v, 
 
 void init_normal(float* dst, long long n, float std, unsigned long long seed, cudaStream_t s) {
     if (n == 0) return;
-    init_normal_k<<<grid_for(n, 256), 256, 0, s>>>(dst, n, std, seed);
+    launch_k(init_normal_k, grid_for(n, 256), 256, 0, s, dst, n, std, seed);
     EPP_CHECK_LAUNCH();
 }
 
 void init_const(float* dst, long long n, float v, cudaStream_t s) {
     if (n == 0) return;
-    init_const_k<<<grid_for(n, 256), 256, 0, s>>>(dst, n, v);
+    launch_k(init_const_k, grid_for(n, 256), 256, 0, s, dst, n, v);
     EPP_CHECK_LAUNCH();
 }
 

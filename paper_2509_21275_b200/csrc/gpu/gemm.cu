@@ -230,6 +230,8 @@ template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, const TcParams p) {
+    pdl_wait();
+    pdl_trigger();
     using L = TcSmem<BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -435,6 +437,8 @@ template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b, const TcParams p) {
+    pdl_wait();
+    pdl_trigger();
     using L = Tc2Smem<BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -666,7 +670,7 @@ void launch_tc(const GemmArgs& g, cudaStream_t s) {
         EPP_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
     }
     const int tiles = ceil_div(g.N, BN) * ceil_div(g.M, kBM);
-    kern<<<std::min(tiles, num_sms), kThreads, L::kTotal, s>>>(ma, mb, p);
+    launch_k(kern, std::min(tiles, num_sms), kThreads, L::kTotal, s, ma, mb, p);
     EPP_CHECK_LAUNCH();
     g_gemm_launches.fetch_add(1);
 }
@@ -721,7 +725,7 @@ void launch_tc2(const GemmArgs& g, cudaStream_t s) {
     }
     const int tiles = ceil_div(g.N, BN) * ceil_div(g.M, 2 * kBM);
     const int clusters = std::min(tiles, num_sms / 2);
-    kern<<<2 * clusters, kThreads, L::kTotal, s>>>(ma, mb, p);
+    launch_k(kern, 2 * clusters, kThreads, L::kTotal, s, ma, mb, p);
     EPP_CHECK_LAUNCH();
     g_gemm_launches.fetch_add(1);
 }
@@ -754,6 +758,8 @@ void dispatch_epi2(const GemmArgs& g, cudaStream_t s) {
 // ---------------------------------------------------------------- SIMT f32
 template <typename T>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int TM = 64, TN = 64, TK = 16;
     __shared__ float As[TK][TM + 1];
     __shared__ float Bs[TK][TN + 1];
@@ -833,7 +839,7 @@ void gemm(const GemmArgs& g, cudaStream_t s) {
     ProfScope prof(kProfGemm, 2.0 * g.M * g.N * g.K, s);
     if (g.dtype == DType::F32) {
         dim3 grid(ceil_div(g.N, 64), ceil_div(g.M, 64));
-        gemm_simt_kernel<float><<<grid, 256, 0, s>>>(g);
+        launch_k(gemm_simt_kernel<float>, grid, 256, 0, s, g);
         EPP_CHECK_LAUNCH();
         g_gemm_launches.fetch_add(1);
         return;

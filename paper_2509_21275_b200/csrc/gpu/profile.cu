@@ -1,6 +1,7 @@
 // epp-b200: opt-in per-launch timing of the dominant kernels (GEMM,
 // attention) with CUDA events recorded on the launching stream, so bench.py
 // can report achieved TFLOP/s of the kernel class live over its timed region.
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -101,3 +102,13 @@ int epp_gpu_profile_read(int32_t cls, double* ms, double* flops, int64_t* launch
     return 0;
 }
 }
+
+namespace eppk {
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* v = getenv("EPP_PDL");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+}  // namespace eppk

@@ -205,6 +205,8 @@ public:
         EPP_REQUIRE(dt == DType::F32 || m.head_dim == 64 || m.head_dim == 128,
                     "bf16 attention supports head_dim 64 or 128");
         keep_pool_reserved();
+        if (const char* e = getenv("EPP_SMEM_PREF"); e && e[0] == '1')
+            EPP_CUDA(cudaDeviceSetCacheConfig(cudaFuncCachePreferShared));
         D_ = m.hidden;
         H_ = m.heads;
         Hkv_ = m.kv_heads;
