@@ -6,7 +6,7 @@ set -x
 TAG=${1:-r01}
 B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --seqs-per-gpu 32"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 6000 -c 2500 --csv --log-file gpurun_out/launches_$TAG.csv $B > gpurun_out/ncu_launch.log 2>&1
-for k in attn_bwd_dkv_tc attn_bwd_dq_tc attn_fwd_tc gemm_tc2_kernel norm_bwd_dx_k rope_gather_grad_k; do
+for k in attn_bwd_dkv_tc attn_bwd_dq_tc attn_fwd_tc gemm_tc2_kernel norm_bwd_dx_row_k norm_fwd_row_k rope_gather_grad_k; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 20 -c 1 -o gpurun_out/prof_${TAG}_$k $B > gpurun_out/ncu_$k.log 2>&1
 done
 ls -la gpurun_out

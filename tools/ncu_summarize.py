@@ -18,7 +18,8 @@ ROOT = Path(__file__).resolve().parents[1]
 OUT = ROOT / "gpurun_out"
 PROF = ROOT / "profiles"
 CLASS = {"gemm_tc2_kernel": "gemm", "attn_fwd_tc": "attn_fwd", "attn_bwd_dq_tc": "attn_bwd_dq",
-         "attn_bwd_dkv_tc": "attn_bwd_dkv", "norm_bwd_dx_k": "norm_bwd", "rope_gather_grad_k": "rope"}
+         "attn_bwd_dkv_tc": "attn_bwd_dkv", "norm_bwd_dx_row_k": "norm_bwd", "norm_fwd_row_k": "norm_fwd",
+         "rope_gather_grad_k": "rope"}
 KEYS = {"duration": "gpu__time_duration.sum",
         "dram_read_bytes": "dram__bytes_read.sum", "dram_write_bytes": "dram__bytes_write.sum",
         "tensor_pipe_active_pct": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
