@@ -154,16 +154,15 @@ def run_ours(args):
 
     world = args.gpus
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
+    torch.cuda.set_device(local)     # before the process group: NCCL binds the current device
+    dev = torch.device("cuda", local)
     if world > 1:
         # EPP_BENCH_BACKEND=gloo runs the multi-rank code path with several
         # ranks sharing one GPU (messages staged through host memory): a
         # functional check only, never a reported number
         dist.init_process_group(os.environ.get("EPP_BENCH_BACKEND", "nccl"))
         assert dist.get_world_size() == world
-    local = local % torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
     m = M.MODELS[args.model]
     dp = args.pp or world                    # pipeline degree d_p
     assert world % dp == 0, "--gpus must be a multiple of --pp"
