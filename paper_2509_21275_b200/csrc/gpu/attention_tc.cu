@@ -1227,19 +1227,89 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
         float* drow = base + a.layer * sg.dkv_layer_stride + kvh * HD + (k0 + min(r, nkeys - 1)) * kvs;
         const float mul = grp == 0 ? a.scale : 1.f;
         const uint32_t col = grp == 0 ? kColK : kColV;
+        if (!FUSED && a.dqkv_out != nullptr) {
+            // Rows of this chunk's own tokens are complete here (later slices,
+            // which also attend to them, ran their backward first): add the
+            // accumulated fp32 partials, undo RoPE (dK) and write bf16 straight
+            // into the k / v columns of dqkv.  Context rows (earlier slices)
+            // keep accumulating in fp32.
+            constexpr int HALF = HD / 2;
+            const int kp = k0 + r;
+            const bool valid = r < nkeys;
+            const bool own = valid && kp >= sg.kv_ctx;
+            const long long t_out = sg.q_start + (kp - sg.kv_ctx);
+            bf16* orow = static_cast<bf16*>(a.dqkv_out) + t_out * (a.H + 2 * a.Hkv) * HD +
+                         (grp == 0 ? a.H + kvh : a.H + a.Hkv + kvh) * HD;
 #pragma unroll 1
-        for (int c = 0; c < HD / 32; ++c) {
-            float v[32];
-            tc::tmem_ld32(lane_base + col + c * 32, v);    // warp-collective: all lanes
-            if (r < nkeys) {
+            for (int cc = 0; cc < HALF; cc += 32) {
+                float g1[32], g2[32];
+                tc::tmem_ld32(lane_base + col + cc, g1);          // warp-collective: all lanes
+                tc::tmem_ld32(lane_base + col + HALF + cc, g2);
+                if (!valid) continue;
 #pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                    float4 x = make_float4(v[i] * mul, v[i + 1] * mul, v[i + 2] * mul, v[i + 3] * mul);
-                    if (sg.dkv_accum) {   // later slices' contributions are already there
-                        const float4 o = *reinterpret_cast<const float4*>(drow + c * 32 + i);
-                        x.x += o.x; x.y += o.y; x.z += o.z; x.w += o.w;
+                for (int i = 0; i < 32; ++i) {
+                    g1[i] *= mul;
+                    g2[i] *= mul;
+                }
+                if (sg.dkv_accum) {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        const float4 o1 = *reinterpret_cast<const float4*>(drow + cc + i);
+                        const float4 o2 = *reinterpret_cast<const float4*>(drow + HALF + cc + i);
+                        g1[i] += o1.x; g1[i + 1] += o1.y; g1[i + 2] += o1.z; g1[i + 3] += o1.w;
+                        g2[i] += o2.x; g2[i + 1] += o2.y; g2[i + 2] += o2.z; g2[i + 3] += o2.w;
                     }
-                    *reinterpret_cast<float4*>(drow + c * 32 + i) = x;
+                }
+                if (!own) {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        *reinterpret_cast<float4*>(drow + cc + i) = make_float4(g1[i], g1[i + 1], g1[i + 2], g1[i + 3]);
+                        *reinterpret_cast<float4*>(drow + HALF + cc + i) =
+                            make_float4(g2[i], g2[i + 1], g2[i + 2], g2[i + 3]);
+                    }
+                    continue;
+                }
+                if (grp == 0) {   // dK: undo the rotation at position kp
+                    const float4* c4 = reinterpret_cast<const float4*>(a.rope_cs + static_cast<long long>(kp) * HALF + cc);
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float4 cs = c4[k];
+                        const float x0 = g1[2 * k], y0 = g2[2 * k], x1 = g1[2 * k + 1], y1 = g2[2 * k + 1];
+                        g1[2 * k] = x0 * cs.x + y0 * cs.y;
+                        g2[2 * k] = y0 * cs.x - x0 * cs.y;
+                        g1[2 * k + 1] = x1 * cs.z + y1 * cs.w;
+                        g2[2 * k + 1] = y1 * cs.z - x1 * cs.w;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 32; i += 8) {
+                    uint4 ra, rb;
+                    __nv_bfloat162* ha = reinterpret_cast<__nv_bfloat162*>(&ra);
+                    __nv_bfloat162* hb = reinterpret_cast<__nv_bfloat162*>(&rb);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        ha[j] = __floats2bfloat162_rn(g1[i + 2 * j], g1[i + 2 * j + 1]);
+                        hb[j] = __floats2bfloat162_rn(g2[i + 2 * j], g2[i + 2 * j + 1]);
+                    }
+                    *reinterpret_cast<uint4*>(orow + cc + i) = ra;
+                    *reinterpret_cast<uint4*>(orow + HALF + cc + i) = rb;
+                }
+            }
+        } else {
+#pragma unroll 1
+            for (int c = 0; c < HD / 32; ++c) {
+                float v[32];
+                tc::tmem_ld32(lane_base + col + c * 32, v);    // warp-collective: all lanes
+                if (r < nkeys) {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        float4 x = make_float4(v[i] * mul, v[i + 1] * mul, v[i + 2] * mul, v[i + 3] * mul);
+                        if (sg.dkv_accum) {   // later slices' contributions are already there
+                            const float4 o = *reinterpret_cast<const float4*>(drow + c * 32 + i);
+                            x.x += o.x; x.y += o.y; x.z += o.z; x.w += o.w;
+                        }
+                        *reinterpret_cast<float4*>(drow + c * 32 + i) = x;
+                    }
                 }
             }
         }

@@ -784,9 +784,10 @@ private:
         attn_bwd(a, s);
         dout.release();
         delta.release();
-        rope_qkv_gather_grad(dt_, dq.get<float>(), cs.segs_dev.get<AttnSeg>(), cs.tok_seg.get<int>(),
-                             cs.tok_pos.get<int>(), dqkv.get(), T, H_, Hkv_, hd_, j, m_.rope_theta, s,
-                             /*kv_only=*/tc_bwd && !fused);
+        // (the tcgen05 kernels already wrote un-rotated bf16 dQ, dK, dV into dqkv)
+        if (!tc_bwd || fused)
+            rope_qkv_gather_grad(dt_, dq.get<float>(), cs.segs_dev.get<AttnSeg>(), cs.tok_seg.get<int>(),
+                                 cs.tok_pos.get<int>(), dqkv.get(), T, H_, Hkv_, hd_, j, m_.rope_theta, s);
         dq.release();
         gemm(mk(T, D_, Nqkv_, dqkv.get(), Nqkv_, true, work(P.wqkv), D_, false, dxn.get(), D_), s);
         norm_apply(dt_, llama_, x, work(P.ln1_w), P.ln1_b >= 0 ? work(P.ln1_b) : nullptr,
