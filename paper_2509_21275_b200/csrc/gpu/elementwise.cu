@@ -522,18 +522,17 @@ __global__ void rope_scatter_k(const T* qkv, T* q_out, const AttnSeg* segs, cons
 template <typename T>
 __global__ void rope_gather_grad_k(const float* dq, const AttnSeg* segs, const int* tok_seg,
                                    const int* tok_pos, const float2* cs, T* dqkv, int Tn, int H,
-                                   int Hkv, int hd, int layer, int slot0) {
+                                   int Hkv, int hd, int layer) {
     pdl_wait();
     pdl_trigger();
     const int half = hd / 2;
     const int per_slot = half / 8;
     const int slots = H + 2 * Hkv;
-    const int nslot = slots - slot0;      // slot0 = H: q already written by the dQ kernel
     const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= static_cast<long long>(Tn) * nslot * per_slot) return;
+    if (idx >= static_cast<long long>(Tn) * slots * per_slot) return;
     const int j = static_cast<int>(idx % per_slot) * 8;
-    const int slot = slot0 + static_cast<int>((idx / per_slot) % nslot);
-    const long long t = idx / (static_cast<long long>(per_slot) * nslot);
+    const int slot = static_cast<int>((idx / per_slot) % slots);
+    const long long t = idx / (static_cast<long long>(per_slot) * slots);
     const int pos = tok_pos[t];
     const float* src;
     if (slot < H) {
@@ -984,17 +983,16 @@ void rope_qkv_scatter(DType t, const void* qkv, void* q_out, const AttnSeg* segs
 
 void rope_qkv_gather_grad(DType t, const float* dq, const AttnSeg* segs_dev, const int* tok_seg,
                           const int* tok_pos, void* dqkv, int T, int H, int Hkv, int hd, int layer,
-                          float theta, cudaStream_t s, bool kv_only) {
-    const int slot0 = kv_only ? H : 0;
-    ProfScope prof_(kProfRope, double(T) * (H + 2 * Hkv - slot0) * hd * (4 + dtype_size(t)), s);
+                          float theta, cudaStream_t s) {
+    ProfScope prof_(kProfRope, double(T) * (H + 2 * Hkv) * hd * (4 + dtype_size(t)), s);
     if (T == 0) return;
     const float2* cs = rope_table(0, hd, theta, s);
-    const long long n = static_cast<long long>(T) * (H + 2 * Hkv - slot0) * (hd / 16);
+    const long long n = static_cast<long long>(T) * (H + 2 * Hkv) * (hd / 16);
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
         launch_k(rope_gather_grad_k<E>, grid_for(n, 256), 256, 0, s, dq, segs_dev, tok_seg, tok_pos, cs,
                                                                static_cast<E*>(dqkv), T, H, Hkv,
-                                                               hd, layer, slot0);
+                                                               hd, layer);
     });
     EPP_CHECK_LAUNCH();
 }

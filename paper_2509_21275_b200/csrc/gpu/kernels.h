@@ -182,7 +182,7 @@ void rope_qkv_scatter(DType t, const void* qkv, void* q_out, const AttnSeg* segs
 // un-rotating dq/dk.
 void rope_qkv_gather_grad(DType t, const float* dq, const AttnSeg* segs_dev, const int* tok_seg,
                           const int* tok_pos, void* dqkv, int T, int H, int Hkv, int hd,
-                          int layer, float theta, cudaStream_t s, bool kv_only = false);
+                          int layer, float theta, cudaStream_t s);
 
 // act: 0 = GELU(tanh), 1 = SwiGLU (input [T,2F] gate|up -> [T,F])
 void act_fwd(DType t, int act, const void* h, void* a, int T, int F, cudaStream_t s);
