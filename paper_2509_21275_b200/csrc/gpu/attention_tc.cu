@@ -503,12 +503,13 @@ constexpr int TB = 64;    // secondary tile (keys in dq, queries in dkv)
 constexpr int kDqStages = 7;    // K/V ring depth of the dq kernel
 constexpr int kDkvStages = 4;   // Q/dO ring depth of the dk/dv kernel
 
-// dS for one 64-key tile of a query row: dS = 2^(s*c2 - lse) * (dP - delta).
-// MASK: keys k > lim are invisible (causal diagonal / ragged block).
+// Two phases of dS for one 64-key tile of a query row, so the exponentials
+// run while the dP MMA is still in flight: dq_p_tile turns the scores into
+// P = 2^(s*c2 - lse) in place (MASK: keys k > lim are invisible, P = 0),
+// dq_ds_tile forms dS = P * (dP - delta) as bf16 pairs.
 template <bool MASK>
-__device__ __forceinline__ void dq_row_tile(const float (&s)[TB / 32][32], const float (&dp)[TB / 32][32],
-                                            float c2, float lse, float dlt, int lim0, uint32_t (&pk)[32]) {
-    const uint64_t c2x = f2pack(c2, c2), nl = f2pack(-lse, -lse), dl = f2pack(dlt, dlt);
+__device__ __forceinline__ void dq_p_tile(float (&s)[TB / 32][32], float c2, float lse, int lim0) {
+    const uint64_t c2x = f2pack(c2, c2), nl = f2pack(-lse, -lse);
 #pragma unroll
     for (int c = 0; c < TB / 32; ++c) {
 #pragma unroll
@@ -523,13 +524,25 @@ __device__ __forceinline__ void dq_row_tile(const float (&s)[TB / 32][32], const
                 p0 = ex2(x0);
                 p1 = ex2(x1);
             }
-            float d0, d1;
-            f2unpack(fmul2(f2pack(p0, p1), fsub2(f2pack(dp[c][i], dp[c][i + 1]), dl)), d0, d1);
             if (MASK) {
                 const int lim = lim0 - c * 32;
-                d0 = i <= lim ? d0 : 0.f;
-                d1 = i + 1 <= lim ? d1 : 0.f;
+                p0 = i <= lim ? p0 : 0.f;
+                p1 = i + 1 <= lim ? p1 : 0.f;
             }
+            s[c][i] = p0;
+            s[c][i + 1] = p1;
+        }
+    }
+}
+__device__ __forceinline__ void dq_ds_tile(const float (&p)[TB / 32][32], const float (&dp)[TB / 32][32],
+                                           float dlt, uint32_t (&pk)[32]) {
+    const uint64_t dl = f2pack(dlt, dlt);
+#pragma unroll
+    for (int c = 0; c < TB / 32; ++c) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+            float d0, d1;
+            f2unpack(fmul2(f2pack(p[c][i], p[c][i + 1]), fsub2(f2pack(dp[c][i], dp[c][i + 1]), dl)), d0, d1);
             pk[c * 16 + (i >> 1)] = bf2(d0, d1);
         }
     }
@@ -566,7 +579,8 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
     uint64_t* p_full = s_full + 2;                    // [2]
     uint64_t* acc_full = p_full + 2;                  // all MMAs retired (epilogue)
     uint64_t* d_full = acc_full + 1;                  // per-row delta in shared memory
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + 1);
+    uint64_t* dp_full = d_full + 1;                   // [2] dP of the step (s_full: S)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dp_full + 2);
 
     const AttnWork w = a.qwork128[EPP_WORK_INDEX];
     const AttnSeg sg = a.segs[w.seg];
@@ -588,6 +602,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
         }
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&s_full[b], 1);
+            tc::mbar_init(&dp_full[b], 1);
             tc::mbar_init(&p_full[b], TQ);
         }
         tc::mbar_init(acc_full, 1);
@@ -647,12 +662,16 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
             const uint32_t sK = (sbase + L::kK + st * L::kSmall);
             const uint32_t sV = (sbase + L::kV + st * L::kSmall);
             const uint64_t dk = tc::smem_desc(sK, 16, 1024), dv = tc::smem_desc(sV, 16, 1024);
+            // S first, committed on its own: the softmax group starts its
+            // exponentials while dP is still on the tensor core
 #pragma unroll
-            for (int cb = 0; cb < HD / 64; ++cb) {   // 64 hd per block: A +32 TMEM columns, B +8 KB
+            for (int cb = 0; cb < HD / 64; ++cb)   // 64 hd per block: A +32 TMEM columns, B +8 KB
                 tc::mma4_ts<8, 2>(tmem_u + kColS + b * TB, tmem_u + kColQin + cb * 32, dk + cb * 512, idS, cb != 0);
-                tc::mma4_ts<8, 2>(tmem_u + kColP + b * TB, tmem_u + kColOin + cb * 32, dv + cb * 512, idS, cb != 0);
-            }
             tc::commit_w(&s_full[b]);
+#pragma unroll
+            for (int cb = 0; cb < HD / 64; ++cb)
+                tc::mma4_ts<8, 2>(tmem_u + kColP + b * TB, tmem_u + kColOin + cb * 32, dv + cb * 512, idS, cb != 0);
+            tc::commit_w(&dp_full[b]);
         };
         // one step of lookahead: the scores of step j+1 run on the
         // tensor core while the softmax group of step j works
@@ -730,23 +749,20 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
             uint32_t pk[32];
             float sall[TB / 32][32], pall[TB / 32][32];
 #pragma unroll
-            for (int c = 0; c < TB / 32; ++c) {
-                tc::tmem_ld32_async(lane_base + kColS + b * TB + c * 32, sall[c]);
-                tc::tmem_ld32_async(lane_base + kColP + b * TB + c * 32, pall[c]);
-            }
+            for (int c = 0; c < TB / 32; ++c) tc::tmem_ld32_async(lane_base + kColS + b * TB + c * 32, sall[c]);
             tc::tmem_wait_ld();
 #pragma unroll
-            for (int c = 0; c < TB / 32; ++c) {
-                tc::reg_fence(sall[c]);
-                tc::reg_fence(pall[c]);
-            }
-#ifdef EPP_BWD_FAKE_SOFTMAX   // pipeline-bound experiment (wrong results)
+            for (int c = 0; c < TB / 32; ++c) tc::reg_fence(sall[c]);
+            if (need_mask) dq_p_tile<true>(sall, c2, lse, qp - key0);
+            else dq_p_tile<false>(sall, c2, lse, 0);
+            tc::mbar_wait(&dp_full[b], (j >> 1) & 1);
+            tc::fence_after();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) pk[i] = __float_as_uint(sall[i >> 4][(i & 15) * 2] + pall[i >> 4][(i & 15) * 2]);
-#else
-            if (need_mask) dq_row_tile<true>(sall, pall, c2, lse, dlt, qp - key0, pk);
-            else dq_row_tile<false>(sall, pall, c2, lse, dlt, 0, pk);
-#endif
+            for (int c = 0; c < TB / 32; ++c) tc::tmem_ld32_async(lane_base + kColP + b * TB + c * 32, pall[c]);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < TB / 32; ++c) tc::reg_fence(pall[c]);
+            dq_ds_tile(sall, pall, dlt, pk);
             // dS (bf16 pairs) over the first 32 columns of S buffer b: the A
             // operand of the dQ MMA
             tc::tmem_st32u(lane_base + kColS + b * TB, pk);
@@ -820,13 +836,14 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
     }
 }
 
-// P^T and dS^T for one 64-query tile of a key row.  The scores arrive with
+// P^T and dS^T for one 64-query tile of a key row, in two phases (the
+// exponentials run while the dP^T MMA is in flight).  The scores arrive with
 // lse and delta already subtracted (augmented K-step, see attn_bwd_dkv_tc):
-// P^T = 2^(S'^T c2), dS^T = P^T * dP'^T.  MASK: query qi is visible iff
-// qmin <= qi < qmax.
+// P^T = 2^(S'^T c2) (in place, MASK: query qi is visible iff qmin <= qi <
+// qmax), then dS^T = P^T * dP'^T.
 template <bool MASK>
-__device__ __forceinline__ void dkv_row_tile(const float (&s)[TB / 32][32], const float (&dp)[TB / 32][32],
-                                             float c2, int qmin, int qmax, uint32_t (&pk)[32], uint32_t (&dk)[32]) {
+__device__ __forceinline__ void dkv_p_tile(float (&s)[TB / 32][32], float c2, int qmin, int qmax,
+                                           uint32_t (&pk)[32]) {
     const uint64_t c2x = f2pack(c2, c2);
 #pragma unroll
     for (int c = 0; c < TB / 32; ++c) {
@@ -847,9 +864,20 @@ __device__ __forceinline__ void dkv_row_tile(const float (&s)[TB / 32][32], cons
                 p0 = (q >= qmin && q < qmax) ? p0 : 0.f;
                 p1 = (q + 1 >= qmin && q + 1 < qmax) ? p1 : 0.f;
             }
-            float d0, d1;
-            f2unpack(fmul2(f2pack(p0, p1), f2pack(dp[c][i], dp[c][i + 1])), d0, d1);
+            s[c][i] = p0;
+            s[c][i + 1] = p1;
             pk[c * 16 + (i >> 1)] = bf2(p0, p1);
+        }
+    }
+}
+__device__ __forceinline__ void dkv_ds_tile(const float (&p)[TB / 32][32], const float (&dp)[TB / 32][32],
+                                            uint32_t (&dk)[32]) {
+#pragma unroll
+    for (int c = 0; c < TB / 32; ++c) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+            float d0, d1;
+            f2unpack(fmul2(f2pack(p[c][i], p[c][i + 1]), f2pack(dp[c][i], dp[c][i + 1])), d0, d1);
             dk[c * 16 + (i >> 1)] = bf2(d0, d1);
         }
     }
@@ -938,7 +966,9 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
     uint64_t* acc_full = p_full + 2;                  // all MMAs retired (epilogue)
     uint64_t* dq_full = acc_full + 1;                 // [2] FUSED: dQ^T of the step done
     uint64_t* dq_free = dq_full + 2;                  // [2] FUSED: dQ^T drained
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_free + 2);
+    uint64_t* dp_full = dq_free + 2;                  // [2] dP^T of the step (s_full: S^T)
+    uint64_t* pt_full = dp_full + 2;                  // [2] P^T in TMEM (p_full: dS^T)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pt_full + 2);
 
     const AttnWork w = a.kwork128[EPP_WORK_INDEX];
     const AttnSeg sg = a.segs[w.seg];
@@ -967,6 +997,8 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&dq_full[b], 1);
             tc::mbar_init(&dq_free[b], TQ);
+            tc::mbar_init(&dp_full[b], 1);
+            tc::mbar_init(&pt_full[b], TQ);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -1061,12 +1093,14 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
         constexpr uint32_t kColDs = FUSED ? kColS + TB / 2 : kColP;
         auto grad = [&](int it) {   // dV += P^T dO ; dK += dS^T Q  (P^T, dS^T from TMEM)
             const int b = it & 1, st = it % kDkvStages;
-            tc::mbar_wait(&p_full[b], (it >> 1) & 1);
+            tc::mbar_wait(&pt_full[b], (it >> 1) & 1);   // P^T is published before dS^T
             tc::fence_after();
             const uint32_t sQ = (sbase + L::kQ + st * L::kSmall);
             const uint32_t sO = (sbase + L::kO + st * L::kSmall);
             tc::mma4_ts<8, 128>(tmem_u + kColV, tmem_u + kColS + b * TB, tc::smem_desc(sO, TB * 128, 1024), idD,
                                 it != 0);
+            tc::mbar_wait(&p_full[b], (it >> 1) & 1);
+            tc::fence_after();
             tc::mma4_ts<8, 128>(tmem_u + kColK, tmem_u + kColDs + b * TB, tc::smem_desc(sQ, TB * 128, 1024), idD,
                                 it != 0);
             tc::commit_w(&qd_empty[st]);
@@ -1098,6 +1132,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
                 tc::mma4_ss<2, 2>(tmem_u + kColS + b * TB, dK + cb * 1024, dq + cb * 512, idS, cb != 0);
             tc::mma_bf16_w(tmem_u + kColS + b * TB, smem_desc_sw32(sKa),
                          smem_desc_sw32((sbase + L::kQa + st * TB * 32)), idS, 1);
+            tc::commit_w(&s_full[b]);   // S^T on its own: the exponentials overlap the dP^T MMA
             if (FUSED && it >= 2) {   // the dP^T buffer held dQ^T of step it-2
                 tc::mbar_wait(&dq_free[b], ((it - 2) >> 1) & 1);
                 tc::fence_after();
@@ -1107,7 +1142,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
                 tc::mma4_ss<2, 2>(tmem_u + kColP + b * TB, dV + cb * 1024, dO + cb * 512, idS, cb != 0);
             tc::mma_bf16_w(tmem_u + kColP + b * TB, smem_desc_sw32(sVa),
                          smem_desc_sw32((sbase + L::kOa + st * TB * 32)), idS, 1);
-            tc::commit_w(&s_full[b]);
+            tc::commit_w(&dp_full[b]);
         };
         tc::mbar_wait(kv_full, 0);
         scores(0);
@@ -1135,31 +1170,29 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
             uint32_t pk[32], dk[32];
             float sall[TB / 32][32], dall[TB / 32][32];
 #pragma unroll
-            for (int c = 0; c < TB / 32; ++c) {
-                tc::tmem_ld32_async(lane_base + kColS + b * TB + c * 32, sall[c]);
-                tc::tmem_ld32_async(lane_base + kColP + b * TB + c * 32, dall[c]);
-            }
+            for (int c = 0; c < TB / 32; ++c) tc::tmem_ld32_async(lane_base + kColS + b * TB + c * 32, sall[c]);
             tc::tmem_wait_ld();
 #pragma unroll
-            for (int c = 0; c < TB / 32; ++c) {
-                tc::reg_fence(sall[c]);
-                tc::reg_fence(dall[c]);
-            }
+            for (int c = 0; c < TB / 32; ++c) tc::reg_fence(sall[c]);
             // query qi visible to key kp iff kp - first_q <= qi < rows
-#ifdef EPP_BWD_FAKE_SOFTMAX
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                pk[i] = __float_as_uint(sall[i >> 4][(i & 15) * 2]);
-                dk[i] = __float_as_uint(dall[i >> 4][(i & 15) * 2]);
-            }
-#else
-            if (need_mask) dkv_row_tile<true>(sall, dall, c2, kp - first_q, rows, pk, dk);
-            else dkv_row_tile<false>(sall, dall, c2, 0, TB, pk, dk);
-#endif
-            // P^T / dS^T (bf16 pairs) over the first 32 columns of the S^T /
-            // dP^T buffers (FUSED: both halves of the S^T buffer): the A
-            // operands of the dV / dK MMAs
+            if (need_mask) dkv_p_tile<true>(sall, c2, kp - first_q, rows, pk);
+            else dkv_p_tile<false>(sall, c2, 0, TB, pk);
+            // P^T (bf16 pairs) over the first 32 columns of the S^T buffer: the
+            // A operand of the dV MMA, published before dS^T exists
             tc::tmem_st32u(lane_base + kColS + b * TB, pk);
+            tc::tmem_wait_st();
+            tc::fence_before();
+            tc::mbar_arrive(&pt_full[b]);
+            tc::mbar_wait(&dp_full[b], (it >> 1) & 1);
+            tc::fence_after();
+#pragma unroll
+            for (int c = 0; c < TB / 32; ++c) tc::tmem_ld32_async(lane_base + kColP + b * TB + c * 32, dall[c]);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < TB / 32; ++c) tc::reg_fence(dall[c]);
+            dkv_ds_tile(sall, dall, dk);
+            // dS^T (bf16 pairs) over the first 32 columns of the dP^T buffer
+            // (FUSED: the second half of the S^T buffer): the dK MMA's A operand
             tc::tmem_st32u(lane_base + (FUSED ? kColS + TB / 2 : kColP) + b * TB, dk);
             if constexpr (FUSED) {
                 // dS^T row r (64 queries = 128 B) into the 128B-swizzled tile
