@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(128) norm_fwd_row_k(bool rms, const bf16* x, c
 template <int NPT>
 __global__ void __launch_bounds__(128) norm_bwd_dx_row_k(bool rms, const bf16* x, const bf16* w, const bf16* dy,
                                                          const float* mean, const float* rstd, const bf16* dres,
-                                                         bf16* dx) {
+                                                         bf16* dx, const bf16* bias, bf16* xn_out) {
     pdl_wait();
     pdl_trigger();
     constexpr int D = 1024 * NPT;
@@ -310,6 +310,13 @@ __global__ void __launch_bounds__(128) norm_bwd_dx_row_k(bool rms, const bf16* x
 #pragma unroll
         for (int i = 0; i < 8; ++i) out[i] = rv[i] + rs * (gv[i] * wv[i] - m1 - (xv[i] - mu) * rs * m2);
         store8(dx + off + c, out);
+        if (xn_out) {   // y = norm(x) from the registers already holding x
+            float bv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (bias) load8(bias + c, bv);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) out[i] = (xv[i] - mu) * rs * wv[i] + bv[i];
+            store8(xn_out + off + c, out);
+        }
     }
 }
 
@@ -919,8 +926,8 @@ void norm_apply(DType t, bool rms, const void* x, const void* w, const void* b, 
 
 void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy, const float* mean,
               const float* rstd, const void* dres, void* dx, float* dw, float* db, int T, int D,
-              cudaStream_t s) {
-    ProfScope prof_(kProfNormBwd, double(T) * D * 6 * dtype_size(t), s);
+              cudaStream_t s, const void* bias, void* xn_out) {
+    ProfScope prof_(kProfNormBwd, double(T) * D * (xn_out ? 7 : 6) * dtype_size(t), s);
     EPP_REQUIRE(D % 8 == 0 && D <= 8 * 256 * kNormMaxG, "norm_bwd: unsupported D");
     if (T == 0) return;
     // ~4 waves of 148 SMs for the partial-sum kernel (256 columns per CTA)
@@ -939,7 +946,8 @@ void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy, c
                 constexpr int NPT = decltype(npt)::value;
                 launch_k(norm_bwd_dx_row_k<NPT>, T, 128, 0, s, rms, static_cast<const bf16*>(x), static_cast<const bf16*>(w),
                                                          static_cast<const bf16*>(dy), mean, rstd,
-                                                         static_cast<const bf16*>(dres), static_cast<bf16*>(dx));
+                                                         static_cast<const bf16*>(dres), static_cast<bf16*>(dx),
+                                                         static_cast<const bf16*>(bias), static_cast<bf16*>(xn_out));
                 done = true;
             };
             if (D == 1024) row_kernel(std::integral_constant<int, 1>{});
@@ -947,6 +955,7 @@ void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy, c
             else if (D == 4096) row_kernel(std::integral_constant<int, 4>{});
             else if (D == 8192) row_kernel(std::integral_constant<int, 8>{});
         }
+        if (!done && xn_out) norm_apply(t, rms, x, w, bias, mean, rstd, xn_out, T, D, s);
         if (!done)
             launch_k(norm_bwd_dx_k<E>, ceil_div(static_cast<long long>(T) * 32, 256), 256, 0, s, 
                 rms, static_cast<const E*>(x), static_cast<const E*>(w), static_cast<const E*>(dy), mean,

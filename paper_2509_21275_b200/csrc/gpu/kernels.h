@@ -161,10 +161,12 @@ void embed_bwd(DType t, const int32_t* ids, const void* dout, float* dtable, int
 // LayerNorm (has_bias, rms=false) or RMSNorm (rms=true): y = norm(x)*w (+b)
 void norm_fwd(DType t, bool rms, const void* x, const void* w, const void* b, void* y,
               float* mean, float* rstd, int T, int D, float eps, cudaStream_t s);
-// dx = dres + norm_bwd(dy);  dw/db accumulated (fp32) via per-block partials
+// dx = dres + norm_bwd(dy);  dw/db accumulated (fp32) via per-block partials.
+// xn_out (optional): also re-create y = norm(x)*w (+bias) from the saved stats
+// in the same pass over x (the weight-gradient GEMM's operand).
 void norm_bwd(DType t, bool rms, const void* x, const void* w, const void* dy,
               const float* mean, const float* rstd, const void* dres, void* dx, float* dw,
-              float* db, int T, int D, cudaStream_t s);
+              float* db, int T, int D, cudaStream_t s, const void* bias = nullptr, void* xn_out = nullptr);
 // Recompute y = norm(x) from saved stats.
 void norm_apply(DType t, bool rms, const void* x, const void* w, const void* b,
                 const float* mean, const float* rstd, void* y, int T, int D, cudaStream_t s);

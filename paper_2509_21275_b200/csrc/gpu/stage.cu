@@ -739,15 +739,16 @@ private:
         }
         Buf dxn(&pool_, static_cast<size_t>(T) * D_ * e, s);
         gemm(mk(T, D_, F1_, dh.get(), F1_, true, work(P.w1), D_, false, dxn.get(), D_), s);  // dXn2
+        // norm backward also re-creates xn = norm(x_mid) (one pass over x_mid)
+        // for the dW1 weight gradient
         Buf xn(&pool_, static_cast<size_t>(T) * D_ * e, s);
-        norm_apply(dt_, llama_, L.x_mid.get(), work(P.ln2_w), P.ln2_b >= 0 ? work(P.ln2_b) : nullptr,
-                   llama_ ? nullptr : L.mean2.get<float>(), L.rstd2.get<float>(), xn.get(), T, D_, s);
-        wgrad(F1_, D_, T, dh.get(), F1_, xn.get(), D_, grad(P.w1), s);                     // dW1
-        dh.release();
         Buf dxm(&pool_, static_cast<size_t>(T) * D_ * e, s);
         norm_bwd(dt_, llama_, L.x_mid.get(), work(P.ln2_w), dxn.get(),
                  llama_ ? nullptr : L.mean2.get<float>(), L.rstd2.get<float>(), dy, dxm.get(),
-                 grad(P.ln2_w), P.ln2_b >= 0 ? grad(P.ln2_b) : nullptr, T, D_, s);
+                 grad(P.ln2_w), P.ln2_b >= 0 ? grad(P.ln2_b) : nullptr, T, D_, s,
+                 P.ln2_b >= 0 ? work(P.ln2_b) : nullptr, xn.get());
+        wgrad(F1_, D_, T, dh.get(), F1_, xn.get(), D_, grad(P.w1), s);                     // dW1
+        dh.release();
         // ---- attention ----
         Buf dout(&pool_, static_cast<size_t>(T) * Dq * e, s);
         gemm(mk(T, Dq, D_, dxm.get(), D_, true, work(P.wo), Dq, false, dout.get(), Dq), s);  // dO
@@ -790,14 +791,13 @@ private:
                                  cs.tok_pos.get<int>(), dqkv.get(), T, H_, Hkv_, hd_, j, m_.rope_theta, s);
         dq.release();
         gemm(mk(T, D_, Nqkv_, dqkv.get(), Nqkv_, true, work(P.wqkv), D_, false, dxn.get(), D_), s);
-        norm_apply(dt_, llama_, x, work(P.ln1_w), P.ln1_b >= 0 ? work(P.ln1_b) : nullptr,
-                   llama_ ? nullptr : L.mean1.get<float>(), L.rstd1.get<float>(), xn.get(), T, D_, s);
+        norm_bwd(dt_, llama_, x, work(P.ln1_w), dxn.get(), llama_ ? nullptr : L.mean1.get<float>(),
+                 L.rstd1.get<float>(), dxm.get(), dx, grad(P.ln1_w),
+                 P.ln1_b >= 0 ? grad(P.ln1_b) : nullptr, T, D_, s,
+                 P.ln1_b >= 0 ? work(P.ln1_b) : nullptr, xn.get());
         wgrad(Nqkv_, D_, T, dqkv.get(), Nqkv_, xn.get(), D_, grad(P.wqkv), s);
         dqkv.release();
         xn.release();
-        norm_bwd(dt_, llama_, x, work(P.ln1_w), dxn.get(), llama_ ? nullptr : L.mean1.get<float>(),
-                 L.rstd1.get<float>(), dxm.get(), dx, grad(P.ln1_w),
-                 P.ln1_b >= 0 ? grad(P.ln1_b) : nullptr, T, D_, s);
     }
 
     // Last stage: final norm, LM head, cross-entropy and its backward through
