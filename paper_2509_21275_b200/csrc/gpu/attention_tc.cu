@@ -1110,10 +1110,8 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
                 constexpr uint32_t idQ = tc::instr_desc_mn(HD, TB, true, true);
                 const uint64_t aK = tc::smem_desc(sK, 128 * 128, 1024);
                 const uint64_t bS = tc::smem_desc(sbase + L::kDS + b * (128 * TB * 2), 128 * 128, 1024);
-#ifndef EPP_FUSED_NO_DQ
                 tc::mma4_ss<128, 128>(tmem_u + kColP + b * TB, aK, bS, idQ, 0);
                 tc::mma4_ss<128, 128>(tmem_u + kColP + b * TB, aK + 4 * 128, bS + 4 * 128, idQ, 1);
-#endif
                 tc::commit_w(&dq_full[b]);
             }
         };
