@@ -2,28 +2,36 @@
 """EPP training-step benchmark on B200 (BASELINE.json metric: training
 tokens/s + MFU, skewed-length GPT EPP at 1/2/4/8 B200).
 
-A step = one global batch of skewed-length sequences (github_like lengths,
-seeded uniform tokens, random-init weights), planned by the C++ planner
-(sequence processor + elastic 1F1B + checkpoint MILP), executed by the CUDA
-stage executors (d_p = number of GPUs, one stage per GPU), followed by the
-AdamW step.  Weak scaling: the batch holds `--seqs-per-gpu` x N sequences.
+Default workload = configs[2]: GPT-7B shape, github_like lengths capped at
+16K, 64 sequences per GPU per step (512 at 8 GPUs), d_p = N
+pipeline stages, elastic schedule + chunk-level adaptive checkpointing (at
+N=1 the 7B model's optimizer state leaves ~60 GB for activations, so the
+checkpoint ladder is active).  A step = one global batch, planned by the C++
+planner, executed by the CUDA stage executors, followed by AdamW.
 
-  value : tokens/s with the step's token ids already resident in HBM and the
-          plans pre-solved (paper: plans are pre-solved on the host,
-          PAPER.md:712-715), timed with CUDA events, max over ranks.
-  e2e   : same metric through the public API from host buffers — planning of
-          batch i+1 runs on a host thread during step i, token ids are copied
-          from pinned host memory each step, the loss is read back each step.
+  value : tokens/s with the step's token ids resident in HBM and the plans
+          pre-solved, CUDA events, max over ranks.  No
+          per-launch instrumentation in this pass.
+  e2e   : same metric through the public API from host buffers: batch i+1 is
+          planned on a host thread during step i, token ids are copied from
+          pinned host memory every step, every step's loss is read back.
+  kernel_classes / roofline : a separate instrumented pass over the first
+          timed batches (CUDA events around every launch on its stream).
+  cpu_baseline : the reference planner (oracle/_ref) + fp32 CPU numerics on
+          the host cores (rank 0).
 
-`--impl reference` times the reference's own CPU path on the host cores:
-the compiled reference planner (oracle/_ref) on the step's batch plus the
-fp32 CPU numerics of the same model on a bounded token sample.
+Both arms plan with the same SystemConfig (bench_config): the committed Eq. 1
+fit profiles/cost_<model>.json (bench.py --save-cost refreshes it) and
+mem_capacity = model.B200_MEM_CAPACITY.  The warmup step is still timed per
+stage op and refitted (closed loop, §8f.1); --replan plans the timed batches
+with that fresh fit instead.
+
+`--impl reference` times the reference's own CPU path on the host cores.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -35,8 +43,11 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
+
+METRIC = "training tokens/s + MFU, skewed-length GPT EPP at 1/2/4/8 B200"
+DATA = "synthetic (seeded github_like lengths, uniform tokens, random-init weights)"
+REF_SO = ROOT / "oracle" / "_ref" / "libepp_ref.so"
 
 
 def parse():
@@ -45,21 +56,26 @@ def parse():
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--model", default="gpt-1.3b")
+    ap.add_argument("--model", default="gpt-7b")
     ap.add_argument("--seqs-per-gpu", type=int, default=64)
-    ap.add_argument("--cap", type=int, default=32768)
+    ap.add_argument("--cap", type=int, default=16384)
     ap.add_argument("--preset", default="github_like")
     ap.add_argument("--slices", type=int, default=0, help="fixed slice count N (0 = planner auto-N)")
     ap.add_argument("--pp", type=int, default=0,
                     help="pipeline degree d_p (default: --gpus); --gpus / d_p data-parallel replicas")
-    ap.add_argument("--no-calibrate", action="store_true",
-                    help="keep the analytic Eq. 1 coefficients (default: fit them on warmup step 0)")
+    ap.add_argument("--cost", default="auto",
+                    help="Eq. 1 coefficients: 'auto' (profiles/cost_<model>.json if present, else analytic), "
+                         "'analytic', or a JSON path")
+    ap.add_argument("--replan", action="store_true",
+                    help="plan the timed batches with the fit of the last warmup step (closed loop)")
+    ap.add_argument("--save-cost", default="", help="write the warmup fit to this path")
     ap.add_argument("--uniform-min", type=int, default=1, help="preset=uniform: shortest length")
     ap.add_argument("--uniform-max", type=int, default=0, help="preset=uniform: longest length")
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample-tokens", type=int, default=256)
+    ap.add_argument("--prof-steps", type=int, default=2, help="batches re-run in the instrumented pass")
+    ap.add_argument("--cpu-sample-tokens", type=int, default=1024)
     return ap.parse_args()
 
 
@@ -132,16 +148,53 @@ def step_flops(m, plan):
     return total
 
 
-def make_batches(args, n_batches, world, vocab, replica=0):
-    """Synthetic batches of `seqs_per_gpu * world` sequences (world = the
-    pipeline's GPUs); data-parallel replicas draw from disjoint seeds."""
-    from paper_2509_21275_b200 import planner, schedule
+def bench_config(args, m, dp):
+    """(SystemConfig, stage layer counts, cost source): identical in both arms
+    (pure Python; loads no native library)."""
+    from paper_2509_21275_b200 import model as M
+    from paper_2509_21275_b200.executor import balanced_stage_counts
+    counts = balanced_stage_counts(m.layers, dp, M.head_layer_equivalents(m))
+    src, cost = "analytic (model.default_cost)", M.default_cost(m)
+    path = ROOT / "profiles" / f"cost_{args.model}.json" if args.cost == "auto" else Path(args.cost)
+    if args.cost != "analytic" and path.exists():
+        cost = json.loads(path.read_text())["cost"]
+        src = f"{path.relative_to(ROOT) if path.is_relative_to(ROOT) else path} (Eq. 1 fit of GPU stage timings)"
+    cfg = M.planner_config(m, dp, mem_capacity=M.B200_MEM_CAPACITY, cost=cost, stage_counts=counts,
+                           max_seq_len=args.cap)
+    return cfg, counts, src
+
+
+def make_lengths(args, n_batches, world, replica=0, _lib=None):
+    from paper_2509_21275_b200 import planner
     out = []
     for i in range(n_batches):
         seed = 1000 + i + 100003 * replica
-        lengths = planner.generate_workload(args.preset, args.seqs_per_gpu * world, seed, args.cap,
-                                            args.uniform_min, args.uniform_max)
-        out.append((lengths, schedule.synthetic_tokens(lengths, vocab, seed=seed)))
+        out.append((seed, planner.generate_workload(args.preset, args.seqs_per_gpu * world, seed, args.cap,
+                                                    args.uniform_min, args.uniform_max, _lib=_lib)))
+    return out
+
+
+def make_batches(args, n_batches, world, vocab, replica=0):
+    """Synthetic batches of `seqs_per_gpu * world` sequences (world = the
+    pipeline's GPUs); data-parallel replicas draw from disjoint seeds."""
+    from paper_2509_21275_b200 import schedule
+    return [(lengths, schedule.synthetic_tokens(lengths, vocab, seed=seed))
+            for seed, lengths in make_lengths(args, n_batches, world, replica)]
+
+
+PROF_CLASSES = ((0, "gemm"), (1, "attn_fwd"), (2, "attn_bwd"), (3, "attn_bwd_dq"), (4, "attn_bwd_dkv"),
+                (5, "norm_fwd"), (6, "norm_bwd"), (7, "rope"), (8, "act"), (9, "cross_entropy"),
+                (10, "adamw"), (11, "embed"), (12, "copy_fill"))
+
+
+def read_profile(lib):
+    import ctypes
+    from paper_2509_21275_b200 import gpu
+    out = {}
+    for cls, name in PROF_CLASSES:
+        a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        gpu.check(lib.epp_gpu_profile_read(cls, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), 1))
+        out[name] = {"ms": a.value, "flops": b.value, "launches": c.value}
     return out
 
 
@@ -150,7 +203,7 @@ def run_ours(args):
 
     from paper_2509_21275_b200 import calibrate, gpu, model as M, planner, schedule
     from paper_2509_21275_b200.executor import (DistributedPipeline, LocalPipeline, _ChunkTokens, allreduce_grads,
-                                                balanced_stage_counts, pipeline_groups, stage_layers)
+                                                pipeline_groups, stage_layers)
 
     world = args.gpus
     rank = int(os.environ.get("RANK", "0"))
@@ -170,10 +223,8 @@ def run_ours(args):
     replica, prank = rank // dp, rank % dp   # data-parallel replica, stage index
     pipes, dp_groups = pipeline_groups(dp, replicas) if world > 1 else ([None], [None])
     free, total_mem = torch.cuda.mem_get_info()
-    # the last stage also runs the LM head: give it fewer layers when that
-    # lowers the bottleneck stage (GPT-1.3B at d_p 8: 4,3,3,3,3,3,3,2)
-    counts = balanced_stage_counts(m.layers, dp, M.head_layer_equivalents(m))
-    cfg = M.planner_config(m, dp, mem_capacity=float(total_mem) - 2e9, cost=M.default_cost(m), stage_counts=counts)
+    assert total_mem >= M.B200_MEM_CAPACITY, "planner capacity exceeds this device"
+    cfg, counts, cost_src = bench_config(args, m, dp)
     jobs = os.cpu_count() or 8
 
     batches = make_batches(args, args.warmup + args.steps, dp, m.vocab, replica)
@@ -188,7 +239,8 @@ def run_ours(args):
     plans, planner_s = plan_all(cfg, 0)
 
     first, num = stage_layers(m.layers, dp, prank, counts)
-    stage = gpu.CudaStage(m, first, num, prank == 0, prank == dp - 1, dtype=args.dtype, device=local)
+    stage = gpu.CudaStage(m, first, num, prank == 0, prank == dp - 1, dtype=args.dtype, device=local,
+                          plan_stage_layers=m.layers // dp)
     stage.init_weights(1234)
     timed_stage = calibrate.TimedStage(stage)
 
@@ -219,13 +271,12 @@ def run_ours(args):
     if os.environ.get("EPP_BENCH_BACKEND", "nccl") == "nccl":   # (ranks own their GPU)
         free_b, _ = torch.cuda.mem_get_info()
         gpu.pool_reserve(free_b - int(6e9))
-    cost_report = {"source": "analytic (model.default_cost)"}
-    cal_step = args.warmup - 1          # calibrate on the last (warm) warmup step
+    cost_report = {"source": cost_src}
+    cal_step = args.warmup - 1          # time the last (warm) warmup step per stage op
     for i in range(args.warmup):
-        if i == cal_step and not args.no_calibrate:
-            # closed loop: time every stage op of the last warmup step, fit
-            # Eq. 1 to it (all ranks' samples, so every rank plans
-            # identically) and re-plan the timed batches with the fit
+        if i == cal_step:
+            # closed loop: fit Eq. 1 to every stage op of this step (all
+            # ranks' samples, so every rank plans identically)
             make_driver(timed_stage).run_step(plans[i], batches[i][1])
             optimizer()
             sync_all()
@@ -236,35 +287,35 @@ def run_ours(args):
                 samples = [x for part in gathered for x in part]
             try:
                 fitted = calibrate.calibrated_config(cfg, samples)
-                cfg_fit = calibrate.planner_config_only(fitted)
-                rest, planner_s = plan_all(cfg_fit, args.warmup)
-                cfg = cfg_fit
-                plans = plans[:args.warmup] + rest
-                cost_report = {"source": f"fitted on warmup step {i} ({fitted['_fit']['samples']} stage-op samples)",
-                               "fwd_residual": fitted["_fit"]["fwd_residual"],
-                               "bwd_residual": fitted["_fit"]["bwd_residual"], "cost": cfg["cost"]}
+                cost_report.update({"warmup_fit": {"samples": fitted["_fit"]["samples"],
+                                                   "fwd_residual": fitted["_fit"]["fwd_residual"],
+                                                   "bwd_residual": fitted["_fit"]["bwd_residual"],
+                                                   "cost": fitted["cost"]}})
+                if args.save_cost and rank == 0:
+                    Path(args.save_cost).write_text(json.dumps(
+                        {"model": args.model, "cap": args.cap, "pp": dp, "fitted_on": f"warmup step {i}",
+                         "fwd_residual": fitted["_fit"]["fwd_residual"],
+                         "bwd_residual": fitted["_fit"]["bwd_residual"], "cost": fitted["cost"]}, indent=1))
+                if args.replan:
+                    cfg = calibrate.planner_config_only(fitted)
+                    rest, planner_s = plan_all(cfg, args.warmup)
+                    plans = plans[:args.warmup] + rest
+                    cost_report["source"] = f"fitted on warmup step {i} (--replan)"
             except planner.Error as e:
-                cost_report = {"source": "analytic (fit failed: %s)" % e}
+                cost_report["warmup_fit"] = f"fit failed: {e}"
             continue
         driver.run_step(plans[i], batches[i][1])
         optimizer()
     sync_all()
     stage.loss(reset=True)
 
-    # ---- device-resident timed region (value) -------------------------------
+    # ---- device-resident timed region (value): no instrumentation ----------
     timed = list(range(args.warmup, args.warmup + args.steps))
     pre = [_ChunkTokens(plans[i], batches[i][1], dev, prank == 0, prank == dp - 1) for i in timed]
     sync_all()
     launches0 = gpu.kernel_launches()
-    lib = gpu.lib()
-    lib.epp_gpu_profile(1)
+    p2p0 = getattr(driver, "p2p_bytes", 0)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    trace = os.environ.get("EPP_BENCH_TRACE")   # diagnostics only: a profiler-perturbed run
-    tracer = None
-    if trace:
-        tracer = torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA,
-                                                    torch.profiler.ProfilerActivity.CPU])
-        tracer.__enter__()
     with ClockSampler(local) as clk:
         sync_all()
         ev0.record()
@@ -273,11 +324,8 @@ def run_ours(args):
             optimizer()
         ev1.record()
         sync_all()
-    if tracer is not None:
-        tracer.__exit__(None, None, None)
-        tracer.export_chrome_trace(trace)
-    lib.epp_gpu_profile(0)
     launches = gpu.kernel_launches() - launches0
+    p2p_bytes = getattr(driver, "p2p_bytes", 0) - p2p0
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -290,76 +338,31 @@ def run_ours(args):
                          dtype=torch.float64)
         dist.all_reduce(t)
         tokens, flops = int(t[0].item()), float(t[1].item())
-    prof = {}
-    classes = ((0, "gemm"), (1, "attn_fwd"), (2, "attn_bwd"), (3, "attn_bwd_dq"), (4, "attn_bwd_dkv"),
-               (5, "norm_fwd"), (6, "norm_bwd"), (7, "rope"), (8, "act"), (9, "cross_entropy"),
-               (10, "adamw"), (11, "embed"), (12, "copy_fill"))
-    for cls, name in classes:
-        a, b, c = (ctypes_double(), ctypes_double(), ctypes_i64())
-        gpu.check(lib.epp_gpu_profile_read(cls, ctypes_ref(a), ctypes_ref(b), ctypes_ref(c), 1))
-        prof[name] = {"ms": a.value, "flops": b.value, "launches": c.value}
     loss_sum, loss_cnt = (stage.loss(reset=True) if prank == dp - 1 else (0.0, 0.0))
+
+    # ---- instrumented pass (kernel classes, roofline): first timed batches --
+    lib = gpu.lib()
+    nprof = max(1, min(args.prof_steps, args.steps))
+    read_profile(lib)                         # drop anything recorded so far
+    sync_all()
+    lib.epp_gpu_profile(1)
+    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pe0.record()
+    for j, i in enumerate(timed[:nprof]):
+        driver.run_step(plans[i], batches[i][1], staged=pre[j])
+        optimizer()
+    pe1.record()
+    sync_all()
+    lib.epp_gpu_profile(0)
+    prof = read_profile(lib)
+    prof_ms = pe0.elapsed_time(pe1)
+    stage.loss(reset=True) if prank == dp - 1 else None
 
     # ---- end-to-end timed region (e2e) ---------------------------------------
     e2e = None
     if not args.no_e2e:
-        # the same batches as the device-timed leg, re-planned on the fly
-        e2e_batches = batches[args.warmup:]
-        ahead = {}
-
-        def solve(k):
-            lengths = e2e_batches[k][0]
-            ahead[k] = schedule.parse_plan(planner.make_plan_document(cfg, lengths, args.slices or None, "main", jobs),
-                                           lengths)
-
-        solve(0)    # batch 0's plan is solved during the (untimed) previous step
-        h2d = d2h = 0
-        # per-step loss: D2H into pinned memory, read one step later (the
-        # host enqueues step k+1 before waiting for step k's loss)
-        loss_host = torch.zeros((len(e2e_batches), 2), dtype=torch.float32).pin_memory()
-        loss_ev = [torch.cuda.Event() for _ in e2e_batches]
-        losses = []
-        sync_all()
-        e0 = time.perf_counter()
-        for k in range(len(e2e_batches)):
-            th = None
-            if k + 1 < len(e2e_batches):
-                th = threading.Thread(target=solve, args=(k + 1,))
-                th.start()
-            st = driver.run_step(ahead.pop(k), e2e_batches[k][1])
-            h2d += st["h2d_bytes"]
-            optimizer()
-            if prank == dp - 1:
-                stage.loss_async(loss_host[k], reset=True)
-                loss_ev[k].record()
-                d2h += 8
-                if k > 0:
-                    loss_ev[k - 1].synchronize()
-                    losses.append(float(loss_host[k - 1, 0] / max(1.0, float(loss_host[k - 1, 1]))))
-            if th:
-                th.join()
-        if prank == dp - 1:
-            loss_ev[-1].synchronize()
-            losses.append(float(loss_host[-1, 0] / max(1.0, float(loss_host[-1, 1]))))
-        sync_all()
-        e_s = time.perf_counter() - e0
-        if world > 1:
-            # slowest rank's wall time; H2D (stage 0) and D2H (last stage)
-            # bytes are counted where they happen and summed over ranks
-            t = torch.tensor([e_s], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_s = float(t.item())
-            b = torch.tensor([float(h2d), float(d2h)], device=dev)
-            dist.all_reduce(b, op=dist.ReduceOp.SUM)
-            h2d, d2h = int(b[0].item()), int(b[1].item())
-        e_tokens = sum(sum(b[0]) for b in e2e_batches)
-        if replicas > 1:
-            t = torch.tensor([float(e_tokens) if prank == 0 else 0.0], device=dev, dtype=torch.float64)
-            dist.all_reduce(t)
-            e_tokens = int(t.item())
-        nb = len(e2e_batches)
-        e2e = {"value": e_tokens / e_s, "unit": "tokens/s", "h2d_bytes_per_step": h2d // nb,
-               "d2h_bytes_per_step": d2h // nb}
+        e2e = run_e2e(args, driver, stage, cfg, batches[args.warmup:], jobs, dev, world, dp, prank, replicas,
+                      optimizer, sync_all, dist)
 
     if rank != 0:
         if world > 1:
@@ -367,24 +370,25 @@ def run_ours(args):
             dist.destroy_process_group()
         return
     hbm, tf_burst, tf_sus, peak_src = peaks()
-    # the planner's simulated makespan of the timed plans vs the measured step
     predicted = sum(calibrate.predicted_seconds(plans[i].doc) for i in timed) / len(timed)
     cost_model = dict(cost_report, predicted_step_s=predicted, measured_step_s=ms / 1e3 / args.steps,
                       measured_over_predicted=(ms / 1e3 / args.steps) / predicted if predicted > 0 else None)
-    # dominant kernel class by device time in the timed region
-    names = {"gemm": "gemm_tc_kernel (tcgen05 BF16 GEMM, fwd/dgrad/wgrad)",
-             "attn_fwd": "attn_fwd (slice-causal flash attention forward)",
-             "attn_bwd": "attn_bwd (delta + dQ + dK/dV kernels)"}
+    names = {"gemm": "gemm_tc2_kernel / gemm_tc_kernel (tcgen05 BF16 GEMM, fwd/dgrad/wgrad)",
+             "attn_fwd": "attn_fwd_tc (slice-causal flash attention forward)",
+             "attn_bwd": "attn_bwd_dq_tc + attn_bwd_dkv_tc (slice-causal flash attention backward)"}
     dom = max(("gemm", "attn_fwd", "attn_bwd"), key=lambda k: prof[k]["ms"])
     g = prof[dom]
     achieved = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
-    traffic = None
+    traffic, traffic_src = None, None
     summ = ROOT / "profiles" / "ncu_summary.json"
     if summ.exists():
-        traffic = json.loads(summ.read_text()).get("dram_bytes_per_launch", {}).get(dom)
+        sj = json.loads(summ.read_text())
+        traffic = sj.get("dram_bytes_per_launch", {}).get(dom)
+        traffic_src = sj.get("source")
     sec = ms / 1e3
+    gemm_flops_class = {k: v for k, v in prof.items()}
     out = {
-        "metric": "training tokens/s + MFU, skewed-length GPT EPP at 1/2/4/8 B200",
+        "metric": METRIC,
         "value": tokens / sec,
         "unit": "tokens/s",
         "n_gpus": world,
@@ -395,13 +399,16 @@ def run_ours(args):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": args.dtype,
-        "data": "synthetic (seeded github_like lengths, uniform tokens, random-init weights)",
+        "data": DATA,
         "config": {"workload": f"{args.model} EPP, {args.preset} lengths cap {args.cap}, "
                                f"{args.seqs_per_gpu} seqs/GPU/step, d_p={dp}",
                    "model": args.model, "global_batch_seqs": args.seqs_per_gpu * world,
                    "tokens_per_step": tokens / args.steps, "seq_len_cap": args.cap,
                    "slices": args.slices or "auto", "stage_layers": counts,
-                   "parallelism": f"pp{dp}" + (f"xdp{replicas}" if replicas > 1 else ""), "l2": "inputs larger than L2 (activations GBs/step)"},
+                   "ckpt_layers_per_step": sum(sum(sum(r) for r in u.ckpt) for i in timed for u in plans[i].units)
+                                           / args.steps,
+                   "parallelism": f"pp{dp}" + (f"xdp{replicas}" if replicas > 1 else ""),
+                   "l2": "inputs larger than L2 (activations GBs/step)"},
         "mfu": flops / (sec * world * tf_burst * 1e12),
         "mfu_vs_sustained": flops / (sec * world * tf_sus * 1e12),
         "model_tflops_per_gpu": flops / sec / world / 1e12,
@@ -412,54 +419,121 @@ def run_ours(args):
         "roofline": {"bound": "tensor", "kernel": names[dom],
                      "achieved": achieved, "peak": tf_sus, "unit": "TFLOP/s",
                      "frac": achieved / tf_sus if tf_sus else None, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
-                     "share_of_step": g["ms"] / ms if ms else None},
-        "kernel_classes": {k: {"ms_per_step": v["ms"] / args.steps,
+                     "share_of_step": g["ms"] / prof_ms if prof_ms else None,
+                     "timed_in": f"instrumented pass over {nprof} of the timed batches"},
+        "kernel_classes": {k: {"ms_per_step": v["ms"] / nprof,
                                ("tflops" if k.startswith(("gemm", "attn")) else "gbs"):
                                    ((v["flops"] / (v["ms"] / 1e3) / 1e12) if k.startswith(("gemm", "attn"))
                                     else (v["flops"] / (v["ms"] / 1e3) / 1e9)) if v["ms"] else 0.0,
-                               "launches_per_step": v["launches"] / args.steps}
-                           for k, v in prof.items()},
-        "unattributed_ms_per_step": (ms - sum(v["ms"] for k, v in prof.items()
-                                               if k not in ("attn_bwd_dq", "attn_bwd_dkv"))) / args.steps,
+                               "launches_per_step": v["launches"] / nprof}
+                           for k, v in gemm_flops_class.items()},
+        "instrumented_ms_per_step": prof_ms / nprof,
+        "unattributed_ms_per_step": (prof_ms - sum(v["ms"] for k, v in prof.items()
+                                                   if k not in ("attn_bwd_dq", "attn_bwd_dkv"))) / nprof,
         "clocks": clk.summary(),
         "e2e": e2e,
     }
-    if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args, m, batches[args.warmup][0], cfg)
+    if world > 1:
+        # stage-to-stage activations/gradients (this rank's sends; rank 0 is a
+        # first stage, so its sends are the forward activations of one hop)
+        hop_bytes = p2p_bytes / args.steps
+        out["p2p"] = {"bytes_per_step_rank0": hop_bytes,
+                      "gbs_rank0_avg_over_step": hop_bytes / (sec / args.steps) / 1e9,
+                      "nvlink_gbs_per_direction": 900.0,
+                      "note": "rank 0's send volume over the whole step time (not per-transfer bandwidth)"}
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"], out["planner"] = cpu_side(args, m, dp, cfg, tokens / args.steps,
+                                                      flops / args.steps / max(1, replicas),
+                                                      batches[args.warmup][0], jobs)
     print(json.dumps(out))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def ctypes_double():
-    import ctypes
-    return ctypes.c_double()
+def run_e2e(args, driver, stage, cfg, e2e_batches, jobs, dev, world, dp, prank, replicas, optimizer, sync_all,
+            dist):
+    """Public-API step from host buffers: plans solved on a host thread one
+    step ahead, token ids H2D from pinned memory, per-step loss D2H."""
+    from paper_2509_21275_b200 import planner, schedule
+    ahead = {}
 
+    def solve(k):
+        lengths = e2e_batches[k][0]
+        ahead[k] = schedule.parse_plan(planner.make_plan_document(cfg, lengths, args.slices or None, "main", jobs),
+                                       lengths)
 
-def ctypes_ref(x):
-    import ctypes
-    return ctypes.byref(x)
-
-
-def ctypes_i64():
-    import ctypes
-    return ctypes.c_int64()
+    solve(0)    # batch 0's plan is solved during the (untimed) previous step
+    h2d = d2h = 0
+    # per-step loss: D2H into pinned memory, read one step later (the host
+    # enqueues step k+1 before waiting for step k's loss)
+    loss_host = torch.zeros((len(e2e_batches), 2), dtype=torch.float64).pin_memory()
+    loss_ev = [torch.cuda.Event() for _ in e2e_batches]
+    losses = []
+    sync_all()
+    e0 = time.perf_counter()
+    for k in range(len(e2e_batches)):
+        th = None
+        if k + 1 < len(e2e_batches):
+            th = threading.Thread(target=solve, args=(k + 1,))
+            th.start()
+        st = driver.run_step(ahead.pop(k), e2e_batches[k][1])
+        h2d += st["h2d_bytes"]
+        optimizer()
+        if prank == dp - 1:
+            stage.loss_async(loss_host[k], reset=True)
+            loss_ev[k].record()
+            d2h += 16
+            if k > 0:
+                loss_ev[k - 1].synchronize()
+                losses.append(float(loss_host[k - 1, 0] / max(1.0, float(loss_host[k - 1, 1]))))
+        if th:
+            th.join()
+    if prank == dp - 1:
+        loss_ev[-1].synchronize()
+        losses.append(float(loss_host[-1, 0] / max(1.0, float(loss_host[-1, 1]))))
+    sync_all()
+    e_s = time.perf_counter() - e0
+    if world > 1:
+        # slowest rank's wall time; H2D (stage 0) and D2H (last stage) bytes
+        # are counted where they happen and summed over ranks
+        t = torch.tensor([e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_s = float(t.item())
+        b = torch.tensor([float(h2d), float(d2h)], device=dev)
+        dist.all_reduce(b, op=dist.ReduceOp.SUM)
+        h2d, d2h = int(b[0].item()), int(b[1].item())
+    e_tokens = sum(sum(b[0]) for b in e2e_batches)
+    if replicas > 1:
+        t = torch.tensor([float(e_tokens) if prank == 0 else 0.0], device=dev, dtype=torch.float64)
+        dist.all_reduce(t)
+        e_tokens = int(t.item())
+    nb = len(e2e_batches)
+    out = {"value": e_tokens / e_s, "unit": "tokens/s", "h2d_bytes_per_step": h2d // nb,
+           "d2h_bytes_per_step": d2h // nb}
+    if losses:
+        out["loss_per_step"] = losses
+    return out
 
 
 # ----------------------------------------------------------------- CPU side --
-def cpu_numerics_rate(m, sample_tokens: int, threads: int, seed: int = 0):
-    """fp32 CPU oracle (oracle/numerics.py) fwd+bwd of the full model on one
-    sample sequence of `sample_tokens` tokens; returns (tokens/s, seconds)."""
+def cpu_flops_rate(m, sample_tokens: int, threads: int, seed: int = 0):
+    """fp32 CPU oracle (oracle/numerics.py) FLOP rate on the benched model:
+    fwd+bwd of ONE transformer layer plus the head (final norm, LM head,
+    softmax-CE) on one `sample_tokens`-token sequence.  Returns (model FLOP/s,
+    seconds): the whole model's step time is then its FLOP count over this
+    rate (same model-FLOP accounting as MFU).  Bounded: two layers' worth of
+    parameters, not the whole 7B model."""
     from oracle import numerics as O
     torch.set_num_threads(threads)
-    spec = O.ModelSpec(m.arch, m.layers, m.hidden, m.heads, m.kv_heads, m.head_dim, m.ffn, m.vocab,
+    spec = O.ModelSpec(m.arch, 1, m.hidden, m.heads, m.kv_heads, m.head_dim, m.ffn, m.vocab,
                        m.rope_theta, m.norm_eps)
     g = torch.Generator().manual_seed(seed)
     params = {}
-    for name, shape, kind in O.param_shapes(spec, 0, spec.layers, True, True):
-        if kind in ("one",):
+    for name, shape, kind in O.param_shapes(spec, 0, 1, True, True):
+        if kind == "one":
             params[name] = torch.ones(shape)
         elif kind == "zero":
             params[name] = torch.zeros(shape)
@@ -469,73 +543,107 @@ def cpu_numerics_rate(m, sample_tokens: int, threads: int, seed: int = 0):
     t0 = time.perf_counter()
     O.whole_batch_grads(spec, params, [tokens])
     dt = time.perf_counter() - t0
-    return sample_tokens / dt, dt
+    T = sample_tokens
+    flops = 3 * (m.linear_flops_per_token_layer() * T + m.attn_flops_per_pair_layer() * T * (T + 1) / 2
+                 + 2 * T * m.hidden * m.vocab)
+    return flops / dt, dt
 
 
-def ref_planner_seconds(cfg, lengths, jobs):
+def plan_timed(cfg, lengths, jobs, lib):
     from paper_2509_21275_b200 import planner
-    so = ROOT / "oracle" / "_ref" / "libepp_ref.so"
-    if not so.exists():
-        return None
-    ref = planner._Api(so, prefix="epp_ref_")
     t0 = time.perf_counter()
-    planner.make_plan_document(cfg, lengths, None, "main", jobs, _lib=ref)
-    return time.perf_counter() - t0
+    doc = planner.make_plan_document(cfg, lengths, None, "main", jobs, _lib=lib)
+    return doc, time.perf_counter() - t0
 
 
-def cpu_baseline(args, m, lengths, cfg):
+def cpu_side(args, m, dp, cfg, tokens_per_step, flops_per_step, lengths, jobs):
+    """(cpu_baseline, planner block) on rank 0's host cores: the reference
+    planner (oracle/_ref) at jobs = nproc and 1 on the step's lengths, our
+    planner likewise, byte identity of all four documents,
+    and the fp32 CPU numerics rate of the benched model."""
+    from paper_2509_21275_b200 import planner
     cores = os.cpu_count() or 1
-    rate, secs = cpu_numerics_rate(m, args.cpu_sample_tokens, cores)
-    plan_s = ref_planner_seconds(cfg, lengths, cores)
-    tokens = sum(lengths)
-    # CPU time for the whole step = reference planning of the batch + fp32
-    # numerics of all its tokens at the sampled rate.
-    step_s = (plan_s or 0.0) + tokens / rate
-    return {"value": tokens / step_s, "unit": "tokens/s", "cores": cores,
-            "kind": "reference" if plan_s is not None else "port",
-            "sample": f"reference planner (oracle/_ref make_plan, jobs={cores}) on the step's "
-                      f"{len(lengths)}-sequence batch ({plan_s:.3f}s) + fp32 torch-CPU oracle "
-                      f"fwd+bwd of {args.model} on a {args.cpu_sample_tokens}-token sample "
-                      f"({secs:.1f}s, {rate:.1f} tokens/s), extrapolated to the batch's {tokens} tokens"}
+    block = {"cores": cores, "sequences": len(lengths)}
+    docs = {}
+    if REF_SO.exists():
+        ref = planner._Api(REF_SO, prefix="epp_ref_")
+        docs["ref_jobs_n"], block["reference_seconds_jobs_n"] = plan_timed(cfg, lengths, cores, ref)
+        docs["ref_jobs_1"], block["reference_seconds_jobs_1"] = plan_timed(cfg, lengths, 1, ref)
+    docs["ours_jobs_n"], block["ours_seconds_jobs_n"] = plan_timed(cfg, lengths, cores, None)
+    docs["ours_jobs_1"], block["ours_seconds_jobs_1"] = plan_timed(cfg, lengths, 1, None)
+    block["byte_identical"] = len(set(docs.values())) == 1
+    block["documents_compared"] = sorted(docs)
+    rate, secs = cpu_flops_rate(m, args.cpu_sample_tokens, cores)
+    plan_s = block.get("reference_seconds_jobs_n", block["ours_seconds_jobs_n"])
+    step_s = plan_s + flops_per_step / rate
+    base = {"value": tokens_per_step / step_s, "unit": "tokens/s", "cores": cores,
+            "kind": "reference" if REF_SO.exists() else "port",
+            "sample": f"reference planner (oracle/_ref make_plan, jobs={cores}) on the step's {len(lengths)} "
+                      f"lengths ({plan_s:.3f} s) + the step's model FLOPs ({flops_per_step:.3e}) at the fp32 "
+                      f"torch-CPU oracle rate measured on 1 layer + head of {args.model} over a "
+                      f"{args.cpu_sample_tokens}-token sample ({rate / 1e9:.1f} GFLOP/s, {secs:.1f} s)"}
+    return base, block
 
 
 def run_reference(args):
+    """The reference's CPU path on the host cores (rank 0 only): per step,
+    the compiled reference planner (oracle/_ref, jobs = nproc) on the step's
+    batch, generated by the reference's own generate_workload, plus the fp32
+    CPU numerics of the same model (1 layer + head sample, scaled by model
+    FLOPs).  Loads only oracle/ native code."""
     world = args.gpus
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_2509_21275_b200 import model as M, planner
     m = M.MODELS[args.model]
-    cfg = M.planner_config(m, world, mem_capacity=181e9, cost=M.default_cost(m))
+    dp = args.pp or world
+    cfg, counts, cost_src = bench_config(args, m, dp)
     cores = os.cpu_count() or 1
-    batches = make_batches(args, args.warmup + args.steps, world, m.vocab)
-    so = ROOT / "oracle" / "_ref" / "libepp_ref.so"
-    ref = planner._Api(so, prefix="epp_ref_") if so.exists() else None
-    kind = "reference" if ref else "port"
-    times, toks = [], []
-    for i, (lengths, _) in enumerate(batches):
-        t0 = time.perf_counter()
-        planner.make_plan_document(cfg, lengths, None, "main", cores, _lib=ref)
-        plan_s = time.perf_counter() - t0
-        rate, secs = cpu_numerics_rate(m, args.cpu_sample_tokens, cores, seed=i)
+    if not REF_SO.exists():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libepp_ref.so not built"}))
+        return
+    ref = planner._Api(REF_SO, prefix="epp_ref_")
+    batches = make_lengths(args, args.warmup + args.steps, dp, _lib=ref)
+    times, toks, plan_ts = [], [], []
+    for i, (_, lengths) in enumerate(batches):
+        doc, plan_s = plan_timed(cfg, lengths, cores, ref)
+        flops = step_flops_from_doc(m, doc)
+        rate, secs = cpu_flops_rate(m, args.cpu_sample_tokens, cores, seed=i)
         if i >= args.warmup:
-            times.append(plan_s + secs)
-            toks.append(args.cpu_sample_tokens)
+            times.append(plan_s + flops / rate)
+            toks.append(sum(lengths))
+            plan_ts.append(plan_s)
     value = sum(toks) / sum(times)
-    sample = (f"per step: reference planner (oracle/_ref, jobs={cores}) on the step's "
-              f"{len(batches[0][0])}-sequence batch + fp32 torch-CPU oracle fwd+bwd of {args.model} "
-              f"on a {args.cpu_sample_tokens}-token sample; value = sample tokens / step time")
-    out = {"metric": "training tokens/s + MFU, skewed-length GPT EPP at 1/2/4/8 B200", "impl": "reference",
+    sample = (f"per step: reference planner (oracle/_ref, jobs={cores}) on the step's {len(batches[0][1])} "
+              f"lengths (mean {statistics.mean(plan_ts):.3f} s) + the step's model FLOPs at the fp32 torch-CPU "
+              f"oracle rate measured that step on 1 layer + head of {args.model} over a "
+              f"{args.cpu_sample_tokens}-token sample")
+    out = {"metric": METRIC, "impl": "reference",
            "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f32",
-           "data": "synthetic (seeded github_like lengths, uniform tokens, random-init weights)",
+           "vs_baseline": None, "dtype": "f32", "data": DATA,
            "config": {"workload": f"{args.model} EPP, {args.preset} lengths cap {args.cap}, "
-                                  f"{args.seqs_per_gpu} seqs/GPU/step, d_p={world}",
-                      "model": args.model, "parallelism": f"pp{world}"},
-           "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": kind, "sample": sample},
+                                  f"{args.seqs_per_gpu} seqs/GPU/step, d_p={dp}",
+                      "model": args.model, "parallelism": f"pp{dp}", "stage_layers": counts,
+                      "cost": cost_src, "same_config_as_ours": True},
+           "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "reference",
+                            "sample": sample},
            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
+
+
+def step_flops_from_doc(m, doc):
+    """Model FLOPs of a plan document's chunks (same count as step_flops)."""
+    d = json.loads(doc)
+    lin, per_pair = m.linear_flops_per_token_layer(), m.attn_flops_per_pair_layer()
+    total = 0.0
+    for c in d["chunks"]:
+        sl = c["slices"]
+        T = sum(sl)
+        pairs = sum(s * (c["context"] if (i == 0 and "seq" in c) else 0) + s * (s + 1) / 2 for i, s in enumerate(sl))
+        total += 3 * (m.layers * (lin * T + per_pair * pairs) + 2 * T * m.hidden * m.vocab)
+    return total
 
 
 def main():

@@ -107,11 +107,19 @@ int epp_stage_backward(epp_stage* st, const epp_chunk_desc* chunk, const void* g
 int epp_seq_release(epp_stage* st, int32_t seq);
 
 /* Last stage: accumulated (sum of token losses, #targets) since the last
- * reset.  Synchronises `stream`. */
+ * reset.  Each chunk's losses are reduced in fp64 in a fixed order (no
+ * atomics), then added to the fp64 accumulator in stream order: the result
+ * is deterministic.  Synchronises `stream`. */
 int epp_stage_loss(epp_stage* st, double out[2], int32_t reset, void* stream);
-/* Same, stream-ordered and non-blocking: copies the two fp32 accumulators to
+/* Same, stream-ordered and non-blocking: copies the two fp64 accumulators to
  * out2 (pinned host or device memory) when `stream` reaches this point. */
-int epp_stage_loss_async(epp_stage* st, float* out2, int32_t reset, void* stream);
+int epp_stage_loss_async(epp_stage* st, double* out2, int32_t reset, void* stream);
+/* Per-micro-batch loss (SURVEY §8b `epp_stage_loss(stage, chunk_id, ...)`;
+ * the unit is one epp::Chunk, proj/include/epp/chunk.hpp:32-46): (sum of the
+ * chunk's token losses, #targets) of the latest forward of `chunk_id` since
+ * the last loss reset.  EPP_GPU_EARG if the chunk was not forwarded on this
+ * (last) stage.  Synchronises `stream`. */
+int epp_stage_chunk_loss(epp_stage* st, int32_t chunk_id, double out[2], void* stream);
 int epp_stage_zero_grads(epp_stage* st, void* stream);
 /* Pre-reserve `bytes` in the device's stream-ordered pool that backs all
  * stage activations (kept reserved: later steps never wait on the driver to
@@ -123,6 +131,44 @@ int epp_stage_adamw_step(epp_stage* st, float lr, float beta1, float beta2, floa
 /* Device bytes held by this stage's in-flight chunks and sequences. */
 int epp_stage_memory(epp_stage* st, int64_t* live_bytes, int64_t* peak_bytes);
 
+/* ---- stage-to-stage P2P over peer memory (NVLink) ------------------------
+ * epp_p2p_init + epp_send / epp_recv between adjacent stages
+ * (PAPER.md:726 uses NCCL; proj/src/pipeline.cpp:168-193 models the hand-off
+ * as zero-latency).  One channel = one directed message stream (forward
+ * activations p -> p+1 or backward gradients p+1 -> p) between two
+ * endpoints, possibly in different processes / on different GPUs:
+ *   1. each side: epp_p2p_create(role, arena_bytes, &ch, handle) on its own
+ *      device (the receiver allocates the mailbox arena, >= the largest
+ *      message); exchange the EPP_P2P_HANDLE_BYTES handles out of band (e.g.
+ *      torch.distributed); each side: epp_p2p_open(ch, peer_handle).  Across
+ *      processes the memory is mapped with CUDA IPC; in one process, call
+ *      epp_p2p_init(ndev, devs) first (peer access).
+ *   2. sender, per message: epp_p2p_send_reserve -> *dst (peer address; the
+ *      stream waits until that region is free), write it (e.g. pass it as
+ *      act_out / grad_out of epp_stage_forward / _backward: the last kernel
+ *      stores over NVLink, no send buffer), epp_p2p_send_commit.
+ *      receiver, per message: epp_p2p_recv_wait -> *src (the stream waits
+ *      until the message has landed), read it, epp_p2p_recv_release.
+ *   Messages must be consumed in the order they were sent and both sides
+ *   must pass the same byte counts (both derive them from the plan).  All
+ *   synchronisation is stream-ordered (flag stores + cuStreamWaitValue32); the
+ *   host never blocks.  epp_p2p_send / epp_p2p_recv are the copying forms. */
+#define EPP_P2P_HANDLE_BYTES 256
+enum { EPP_P2P_SENDER = 0, EPP_P2P_RECEIVER = 1 };
+typedef struct epp_p2p epp_p2p;
+int epp_p2p_init(int ndev, const int* devs);
+int epp_p2p_create(int role, uint64_t arena_bytes, epp_p2p** out, void* handle_out);
+int epp_p2p_open(epp_p2p* ch, const void* peer_handle);
+int epp_p2p_send_reserve(epp_p2p* ch, uint64_t bytes, void* stream, void** dst);
+int epp_p2p_send_commit(epp_p2p* ch, void* stream);
+int epp_p2p_recv_wait(epp_p2p* ch, uint64_t bytes, void* stream, const void** src);
+int epp_p2p_recv_release(epp_p2p* ch, void* stream);
+int epp_p2p_send(epp_p2p* ch, const void* src, uint64_t bytes, void* stream);
+int epp_p2p_recv(epp_p2p* ch, void* dst, uint64_t bytes, void* stream);
+/* messages and payload bytes this endpoint has sent / received */
+int epp_p2p_stats(epp_p2p* ch, int64_t* messages, int64_t* bytes);
+int epp_p2p_destroy(epp_p2p* ch);
+
 /* ---- kernel-level entry points (unit tests, benchmarks) ------------------ */
 /* C[M,N] = epi(A(m,k) B(n,k)); *_kmajor selects the operand layout
  * (kernels.h GemmArgs); epi: 0 store, 1 fp32 accumulate, 2 add residual R,
@@ -131,6 +177,13 @@ int epp_kernel_gemm(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda,
                     int32_t a_kmajor, const void* B, int64_t ldb, int32_t b_kmajor, void* C,
                     int64_t ldc, const void* R, int64_t ldr, int32_t epi, int32_t dtype,
                     void* stream);
+/* Same with the fused MLP epilogues: epi 4 = StoreGelu (C = acc, C2 =
+ * gelu_tanh(acc)), 5 = GeluBwd (C = acc * gelu_tanh'(R)); bf16 only for 4/5
+ * outputs in the stage dtype. */
+int epp_kernel_gemm_ex(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_kmajor,
+                       const void* B, int64_t ldb, int32_t b_kmajor, void* C, int64_t ldc,
+                       const void* R, int64_t ldr, void* C2, int64_t ldc2, int32_t epi, int32_t dtype,
+                       void* stream);
 /* Slice-causal attention over nseg segments (host arrays).  Segment i: query
  * rows [q_start[i], +q_len[i]) of q/o, keys at k[i]/v[i] (row stride
  * Hkv*hd), kv_ctx[i] context keys before the first query. lse: [H, T] log2. */
@@ -154,9 +207,11 @@ int epp_kernel_attention_bwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, floa
 int epp_gpu_profile(int32_t enable);
 int epp_gpu_profile_read(int32_t cls, double* ms, double* flops, int64_t* launches, int32_t reset);
 
-/* Attention kernel family: 1 = tcgen05 (default), 2 = tcgen05 with the fused
- * dK/dV/dQ backward (hd 128), 0 = mma.sync FA2-style. */
-int epp_gpu_set_attention_impl(int32_t impl);
+/* Kernel launches of this library so far, per kernel (demangled name, sorted):
+ * idx 0 takes a snapshot, idx 1.. read it; EPP_GPU_EARG past the end.  Shows
+ * which kernel variants (e.g. the CTA-pair GEMM with the RopeScatter
+ * epilogue) a test or benchmark really ran. */
+int epp_gpu_kernel_stats(int32_t idx, const char** name, int64_t* count);
 
 const char* epp_gpu_last_error(void);
 /* Kernel launches issued by this library in this process (for bench claims). */

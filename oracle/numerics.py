@@ -17,6 +17,11 @@ UNPINNED by reference golden vectors.  What pins it:
     through `TorchStage` (any plan, any stage split) reproduces whole-sequence
     autograd loss and gradients to fp32 round-off.
 
+Device-agnostic: the same code runs on CPU (small cases) or, for the
+benchmark-width parity tests, on the GPU in fp32 with TF32 off
+(tests/test_gpu_bench_shapes.py); attention over long sequences is evaluated
+in checkpointed query blocks so its memory stays bounded.
+
 Model (both archs, pre-norm, RoPE rotate-half, no linear biases):
   GPT   : LayerNorm(w,b), MHA, GELU(tanh) MLP ffn
   Llama : RMSNorm(w), GQA, SwiGLU MLP (w13 = [gate; up])
@@ -120,8 +125,9 @@ def apply_rope(x: torch.Tensor, pos: torch.Tensor, theta: float) -> torch.Tensor
     hd = x.shape[-1]
     half = hd // 2
     cos, sin = rope_cos_sin(int(pos.max().item()) + 1, hd, theta)
-    c = cos[pos].to(x.dtype)[:, None, :]
-    s = sin[pos].to(x.dtype)[:, None, :]
+    pc = pos.cpu()
+    c = cos[pc].to(x.device, x.dtype)[:, None, :]
+    s = sin[pc].to(x.device, x.dtype)[:, None, :]
     x1, x2 = x[..., :half], x[..., half:]
     return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1)
 
@@ -138,18 +144,38 @@ def gelu_tanh(x):
     return F.gelu(x, approximate="tanh")
 
 
-def attend(q, k, v, qpos):
-    """q [T,H,hd], k/v [S,Hkv,hd]; query i sees keys j <= qpos[i]."""
+def _attend_dense(q, k, v, qpos):
     T, H, hd = q.shape
     S, Hkv, _ = k.shape
     g = H // Hkv
     kk = k.repeat_interleave(g, dim=1)
     vv = v.repeat_interleave(g, dim=1)
     s = torch.einsum("thd,shd->hts", q, kk) / math.sqrt(hd)
-    mask = torch.arange(S)[None, :] > qpos[:, None]
+    mask = torch.arange(S, device=q.device)[None, :] > qpos.to(q.device)[:, None]
     s = s.masked_fill(mask[None], float("-inf"))
     p = torch.softmax(s, dim=-1)
     return torch.einsum("hts,shd->thd", p, vv)
+
+
+# score elements per dense evaluation; larger problems go through
+# checkpointed query blocks (the backward recomputes each block's scores)
+_ATTN_DENSE_LIMIT = 1 << 28
+
+
+def attend(q, k, v, qpos):
+    """q [T,H,hd], k/v [S,Hkv,hd]; query i sees keys j <= qpos[i]."""
+    T, H, _ = q.shape
+    S = k.shape[0]
+    if T * S * H <= _ATTN_DENSE_LIMIT:
+        return _attend_dense(q, k, v, qpos)
+    from torch.utils.checkpoint import checkpoint
+    block = max(64, _ATTN_DENSE_LIMIT // (S * H))
+    outs = []
+    for i in range(0, T, block):
+        qp = qpos[i:i + block]
+        kv = int(qp.max().item()) + 1          # keys past the block's last query are masked anyway
+        outs.append(checkpoint(_attend_dense, q[i:i + block], k[:kv], v[:kv], qp, use_reentrant=False))
+    return torch.cat(outs)
 
 
 def _p(params, name):
@@ -187,7 +213,9 @@ def sequence_token_losses(spec: ModelSpec, params, tokens: torch.Tensor) -> torc
     """Per-position CE of one whole sequence (next-token targets); the last
     position has no target and gets 0."""
     T = tokens.shape[0]
-    pos = torch.arange(T)
+    dev = params["embed.weight"].device
+    tokens = tokens.to(dev)
+    pos = torch.arange(T, device=dev)
     x = params["embed.weight"][tokens]
     for j in range(spec.layers):
         pre = f"layers.{j}."
@@ -196,27 +224,35 @@ def sequence_token_losses(spec: ModelSpec, params, tokens: torch.Tensor) -> torc
         x = x + o @ params[pre + "attn.wo"].T
         x = x + mlp(spec, params, pre, x)
     logits = head_logits(spec, params, x)
-    losses = torch.zeros(T, dtype=logits.dtype)
+    logits = logits.float()
+    losses = torch.zeros(T, dtype=logits.dtype, device=dev)
     if T > 1:
         losses = torch.cat([F.cross_entropy(logits[:-1], tokens[1:], reduction="none"),
-                            torch.zeros(1, dtype=logits.dtype)])
+                            torch.zeros(1, dtype=logits.dtype, device=dev)])
     return losses
 
 
-def whole_batch_grads(spec: ModelSpec, params: Dict[str, torch.Tensor], sequences: Sequence[torch.Tensor]):
+def whole_batch_grads(spec: ModelSpec, params: Dict[str, torch.Tensor], sequences: Sequence[torch.Tensor],
+                      autocast_bf16: bool = False):
     """Reference loss/grads: mean next-token CE over every target of every
-    sequence, each sequence attended independently and causally."""
+    sequence, each sequence attended independently and causally.  The
+    parameters' device decides where it runs.  autocast_bf16 (CUDA): the same
+    model under torch.autocast(bfloat16) — the error yardstick the bf16
+    executor is held to (tests/test_gpu_bench_shapes.py).  Each sequence is
+    back-propagated on its own (bounded memory); gradients accumulate."""
     leaf = {k: v.detach().clone().requires_grad_(True) for k, v in params.items()}
     n_targets = sum(max(0, s.shape[0] - 1) for s in sequences)
     total = 0.0
     per_seq = []
+    dev = next(iter(leaf.values())).device
     for s in sequences:
-        l = sequence_token_losses(spec, leaf, s)
+        with torch.autocast(dev.type, dtype=torch.bfloat16, enabled=autocast_bf16):
+            l = sequence_token_losses(spec, leaf, s)
         per_seq.append(l.detach())
-        total = total + l.sum()
-    loss = total / n_targets
-    loss.backward()
-    return loss.detach(), {k: v.grad.detach() for k, v in leaf.items()}, per_seq
+        (l.sum() / n_targets).backward()
+        total += float(l.detach().double().sum())
+    loss = torch.tensor(total / n_targets, dtype=torch.float64)
+    return loss, {k: v.grad.detach() for k, v in leaf.items()}, per_seq
 
 
 # --------------------------------------------------------------- chunked ---
@@ -283,7 +319,7 @@ class TorchStage:
         for j in range(self.num):
             lj = self.first + j
             pre = f"layers.{lj}."
-            pos = torch.cat([torch.arange(ctx, ctx + n) for (_, n, ctx, _) in segs])
+            pos = torch.cat([torch.arange(ctx, ctx + n, device=x.device) for (_, n, ctx, _) in segs])
             q, k, v = qkv_proj(spec, P, pre, x, pos)
             outs = []
             for (st, n, ctx, is_seq) in segs:
@@ -301,7 +337,7 @@ class TorchStage:
                     own_kv.append((ks, vs, leaf_k, leaf_v))
                 else:
                     kk, vv = ks, vs
-                outs.append(attend(qs, kk, vv, torch.arange(ctx, ctx + n)))
+                outs.append(attend(qs, kk, vv, torch.arange(ctx, ctx + n, device=x.device)))
             o = torch.cat(outs).reshape(T, -1)
             x = x + o @ P[pre + "attn.wo"].T
             x = x + mlp(spec, P, pre, x)

@@ -54,25 +54,52 @@ class TimedStage:
         return self._timed("backward", self.stage.backward, op, grad_in)
 
     def samples(self) -> List[Dict]:
-        """Fit samples.  A backward that first re-ran `ckpt_layers` of the
-        stage's `num` layers is charged its recompute, estimated from the same
-        chunk's measured forward (ckpt_layers / num of it), which Eq. 1
-        prices separately (recompute_time, cost_model.cpp:68-78)."""
+        """Fit samples.  A backward that first re-ran `ckpt` of the stage's
+        `num` layers is charged its recompute, estimated from the same
+        chunk's measured forward, which Eq. 1 prices separately
+        (recompute_time, cost_model.cpp:68-78).  Only the layers' share of
+        that forward is scaled: on the last stage the forward call also runs
+        the LM head (forward and backward), which recompute never repeats;
+        its share is split off by model FLOPs."""
+        st = self.stage
+        layers = max(1, int(getattr(st, "num", 1)))
+        m = getattr(st, "model", None)
         fwd = {}
         for op, phase, a, b in self.records:
             if phase == "forward":
                 fwd[op.id] = a.elapsed_time(b) / 1e3
-        layers = max(1, int(getattr(self.stage, "num", 1)))
         out = []
         for op, phase, a, b in self.records:
             sec = a.elapsed_time(b) / 1e3
             if phase == "backward" and op.ckpt_layers > 0:
                 if op.id not in fwd:
                     continue
-                sec -= fwd[op.id] * op.ckpt_layers / layers
+                ckpt = _stage_ckpt(st, op.ckpt_layers, layers)
+                sec -= _layer_forward_share(m, op, layers, getattr(st, "has_head", False)) * fwd[op.id] * ckpt / layers
             out.append({"context": int(op.context), "slices": [int(s) for s in op.slices], "phase": phase,
                         "seconds": sec})
         return out
+
+
+def _stage_ckpt(stage, plan_count: int, layers: int) -> int:
+    """Layers the stage actually re-ran for a plan count (gpu.CudaStage
+    rescales counts of non-uniform stages; never more than the stage has)."""
+    f = getattr(stage, "_ckpt_layers", None)
+    return int(f(plan_count)) if f else min(int(plan_count), layers)
+
+
+def _layer_forward_share(m, op, layers: int, has_head: bool) -> float:
+    """Fraction of a forward call spent in the transformer layers (model
+    FLOPs): 1 except on the last stage, whose forward also runs the LM head
+    forward + backward (3 x 2 T D V)."""
+    if m is None or not has_head:
+        return 1.0
+    T = sum(op.slices)
+    pairs = sum(s * (op.context if (i == 0 and op.seq >= 0) else 0) + s * (s + 1) / 2
+                for i, s in enumerate(op.slices))
+    lay = layers * (m.linear_flops_per_token_layer() * T + m.attn_flops_per_pair_layer() * pairs)
+    head = 3.0 * 2.0 * T * m.hidden * m.vocab
+    return lay / (lay + head) if lay + head > 0 else 1.0
 
 
 def calibrated_config(cfg: Dict, samples: List[Dict]) -> Dict:

@@ -909,19 +909,16 @@ __device__ __forceinline__ uint64_t smem_desc_sw32(uint32_t addr) {
     return d;
 }
 
-// FUSED: the kernel also forms dQ (see attn_bwd_dkv_tc); its dS^T tiles
-// take the shared memory of one Q/dO stage pair.
-template <int HD, bool FUSED>
+template <int HD>
 struct DkvSmem {
-    static constexpr int kStages = FUSED ? kDkvStages - 1 : kDkvStages;
+    static constexpr int kStages = kDkvStages;
     static constexpr int kBig = 128 * HD * 2;       // K / V tiles
     static constexpr int kSmall = TB * HD * 2;      // Q / dO tiles
     static constexpr int kK = 0;
     static constexpr int kV = kK + kBig;
     static constexpr int kQ = kV + kBig;                     // kStages stages
     static constexpr int kO = kQ + kStages * kSmall;
-    static constexpr int kDS = kO + kStages * kSmall;        // FUSED: dS^T [128 keys x 64 queries] bf16, x2
-    static constexpr int kKa = kDS + (FUSED ? 2 * 128 * TB * 2 : 0);   // augmented K-step: K, V [128 x 16] (ones)
+    static constexpr int kKa = kO + kStages * kSmall;        // augmented K-step: K, V [128 x 16] (ones)
     static constexpr int kVa = kKa + 128 * 32;
     static constexpr int kQa = kVa + 128 * 32;               // Q, dO [64 x 16] per stage (-lse/c2, -delta)
     static constexpr int kOa = kQa + kStages * TB * 32;
@@ -930,27 +927,13 @@ struct DkvSmem {
     static constexpr int kAlloc = kBytes + 1024;
 };
 
-// FUSED (hd 128): one pass forms dQ as well, so the dq kernel (and its
-// recomputation of S and dP) is skipped.  Per 64-query step, after the
-// softmax group has turned S^T / dP^T into P^T / dS^T:
-//   * P^T and dS^T (bf16 pairs) both go over the step's S^T buffer, freeing
-//     its 64-column dP^T buffer;
-//   * dS^T is also written to shared memory ([key][query], 128-byte swizzle:
-//     an MN-major B operand) and dQ^T = K^T dS^T (M = hd, N = 64 queries,
-//     K = 128 keys; K^T is the resident K tile read MN-major) accumulates in
-//     that free dP^T buffer;
-//   * the same softmax group drains dQ^T (tcgen05.ld) and reduces it into the
-//     zeroed fp32 a.dq with coalesced red.global.add (thread = hd column).
-// The dP^T of step it+2 reuses the buffer, so its MMA waits for the drain
-// (dq_free), which runs under the S^T MMA of the same step.
-template <int HD, bool FUSED>
+template <int HD>
 __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs a,
                                                                   const __grid_constant__ AttnMaps mp) {
     pdl_wait();
     pdl_trigger();
-    using L = DkvSmem<HD, FUSED>;
+    using L = DkvSmem<HD>;
     constexpr int kDkvStages = L::kStages;
-    static_assert(!FUSED || HD == 128, "fused dQ^T needs M = hd = 128");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -964,9 +947,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
     uint64_t* s_full = qd_empty + kDkvStages;         // [2]
     uint64_t* p_full = s_full + 2;                    // [2]
     uint64_t* acc_full = p_full + 2;                  // all MMAs retired (epilogue)
-    uint64_t* dq_full = acc_full + 1;                 // [2] FUSED: dQ^T of the step done
-    uint64_t* dq_free = dq_full + 2;                  // [2] FUSED: dQ^T drained
-    uint64_t* dp_full = dq_free + 2;                  // [2] dP^T of the step (s_full: S^T)
+    uint64_t* dp_full = acc_full + 1;                 // [2] dP^T of the step (s_full: S^T)
     uint64_t* pt_full = dp_full + 2;                  // [2] P^T in TMEM (p_full: dS^T)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pt_full + 2);
 
@@ -995,8 +976,6 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
         }
         tc::mbar_init(acc_full, 1);
         for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&dq_full[b], 1);
-            tc::mbar_init(&dq_free[b], TQ);
             tc::mbar_init(&dp_full[b], 1);
             tc::mbar_init(&pt_full[b], TQ);
         }
@@ -1089,8 +1068,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
         const uint32_t sKa = (sbase + L::kKa);
         const uint32_t sVa = (sbase + L::kVa);
         const uint64_t dK = tc::smem_desc(sK, 16, 1024), dV = tc::smem_desc(sV, 16, 1024);
-        // FUSED: dS^T lives over the second half of the S^T buffer
-        constexpr uint32_t kColDs = FUSED ? kColS + TB / 2 : kColP;
+        constexpr uint32_t kColDs = kColP;
         auto grad = [&](int it) {   // dV += P^T dO ; dK += dS^T Q  (P^T, dS^T from TMEM)
             const int b = it & 1, st = it % kDkvStages;
             tc::mbar_wait(&pt_full[b], (it >> 1) & 1);   // P^T is published before dS^T
@@ -1104,16 +1082,6 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
             tc::mma4_ts<8, 128>(tmem_u + kColK, tmem_u + kColDs + b * TB, tc::smem_desc(sQ, TB * 128, 1024), idD,
                                 it != 0);
             tc::commit_w(&qd_empty[st]);
-            if constexpr (FUSED) {
-                // dQ^T = K^T dS^T: A = K tile MN-major (hd blocks 16 KB apart),
-                // B = dS^T tile MN-major (one 64-query block); +2 KB per 16 keys
-                constexpr uint32_t idQ = tc::instr_desc_mn(HD, TB, true, true);
-                const uint64_t aK = tc::smem_desc(sK, 128 * 128, 1024);
-                const uint64_t bS = tc::smem_desc(sbase + L::kDS + b * (128 * TB * 2), 128 * 128, 1024);
-                tc::mma4_ss<128, 128>(tmem_u + kColP + b * TB, aK, bS, idQ, 0);
-                tc::mma4_ss<128, 128>(tmem_u + kColP + b * TB, aK + 4 * 128, bS + 4 * 128, idQ, 1);
-                tc::commit_w(&dq_full[b]);
-            }
         };
         // Buffer b of step it is rewritten by the scores of step it+2,
         // issued after grad(it): in-order tcgen05 execution orders the
@@ -1131,10 +1099,6 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
             tc::mma_bf16_w(tmem_u + kColS + b * TB, smem_desc_sw32(sKa),
                          smem_desc_sw32((sbase + L::kQa + st * TB * 32)), idS, 1);
             tc::commit_w(&s_full[b]);   // S^T on its own: the exponentials overlap the dP^T MMA
-            if (FUSED && it >= 2) {   // the dP^T buffer held dQ^T of step it-2
-                tc::mbar_wait(&dq_free[b], ((it - 2) >> 1) & 1);
-                tc::fence_after();
-            }
 #pragma unroll
             for (int cb = 0; cb < HD / 64; ++cb)
                 tc::mma4_ss<2, 2>(tmem_u + kColP + b * TB, dV + cb * 1024, dO + cb * 512, idS, cb != 0);
@@ -1189,66 +1153,12 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
 #pragma unroll
             for (int c = 0; c < TB / 32; ++c) tc::reg_fence(dall[c]);
             dkv_ds_tile(sall, dall, dk);
-            // dS^T (bf16 pairs) over the first 32 columns of the dP^T buffer
-            // (FUSED: the second half of the S^T buffer): the dK MMA's A operand
-            tc::tmem_st32u(lane_base + (FUSED ? kColS + TB / 2 : kColP) + b * TB, dk);
-            if constexpr (FUSED) {
-                // dS^T row r (64 queries = 128 B) into the 128B-swizzled tile
-                // (its previous contents, this warp's dQ staging of step it-2,
-                // were consumed by the warp itself)
-                uint8_t* row = smem + L::kDS + b * (128 * TB * 2) + r * 128;
-#pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    *reinterpret_cast<uint4*>(row + ((c ^ (r & 7)) << 4)) =
-                        make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
-                tc::fence_proxy_async();
-            }
+            // dS^T (bf16 pairs) over the first 32 columns of the dP^T buffer:
+            // the dK MMA's A operand
+            tc::tmem_st32u(lane_base + kColP + b * TB, dk);
             tc::tmem_wait_st();
             tc::fence_before();
             tc::mbar_arrive(&p_full[b]);
-            if constexpr (FUSED) {
-                // drain dQ^T (lane = hd column r, column = query) and reduce it
-                // into a.dq with bulk async reductions: each warp stages
-                // [32 queries][its 32 hd columns] fp32 over its own 4 KB of
-                // the dS^T tile (the rows it wrote; the dQ^T MMA has finished
-                // reading them), lane q then reduce-adds one 128-byte row
-                tc::mbar_wait(&dq_full[b], (it >> 1) & 1);
-                tc::fence_after();
-                float v[2][32];
-                tc::tmem_ld32_async(lane_base + kColP + b * TB, v[0]);
-                tc::tmem_ld32_async(lane_base + kColP + b * TB + 32, v[1]);
-                tc::tmem_wait_ld();
-                tc::reg_fence(v[0]);
-                tc::reg_fence(v[1]);
-                tc::fence_before();
-                tc::mbar_arrive(&dq_free[b]);
-                const int hq = kvh * group + it / per_head;
-                // stage [32 queries][this warp's 32 hd columns] fp32 over the
-                // warp's own 4 KB of the dS^T tile (the rows it wrote; the
-                // dQ^T MMA is done with them), then 16-byte reductions: 8
-                // lanes per 128-byte row, 4 rows per instruction
-                float* stg = reinterpret_cast<float*>(smem + L::kDS + b * (128 * TB * 2) + (warp & 3) * 4096);
-                float* dst = a.dq + ((sg.q_start + q0) * static_cast<long long>(a.H) + hq) * HD + (warp & 3) * 32 +
-                             (lane & 7) * 4;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    __syncwarp();
-#pragma unroll
-                    for (int q = 0; q < 32; ++q) stg[q * 32 + lane] = v[h][q] * a.scale;
-                    __syncwarp();
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const int q = k * 4 + (lane >> 3);
-                        const float4 x = *reinterpret_cast<const float4*>(stg + q * 32 + (lane & 7) * 4);
-                        if (32 * h + q < rows)
-                            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(
-                                             dst + (32LL * h + q) * a.H * HD),
-                                         "f"(x.x), "f"(x.y), "f"(x.z), "f"(x.w)
-                                         : "memory");
-                    }
-                }
-                __syncwarp();
-            }
         }
         tc::mbar_wait(acc_full, 0);
         tc::fence_after();
@@ -1258,7 +1168,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
         float* drow = base + a.layer * sg.dkv_layer_stride + kvh * HD + (k0 + min(r, nkeys - 1)) * kvs;
         const float mul = grp == 0 ? a.scale : 1.f;
         const uint32_t col = grp == 0 ? kColK : kColV;
-        if (!FUSED && a.dqkv_out != nullptr) {
+        if (a.dqkv_out != nullptr) {
             // Rows of this chunk's own tokens are complete here (later slices,
             // which also attend to them, ran their backward first): add the
             // accumulated fp32 partials, undo RoPE (dK) and write bf16 straight
@@ -1359,30 +1269,9 @@ void launch_bwd_tc(const AttnArgs& a, cudaStream_t s) {
     if (!cfg) {
         EPP_CUDA(cudaFuncSetAttribute(attn_bwd_dq_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       DqSmem<HD>::kAlloc));
-        EPP_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_tc<HD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      DkvSmem<HD, false>::kAlloc));
-        if constexpr (HD == 128)
-            EPP_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_tc<HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          DkvSmem<HD, true>::kAlloc));
+        EPP_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      DkvSmem<HD>::kAlloc));
         cfg = true;
-    }
-    if constexpr (HD == 128) {
-        if (attn_bwd_fused(a)) {
-            // delta pass, zeroed dQ, then the single fused kernel
-            if (a.T > 0) {
-                attn_delta(a, s);
-                EPP_CUDA(cudaMemsetAsync(a.dq, 0, sizeof(float) * a.T * a.H * HD, s));
-            }
-            if (a.nkwork128 > 0) {
-                ProfScope prof(kProfAttnBwdDkv, 10.0 * a.H * a.hd * a.pairs, s);    // executed: 5 matmuls
-                AttnArgs b = a;
-                b.hfast = attn_hfast(a.Hkv, a.nkwork128);
-                launch_k(attn_bwd_dkv_tc<HD, true>, attn_grid(a.Hkv, a.nkwork128), kThreadsBwd, DkvSmem<HD, true>::kAlloc,
-                                            s, b, *a.maps);
-                EPP_CHECK_LAUNCH();
-            }
-            return;
-        }
     }
     if (a.nqwork128 > 0) {
         ProfScope prof(kProfAttnBwdDq, 6.0 * a.H * a.hd * a.pairs, s);     // executed: 3 matmuls
@@ -1395,7 +1284,7 @@ void launch_bwd_tc(const AttnArgs& a, cudaStream_t s) {
         ProfScope prof(kProfAttnBwdDkv, 8.0 * a.H * a.hd * a.pairs, s);    // executed: 4 matmuls
         AttnArgs b = a;
         b.hfast = attn_hfast(a.Hkv, a.nkwork128);
-        launch_k(attn_bwd_dkv_tc<HD, false>, attn_grid(a.Hkv, a.nkwork128), kThreadsBwd, DkvSmem<HD, false>::kAlloc,
+        launch_k(attn_bwd_dkv_tc<HD>, attn_grid(a.Hkv, a.nkwork128), kThreadsBwd, DkvSmem<HD>::kAlloc,
                                      s, b, *a.maps);
         EPP_CHECK_LAUNCH();
     }
@@ -1406,10 +1295,6 @@ void launch_bwd_tc(const AttnArgs& a, cudaStream_t s) {
 bool attn_fwd_tc_supported(const AttnArgs& a) {
     return a.dtype == DType::BF16 && (a.hd == 64 || a.hd == 128) && a.qwork256 != nullptr &&
            a.maps != nullptr;
-}
-
-bool attn_bwd_fused(const AttnArgs& a) {
-    return attention_impl() == 2 && a.hd == 128 && a.dqkv_out == nullptr && a.dq != nullptr;
 }
 
 bool attn_bwd_tc_supported(const AttnArgs& a) {

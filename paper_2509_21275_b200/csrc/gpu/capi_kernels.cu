@@ -120,26 +120,35 @@ struct AttnTables {
 
 extern "C" {
 
-int epp_gpu_set_attention_impl(int32_t impl) {
-    if (impl < 0 || impl > 2) return EPP_GPU_EARG;
-    eppk::attention_impl() = impl;
-    return EPP_GPU_OK;
-}
-
-int epp_kernel_gemm(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_kmajor,
-                    const void* B, int64_t ldb, int32_t b_kmajor, void* C, int64_t ldc,
-                    const void* R, int64_t ldr, int32_t epi, int32_t dtype, void* stream) {
+int epp_kernel_gemm_ex(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_kmajor,
+                       const void* B, int64_t ldb, int32_t b_kmajor, void* C, int64_t ldc,
+                       const void* R, int64_t ldr, void* C2, int64_t ldc2, int32_t epi, int32_t dtype,
+                       void* stream) {
     return eppk::kguard([&] {
         eppk::GemmArgs g;
         g.M = M; g.N = N; g.K = K;
         g.A = A; g.lda = lda; g.a_kmajor = a_kmajor != 0;
         g.B = B; g.ldb = ldb; g.b_kmajor = b_kmajor != 0;
         g.C = C; g.ldc = ldc; g.R = R; g.ldr = ldr;
-        EPP_REQUIRE(epi >= 0 && epi <= 3, "bad epilogue");
+        g.C2 = C2; g.ldc2 = ldc2;
+        EPP_REQUIRE(epi >= 0 && epi <= 5, "bad epilogue");
         g.epi = static_cast<eppk::Epi>(epi);
+        EPP_REQUIRE(g.epi != eppk::Epi::StoreGelu || C2 != nullptr, "StoreGelu needs C2");
+        EPP_REQUIRE(g.epi != eppk::Epi::GeluBwd || R != nullptr, "GeluBwd needs R (the pre-activation)");
         g.dtype = static_cast<eppk::DType>(dtype);
         eppk::gemm(g, static_cast<cudaStream_t>(stream));
     });
+}
+
+int epp_kernel_gemm(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_kmajor,
+                    const void* B, int64_t ldb, int32_t b_kmajor, void* C, int64_t ldc,
+                    const void* R, int64_t ldr, int32_t epi, int32_t dtype, void* stream) {
+    if (epi < 0 || epi > 3) {
+        eppk::gpu_error_slot() = "epp: bad epilogue";
+        return EPP_GPU_EARG;
+    }
+    return epp_kernel_gemm_ex(M, N, K, A, lda, a_kmajor, B, ldb, b_kmajor, C, ldc, R, ldr, nullptr, 0, epi,
+                              dtype, stream);
 }
 
 int epp_kernel_attention_fwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, float scale, int32_t nseg,

@@ -45,6 +45,9 @@ long long& launch_counter();
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 bool pdl_enabled();
+// Per-kernel launch counts of this library (epp_gpu_kernel_stats): which
+// kernel variants a run actually executed.
+void note_launch(const void* kernel);
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args&&... args) {
@@ -59,6 +62,7 @@ inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
     cfg.attrs = at;
     cfg.numAttrs = 1;
     EPP_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+    note_launch(reinterpret_cast<const void*>(kernel));
 }
 
 #define EPP_REQUIRE(cond, msg)                                                           \
@@ -110,22 +114,28 @@ __device__ __forceinline__ float gelu_tanh_grad_f(float x) {
     return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k * (1.f + 3.f * 0.044715f * x * x);
 }
 
-// bf16-path variants: MUFU.TANH (tanh.approx, rel. err ~5e-4, far below the
-// bf16 rounding of the result) instead of the ~20-instruction tanhf.
-__device__ __forceinline__ float tanh_fast(float x) {
-    float y;
-    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
+// bf16-path variants: gelu_tanh(x) = 0.5 x (1 + tanh(u)) = x * sigmoid(2u),
+// u = k (x + 0.044715 x^3), with the sigmoid from MUFU exp2 + a fast divide
+// (relative error ~1e-7 everywhere).  tanh.approx (abs. error ~5e-4) was
+// cheaper by one MUFU op but its error is relative to 1 + tanh(u): ~20 % of
+// gelu(x) at x = -3, a systematic bias that made the GPT-width gradients 1.6x
+// less accurate than a torch autocast run of the same model
+// (tools/bf16_error_table.py).
+__device__ __forceinline__ float gelu_sigmoid_arg_(float x, float& du) {
+    const float k2 = 2.f * 0.7978845608028654f;
+    du = k2 * fmaf(3.f * 0.044715f * x, x, 1.f);            // d(2u)/dx
+    return k2 * fmaf(0.044715f * x, x * x, x);               // 2u
 }
 __device__ __forceinline__ float gelu_tanh_fast_f(float x) {
-    const float k = 0.7978845608028654f;
-    const float h = 0.5f * x;
-    return fmaf(h, tanh_fast(k * fmaf(0.044715f * x, x * x, x)), h);
+    float du;
+    const float z = gelu_sigmoid_arg_(x, du);
+    return __fdividef(x, 1.f + __expf(-z));
 }
 __device__ __forceinline__ float gelu_tanh_grad_fast_f(float x) {
-    const float k = 0.7978845608028654f;
-    const float t = tanh_fast(k * fmaf(0.044715f * x, x * x, x));
-    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k * (1.f + 3.f * 0.044715f * x * x);
+    float du;
+    const float z = gelu_sigmoid_arg_(x, du);
+    const float s = __fdividef(1.f, 1.f + __expf(-z));
+    return fmaf(x * s * (1.f - s), du, s);
 }
 
 inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }

@@ -651,9 +651,10 @@ __global__ void act_bwd_k(int act, const T* h, const T* da, T* dh, long long Tn,
 }
 
 // -------------------------------------------------------- cross entropy ---
-// One CTA per row; logits overwritten with grad_scale * (softmax - onehot).
+// One CTA per row; logits overwritten with grad_scale * (softmax - onehot);
+// row_loss[row] = lse - logit[target] (0 for rows without a target).
 template <typename T>
-__global__ void ce_k(T* logits, const int32_t* targets, float* loss_acc, int V, float gscale) {
+__global__ void ce_k(T* logits, const int32_t* targets, float* row_loss, int V, float gscale) {
     pdl_wait();
     pdl_trigger();
     __shared__ float scratch[32];
@@ -702,11 +703,7 @@ __global__ void ce_k(T* logits, const int32_t* targets, float* loss_acc, int V, 
     const float M = scratch[0];
     const float lse = M + logf(scratch[1]);
     const bool valid = tgt >= 0;
-    if (threadIdx.x == 0 && valid) {
-        const float xt = to_f(lr[tgt]);
-        atomicAdd(loss_acc, lse - xt);
-        atomicAdd(loss_acc + 1, 1.f);
-    }
+    if (threadIdx.x == 0) row_loss[row] = valid ? lse - to_f(lr[tgt]) : 0.f;
     __syncthreads();   // target logit read before overwrite
     for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
         float v[8];
@@ -718,6 +715,43 @@ __global__ void ce_k(T* logits, const int32_t* targets, float* loss_acc, int V, 
             v[i] = p * gscale;
         }
         store8(lr + c, v);
+    }
+}
+
+// Per-chunk loss: (sum of row losses, #rows with a target) in fp64, one CTA,
+// fixed reduction order (deterministic); written to slot[0..1] and added to
+// the stage accumulator acc[0..1] (stream-ordered, so no atomics).
+__global__ void __launch_bounds__(1024) chunk_loss_k(const float* row_loss, const int32_t* targets, int Tn,
+                                                     double* slot, double* acc) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ double red_s[32], red_c[32];
+    double s = 0.0, c = 0.0;
+    for (int i = threadIdx.x; i < Tn; i += blockDim.x) {
+        s += static_cast<double>(row_loss[i]);
+        c += targets[i] >= 0 ? 1.0 : 0.0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        red_s[wid] = s;
+        red_c[wid] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double S = 0.0, C = 0.0;
+        for (int i = 0; i < (blockDim.x + 31) / 32; ++i) {
+            S += red_s[i];
+            C += red_c[i];
+        }
+        slot[0] = S;
+        slot[1] = C;
+        acc[0] += S;
+        acc[1] += C;
     }
 }
 
@@ -1033,15 +1067,21 @@ void act_bwd(DType t, int act, const void* h, const void* da, void* dh, int T, i
     EPP_CHECK_LAUNCH();
 }
 
-void cross_entropy(DType t, void* logits, const int32_t* targets, float* loss_acc, int T, int V,
+void cross_entropy(DType t, void* logits, const int32_t* targets, float* row_loss, int T, int V,
                    float grad_scale, cudaStream_t s) {
     ProfScope prof_(kProfCe, double(T) * V * 2 * dtype_size(t), s);
     EPP_REQUIRE(V % 8 == 0, "ce: V must be a multiple of 8");
     if (T == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        launch_k(ce_k<E>, T, 256, 0, s, static_cast<E*>(logits), targets, loss_acc, V, grad_scale);
+        launch_k(ce_k<E>, T, 256, 0, s, static_cast<E*>(logits), targets, row_loss, V, grad_scale);
     });
+    EPP_CHECK_LAUNCH();
+}
+
+void chunk_loss(const float* row_loss, const int32_t* targets, int T, double* slot, double* acc, cudaStream_t s) {
+    ProfScope prof_(kProfCe, double(T) * 8, s);
+    launch_k(chunk_loss_k, 1, 1024, 0, s, row_loss, targets, T, slot, acc);
     EPP_CHECK_LAUNCH();
 }
 

@@ -29,14 +29,6 @@ namespace eppk {
 static std::atomic<long long> g_gemm_launches{0};
 long long gemm_launch_count() { return g_gemm_launches.load(); }
 
-// CTA-pair GEMM on by default; EPP_GEMM_PAIR=0 selects the single-CTA kernel (A/B runs).
-static bool gemm_pair_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("EPP_GEMM_PAIR");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
 
 
 // =========================================================================
@@ -858,7 +850,7 @@ void gemm(const GemmArgs& g, cudaStream_t s) {
     // use 128-wide tiles to expose more CTAs.
     const long long tiles256 = static_cast<long long>(ceil_div(g.N, 256)) * ceil_div(g.M, kBM);
     const long long pair_tiles = static_cast<long long>(ceil_div(g.N, 256)) * ceil_div(g.M, 2 * kBM);
-    if (g.K > 0 && g.N % 256 == 0 && pair_tiles >= 60 && gemm_pair_enabled())
+    if (g.K > 0 && g.N % 256 == 0 && pair_tiles >= 60)
         dispatch_epi2<256, 6>(g, s);      // CTA pairs: 256 x 256 tiles
     else if (g.N % 256 == 0 && tiles256 >= 120)
         dispatch_epi<256, 4>(g, s);

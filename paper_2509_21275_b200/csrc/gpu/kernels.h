@@ -140,15 +140,10 @@ struct AttnArgs {
 };
 
 void attn_fwd(const AttnArgs& a, cudaStream_t s);
-// tcgen05 variants (attention_tc.cu); attn_fwd dispatches to them when
-// supported unless EPP_ATTN_IMPL=fa2 is set.
-int& attention_impl();
+// tcgen05 kernels (attention_tc.cu): the bf16 implementation.
 bool attn_fwd_tc_supported(const AttnArgs& a);
 void attn_fwd_tc(const AttnArgs& a, cudaStream_t s);
 bool attn_bwd_tc_supported(const AttnArgs& a);
-// attention_impl() == 2 (hd 128, fp32 a.dq output): one fused tcgen05 kernel
-// forms dK, dV and dQ (reduced into a.dq) after a separate delta pass.
-bool attn_bwd_fused(const AttnArgs& a);
 void attn_delta(const AttnArgs& a, cudaStream_t s);   // delta = rowsum(dO * O)
 void attn_bwd_tc_main(const AttnArgs& a, cudaStream_t s);
 void attn_bwd(const AttnArgs& a, cudaStream_t s);
@@ -192,10 +187,12 @@ void act_fwd(DType t, int act, const void* h, void* a, int T, int F, cudaStream_
 void act_bwd(DType t, int act, const void* h, const void* da, void* dh, int T, int F,
              cudaStream_t s);
 
-// Cross entropy over logits rows [T, V] (in place: logits -> dlogits * scale).
-// loss_acc[0] += sum of losses over valid targets; loss_acc[1] += #valid.
-void cross_entropy(DType t, void* logits, const int32_t* targets, float* loss_acc, int T, int V,
+// Cross entropy over logits rows [T, V] (in place: logits -> dlogits * scale);
+// row_loss[t] = CE of row t (0 where targets[t] < 0).
+void cross_entropy(DType t, void* logits, const int32_t* targets, float* row_loss, int T, int V,
                    float grad_scale, cudaStream_t s);
+// slot = (sum row_loss, #targets >= 0) in fp64 (fixed order); acc += slot.
+void chunk_loss(const float* row_loss, const int32_t* targets, int T, double* slot, double* acc, cudaStream_t s);
 
 void fill_zero(void* p, size_t bytes, cudaStream_t s);
 void cast_f32_to(DType t, const float* src, void* dst, long long n, cudaStream_t s);

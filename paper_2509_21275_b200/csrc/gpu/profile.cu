@@ -1,8 +1,14 @@
 // epp-b200: opt-in per-launch timing of the dominant kernels (GEMM,
 // attention) with CUDA events recorded on the launching stream, so bench.py
 // can report achieved TFLOP/s of the kernel class live over its timed region.
+#include <cxxabi.h>
+
+#include <algorithm>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -101,6 +107,42 @@ int epp_gpu_profile_read(int32_t cls, double* ms, double* flops, int64_t* launch
     if (launches) *launches = a.n;
     return 0;
 }
+}
+
+namespace eppk {
+namespace {
+std::mutex g_kmu;
+std::unordered_map<const void*, long long> g_kcount;
+std::vector<std::pair<std::string, long long>> g_kview;   // last epp_gpu_kernel_stats snapshot
+}  // namespace
+
+void note_launch(const void* kernel) {
+    std::lock_guard<std::mutex> lk(g_kmu);
+    ++g_kcount[kernel];
+}
+}  // namespace eppk
+
+extern "C" int epp_gpu_kernel_stats(int32_t idx, const char** name, int64_t* count) {
+    std::lock_guard<std::mutex> lk(eppk::g_kmu);
+    if (idx == 0) {   // snapshot: demangled name -> launches, sorted by name
+        std::map<std::string, long long> agg;
+        for (const auto& kv : eppk::g_kcount) {
+            const char* raw = nullptr;
+            std::string nm = "?";
+            if (cudaFuncGetName(&raw, kv.first) == cudaSuccess && raw) {
+                int st = 0;
+                char* dm = abi::__cxa_demangle(raw, nullptr, nullptr, &st);
+                nm = (st == 0 && dm) ? dm : raw;
+                std::free(dm);
+            }
+            agg[nm] += kv.second;
+        }
+        eppk::g_kview.assign(agg.begin(), agg.end());
+    }
+    if (idx < 0 || idx >= static_cast<int32_t>(eppk::g_kview.size())) return EPP_GPU_EARG;
+    if (name) *name = eppk::g_kview[idx].first.c_str();
+    if (count) *count = eppk::g_kview[idx].second;
+    return EPP_GPU_OK;
 }
 
 namespace eppk {

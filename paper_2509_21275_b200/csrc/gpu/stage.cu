@@ -250,8 +250,10 @@ public:
                 EPP_CUDA(cudaMalloc(&p.work, 2 * p.numel));
             }
         }
-        EPP_CUDA(cudaMalloc(&loss_acc_, sizeof(float) * 2));
-        EPP_CUDA(cudaMemset(loss_acc_, 0, sizeof(float) * 2));
+        // fp64 loss records: [0..1] the stage accumulator, then one
+        // (sum, #targets) slot per chunk id forwarded since the last reset
+        EPP_CUDA(cudaMalloc(&loss_acc_, sizeof(double) * 2 * (1 + kLossSlots)));
+        EPP_CUDA(cudaMemset(loss_acc_, 0, sizeof(double) * 2 * (1 + kLossSlots)));
         // Keep freed chunk memory in the pool instead of returning it to the OS.
         int dev = 0;
         EPP_CUDA(cudaGetDevice(&dev));
@@ -316,19 +318,32 @@ public:
     }
 
     void loss(double out[2], bool reset, cudaStream_t s) {
-        float h[2];
-        EPP_CUDA(cudaMemcpyAsync(h, loss_acc_, sizeof(h), cudaMemcpyDeviceToHost, s));
+        EPP_CUDA(cudaMemcpyAsync(out, loss_acc_, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
         EPP_CUDA(cudaStreamSynchronize(s));
-        out[0] = h[0];
-        out[1] = h[1];
-        if (reset) EPP_CUDA(cudaMemsetAsync(loss_acc_, 0, sizeof(float) * 2, s));
+        if (reset) reset_loss(s);
     }
 
     // Stream-ordered copy of the accumulator into caller memory (pinned host
     // or device), optional reset; no synchronisation.
-    void loss_async(float* out2, bool reset, cudaStream_t s) {
-        EPP_CUDA(cudaMemcpyAsync(out2, loss_acc_, sizeof(float) * 2, cudaMemcpyDefault, s));
-        if (reset) EPP_CUDA(cudaMemsetAsync(loss_acc_, 0, sizeof(float) * 2, s));
+    void loss_async(double* out2, bool reset, cudaStream_t s) {
+        EPP_CUDA(cudaMemcpyAsync(out2, loss_acc_, sizeof(double) * 2, cudaMemcpyDefault, s));
+        if (reset) reset_loss(s);
+    }
+
+    // (sum of token losses, #targets) of the latest forward of `chunk_id`
+    // since the last reset (a plan's chunk ids repeat from step to step).
+    void read_chunk_loss(int chunk_id, double out[2], cudaStream_t s) {
+        EPP_REQUIRE(has_head_, "chunk loss: not the last stage");
+        auto it = loss_slot_.find(chunk_id);
+        EPP_REQUIRE(it != loss_slot_.end(), "chunk loss: chunk not forwarded since the last reset");
+        EPP_CUDA(cudaMemcpyAsync(out, loss_acc_ + 2 * (1 + it->second), sizeof(double) * 2,
+                                 cudaMemcpyDeviceToHost, s));
+        EPP_CUDA(cudaStreamSynchronize(s));
+    }
+
+    void reset_loss(cudaStream_t s) {
+        EPP_CUDA(cudaMemsetAsync(loss_acc_, 0, sizeof(double) * 2, s));
+        loss_slot_.clear();
     }
 
     void release_seq(int seq) { seqs_.erase(seq); }
@@ -355,23 +370,27 @@ public:
             const void* x = cs.x_in.get();
             for (int j = 0; j < nl_; ++j) {
                 LayerSaved& L = cs.layers[j];
-                const bool last = j == nl_ - 1;
-                L.x_out = Buf(&pool_, act_bytes, s);
-                layer_forward(cs, j, x, L, /*out=*/L.x_out.get(), /*skip_out=*/false, s);
+                // the last layer of a non-head stage writes its output straight
+                // into act_out (the caller's buffer, e.g. the next stage's P2P
+                // mailbox in peer memory): its backward never reads it
+                void* out = nullptr;
+                if (j == nl_ - 1 && !has_head_) {
+                    EPP_REQUIRE(act_out != nullptr, "act_out is null");
+                    out = act_out;
+                } else {
+                    L.x_out = Buf(&pool_, act_bytes, s);
+                    out = L.x_out.get();
+                }
+                layer_forward(cs, j, x, L, out, /*skip_out=*/false, s);
                 if (j < cs.ckpt) drop_full(L);
-                x = L.x_out.get();
-                (void)last;
+                x = out;
             }
             if (has_head_) {
                 head_forward(cs, c, x, s);
-            } else {
+            } else if (nl_ == 0) {
                 EPP_REQUIRE(act_out != nullptr, "act_out is null");
                 EPP_CUDA(cudaMemcpyAsync(act_out, x, act_bytes, cudaMemcpyDeviceToDevice, s));
             }
-            // The last layer's output is only needed downstream (or by the
-            // head, already consumed); keep it only where the final norm's
-            // backward needs it (last stage).
-            if (!has_head_ && nl_ > 0) cs.layers[nl_ - 1].x_out.release();
         } catch (...) {
             chunks_.erase(c.id);
             throw;
@@ -383,17 +402,21 @@ public:
         EPP_REQUIRE(it != chunks_.end(), "backward of a chunk that was not forwarded");
         ChunkState& cs = it->second;
         const size_t act_bytes = static_cast<size_t>(cs.T) * D_ * esz();
-        // d(stage output)
-        Buf dy(&pool_, act_bytes, s);
+        // d(stage output): the head's final-norm backward, or grad_in used in
+        // place (read by the last layer's backward only; the caller keeps it
+        // valid until this call's work has run)
+        Buf dy;
+        const void* dy_ptr = grad_in;
         if (has_head_) {
+            dy = Buf(&pool_, act_bytes, s);
             const void* xl = nl_ > 0 ? cs.layers[nl_ - 1].x_out.get() : cs.x_in.get();
             norm_bwd(dt_, llama_, xl, work(lnf_w_), cs.dxf.get(), cs.meanf.get<float>(),
                      cs.rstdf.get<float>(), nullptr, dy.get(), grad(lnf_w_),
                      lnf_b_ >= 0 ? grad(lnf_b_) : nullptr, cs.T, D_, s);
             cs.dxf.release();
+            dy_ptr = dy.get();
         } else {
             EPP_REQUIRE(grad_in != nullptr, "grad_in is null");
-            EPP_CUDA(cudaMemcpyAsync(dy.get(), grad_in, act_bytes, cudaMemcpyDeviceToDevice, s));
         }
         attach_dkv(cs, c, s);
 
@@ -401,17 +424,28 @@ public:
             LayerSaved& L = cs.layers[j];
             const void* x = j == 0 ? cs.x_in.get() : cs.layers[j - 1].x_out.get();
             if (!L.full) layer_forward(cs, j, x, L, nullptr, /*skip_out=*/true, s);   // recompute
-            Buf dx(&pool_, act_bytes, s);
-            layer_backward(cs, j, x, L, dy.get(), dx.get(), s);
+            // the first layer of a non-embedding stage writes d(stage input)
+            // straight into grad_out (e.g. the previous stage's P2P mailbox)
+            Buf dx;
+            void* dx_ptr = nullptr;
+            if (j == 0 && !has_embed_) {
+                EPP_REQUIRE(grad_out != nullptr, "grad_out is null");
+                dx_ptr = grad_out;
+            } else {
+                dx = Buf(&pool_, act_bytes, s);
+                dx_ptr = dx.get();
+            }
+            layer_backward(cs, j, x, L, dy_ptr, dx_ptr, s);
             drop_full(L);
             L.x_out.release();
             dy = std::move(dx);
+            dy_ptr = dx_ptr;
         }
         if (has_embed_) {
-            embed_bwd(dt_, c.token_ids, dy.get(), grad(emb_), cs.T, D_, s);
-        } else {
+            embed_bwd(dt_, c.token_ids, dy_ptr, grad(emb_), cs.T, D_, s);
+        } else if (nl_ == 0) {
             EPP_REQUIRE(grad_out != nullptr, "grad_out is null");
-            EPP_CUDA(cudaMemcpyAsync(grad_out, dy.get(), act_bytes, cudaMemcpyDeviceToDevice, s));
+            EPP_CUDA(cudaMemcpyAsync(grad_out, dy_ptr, act_bytes, cudaMemcpyDeviceToDevice, s));
         }
         dy.release();
         const bool first_slice = c.seq >= 0 && c.context == 0;
@@ -756,13 +790,12 @@ private:
         Buf delta(&pool_, sizeof(float) * static_cast<size_t>(H_) * T, s);
         Buf dqkv(&pool_, static_cast<size_t>(T) * Nqkv_ * e, s);
         AttnArgs a = attn_args(cs, j);
-        // tcgen05 backward: the dK/dV kernel writes every key row of a packed
-        // segment exactly once (dkv_accum = 0) and the dQ kernel writes the
-        // un-rotated bf16 dQ straight into dqkv; the other kernels accumulate
-        // into zeroed buffers and leave dQ in fp32 for the gather pass
-        // (fused: one kernel forms dK/dV and reduces dQ into fp32 dq)
-        const bool fused = dt_ == DType::BF16 && attention_impl() == 2 && hd_ == 128;
-        const bool tc_bwd = dt_ == DType::BF16 && attention_impl() >= 1;
+        // bf16 (tcgen05): the dK/dV kernel writes every key row of a packed
+        // segment exactly once (dkv_accum = 0), and the dQ and dK/dV kernels
+        // write un-rotated bf16 dQ / dK / dV straight into dqkv.  fp32 parity
+        // kernels: accumulate into zeroed buffers, fp32 dQ, then the RoPE
+        // gather pass.
+        const bool tc_bwd = dt_ == DType::BF16;
         if (!tc_bwd) fill_zero(cs.dkv_local.get(), 2 * static_cast<size_t>(T) * kvw() * sizeof(float), s);
         a.q = L.q.get();
         a.o = L.o.get();
@@ -770,23 +803,20 @@ private:
         a.dout = dout.get();
         a.delta = delta.get<float>();
         Buf dq;
-        if (tc_bwd && !fused) {
+        if (tc_bwd) {
             a.dqkv_out = dqkv.get();
             a.tok_pos = cs.tok_pos.get<int>();
             a.rope_cs = rope_table_ptr(hd_, m_.rope_theta, s);
+            attn_maps_q(cs.maps, L.q.get(), dout.get(), T, H_, hd_);
+            a.maps = &cs.maps;
         } else {
             dq = Buf(&pool_, sizeof(float) * static_cast<size_t>(T) * Dq, s);
             a.dq = dq.get<float>();
         }
-        if (dt_ == DType::BF16) {
-            attn_maps_q(cs.maps, L.q.get(), dout.get(), T, H_, hd_);
-            a.maps = &cs.maps;
-        }
         attn_bwd(a, s);
         dout.release();
         delta.release();
-        // (the tcgen05 kernels already wrote un-rotated bf16 dQ, dK, dV into dqkv)
-        if (!tc_bwd || fused)
+        if (!tc_bwd)
             rope_qkv_gather_grad(dt_, dq.get<float>(), cs.segs_dev.get<AttnSeg>(), cs.tok_seg.get<int>(),
                                  cs.tok_pos.get<int>(), dqkv.get(), T, H_, Hkv_, hd_, j, m_.rope_theta, s);
         dq.release();
@@ -816,16 +846,24 @@ private:
         cs.dxf = Buf(&pool_, static_cast<size_t>(T) * D_ * e, s);
         const int rows = std::max(1, std::min(T, static_cast<int>((512LL << 20) / (static_cast<long long>(V) * e))));
         Buf logits(&pool_, static_cast<size_t>(rows) * V * e, s);
+        Buf row_loss(&pool_, sizeof(float) * T, s);
         for (int r0 = 0; r0 < T; r0 += rows) {
             const int n = std::min(rows, T - r0);
             const uint8_t* xr = xf.get<uint8_t>() + static_cast<size_t>(r0) * D_ * e;
             gemm(mk(n, V, D_, xr, D_, true, work(lm_), D_, true, logits.get(), V), s);
-            cross_entropy(dt_, logits.get(), c.target_ids + r0, loss_acc_, n, V, c.loss_scale, s);
+            cross_entropy(dt_, logits.get(), c.target_ids + r0, row_loss.get<float>() + r0, n, V, c.loss_scale, s);
             // dXf = dLogits Wlm ; dWlm += dLogits^T Xf
             gemm(mk(n, D_, V, logits.get(), V, true, work(lm_), D_, false,
                     cs.dxf.get<uint8_t>() + static_cast<size_t>(r0) * D_ * e, D_), s);
             wgrad(V, D_, n, logits.get(), V, xr, D_, grad(lm_), s);
         }
+        auto slot = loss_slot_.find(c.id);
+        if (slot == loss_slot_.end()) {
+            EPP_REQUIRE(loss_slot_.size() < static_cast<size_t>(kLossSlots),
+                        "chunk loss: too many chunks since the last loss reset");
+            slot = loss_slot_.emplace(c.id, static_cast<int>(loss_slot_.size())).first;
+        }
+        chunk_loss(row_loss.get<float>(), c.target_ids, T, loss_acc_ + 2 * (1 + slot->second), loss_acc_, s);
     }
 
     GemmArgs mk(int M, int N, int K, const void* A, long long lda, bool ak, const void* B,
@@ -855,7 +893,9 @@ private:
     std::vector<Param> params_;
     std::vector<LayerParams> lps_;
     int emb_ = -1, lnf_w_ = -1, lnf_b_ = -1, lm_ = -1;
-    float* loss_acc_ = nullptr;
+    static constexpr int kLossSlots = 1 << 16;
+    double* loss_acc_ = nullptr;
+    std::map<int, int> loss_slot_;   // chunk id -> loss record
     Pool pool_;
     PinnedRing ring_{32u << 20};
     std::map<int, ChunkState> chunks_;
@@ -965,7 +1005,14 @@ int epp_stage_loss(epp_stage* st, double out[2], int32_t reset, void* stream) {
     return guard([&] { st->impl->loss(out, reset != 0, S(stream)); });
 }
 
-int epp_stage_loss_async(epp_stage* st, float* out2, int32_t reset, void* stream) {
+int epp_stage_chunk_loss(epp_stage* st, int32_t chunk_id, double out[2], void* stream) {
+    return guard([&] {
+        EPP_REQUIRE(out != nullptr, "out is null");
+        st->impl->read_chunk_loss(chunk_id, out, S(stream));
+    });
+}
+
+int epp_stage_loss_async(epp_stage* st, double* out2, int32_t reset, void* stream) {
     return guard([&] {
         EPP_REQUIRE(out2 != nullptr, "out2 is null");
         st->impl->loss_async(out2, reset != 0, S(stream));

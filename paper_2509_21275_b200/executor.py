@@ -200,33 +200,73 @@ def allreduce_grads(stage, group, replicas: int) -> None:
 class DistributedPipeline:
     """One stage per rank (rank = stage) of a pipeline.
 
-    Transport: device tensors go straight to NCCL (B200s: NVLink P2P);
-    with a gloo group and CUDA stages (the multi-process test that shares one
-    GPU) messages are staged through host memory instead.  `pipe` =
-    (global ranks of the stages, fwd groups, bwd groups) from
-    pipeline_groups(); by default the whole world is one pipeline."""
+    Transport:
+      * CUDA stages (gpu.CudaStage): the C-ABI P2P channels over peer memory
+        (include/epp_gpu.h epp_p2p_*; NVLink between the 8 B200s, CUDA IPC
+        between processes).  The sending stage's last kernel stores its
+        output straight into the receiver's mailbox, the receiver copies an
+        activation into its own input buffer (a gradient is read in place)
+        and releases the slot; all waits are stream-ordered, the host never
+        blocks, nothing stays alive after the call that consumed it.
+        torch.distributed only exchanges the channel handles at setup.
+      * other stages (the CPU oracle stages in the gloo tests):
+        torch.distributed isend / irecv, two groups per adjacent pair so the
+        forward and backward message streams never block each other.
+    Both sides derive every message size from the plan, no handshake.
+    `pipe` = (global ranks of the stages, fwd groups, bwd groups) from
+    pipeline_groups(); by default the whole world is one pipeline.
+    `max_tokens`: the largest chunk any plan will send (sizes the mailboxes:
+    two such messages per channel)."""
 
     def __init__(self, stage, rank: int, world: int, device: torch.device, hidden: int,
-                 act_dtype: torch.dtype, pipe=None):
+                 act_dtype: torch.dtype, pipe=None, max_tokens: int = 0):
         import torch.distributed as dist
         self.dist = dist
         self.stage, self.rank, self.world = stage, rank, world
         self.device, self.hidden, self.act_dtype = device, hidden, act_dtype
-        self.via_host = device.type == "cuda" and dist.get_backend() == "gloo"
         if pipe is None:
             (pipe,), _ = pipeline_groups(world, 1)
         self.ranks, self.fwd_groups, self.bwd_groups = pipe
         self.p2p_bytes = 0
+        self.p2p = bool(getattr(stage, "supports_p2p", False))
+        self.ch = {}
+        if self.p2p:
+            self._open_channels(max_tokens)
 
+    def _open_channels(self, max_tokens: int):
+        """Endpoints: 'fin' (activations from p-1), 'fout' (to p+1), 'bin'
+        (gradients from p+1), 'bout' (to p-1).  Receivers own the arenas."""
+        from .gpu import P2PChannel
+        p, dp = self.rank, self.world
+        esz = torch.tensor([], dtype=self.act_dtype).element_size()
+        arena = 2 * max(1, int(max_tokens)) * self.hidden * esz
+        if p > 0:
+            self.ch["fin"] = P2PChannel("recv", arena)
+            self.ch["bout"] = P2PChannel("send")
+        if p + 1 < dp:
+            self.ch["fout"] = P2PChannel("send")
+            self.ch["bin"] = P2PChannel("recv", arena)
+        mine = {k: c.handle for k, c in self.ch.items()}
+        got = [None] * self.dist.get_world_size()
+        self.dist.all_gather_object(got, (self.ranks[p], mine))
+        by_rank = {r: h for (r, h) in got}
+        peer = {"fin": (p - 1, "fout"), "bout": (p - 1, "bin"), "fout": (p + 1, "fin"), "bin": (p + 1, "bout")}
+        for k, c in self.ch.items():
+            q, their = peer[k]
+            c.open(by_rank[self.ranks[q]][their])
+
+    def close(self):
+        for c in self.ch.values():
+            c.close()
+        self.ch = {}
+
+    # -- torch.distributed transport (CPU oracle stages) ----------------------
     def _recv(self, T: int, src: int, group) -> torch.Tensor:
-        dev = torch.device("cpu") if self.via_host else self.device
-        buf = torch.empty((T, self.hidden), dtype=self.act_dtype, device=dev)
+        buf = torch.empty((T, self.hidden), dtype=self.act_dtype, device=self.device)
         self.dist.irecv(buf, src=src, group=group).wait()
-        return buf.to(self.device) if self.via_host else buf
+        return buf
 
     def _send(self, t: torch.Tensor, dst: int, group, pending: list):
-        if self.via_host:
-            t = t.cpu()
         pending.append((self.dist.isend(t, dst=dst, group=group), t))
         self.p2p_bytes += t.numel() * t.element_size()
 
@@ -235,23 +275,54 @@ class DistributedPipeline:
         if dp != plan.pp_degree:
             raise ValueError(f"plan is for {plan.pp_degree} stages, world size is {dp}")
         toks = staged or _ChunkTokens(plan, tokens, self.device, need_ids=(p == 0), need_targets=(p == dp - 1))
-        pending = []
         for unit in plan.units:
-            n = len(unit.chunks)
-            for kind, pos in stage_ops(n, unit.n_prefill, dp, p + 1, unit.backward_order):
-                T = plan.chunks[unit.chunks[pos]].tokens
-                op = _op(plan, unit, pos, p, toks)
-                if kind == "F":
-                    act_in = self._recv(T, self.ranks[p - 1], self.fwd_groups[p - 1]) if p > 0 else None
-                    out = self.stage.forward(op, act_in)
-                    if p + 1 < dp:
-                        self._send(out, self.ranks[p + 1], self.fwd_groups[p], pending)
-                else:
-                    g_in = self._recv(T, self.ranks[p + 1], self.bwd_groups[p]) if p + 1 < dp else None
-                    g_out = self.stage.backward(op, g_in)
-                    if p > 0:
-                        self._send(g_out, self.ranks[p - 1], self.bwd_groups[p - 1], pending)
-            for w, _ in pending:
-                w.wait()
-            pending.clear()
+            if self.p2p:
+                self._run_unit_p2p(plan, unit, toks)
+            else:
+                self._run_unit_dist(plan, unit, toks)
         return {"h2d_bytes": toks.h2d_bytes}
+
+    def _run_unit_p2p(self, plan: Plan, unit, toks: _ChunkTokens):
+        p, dp, ch = self.rank, self.world, self.ch
+        for kind, pos in stage_ops(len(unit.chunks), unit.n_prefill, dp, p + 1, unit.backward_order):
+            op = _op(plan, unit, pos, p, toks)
+            nbytes = self.stage.act_bytes(op)
+            if kind == "F":
+                src = ch["fin"].recv_wait(nbytes) if p > 0 else None
+                dst = ch["fout"].send_reserve(nbytes) if p + 1 < dp else None
+                self.stage.forward(op, src, out_ptr=dst)
+                if src is not None:
+                    ch["fin"].recv_release()      # the stage copied it (stream-ordered)
+                if dst is not None:
+                    ch["fout"].send_commit()
+                    self.p2p_bytes += nbytes
+            else:
+                g = ch["bin"].recv_wait(nbytes) if p + 1 < dp else None
+                dst = ch["bout"].send_reserve(nbytes) if p > 0 else None
+                self.stage.backward(op, g, out_ptr=dst)
+                if g is not None:
+                    ch["bin"].recv_release()
+                if dst is not None:
+                    ch["bout"].send_commit()
+                    self.p2p_bytes += nbytes
+
+    def _run_unit_dist(self, plan: Plan, unit, toks: _ChunkTokens):
+        p, dp = self.rank, self.world
+        pending = []
+        for kind, pos in stage_ops(len(unit.chunks), unit.n_prefill, dp, p + 1, unit.backward_order):
+            T = plan.chunks[unit.chunks[pos]].tokens
+            op = _op(plan, unit, pos, p, toks)
+            if kind == "F":
+                act_in = self._recv(T, self.ranks[p - 1], self.fwd_groups[p - 1]) if p > 0 else None
+                out = self.stage.forward(op, act_in)
+                if p + 1 < dp:
+                    self._send(out, self.ranks[p + 1], self.fwd_groups[p], pending)
+            else:
+                g_in = self._recv(T, self.ranks[p + 1], self.bwd_groups[p]) if p + 1 < dp else None
+                g_out = self.stage.backward(op, g_in)
+                if p > 0:
+                    self._send(g_out, self.ranks[p - 1], self.bwd_groups[p - 1], pending)
+            # a send's buffer is released as soon as it completed
+            pending = [(w, t) for (w, t) in pending if not w.is_completed()]
+        for w, _ in pending:
+            w.wait()

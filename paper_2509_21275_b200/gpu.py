@@ -73,10 +73,12 @@ def lib():
             "epp_stage_adamw_step": [vp, f32, f32, f32, f32, f32, i32, vp],
             "epp_stage_memory": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)],
             "epp_gpu_profile": [i32],
-            "epp_gpu_set_attention_impl": [i32],
+            "epp_stage_chunk_loss": [vp, i32, ctypes.POINTER(ctypes.c_double), vp],
             "epp_gpu_profile_read": [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(i64), i32],
             "epp_kernel_gemm": [i32, i32, i32, vp, i64, i32, vp, i64, i32, vp, i64, vp, i64, i32, i32, vp],
+            "epp_kernel_gemm_ex": [i32, i32, i32, vp, i64, i32, vp, i64, i32, vp, i64, vp, i64, vp, i64, i32, i32,
+                                   vp],
             "epp_kernel_attention_fwd": [i32, i32, i32, i32, f32, i32, ctypes.POINTER(i32),
                                          ctypes.POINTER(i32), ctypes.POINTER(i32),
                                          ctypes.POINTER(vp), ctypes.POINTER(vp), vp, vp, vp, i32, vp],
@@ -89,6 +91,25 @@ def lib():
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = ctypes.c_int
+        p2p = {
+            "epp_p2p_init": [ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
+            "epp_p2p_create": [ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(vp), ctypes.c_char_p],
+            "epp_p2p_open": [vp, ctypes.c_char_p],
+            "epp_p2p_send_reserve": [vp, ctypes.c_uint64, vp, ctypes.POINTER(vp)],
+            "epp_p2p_send_commit": [vp, vp],
+            "epp_p2p_recv_wait": [vp, ctypes.c_uint64, vp, ctypes.POINTER(vp)],
+            "epp_p2p_recv_release": [vp, vp],
+            "epp_p2p_send": [vp, vp, ctypes.c_uint64, vp],
+            "epp_p2p_recv": [vp, vp, ctypes.c_uint64, vp],
+            "epp_p2p_stats": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)],
+            "epp_p2p_destroy": [vp],
+        }
+        for name, args in p2p.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        L.epp_gpu_kernel_stats.argtypes = [i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(i64)]
+        L.epp_gpu_kernel_stats.restype = ctypes.c_int
         L.epp_gpu_last_error.restype = ctypes.c_char_p
         L.epp_gpu_kernel_launches.restype = ctypes.c_int64
         _lib = L
@@ -100,12 +121,6 @@ def check(rc: int) -> None:
         raise EppGpuError(lib().epp_gpu_last_error().decode())
 
 
-def set_attention_impl(name: str) -> None:
-    """'tc' (tcgen05, default), 'fused' (tcgen05, single-pass dK/dV/dQ
-    backward for hd 128) or 'fa2' (mma.sync) attention kernels."""
-    check(lib().epp_gpu_set_attention_impl({"fa2": 0, "tc": 1, "fused": 2}[name]))
-
-
 def pool_reserve(nbytes: int) -> None:
     """Pre-reserve device memory for stage activations (see epp_gpu.h)."""
     check(lib().epp_gpu_pool_reserve(int(max(0, nbytes)), stream_ptr()))
@@ -115,21 +130,108 @@ def kernel_launches() -> int:
     return int(lib().epp_gpu_kernel_launches())
 
 
+def kernel_stats() -> Dict[str, int]:
+    """{demangled kernel name: launches so far} of this library's kernels."""
+    L, out, i = lib(), {}, 0
+    name, cnt = ctypes.c_char_p(), ctypes.c_int64()
+    while L.epp_gpu_kernel_stats(i, ctypes.byref(name), ctypes.byref(cnt)) == 0:
+        out[name.value.decode()] = int(cnt.value)
+        i += 1
+    return out
+
+
 def stream_ptr(stream: Optional[torch.cuda.Stream] = None) -> ctypes.c_void_p:
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
-    return None if t is None else t.data_ptr()
+def _ptr(t) -> Optional[int]:
+    """Device address of a tensor, or an address passed as an int (e.g. a
+    P2P mailbox slot)."""
+    if t is None or isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+P2P_HANDLE_BYTES = 256
+
+
+class P2PChannel:
+    """One endpoint of a directed stage-to-stage message stream over peer
+    memory (include/epp_gpu.h epp_p2p_*): role 'send' or 'recv'; the
+    receiver owns the mailbox arena (>= the largest message).  Exchange
+    `.handle` with the peer out of band, then open(peer_handle)."""
+
+    def __init__(self, role: str, arena_bytes: int = 0):
+        self.role = role
+        buf = ctypes.create_string_buffer(P2P_HANDLE_BYTES)
+        h = ctypes.c_void_p()
+        check(lib().epp_p2p_create({"send": 0, "recv": 1}[role], int(arena_bytes), ctypes.byref(h), buf))
+        self.h = h
+        self.handle = buf.raw
+
+    def open(self, peer_handle: bytes):
+        check(lib().epp_p2p_open(self.h, peer_handle))
+
+    def send_reserve(self, nbytes: int) -> int:
+        p = ctypes.c_void_p()
+        check(lib().epp_p2p_send_reserve(self.h, int(nbytes), stream_ptr(), ctypes.byref(p)))
+        return p.value
+
+    def send_commit(self):
+        check(lib().epp_p2p_send_commit(self.h, stream_ptr()))
+
+    def recv_wait(self, nbytes: int) -> int:
+        p = ctypes.c_void_p()
+        check(lib().epp_p2p_recv_wait(self.h, int(nbytes), stream_ptr(), ctypes.byref(p)))
+        return p.value
+
+    def recv_release(self):
+        check(lib().epp_p2p_recv_release(self.h, stream_ptr()))
+
+    def send(self, t: torch.Tensor):
+        check(lib().epp_p2p_send(self.h, ctypes.c_void_p(t.data_ptr()), t.numel() * t.element_size(),
+                                 stream_ptr()))
+
+    def recv(self, t: torch.Tensor):
+        check(lib().epp_p2p_recv(self.h, ctypes.c_void_p(t.data_ptr()), t.numel() * t.element_size(),
+                                 stream_ptr()))
+
+    def stats(self):
+        n, b = ctypes.c_int64(), ctypes.c_int64()
+        check(lib().epp_p2p_stats(self.h, ctypes.byref(n), ctypes.byref(b)))
+        return n.value, b.value
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            check(lib().epp_p2p_destroy(self.h))
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def p2p_init(devices) -> None:
+    """Enable peer access among `devices` (one process driving several GPUs)."""
+    arr = (ctypes.c_int * len(devices))(*devices)
+    check(lib().epp_p2p_init(len(devices), arr))
 
 
 class CudaStage:
     """One pipeline stage on the current CUDA device (the CUDA executor)."""
 
     def __init__(self, model: ModelConfig, first: int, num: int, has_embed: bool, has_head: bool,
-                 dtype: str = "bf16", device: Optional[int] = None):
+                 dtype: str = "bf16", device: Optional[int] = None, plan_stage_layers: Optional[int] = None):
+        """plan_stage_layers: the per-stage layer count the planner priced
+        (L / d_p; Eq. 10 assumes uniform stages).  With a head-balanced split
+        this stage may hold `num` != that; checkpoint counts from the plan are
+        rescaled so the full-activation layers kept never exceed what the
+        planner charged (see _ckpt_layers)."""
         self.model, self.first, self.num = model, first, num
+        self.plan_layers = int(plan_stage_layers or num)
         self.has_embed, self.has_head = has_embed, has_head
         self.dtype = dtype
         self.tdtype = TORCH_DTYPES[dtype]
@@ -201,9 +303,17 @@ class CudaStage:
         return out[0], out[1]
 
     def loss_async(self, out2: torch.Tensor, reset: bool = False):
-        """Enqueue a copy of (loss sum, #targets) into `out2` (2 fp32, pinned
+        """Enqueue a copy of (loss sum, #targets) into `out2` (2 fp64, pinned
         host or device) on the current stream; the caller synchronises."""
+        assert out2.dtype == torch.float64 and out2.numel() >= 2
         check(lib().epp_stage_loss_async(self.h, ctypes.c_void_p(out2.data_ptr()), int(reset), stream_ptr()))
+
+    def chunk_loss(self, chunk_id: int):
+        """(sum of token losses, #targets) of one micro-batch (epp::Chunk),
+        its latest forward since the last loss reset (fp64)."""
+        out = (ctypes.c_double * 2)()
+        check(lib().epp_stage_chunk_loss(self.h, int(chunk_id), out, stream_ptr()))
+        return out[0], out[1]
 
     def memory(self):
         live, peak = ctypes.c_int64(), ctypes.c_int64()
@@ -211,31 +321,55 @@ class CudaStage:
         return live.value, peak.value
 
     # -- chunk ops -------------------------------------------------------------
+    def _ckpt_layers(self, c: int) -> int:
+        """Layers to checkpoint for a plan count c of a uniform stage of
+        plan_layers layers: the planner charges (plan_layers - c) /
+        plan_layers of the stage's full activations (model.planner_config
+        scales token_act_bytes to the LARGEST stage), so this stage keeps at
+        most floor((plan_layers - c) * num / plan_layers) full layers."""
+        P, n = self.plan_layers, self.num
+        c = max(0, min(int(c), P))
+        if P == n:
+            return c
+        return max(0, min(n, n - ((P - c) * n) // P))
+
     def _desc(self, c) -> ChunkDesc:
         slices = (ctypes.c_int64 * len(c.slices))(*c.slices)
         self._keep[c.id] = slices
-        # the ladder counts layers of a uniform L/d_p stage; a head-balanced
-        # split can give this stage fewer layers than that
-        ckpt = min(int(c.ckpt_layers), self.num)
+        ckpt = self._ckpt_layers(c.ckpt_layers)
         return ChunkDesc(c.id, c.seq, c.kind, int(c.tail), c.context, c.seq_len, len(c.slices),
                          slices, ckpt, c.loss_scale, _ptr(c.token_ids), _ptr(c.target_ids))
 
-    def forward(self, c, act_in: Optional[torch.Tensor]) -> Optional[torch.Tensor]:
+    supports_p2p = True
+
+    def act_bytes(self, c) -> int:
+        """Bytes of one [T, hidden] activation / gradient of chunk c."""
+        return sum(c.slices) * self.model.hidden * (4 if self.dtype == "f32" else 2)
+
+    def forward(self, c, act_in, out_ptr: Optional[int] = None) -> Optional[torch.Tensor]:
+        """act_in: tensor or device address (read before the call's work
+        ends; the stage copies it).  out_ptr: where the stage output goes
+        (e.g. the next stage's P2P mailbox); default: a new tensor, returned."""
         T = sum(c.slices)
         out = None
-        if not self.has_head:
+        if not self.has_head and out_ptr is None:
             out = torch.empty((T, self.model.hidden), dtype=self.tdtype, device=self.device)
         d = self._desc(c)
-        check(lib().epp_stage_forward(self.h, ctypes.byref(d), _ptr(act_in), _ptr(out), stream_ptr()))
+        check(lib().epp_stage_forward(self.h, ctypes.byref(d), _ptr(act_in),
+                                      out_ptr if out_ptr is not None else _ptr(out), stream_ptr()))
         return out
 
-    def backward(self, c, grad_in: Optional[torch.Tensor]) -> Optional[torch.Tensor]:
+    def backward(self, c, grad_in, out_ptr: Optional[int] = None) -> Optional[torch.Tensor]:
+        """grad_in: tensor or device address, read in place by the last
+        layer's backward.  out_ptr: destination of d(stage input) (e.g. the
+        previous stage's mailbox); default: a new tensor, returned."""
         T = sum(c.slices)
         out = None
-        if not self.has_embed:
+        if not self.has_embed and out_ptr is None:
             out = torch.empty((T, self.model.hidden), dtype=self.tdtype, device=self.device)
         d = self._desc(c)
-        check(lib().epp_stage_backward(self.h, ctypes.byref(d), _ptr(grad_in), _ptr(out), stream_ptr()))
+        check(lib().epp_stage_backward(self.h, ctypes.byref(d), _ptr(grad_in),
+                                       out_ptr if out_ptr is not None else _ptr(out), stream_ptr()))
         self._keep.pop(c.id, None)
         return out
 

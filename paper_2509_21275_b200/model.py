@@ -84,6 +84,11 @@ MODELS: Dict[str, ModelConfig] = {
 }
 
 
+# Planner memory capacity of one B200 stage (mem_capacity =
+# 180e9), used by both benchmark arms so they plan identical documents.
+B200_MEM_CAPACITY = 180e9
+
+
 def activation_bytes_per_token(m: ModelConfig, elem_bytes: int = 2) -> float:
     """Bytes the CUDA stage keeps per token per NON-checkpointed layer until
     the chunk's backward (stage.cu LayerSaved + chunk-local K/V): layer output
@@ -110,14 +115,30 @@ def state_bytes_per_param(dtype: str = "bf16") -> float:
     return 16.0 + (2.0 if dtype == "bf16" else 0.0)
 
 
-def planner_config(m: ModelConfig, pp_degree: int, mem_capacity: float = 180e9,
+def tail_ckpt_excess_bytes(m: ModelConfig) -> float:
+    """Bytes per token per checkpointed layer that a TAIL chunk keeps beyond
+    Eq. 10's (3 - 2I) e D l charge (I = 1, e = 4: 4D): the layer input (2D,
+    bf16), its K/V rows (4 Hkv hd, bf16, in the sequence / chunk KV buffers
+    that recompute rewrites) and 16 B of norm statistics.  Positive for MHA
+    models (GPT: 2D + 16), 0 for GQA 4:1 (Llama: 3D + 16 < 4D)."""
+    kept = 2 * m.hidden + 4 * m.kv_heads * m.head_dim + 16
+    return max(0.0, float(kept - 4 * m.hidden))
+
+
+def planner_config(m: ModelConfig, pp_degree: int, mem_capacity: float = B200_MEM_CAPACITY,
                    cost: Optional[Dict[str, float]] = None, reserve_bytes: float = 12e9,
-                   dtype: str = "bf16", stage_counts: Optional[List[int]] = None) -> Dict:
+                   dtype: str = "bf16", stage_counts: Optional[List[int]] = None,
+                   max_seq_len: int = 0) -> Dict:
     """SystemConfig document for the planner (proj/src/config.cpp:76-113).
 
     token_act_bytes: whole-model, unsharded activation bytes per token;
     stage_state_bytes: parameters/optimizer of each stage + a fixed reserve
-    for workspaces (GEMM/attention scratch, logits blocks, allocator slack).
+    for workspaces (GEMM/attention scratch, logits blocks, allocator slack),
+    plus, when max_seq_len is given, what Eq. 10 does not charge for
+    checkpointed layers of tail chunks (tail_ckpt_excess_bytes) for two
+    in-flight tails of max_seq_len tokens with every stage layer checkpointed.
+    The planner's arithmetic is untouched (bit-exactness); only its inputs
+    describe the executor.
     """
     L = m.layers
     assert L % pp_degree == 0, "layers must divide by pp_degree"
@@ -125,13 +146,14 @@ def planner_config(m: ModelConfig, pp_degree: int, mem_capacity: float = 180e9,
     per_layer = m.params_per_layer()
     sbp = state_bytes_per_param(dtype)
     states = []
+    tail_reserve = 2.0 * tail_ckpt_excess_bytes(m) * max(counts) * max(0, int(max_seq_len))
     for p in range(pp_degree):
         n = per_layer * counts[p]
         if p == 0:
             n += m.vocab * m.hidden
         if p == pp_degree - 1:
             n += m.vocab * m.hidden + 2 * m.hidden
-        states.append(n * sbp + reserve_bytes)
+        states.append(n * sbp + reserve_bytes + tail_reserve)
     cost = dict(cost or default_cost(m))
     return {
         "cluster": {"num_gpus": pp_degree, "pp_degree": pp_degree, "sp_degree": 1,
@@ -139,9 +161,10 @@ def planner_config(m: ModelConfig, pp_degree: int, mem_capacity: float = 180e9,
                     "all2all_bandwidth": {}, "all2all_latency": {}},
         # elem_bytes = 4: Eq. 10 charges the dK/dV accumulators of non-tail
         # chunks as 2 * e * D per token per layer, and the executor keeps them
-        # in fp32 (bf16 would lose the cross-slice accumulation); the
-        # checkpointed-layer term (3 - 2I) e D l is then charged at 2x the
-        # bf16 bytes it keeps, i.e. conservatively.
+        # in fp32 (bf16 would lose the cross-slice accumulation).  The
+        # checkpointed-layer term (3 - 2I) e D l then covers a NON-tail
+        # chunk's kept input + K/V (12D charged vs 2D + 4 Hkv hd + 16 kept);
+        # for tails (4D charged) the excess is in stage_state_bytes above.
         "model": {"layers": L, "hidden_dim": m.hidden, "elem_bytes": 4.0,
                   # Eq. 10 charges L/d_p layers per stage; with a head-balanced
                   # split the largest stage holds max(counts), so scale up
