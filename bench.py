@@ -358,6 +358,10 @@ def run_ours(args):
     prof_ms = pe0.elapsed_time(pe1)
     stage.loss(reset=True) if prank == dp - 1 else None
 
+    # ---- measured trace of one step (trace document v1) vs the simulation --
+    trace_block = measured_trace_step(args, driver, stage, plans[timed[0]], batches[timed[0]][1], pre[0], cfg,
+                                      optimizer, sync_all, dist, world, rank, dp, prank, replicas)
+
     # ---- end-to-end timed region (e2e) ---------------------------------------
     e2e = None
     if not args.no_e2e:
@@ -434,6 +438,7 @@ def run_ours(args):
                                                    if k not in ("attn_bwd_dq", "attn_bwd_dkv"))) / nprof,
         "clocks": clk.summary(),
         "e2e": e2e,
+        "trace": trace_block,
     }
     if world > 1:
         # stage-to-stage activations/gradients (this rank's sends; rank 0 is a
@@ -451,6 +456,44 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def measured_trace_step(args, driver, stage, plan, tokens, staged, cfg, optimizer, sync_all, dist, world, rank, dp,
+                        prank, replicas):
+    """One step with the stages' native per-op trace on (include/epp_gpu.h
+    epp_stage_trace): a measured trace document v1 of replica 0, diffed event
+    by event against the planner's simulation of the same plan with the same
+    cost coefficients (the closed loop's per-op residuals).  Both documents
+    go to gpurun_out/."""
+    from paper_2509_21275_b200 import planner, trace as TR
+    sync_all()
+    stage.trace(True)
+    driver.run_step(plan, tokens, staged=staged)
+    optimizer()
+    sync_all()
+    evs = stage.trace_read()
+    stage.trace(False)
+    if prank == dp - 1:
+        stage.loss(reset=True)
+    mine = (rank // dp, prank, evs, stage.state_bytes())
+    got = [mine]
+    if world > 1:
+        got = [None] * world
+        dist.all_gather_object(got, mine)
+    if rank != 0:
+        return None
+    per_stage = {p + 1: e for (q, p, e, _) in got if q == 0}
+    state = [b for (q, p, _, b) in sorted(got, key=lambda x: x[1]) if q == 0]
+    meas = TR.measured_trace(plan, per_stage, state_bytes=state, mem_capacity=cfg["cluster"]["mem_capacity"])
+    sim_text, _ = planner.simulate_plan_document(plan.doc)
+    res = TR.residuals(meas, sim_text)
+    out_dir = ROOT / "gpurun_out"
+    out_dir.mkdir(exist_ok=True)
+    (out_dir / "trace_measured.json").write_text(json.dumps(meas))
+    (out_dir / "trace_simulated.json").write_text(sim_text)
+    res["events"] = sum(len(u["events"]) for u in meas["units"])
+    res["documents"] = "gpurun_out/trace_measured.json, gpurun_out/trace_simulated.json"
+    return res
 
 
 def run_e2e(args, driver, stage, cfg, e2e_batches, jobs, dev, world, dp, prank, replicas, optimizer, sync_all,

@@ -131,6 +131,25 @@ int epp_stage_adamw_step(epp_stage* st, float lr, float beta1, float beta2, floa
 /* Device bytes held by this stage's in-flight chunks and sequences. */
 int epp_stage_memory(epp_stage* st, int64_t* live_bytes, int64_t* peak_bytes);
 
+/* Measured per-op trace of this stage (the measured counterpart of the
+ * planner's simulated trace, proj/include/epp/pipeline.hpp:43-58 and the
+ * trace document of proj/src/plan_io.cpp:169-209).  enable = 1 clears the
+ * record and marks t = 0 on `stream`; every later forward / backward call is
+ * bracketed by CUDA events (and each recompute layer inside a backward).
+ * trace_read synchronises on the last event and writes up to `cap` events
+ * (*n = the total): op 0 = F, 1 = B, 2 = R; an R event (the summed
+ * recompute time) directly precedes its B event, as the simulator lays them
+ * out; live_bytes = the stage's activation bytes after the op was enqueued. */
+typedef struct epp_trace_event {
+    int32_t chunk_id;
+    int32_t op;
+    double start_s;
+    double end_s;
+    int64_t live_bytes;
+} epp_trace_event;
+int epp_stage_trace(epp_stage* st, int32_t enable, void* stream);
+int epp_stage_trace_read(epp_stage* st, epp_trace_event* out, int32_t cap, int32_t* n);
+
 /* ---- stage-to-stage P2P over peer memory (NVLink) ------------------------
  * epp_p2p_init + epp_send / epp_recv between adjacent stages
  * (PAPER.md:726 uses NCCL; proj/src/pipeline.cpp:168-193 models the hand-off

@@ -190,6 +190,73 @@ struct SeqKV {
     Buf dkv;         // fp32, same layout
 };
 
+// Measured per-op trace (epp_stage_trace*): CUDA events on the stage stream
+// around every forward / backward call and around each recompute
+// layer_forward inside a backward (reference event kinds F / B / R,
+// proj/include/epp/pipeline.hpp:43-51).  Events are recycled.
+struct TraceOp {
+    int chunk = -1;
+    int kind = 0;                 // 0 forward, 1 backward (recompute split out at read)
+    cudaEvent_t a = nullptr, b = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> rec;
+    long long live = 0;           // stage bytes held when the op's work was enqueued
+};
+
+class Tracer {
+public:
+    ~Tracer() {
+        clear();
+        for (cudaEvent_t e : free_) cudaEventDestroy(e);
+    }
+    bool on() const { return on_; }
+    void start(cudaStream_t s) {
+        clear();
+        origin_ = ev();
+        EPP_CUDA(cudaEventRecord(origin_, s));
+        on_ = true;
+    }
+    void stop() { on_ = false; }
+    cudaEvent_t record(cudaStream_t s) {
+        cudaEvent_t e = ev();
+        EPP_CUDA(cudaEventRecord(e, s));
+        return e;
+    }
+    std::vector<TraceOp>& ops() { return ops_; }
+    cudaEvent_t origin() const { return origin_; }
+    void clear() {
+        for (TraceOp& o : ops_) {
+            give(o.a);
+            give(o.b);
+            for (auto& r : o.rec) {
+                give(r.first);
+                give(r.second);
+            }
+        }
+        ops_.clear();
+        give(origin_);
+        origin_ = nullptr;
+    }
+
+private:
+    cudaEvent_t ev() {
+        if (!free_.empty()) {
+            cudaEvent_t e = free_.back();
+            free_.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        EPP_CUDA(cudaEventCreate(&e));
+        return e;
+    }
+    void give(cudaEvent_t e) {
+        if (e) free_.push_back(e);
+    }
+    bool on_ = false;
+    cudaEvent_t origin_ = nullptr;
+    std::vector<TraceOp> ops_;
+    std::vector<cudaEvent_t> free_;
+};
+
 }  // namespace
 
 // ===========================================================================
@@ -353,6 +420,7 @@ public:
         EPP_REQUIRE(chunks_.find(c.id) == chunks_.end(), "chunk already in flight on this stage");
         EPP_REQUIRE(c.ckpt_layers >= 0 && c.ckpt_layers <= nl_, "ckpt_layers out of range");
         ChunkState& cs = chunks_[c.id];
+        TraceOp* tr = trace_begin(c.id, 0, s);
         try {
             setup_chunk(cs, c, s);
             cs.ckpt = c.ckpt_layers;
@@ -395,12 +463,14 @@ public:
             chunks_.erase(c.id);
             throw;
         }
+        trace_end(tr, s);
     }
 
     void backward(const epp_chunk_desc& c, const void* grad_in, void* grad_out, cudaStream_t s) {
         auto it = chunks_.find(c.id);
         EPP_REQUIRE(it != chunks_.end(), "backward of a chunk that was not forwarded");
         ChunkState& cs = it->second;
+        TraceOp* tr = trace_begin(c.id, 1, s);
         const size_t act_bytes = static_cast<size_t>(cs.T) * D_ * esz();
         // d(stage output): the head's final-norm backward, or grad_in used in
         // place (read by the last layer's backward only; the caller keeps it
@@ -423,7 +493,11 @@ public:
         for (int j = nl_ - 1; j >= 0; --j) {
             LayerSaved& L = cs.layers[j];
             const void* x = j == 0 ? cs.x_in.get() : cs.layers[j - 1].x_out.get();
-            if (!L.full) layer_forward(cs, j, x, L, nullptr, /*skip_out=*/true, s);   // recompute
+            if (!L.full) {   // recompute
+                cudaEvent_t ra = tr ? tracer_.record(s) : nullptr;
+                layer_forward(cs, j, x, L, nullptr, /*skip_out=*/true, s);
+                if (tr) tr->rec.emplace_back(ra, tracer_.record(s));
+            }
             // the first layer of a non-embedding stage writes d(stage input)
             // straight into grad_out (e.g. the previous stage's P2P mailbox)
             Buf dx;
@@ -452,6 +526,53 @@ public:
         const int seq = c.seq;
         chunks_.erase(it);
         if (first_slice) seqs_.erase(seq);
+        trace_end(tr, s);
+    }
+
+    // ------------------------------------------------------------ tracing
+    void trace(bool on, cudaStream_t s) {
+        if (on) tracer_.start(s);
+        else tracer_.stop();
+    }
+
+    // Resolves the recorded events (synchronises on the last one).  Per
+    // backward with recompute, an R event [start, start + sum of the
+    // recompute intervals) precedes the B event, as the reference simulator
+    // lays them out (proj/src/pipeline.cpp:246-257).
+    int trace_read(epp_trace_event* out, int cap) {
+        auto& ops = tracer_.ops();
+        for (auto it = ops.rbegin(); it != ops.rend(); ++it)
+            if (it->b) {
+                EPP_CUDA(cudaEventSynchronize(it->b));
+                break;
+            }
+        auto since = [&](cudaEvent_t e) {
+            float ms = 0.f;
+            EPP_CUDA(cudaEventElapsedTime(&ms, tracer_.origin(), e));
+            return static_cast<double>(ms) * 1e-3;
+        };
+        int n = 0;
+        auto put = [&](int chunk, int op, double a, double b, long long live) {
+            if (out && n < cap) out[n] = epp_trace_event{chunk, op, a, b, live};
+            ++n;
+        };
+        for (const TraceOp& o : ops) {
+            if (!o.b) continue;   // a call that failed
+            const double a = since(o.a), b = since(o.b);
+            double rec = 0.0;
+            for (const auto& r : o.rec) {
+                float ms = 0.f;
+                EPP_CUDA(cudaEventElapsedTime(&ms, r.first, r.second));
+                rec += static_cast<double>(ms) * 1e-3;
+            }
+            if (o.kind == 1 && rec > 0.0) {
+                put(o.chunk, 2, a, a + rec, o.live);
+                put(o.chunk, 1, a + rec, b, o.live);
+            } else {
+                put(o.chunk, o.kind, a, b, o.live);
+            }
+        }
+        return n;
     }
 
 private:
@@ -897,6 +1018,22 @@ private:
     double* loss_acc_ = nullptr;
     std::map<int, int> loss_slot_;   // chunk id -> loss record
     Pool pool_;
+    TraceOp* trace_begin(int chunk, int kind, cudaStream_t s) {
+        if (!tracer_.on()) return nullptr;
+        TraceOp op;
+        op.chunk = chunk;
+        op.kind = kind;
+        op.a = tracer_.record(s);
+        tracer_.ops().push_back(std::move(op));
+        return &tracer_.ops().back();
+    }
+    void trace_end(TraceOp* tr, cudaStream_t s) {
+        if (!tr) return;
+        tr->b = tracer_.record(s);
+        tr->live = pool_.live;
+    }
+
+    Tracer tracer_;
     PinnedRing ring_{32u << 20};
     std::map<int, ChunkState> chunks_;
     std::map<int, SeqKV> seqs_;
@@ -1044,6 +1181,17 @@ int epp_stage_memory(epp_stage* st, int64_t* live_bytes, int64_t* peak_bytes) {
     return guard([&] {
         if (live_bytes) *live_bytes = st->impl->pool().live;
         if (peak_bytes) *peak_bytes = st->impl->pool().peak;
+    });
+}
+
+int epp_stage_trace(epp_stage* st, int32_t enable, void* stream) {
+    return guard([&] { st->impl->trace(enable != 0, S(stream)); });
+}
+
+int epp_stage_trace_read(epp_stage* st, epp_trace_event* out, int32_t cap, int32_t* n) {
+    return guard([&] {
+        EPP_REQUIRE(n != nullptr, "n is null");
+        *n = st->impl->trace_read(out, cap);
     });
 }
 

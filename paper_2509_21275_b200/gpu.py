@@ -42,6 +42,11 @@ class ChunkDesc(ctypes.Structure):
                 ("token_ids", ctypes.c_void_p), ("target_ids", ctypes.c_void_p)]
 
 
+class TraceEvent(ctypes.Structure):
+    _fields_ = [("chunk_id", ctypes.c_int32), ("op", ctypes.c_int32), ("start_s", ctypes.c_double),
+                ("end_s", ctypes.c_double), ("live_bytes", ctypes.c_int64)]
+
+
 class ParamInfo(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char_p), ("numel", ctypes.c_int64), ("master", ctypes.c_void_p),
                 ("work", ctypes.c_void_p), ("grad", ctypes.c_void_p)]
@@ -73,6 +78,8 @@ def lib():
             "epp_stage_adamw_step": [vp, f32, f32, f32, f32, f32, i32, vp],
             "epp_stage_memory": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)],
             "epp_gpu_profile": [i32],
+            "epp_stage_trace": [vp, i32, vp],
+            "epp_stage_trace_read": [vp, ctypes.POINTER(TraceEvent), i32, ctypes.POINTER(i32)],
             "epp_stage_chunk_loss": [vp, i32, ctypes.POINTER(ctypes.c_double), vp],
             "epp_gpu_profile_read": [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(i64), i32],
@@ -314,6 +321,27 @@ class CudaStage:
         out = (ctypes.c_double * 2)()
         check(lib().epp_stage_chunk_loss(self.h, int(chunk_id), out, stream_ptr()))
         return out[0], out[1]
+
+    def trace(self, enable: bool = True):
+        """Start (clear + t = 0 on the current stream) or stop recording the
+        measured per-op trace (include/epp_gpu.h epp_stage_trace)."""
+        check(lib().epp_stage_trace(self.h, int(enable), stream_ptr()))
+
+    def trace_read(self):
+        """Recorded events [{chunk, op 'F'/'B'/'R', start, end (s), live}]
+        (synchronises on the last one)."""
+        n = ctypes.c_int32()
+        check(lib().epp_stage_trace_read(self.h, None, 0, ctypes.byref(n)))
+        buf = (TraceEvent * max(1, n.value))()
+        check(lib().epp_stage_trace_read(self.h, buf, n.value, ctypes.byref(n)))
+        ops = {0: "F", 1: "B", 2: "R"}
+        return [{"chunk": e.chunk_id, "op": ops[e.op], "start": e.start_s, "end": e.end_s,
+                 "live": e.live_bytes} for e in buf[:n.value]]
+
+    def state_bytes(self) -> int:
+        """Resident bytes of weights, fp32 grads and Adam state."""
+        per = 16 + (2 if self.dtype == "bf16" else 0)
+        return sum(p["numel"] for p in self.params().values()) * per
 
     def memory(self):
         live, peak = ctypes.c_int64(), ctypes.c_int64()

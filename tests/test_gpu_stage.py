@@ -185,3 +185,48 @@ def test_conventional_launches_match():
     # fp64 per-chunk reductions in a fixed order: bit-identical losses
     assert out["0"][0] == out["1"][0], out
     assert out["0"][1] == out["1"][1], out
+
+
+def test_measured_trace(planner):
+    """Native per-op trace (epp_stage_trace) of a 2-stage step with an active
+    checkpoint ladder: one F and one B per (stage, chunk), an R event exactly
+    where the plan checkpoints, ops of a stage in its op-list order and
+    non-overlapping; the measured trace document is diffable against the
+    planner's simulation of the same plan."""
+    import json
+    from paper_2509_21275_b200 import trace as TR
+    from paper_2509_21275_b200.gpu import CudaStage
+    m = cfg_model("gpt")
+    plan = make_plan(planner, m, LENGTHS, 2, 4, tight=True)
+    tokens = S.synthetic_tokens(LENGTHS, m.vocab, seed=3)
+    stages = []
+    for p in range(2):
+        first, num = stage_layers(m.layers, 2, p)
+        st = CudaStage(m, first, num, p == 0, p == 1, dtype="bf16")
+        st.init_weights(5)
+        stages.append(st)
+    for st in stages:
+        st.trace(True)
+    LocalPipeline(stages, torch.device("cuda")).run_step(plan, tokens)
+    events = {p + 1: st.trace_read() for p, st in enumerate(stages)}
+    for p, evs in events.items():
+        fb = [e for e in evs if e["op"] in "FB"]
+        assert len(fb) == 2 * len(plan.chunks)
+        for a, b in zip(evs, evs[1:]):
+            assert a["end"] <= b["start"] + 1e-9 and a["start"] <= a["end"]
+        want = []
+        for u in plan.units:
+            want += [(k, u.chunks[pos]) for (k, pos) in S.stage_ops(len(u.chunks), u.n_prefill, 2, p,
+                                                                     u.backward_order)]
+        assert [(e["op"], e["chunk"]) for e in fb] == want
+        rec = {e["chunk"] for e in evs if e["op"] == "R"}
+        ck = {u.chunks[pos] for u in plan.units for pos in range(len(u.chunks)) if u.ckpt[p - 1][pos] > 0}
+        assert rec == ck
+    meas = TR.measured_trace(plan, events, state_bytes=[st.state_bytes() for st in stages])
+    sim, _ = planner.simulate_plan_document(plan.doc)
+    r = TR.residuals(meas, sim)
+    assert r["per_op"]["F"]["events"] == 2 * len(plan.chunks)
+    assert meas["total_seconds"] > 0
+    json.dumps(meas)
+    for st in stages:
+        st.close()
