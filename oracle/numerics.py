@@ -5,8 +5,14 @@ leg import this module, as the checker.  The product (paper_2509_21275_b200)
 never does.
 
 The reference ships no model execution ("no model, no loss and
-no gradients"), so this is a from-scratch restatement and its PARITY IS
-UNPINNED by reference golden vectors.  What pins it:
+no gradients"), so this is a from-scratch restatement with no reference
+golden vectors.  What pins it:
+  * an independent implementation of the same model families:
+    tests/test_oracle_hf.py loads the same weights into Hugging Face
+    transformers 5.5.0 LlamaForCausalLM (RMSNorm, GQA, SwiGLU, rotate-half
+    RoPE) and GPTNeoXForCausalLM (sequential residual, LayerNorm, full
+    rotary, tanh-GELU, zero biases) and requires identical per-token losses
+    (max |diff| ~5e-7) and parameter gradients (rel < 1e-4);
   * the chunk semantics are the reference's: slices[0] owns `context`
     (proj/include/epp/chunk.hpp:29-31), Hybrid = tail slice + whole shorts
     (proj/src/processor.cpp:280-299), member order = chunk slice order, a

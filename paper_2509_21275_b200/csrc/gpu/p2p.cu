@@ -221,8 +221,11 @@ int epp_p2p_open(epp_p2p* h, const void* peer_handle) {
         std::memcpy(&hb, peer_handle, sizeof(hb));
         EPP_REQUIRE(hb.magic == eppk::kMagic, "p2p_open: not a channel handle");
         EPP_REQUIRE(hb.role != ch->role, "p2p_open: both ends have the same role");
-        if (ch->role == EPP_P2P_SENDER) ch->arena_bytes = hb.arena_bytes;
-        EPP_REQUIRE(hb.arena_bytes == ch->arena_bytes, "p2p_open: arena sizes disagree");
+        // the receiver owns the arena; the sender adopts its size
+        if (ch->role == EPP_P2P_SENDER) {
+            EPP_REQUIRE(hb.arena_bytes >= eppk::kAlign, "p2p_open: receiver handle without an arena");
+            ch->arena_bytes = hb.arena_bytes;
+        }
         if (hb.pid == static_cast<int32_t>(getpid())) {
             // same process (one host thread driving several GPUs): raw pointers
             // (epp_p2p_init enabled peer access between the devices)

@@ -79,6 +79,23 @@ def worker(rank, world, port, doc, dtype, q):
     torch.distributed.destroy_process_group()
 
 
+def collect(q, procs, n, timeout=600):
+    """n results from the workers; fails fast when a worker died."""
+    import queue
+    import time
+    out, t0 = [], time.time()
+    while len(out) < n:
+        try:
+            out.append(q.get(timeout=5))
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            if dead or time.time() - t0 > timeout:
+                for p in procs:
+                    p.kill()
+                raise AssertionError(f"worker failed (exit codes {dead})" if dead else "workers timed out")
+    return out
+
+
 def free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -97,7 +114,7 @@ def test_two_rank_cuda_pipeline_matches_local(dtype, tight):
     procs = [ctx.Process(target=worker, args=(r, world, port, doc, dtype, q)) for r in range(world)]
     for p in procs:
         p.start()
-    results = [q.get(timeout=600) for _ in range(world)]
+    results = collect(q, procs, world)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
