@@ -72,6 +72,7 @@ def parse():
     ap.add_argument("--uniform-min", type=int, default=1, help="preset=uniform: shortest length")
     ap.add_argument("--uniform-max", type=int, default=0, help="preset=uniform: longest length")
     ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--zero", action="store_true", help="ZeRO-1 optimizer-state sharding across replicas")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--prof-steps", type=int, default=2, help="batches re-run in the instrumented pass")
@@ -164,22 +165,30 @@ def bench_config(args, m, dp):
     return cfg, counts, src
 
 
-def make_lengths(args, n_batches, world, replica=0, _lib=None):
+def make_lengths(args, n_batches, world, replica=0, _lib=None, seed0=1000):
     from paper_2509_21275_b200 import planner
     out = []
     for i in range(n_batches):
-        seed = 1000 + i + 100003 * replica
+        seed = seed0 + i + 100003 * replica
         out.append((seed, planner.generate_workload(args.preset, args.seqs_per_gpu * world, seed, args.cap,
                                                     args.uniform_min, args.uniform_max, _lib=_lib)))
     return out
 
 
-def make_batches(args, n_batches, world, vocab, replica=0):
+def make_batches(args, n_batches, world, vocab, replica=0, seed0=1000):
     """Synthetic batches of `seqs_per_gpu * world` sequences (world = the
     pipeline's GPUs); data-parallel replicas draw from disjoint seeds."""
     from paper_2509_21275_b200 import schedule
     return [(lengths, schedule.synthetic_tokens(lengths, vocab, seed=seed))
-            for seed, lengths in make_lengths(args, n_batches, world, replica)]
+            for seed, lengths in make_lengths(args, n_batches, world, replica, seed0=seed0)]
+
+
+def global_targets(args, n_batches, world, replicas, seed0=1000):
+    """Next-token targets of every step's WHOLE global batch (all replicas):
+    each replica normalises its loss by this, so the replicas' summed
+    gradients are the global per-token mean (GradSync)."""
+    per = [make_lengths(args, n_batches, world, q, seed0=seed0) for q in range(replicas)]
+    return [sum(max(0, n - 1) for q in range(replicas) for n in per[q][i][1]) for i in range(n_batches)]
 
 
 PROF_CLASSES = ((0, "gemm"), (1, "attn_fwd"), (2, "attn_bwd"), (3, "attn_bwd_dq"), (4, "attn_bwd_dkv"),
@@ -202,7 +211,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2509_21275_b200 import calibrate, gpu, model as M, planner, schedule
-    from paper_2509_21275_b200.executor import (DistributedPipeline, LocalPipeline, _ChunkTokens, allreduce_grads,
+    from paper_2509_21275_b200.executor import (DistributedPipeline, GradSync, LocalPipeline, _ChunkTokens,
                                                 pipeline_groups, stage_layers)
 
     world = args.gpus
@@ -228,6 +237,7 @@ def run_ours(args):
     jobs = os.cpu_count() or 8
 
     batches = make_batches(args, args.warmup + args.steps, dp, m.vocab, replica)
+    targets = global_targets(args, args.warmup + args.steps, dp, replicas)
 
     def plan_all(config, first):
         out, t = [], time.perf_counter()
@@ -258,11 +268,21 @@ def run_ours(args):
             dist.barrier()
 
     step_no = [0]
+    # data-parallel replicas: bucketed reductions overlapped with the last
+    # backward (NCCL), optional ZeRO-1 optimizer-state sharding
+    gsync = GradSync(stage, dp_groups[prank], replicas, zero=args.zero)
+
+    def run(drv, i, staged=None, tgt=None):
+        out = drv.run_step(plans[i], batches[i][1], staged=staged,
+                           total_targets=(targets[i] if tgt is None else tgt) if replicas > 1 else None)
+        gsync.launch()
+        return out
 
     def optimizer():
         step_no[0] += 1
-        allreduce_grads(stage, dp_groups[prank], replicas)   # data-parallel replicas (NCCL all-reduce)
+        gsync.finish()
         stage.adamw_step(1e-4, step_no[0])
+        gsync.after_step()
 
     # ---- warmup -------------------------------------------------------------
     # Reserve the activation pool up front (all but 6 GB of what is free after
@@ -277,7 +297,7 @@ def run_ours(args):
         if i == cal_step:
             # closed loop: fit Eq. 1 to every stage op of this step (all
             # ranks' samples, so every rank plans identically)
-            make_driver(timed_stage).run_step(plans[i], batches[i][1])
+            run(make_driver(timed_stage), i)
             optimizer()
             sync_all()
             samples = timed_stage.samples()
@@ -304,7 +324,7 @@ def run_ours(args):
             except planner.Error as e:
                 cost_report["warmup_fit"] = f"fit failed: {e}"
             continue
-        driver.run_step(plans[i], batches[i][1])
+        run(driver, i)
         optimizer()
     sync_all()
     stage.loss(reset=True)
@@ -320,7 +340,7 @@ def run_ours(args):
         sync_all()
         ev0.record()
         for j, i in enumerate(timed):
-            driver.run_step(plans[i], batches[i][1], staged=pre[j])
+            run(driver, i, staged=pre[j])
             optimizer()
         ev1.record()
         sync_all()
@@ -349,7 +369,7 @@ def run_ours(args):
     pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     pe0.record()
     for j, i in enumerate(timed[:nprof]):
-        driver.run_step(plans[i], batches[i][1], staged=pre[j])
+        run(driver, i, staged=pre[j])
         optimizer()
     pe1.record()
     sync_all()
@@ -359,13 +379,22 @@ def run_ours(args):
     stage.loss(reset=True) if prank == dp - 1 else None
 
     # ---- measured trace of one step (trace document v1) vs the simulation --
-    trace_block = measured_trace_step(args, driver, stage, plans[timed[0]], batches[timed[0]][1], pre[0], cfg,
-                                      optimizer, sync_all, dist, world, rank, dp, prank, replicas)
+    trace_block = measured_trace_step(args, lambda: run(driver, timed[0], staged=pre[0]), stage, plans[timed[0]],
+                                      cfg, optimizer, sync_all, dist, world, rank, dp, prank)
 
     # ---- end-to-end timed region (e2e) ---------------------------------------
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, driver, stage, cfg, batches[args.warmup:], jobs, dev, world, dp, prank, replicas,
+        # fresh batches (never trained on): the per-step losses are honest
+        e2e_seed0 = 7000
+        e2e_batches = make_batches(args, args.steps, dp, m.vocab, replica, seed0=e2e_seed0)
+        e2e_targets = global_targets(args, args.steps, dp, replicas, seed0=e2e_seed0)
+
+        def e2e_run(k, plan, tokens):
+            out = driver.run_step(plan, tokens, total_targets=e2e_targets[k] if replicas > 1 else None)
+            gsync.launch()
+            return out
+        e2e = run_e2e(args, e2e_run, stage, cfg, e2e_batches, jobs, dev, world, dp, prank, replicas,
                       optimizer, sync_all, dist)
 
     if rank != 0:
@@ -411,7 +440,7 @@ def run_ours(args):
                    "slices": args.slices or "auto", "stage_layers": counts,
                    "ckpt_layers_per_step": sum(sum(sum(r) for r in u.ckpt) for i in timed for u in plans[i].units)
                                            / args.steps,
-                   "parallelism": f"pp{dp}" + (f"xdp{replicas}" if replicas > 1 else ""),
+                   "parallelism": f"pp{dp}" + (f"xdp{replicas}" if replicas > 1 else "") + ("+zero1" if args.zero and replicas > 1 else ""),
                    "l2": "inputs larger than L2 (activations GBs/step)"},
         "mfu": flops / (sec * world * tf_burst * 1e12),
         "mfu_vs_sustained": flops / (sec * world * tf_sus * 1e12),
@@ -458,8 +487,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def measured_trace_step(args, driver, stage, plan, tokens, staged, cfg, optimizer, sync_all, dist, world, rank, dp,
-                        prank, replicas):
+def measured_trace_step(args, run_step, stage, plan, cfg, optimizer, sync_all, dist, world, rank, dp, prank):
     """One step with the stages' native per-op trace on (include/epp_gpu.h
     epp_stage_trace): a measured trace document v1 of replica 0, diffed event
     by event against the planner's simulation of the same plan with the same
@@ -468,7 +496,7 @@ def measured_trace_step(args, driver, stage, plan, tokens, staged, cfg, optimize
     from paper_2509_21275_b200 import planner, trace as TR
     sync_all()
     stage.trace(True)
-    driver.run_step(plan, tokens, staged=staged)
+    run_step()
     optimizer()
     sync_all()
     evs = stage.trace_read()
@@ -496,7 +524,7 @@ def measured_trace_step(args, driver, stage, plan, tokens, staged, cfg, optimize
     return res
 
 
-def run_e2e(args, driver, stage, cfg, e2e_batches, jobs, dev, world, dp, prank, replicas, optimizer, sync_all,
+def run_e2e(args, run_step, stage, cfg, e2e_batches, jobs, dev, world, dp, prank, replicas, optimizer, sync_all,
             dist):
     """Public-API step from host buffers: plans solved on a host thread one
     step ahead, token ids H2D from pinned memory, per-step loss D2H."""
@@ -522,7 +550,7 @@ def run_e2e(args, driver, stage, cfg, e2e_batches, jobs, dev, world, dp, prank, 
         if k + 1 < len(e2e_batches):
             th = threading.Thread(target=solve, args=(k + 1,))
             th.start()
-        st = driver.run_step(ahead.pop(k), e2e_batches[k][1])
+        st = run_step(k, ahead.pop(k), e2e_batches[k][1])
         h2d += st["h2d_bytes"]
         optimizer()
         if prank == dp - 1:

@@ -125,11 +125,33 @@ int epp_stage_zero_grads(epp_stage* st, void* stream);
  * stage activations (kept reserved: later steps never wait on the driver to
  * map memory).  Synchronises `stream`. */
 int epp_gpu_pool_reserve(uint64_t bytes, void* stream);
-/* AdamW on fp32 masters (bias-corrected, step >= 1); zeroes the grads. */
+/* AdamW on fp32 masters (bias-corrected, step >= 1), one multi-tensor
+ * launch over the stage (or its ZeRO-1 slice); zeroes the grads. */
 int epp_stage_adamw_step(epp_stage* st, float lr, float beta1, float beta2, float eps,
                          float weight_decay, int32_t step, void* stream);
 /* Device bytes held by this stage's in-flight chunks and sequences. */
 int epp_stage_memory(epp_stage* st, int64_t* live_bytes, int64_t* peak_bytes);
+
+/* ---- data parallelism (replicas of a stage) ------------------------------
+ * Parameters live in per-kind arenas (fp32 masters, fp32 grads, working
+ * copies in the stage dtype), in epp_stage_param order, split into BUCKETS:
+ * [embedding] [layer first] ... [layer last] [final norm + LM head], each a
+ * contiguous range padded to 4096 elements.  A replica group all-reduces (or
+ * reduce-scatters) bucket by bucket as soon as the bucket's gradients are
+ * final: with epp_stage_grad_events(st, 1) every backward records one event
+ * per bucket after that bucket's last gradient update, and
+ * epp_stage_bucket_wait makes another stream (the collective's) wait for it,
+ * so the reduction of layer j overlaps the backward of layers < j.
+ * epp_stage_opt_shard(st, r, R) (ZeRO-1): Adam state is kept only for slice r
+ * of R of every bucket (*state_numel = elements held), epp_stage_adamw_step
+ * then updates only those masters (and zeroes every gradient); the caller
+ * all-gathers the masters and calls epp_stage_sync_weights.
+ * offsets: nbuckets + 1 arena element offsets (cap entries written). */
+int epp_stage_arena(epp_stage* st, float** master, void** work, float** grad, int64_t* numel);
+int epp_stage_buckets(epp_stage* st, int64_t* offsets, int32_t cap, int32_t* nbuckets);
+int epp_stage_grad_events(epp_stage* st, int32_t enable);
+int epp_stage_bucket_wait(epp_stage* st, int32_t bucket, void* stream);
+int epp_stage_opt_shard(epp_stage* st, int32_t rank, int32_t nranks, int64_t* state_numel);
 
 /* Measured per-op trace of this stage (the measured counterpart of the
  * planner's simulated trace, proj/include/epp/pipeline.hpp:43-58 and the

@@ -774,53 +774,58 @@ __global__ void add_k(T* y, const T* x, long long n) {
         y[i] = from_f<T>(to_f(y[i]) + to_f(x[i]));
 }
 
+// Multi-tensor AdamW: float4 group i of the concatenated segments is found
+// by binary search over the segments' start4 prefix (a few hundred entries,
+// L1-resident), so the whole stage updates in one launch.
 template <typename T>
-__global__ void adamw_k(float* master, T* work, float* grad, float* m, float* v, long long n,
-                        float lr, float b1, float b2, float eps, float wd, float bc1, float bc2) {
+__global__ void adamw_multi_k(const AdamSeg* __restrict__ segs, int nseg, long long total4, float* master, T* work,
+                              float* grad, float* m, float* v, float lr, float b1, float b2, float eps, float wd,
+                              float bc1, float bc2) {
     pdl_wait();
     pdl_trigger();
-    // 4 parameters per thread and iteration (16-byte fp32 accesses); tensors
-    // are allocated 256-byte aligned, n need not be a multiple of 4
-    const long long n4 = n / 4;
     const float ib1 = 1.f / bc1, ib2 = 1.f / bc2;
-    auto one = [&](float& p, float& mi, float& vi, float g) {
+    auto one = [&](float& p, float& mi, float& vi, float g, float w) {
         mi = b1 * mi + (1.f - b1) * g;
         vi = b2 * vi + (1.f - b2) * g * g;
-        p -= lr * (wd * p + (mi * ib1) / (sqrtf(vi * ib2) + eps));
+        p -= lr * (w * p + (mi * ib1) / (sqrtf(vi * ib2) + eps));
     };
-    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+    int seg = 0;
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total4;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        float4 g = reinterpret_cast<const float4*>(grad)[i];
-        float4 mm = reinterpret_cast<const float4*>(m)[i];
-        float4 vv = reinterpret_cast<const float4*>(v)[i];
-        float4 p = reinterpret_cast<const float4*>(master)[i];
-        one(p.x, mm.x, vv.x, g.x);
-        one(p.y, mm.y, vv.y, g.y);
-        one(p.z, mm.z, vv.z, g.z);
-        one(p.w, mm.w, vv.w, g.w);
-        reinterpret_cast<float4*>(m)[i] = mm;
-        reinterpret_cast<float4*>(v)[i] = vv;
-        reinterpret_cast<float4*>(master)[i] = p;
-        reinterpret_cast<float4*>(grad)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < __ldg(&segs[seg].start4) || (seg + 1 < nseg && i >= __ldg(&segs[seg + 1].start4))) {
+            int lo = 0, hi = nseg - 1;     // last segment with start4 <= i
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (__ldg(&segs[mid].start4) <= i) lo = mid;
+                else hi = mid - 1;
+            }
+            seg = lo;
+        }
+        const long long local = i - __ldg(&segs[seg].start4);
+        const long long e = __ldg(&segs[seg].off) / 4 + local;      // float4 index in the arenas
+        const long long q = __ldg(&segs[seg].mv) / 4 + local;       // float4 index in the state
+        const float w = __ldg(&segs[seg].decay) ? wd : 0.f;
+        float4 g = reinterpret_cast<const float4*>(grad)[e];
+        float4 mm = reinterpret_cast<const float4*>(m)[q];
+        float4 vv = reinterpret_cast<const float4*>(v)[q];
+        float4 p = reinterpret_cast<const float4*>(master)[e];
+        one(p.x, mm.x, vv.x, g.x, w);
+        one(p.y, mm.y, vv.y, g.y, w);
+        one(p.z, mm.z, vv.z, g.z, w);
+        one(p.w, mm.w, vv.w, g.w, w);
+        reinterpret_cast<float4*>(m)[q] = mm;
+        reinterpret_cast<float4*>(v)[q] = vv;
+        reinterpret_cast<float4*>(master)[e] = p;
+        reinterpret_cast<float4*>(grad)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
         if constexpr (std::is_same<T, float>::value) {
-            reinterpret_cast<float4*>(work)[i] = p;
+            reinterpret_cast<float4*>(work)[e] = p;
         } else {
             __nv_bfloat162 lo = __floats2bfloat162_rn(p.x, p.y), hi = __floats2bfloat162_rn(p.z, p.w);
             uint2 raw;
             raw.x = *reinterpret_cast<uint32_t*>(&lo);
             raw.y = *reinterpret_cast<uint32_t*>(&hi);
-            reinterpret_cast<uint2*>(work)[i] = raw;
+            reinterpret_cast<uint2*>(work)[e] = raw;
         }
-    }
-    for (long long i = 4 * n4 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        float p = master[i], mi = m[i], vi = v[i];
-        one(p, mi, vi, grad[i]);
-        m[i] = mi;
-        v[i] = vi;
-        master[i] = p;
-        work[i] = from_f<T>(p);
-        grad[i] = 0.f;
     }
 }
 
@@ -1110,15 +1115,15 @@ void add_inplace(DType t, void* y, const void* x, long long n, cudaStream_t s) {
     EPP_CHECK_LAUNCH();
 }
 
-void adamw(float* master, void* work, DType t, float* grad, float* m, float* v, long long n,
-           float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
-           cudaStream_t s) {
-    ProfScope prof_(kProfAdam, double(n) * (26 + dtype_size(t)), s);
-    if (n == 0) return;
+void adamw_multi(const AdamSeg* segs, int nseg, long long total4, float* master, void* work, DType t, float* grad,
+                 float* m, float* v, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
+                 cudaStream_t s) {
+    ProfScope prof_(kProfAdam, double(total4) * 4 * (26 + dtype_size(t)), s);
+    if (total4 == 0 || nseg == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        launch_k(adamw_k<E>, grid_for((n + 3) / 4, 256), 256, 0, s, master, static_cast<E*>(work), grad, m, v, n,
-                                                     lr, b1, b2, eps, wd, bc1, bc2);
+        launch_k(adamw_multi_k<E>, grid_for(total4, 256), 256, 0, s, segs, nseg, total4, master,
+                 static_cast<E*>(work), grad, m, v, lr, b1, b2, eps, wd, bc1, bc2);
     });
     EPP_CHECK_LAUNCH();
 }

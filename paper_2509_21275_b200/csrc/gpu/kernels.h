@@ -197,10 +197,19 @@ void chunk_loss(const float* row_loss, const int32_t* targets, int T, double* sl
 void fill_zero(void* p, size_t bytes, cudaStream_t s);
 void cast_f32_to(DType t, const float* src, void* dst, long long n, cudaStream_t s);
 void add_inplace(DType t, void* y, const void* x, long long n, cudaStream_t s);
-// AdamW on fp32 master weights; writes the working copy (bf16 or fp32).
-void adamw(float* master, void* work, DType t, float* grad, float* m, float* v, long long n,
-           float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
-           cudaStream_t s);
+// One optimizer segment: arena elements [off, off + n) with Adam state at
+// [mv, mv + n) of the (possibly ZeRO-sharded) state arenas; start4 = prefix
+// of float4 groups over the segment list.
+struct AdamSeg {
+    long long off, n, mv;
+    int decay, pad;
+    long long start4;
+};
+// Multi-tensor AdamW over every segment in ONE launch: fp32 masters, working
+// copy (bf16 or fp32) written, gradients of the segments zeroed.
+void adamw_multi(const AdamSeg* segs, int nseg, long long total4, float* master, void* work, DType t, float* grad,
+                 float* m, float* v, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
+                 cudaStream_t s);
 // Deterministic normal(0, std) init from (seed, offset) counter-based hashing.
 void init_normal(float* dst, long long n, float std, unsigned long long seed, cudaStream_t s);
 void init_const(float* dst, long long n, float v, cudaStream_t s);

@@ -150,8 +150,7 @@ struct Param {
     float* master = nullptr;
     void* work = nullptr;
     float* grad = nullptr;
-    float* m = nullptr;
-    float* v = nullptr;
+    long long off = 0;      // element offset in the stage's arenas
     float init_std = 0.f;   // 0 -> constant init_val
     float init_val = 0.f;
 };
@@ -303,20 +302,45 @@ public:
             if (!llama_) lnf_b_ = add("final_norm.bias", D_, 0.f, 0.f);
             lm_ = add("lm_head.weight", static_cast<long long>(m.vocab) * D_, std0);
         }
-        for (Param& p : params_) {
-            EPP_CUDA(cudaMalloc(&p.master, sizeof(float) * p.numel));
-            EPP_CUDA(cudaMalloc(&p.grad, sizeof(float) * p.numel));
-            EPP_CUDA(cudaMalloc(&p.m, sizeof(float) * p.numel));
-            EPP_CUDA(cudaMalloc(&p.v, sizeof(float) * p.numel));
-            EPP_CUDA(cudaMemset(p.grad, 0, sizeof(float) * p.numel));
-            EPP_CUDA(cudaMemset(p.m, 0, sizeof(float) * p.numel));
-            EPP_CUDA(cudaMemset(p.v, 0, sizeof(float) * p.numel));
-            if (dt_ == DType::F32) {
-                p.work = p.master;
-            } else {
-                EPP_CUDA(cudaMalloc(&p.work, 2 * p.numel));
+        // One arena per kind (fp32 masters, fp32 grads, working copies),
+        // parameters in creation order, each 64-element aligned; buckets
+        // (embedding | one per layer | head) padded to 4096 elements, so a
+        // bucket is one contiguous range for the data-parallel collectives
+        // and splits evenly over up to 16 replicas (ZeRO-1 slices).
+        {
+            long long off = 0;
+            int bucket_of_next = -1;
+            auto close_bucket = [&] {
+                off = (off + kBucketAlign - 1) / kBucketAlign * kBucketAlign;
+                bucket_off_.push_back(off);
+            };
+            bucket_off_.push_back(0);
+            for (size_t i = 0; i < params_.size(); ++i) {
+                const int b = bucket_index(static_cast<int>(i));
+                if (bucket_of_next >= 0 && b != bucket_of_next) close_bucket();
+                bucket_of_next = b;
+                params_[i].off = off;
+                off += (params_[i].numel + 63) / 64 * 64;
             }
+            close_bucket();
+            arena_n_ = off;
         }
+        EPP_CUDA(cudaMalloc(&master_arena_, sizeof(float) * arena_n_));
+        EPP_CUDA(cudaMalloc(&grad_arena_, sizeof(float) * arena_n_));
+        EPP_CUDA(cudaMemset(master_arena_, 0, sizeof(float) * arena_n_));
+        EPP_CUDA(cudaMemset(grad_arena_, 0, sizeof(float) * arena_n_));
+        if (dt_ == DType::F32) {
+            work_arena_ = master_arena_;
+        } else {
+            EPP_CUDA(cudaMalloc(&work_arena_, dtype_size(dt_) * arena_n_));
+            EPP_CUDA(cudaMemset(work_arena_, 0, dtype_size(dt_) * arena_n_));
+        }
+        for (Param& p : params_) {
+            p.master = master_arena_ + p.off;
+            p.grad = grad_arena_ + p.off;
+            p.work = static_cast<char*>(work_arena_) + dtype_size(dt_) * p.off;
+        }
+        set_opt_shard(0, 1);
         // fp64 loss records: [0..1] the stage accumulator, then one
         // (sum, #targets) slot per chunk id forwarded since the last reset
         EPP_CUDA(cudaMalloc(&loss_acc_, sizeof(double) * 2 * (1 + kLossSlots)));
@@ -334,13 +358,13 @@ public:
         chunks_.clear();
         seqs_.clear();
         cudaDeviceSynchronize();
-        for (Param& p : params_) {
-            cudaFree(p.master);
-            cudaFree(p.grad);
-            cudaFree(p.m);
-            cudaFree(p.v);
-            if (p.work != p.master) cudaFree(p.work);
-        }
+        cudaFree(master_arena_);
+        cudaFree(grad_arena_);
+        if (work_arena_ != master_arena_) cudaFree(work_arena_);
+        cudaFree(m_arena_);
+        cudaFree(v_arena_);
+        cudaFree(adam_segs_dev_);
+        for (cudaEvent_t e : bucket_ev_) cudaEventDestroy(e);
         cudaFree(loss_acc_);
     }
 
@@ -365,23 +389,85 @@ public:
 
     void sync_weights(cudaStream_t s) {
         if (dt_ == DType::F32) return;
-        for (Param& p : params_) cast_f32_to(dt_, p.master, p.work, p.numel, s);
+        cast_f32_to(dt_, master_arena_, work_arena_, arena_n_, s);
     }
 
-    void zero_grads(cudaStream_t s) {
-        for (Param& p : params_) fill_zero(p.grad, sizeof(float) * p.numel, s);
-    }
+    void zero_grads(cudaStream_t s) { fill_zero(grad_arena_, sizeof(float) * arena_n_, s); }
 
+    // One multi-tensor launch over the optimizer segments (this replica's
+    // slice of every parameter; no weight decay on norms / biases); zeroes
+    // every gradient.  With a ZeRO-1 shard the masters outside the slice are
+    // left for the caller's all-gather.
     void adamw_step(float lr, float b1, float b2, float eps, float wd, int step, cudaStream_t s) {
         EPP_REQUIRE(step >= 1, "adamw step must be >= 1");
         const float bc1 = 1.f - std::pow(b1, static_cast<float>(step));
         const float bc2 = 1.f - std::pow(b2, static_cast<float>(step));
-        for (Param& p : params_) {
-            // no weight decay on norms / biases
-            const bool decay = p.init_std > 0.f;
-            adamw(p.master, p.work, dt_, p.grad, p.m, p.v, p.numel, lr, b1, b2, eps,
-                  decay ? wd : 0.f, bc1, bc2, s);
+        adamw_multi(adam_segs_dev_, adam_nseg_, adam_total4_, master_arena_, work_arena_, dt_, grad_arena_,
+                    m_arena_, v_arena_, lr, b1, b2, eps, wd, bc1, bc2, s);
+        if (opt_nranks_ > 1) zero_grads(s);
+    }
+
+    // ZeRO-1: Adam state only for this rank's 1/nranks slice of every bucket.
+    void set_opt_shard(int rank, int nranks) {
+        EPP_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "bad optimizer shard");
+        EPP_REQUIRE(kBucketAlign % (64 * nranks) == 0 || nranks == 1, "too many optimizer shards");
+        std::vector<AdamSeg> segs;
+        long long mv = 0;
+        for (size_t b = 0; b + 1 < bucket_off_.size(); ++b) {
+            const long long n = (bucket_off_[b + 1] - bucket_off_[b]) / nranks;
+            const long long lo = bucket_off_[b] + rank * n, hi = lo + n;
+            for (const Param& p : params_) {
+                const long long a = std::max(lo, p.off), e = std::min(hi, p.off + p.numel);
+                if (a >= e) continue;
+                segs.push_back(AdamSeg{a, e - a, mv + (a - lo), p.init_std > 0.f ? 1 : 0, 0});
+            }
+            mv += n;
         }
+        // prefix of float4 groups (segment lengths are multiples of 4)
+        long long acc = 0;
+        for (AdamSeg& g : segs) {
+            EPP_REQUIRE(g.n % 4 == 0 && g.off % 4 == 0, "optimizer segment not float4-aligned");
+            g.start4 = acc;
+            acc += g.n / 4;
+        }
+        cudaFree(m_arena_);
+        cudaFree(v_arena_);
+        cudaFree(adam_segs_dev_);
+        m_arena_ = v_arena_ = nullptr;
+        adam_segs_dev_ = nullptr;
+        EPP_CUDA(cudaMalloc(&m_arena_, sizeof(float) * std::max<long long>(mv, 4)));
+        EPP_CUDA(cudaMalloc(&v_arena_, sizeof(float) * std::max<long long>(mv, 4)));
+        EPP_CUDA(cudaMemset(m_arena_, 0, sizeof(float) * std::max<long long>(mv, 4)));
+        EPP_CUDA(cudaMemset(v_arena_, 0, sizeof(float) * std::max<long long>(mv, 4)));
+        if (!segs.empty()) {
+            EPP_CUDA(cudaMalloc(&adam_segs_dev_, sizeof(AdamSeg) * segs.size()));
+            EPP_CUDA(cudaMemcpy(adam_segs_dev_, segs.data(), sizeof(AdamSeg) * segs.size(), cudaMemcpyHostToDevice));
+        }
+        adam_nseg_ = static_cast<int>(segs.size());
+        adam_total4_ = acc;
+        opt_rank_ = rank;
+        opt_nranks_ = nranks;
+        opt_state_n_ = mv;
+    }
+
+    // --- data-parallel buckets -------------------------------------------
+    long long arena_numel() const { return arena_n_; }
+    float* master_arena() const { return master_arena_; }
+    void* work_arena() const { return work_arena_; }
+    float* grad_arena() const { return grad_arena_; }
+    long long opt_state_numel() const { return opt_state_n_; }
+    const std::vector<long long>& buckets() const { return bucket_off_; }
+    void grad_events(bool on) {
+        grad_events_ = on;
+        if (on && bucket_ev_.empty()) {
+            bucket_ev_.resize(bucket_off_.size() - 1);
+            for (auto& e : bucket_ev_) EPP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+    }
+    void bucket_wait(int b, cudaStream_t s) {
+        EPP_REQUIRE(b >= 0 && b + 1 < static_cast<int>(bucket_off_.size()), "bucket index out of range");
+        EPP_REQUIRE(!bucket_ev_.empty(), "bucket events were never enabled");
+        EPP_CUDA(cudaStreamWaitEvent(s, bucket_ev_[b], 0));
     }
 
     void loss(double out[2], bool reset, cudaStream_t s) {
@@ -485,6 +571,7 @@ public:
                      lnf_b_ >= 0 ? grad(lnf_b_) : nullptr, cs.T, D_, s);
             cs.dxf.release();
             dy_ptr = dy.get();
+            bucket_ready(head_bucket(), s);   // lm_head (forward) + final norm grads
         } else {
             EPP_REQUIRE(grad_in != nullptr, "grad_in is null");
         }
@@ -510,6 +597,7 @@ public:
                 dx_ptr = dx.get();
             }
             layer_backward(cs, j, x, L, dy_ptr, dx_ptr, s);
+            bucket_ready(layer_bucket(j), s);
             drop_full(L);
             L.x_out.release();
             dy = std::move(dx);
@@ -517,6 +605,7 @@ public:
         }
         if (has_embed_) {
             embed_bwd(dt_, c.token_ids, dy_ptr, grad(emb_), cs.T, D_, s);
+            bucket_ready(0, s);
         } else if (nl_ == 0) {
             EPP_REQUIRE(grad_out != nullptr, "grad_out is null");
             EPP_CUDA(cudaMemcpyAsync(grad_out, dy_ptr, act_bytes, cudaMemcpyDeviceToDevice, s));
@@ -584,6 +673,23 @@ private:
         p.init_val = val;
         params_.push_back(p);
         return static_cast<int>(params_.size()) - 1;
+    }
+    // bucket of parameter i: [embedding] [layer 0] ... [layer n-1] [head]
+    int bucket_index(int i) const {
+        if (i == emb_) return 0;
+        const int e = has_embed_ ? 1 : 0;
+        if (i == lnf_w_ || i == lnf_b_ || i == lm_) return e + nl_;
+        for (int j = 0; j < nl_; ++j) {
+            const LayerParams& lp = lps_[j];
+            for (int q : {lp.ln1_w, lp.ln1_b, lp.wqkv, lp.wo, lp.ln2_w, lp.ln2_b, lp.w1, lp.w2})
+                if (q == i) return e + j;
+        }
+        throw std::logic_error("parameter without a bucket");
+    }
+    int layer_bucket(int j) const { return (has_embed_ ? 1 : 0) + j; }
+    int head_bucket() const { return (has_embed_ ? 1 : 0) + nl_; }
+    void bucket_ready(int b, cudaStream_t s) {
+        if (grad_events_) EPP_CUDA(cudaEventRecord(bucket_ev_[b], s));
     }
     void* work(int i) const { return params_[i].work; }
     float* grad(int i) const { return params_[i].grad; }
@@ -1012,6 +1118,21 @@ private:
     int D_ = 0, H_ = 0, Hkv_ = 0, hd_ = 0, F_ = 0, F1_ = 0, Nqkv_ = 0;
     bool llama_ = false;
     std::vector<Param> params_;
+    static constexpr long long kBucketAlign = 4096;
+    std::vector<long long> bucket_off_;
+    long long arena_n_ = 0;
+    float* master_arena_ = nullptr;
+    float* grad_arena_ = nullptr;
+    void* work_arena_ = nullptr;
+    float* m_arena_ = nullptr;
+    float* v_arena_ = nullptr;
+    AdamSeg* adam_segs_dev_ = nullptr;
+    int adam_nseg_ = 0;
+    long long adam_total4_ = 0;
+    int opt_rank_ = 0, opt_nranks_ = 1;
+    long long opt_state_n_ = 0;
+    bool grad_events_ = false;
+    std::vector<cudaEvent_t> bucket_ev_;
     std::vector<LayerParams> lps_;
     int emb_ = -1, lnf_w_ = -1, lnf_b_ = -1, lm_ = -1;
     static constexpr int kLossSlots = 1 << 16;
@@ -1181,6 +1302,39 @@ int epp_stage_memory(epp_stage* st, int64_t* live_bytes, int64_t* peak_bytes) {
     return guard([&] {
         if (live_bytes) *live_bytes = st->impl->pool().live;
         if (peak_bytes) *peak_bytes = st->impl->pool().peak;
+    });
+}
+
+int epp_stage_arena(epp_stage* st, float** master, void** work, float** grad, int64_t* numel) {
+    return guard([&] {
+        if (master) *master = st->impl->master_arena();
+        if (work) *work = st->impl->work_arena();
+        if (grad) *grad = st->impl->grad_arena();
+        if (numel) *numel = st->impl->arena_numel();
+    });
+}
+
+int epp_stage_buckets(epp_stage* st, int64_t* offsets, int32_t cap, int32_t* nbuckets) {
+    return guard([&] {
+        EPP_REQUIRE(nbuckets != nullptr, "nbuckets is null");
+        const auto& b = st->impl->buckets();
+        *nbuckets = static_cast<int32_t>(b.size()) - 1;
+        for (int32_t i = 0; offsets && i < cap && i < static_cast<int32_t>(b.size()); ++i) offsets[i] = b[i];
+    });
+}
+
+int epp_stage_grad_events(epp_stage* st, int32_t enable) {
+    return guard([&] { st->impl->grad_events(enable != 0); });
+}
+
+int epp_stage_bucket_wait(epp_stage* st, int32_t bucket, void* stream) {
+    return guard([&] { st->impl->bucket_wait(bucket, S(stream)); });
+}
+
+int epp_stage_opt_shard(epp_stage* st, int32_t rank, int32_t nranks, int64_t* state_numel) {
+    return guard([&] {
+        st->impl->set_opt_shard(rank, nranks);
+        if (state_numel) *state_numel = st->impl->opt_state_numel();
     });
 }
 

@@ -105,10 +105,14 @@ class _ChunkTokens:
                 self.h2d_bytes += t.numel() * 4
 
 
-def _op(plan: Plan, unit, pos: int, stage: int, toks: _ChunkTokens) -> ChunkOp:
+def _op(plan: Plan, unit, pos: int, stage: int, toks: _ChunkTokens, total_targets: Optional[int] = None) -> ChunkOp:
+    """total_targets: the loss normaliser (default: this plan's targets; with
+    data-parallel replicas, the targets of the whole global batch, so the
+    summed replica gradients are the global per-token mean)."""
     lay: ChunkLayout = plan.chunks[unit.chunks[pos]]
+    n = plan.total_targets if total_targets is None else total_targets
     return ChunkOp(lay.id, lay.seq, lay.kind, lay.tail, lay.context, lay.seq_len, lay.slices,
-                   unit.ckpt[stage][pos], 1.0 / max(1, plan.total_targets),
+                   unit.ckpt[stage][pos], 1.0 / max(1, n),
                    toks.ids.get(lay.id), toks.tgt.get(lay.id))
 
 
@@ -117,14 +121,16 @@ class LocalPipeline:
         self.stages = list(stages)
         self.device = device
 
-    def run_step(self, plan: Plan, tokens: Sequence[np.ndarray], staged: Optional[_ChunkTokens] = None) -> dict:
+    def run_step(self, plan: Plan, tokens: Sequence[np.ndarray], staged: Optional[_ChunkTokens] = None,
+                 total_targets: Optional[int] = None) -> dict:
         """One global batch.  `staged`: token tensors already on the device
         (the device-resident benchmark mode); otherwise they are copied from
-        pinned host memory here."""
+        pinned host memory here.  total_targets: see _op."""
         dp = len(self.stages)
         if dp != plan.pp_degree:
             raise ValueError(f"plan is for {plan.pp_degree} stages, executor has {dp}")
         toks = staged or _ChunkTokens(plan, tokens, self.device, True, True)
+        self._targets = total_targets
         for unit in plan.units:
             self._run_unit(plan, unit, toks)
         return {"h2d_bytes": toks.h2d_bytes}
@@ -147,14 +153,14 @@ class LocalPipeline:
                         if p > 0 and (p - 1, pos) not in acts:
                             break
                         act_in = acts.pop((p - 1, pos)) if p > 0 else None
-                        out = self.stages[p].forward(_op(plan, unit, pos, p, toks), act_in)
+                        out = self.stages[p].forward(_op(plan, unit, pos, p, toks, self._targets), act_in)
                         if p + 1 < dp:
                             acts[(p, pos)] = out
                     else:
                         if p + 1 < dp and (p + 1, pos) not in grads:
                             break
                         g_in = grads.pop((p + 1, pos)) if p + 1 < dp else None
-                        g_out = self.stages[p].backward(_op(plan, unit, pos, p, toks), g_in)
+                        g_out = self.stages[p].backward(_op(plan, unit, pos, p, toks, self._targets), g_in)
                         if p > 0:
                             grads[(p, pos)] = g_out
                     idx[p] += 1
@@ -186,15 +192,99 @@ def pipeline_groups(pp: int, replicas: int = 1):
     return pipes, dp_groups
 
 
+class GradSync:
+    """Data-parallel gradient reduction of one stage across its replicas
+    (the paper's data parallelism across pipeline replicas).
+
+    * Gradients are SUMMED: every replica normalises its loss by the targets
+      of the whole global batch (run_step(total_targets=...)), so the sum is
+      the global per-token mean whatever each replica's share of targets.
+    * CUDA stages: one collective per bucket (embedding | layer | head, each a
+      contiguous arena range, include/epp_gpu.h), issued on a side stream in
+      readiness order (head, last layer, ..., first layer, embedding) right
+      after the step's last backward has been ENQUEUED; each waits only for
+      its bucket's event, so reducing layer j overlaps the backward of the
+      layers below it.  finish() makes the compute stream wait for all.
+    * zero=True (ZeRO-1): reduce-scatter instead of all-reduce, Adam state
+      only for this replica's 1/R slice of every bucket (epp_stage_opt_shard),
+      and after the optimizer step the updated fp32 masters are all-gathered
+      and the working copies re-derived (after_step).
+    * Other stages (the CPU oracle stages of the gloo tests): one all-reduce
+      per gradient tensor, no overlap (zero is ignored: no optimizer there).
+    gloo groups (the 2-processes-on-one-GPU tests) reduce-scatter via an
+    all-reduce and all-gather via a list; NCCL uses the native collectives."""
+
+    def __init__(self, stage, group, replicas: int, zero: bool = False):
+        import torch.distributed as dist
+        self.dist, self.stage, self.group, self.R = dist, stage, group, int(replicas)
+        self.active = group is not None and self.R > 1
+        self.rank = dist.get_rank(group) if self.active else 0
+        self.cuda = hasattr(stage, "arena")
+        self.zero = bool(zero) and self.cuda and self.active
+        self.works = []
+        self.native = self.active and dist.get_backend(group) == "nccl"
+        if self.cuda:
+            a = stage.arena()
+            self.grad, self.master = a["grad"], a["master"]
+            self.off = stage.buckets()
+            stage.grad_events(True)
+            self.side = torch.cuda.Stream(device=stage.device)
+            self.state_numel = stage.opt_shard(self.rank, self.R) if self.zero else self.master.numel()
+
+    def _slice(self, t: torch.Tensor) -> torch.Tensor:
+        n = t.numel() // self.R
+        return t[self.rank * n:(self.rank + 1) * n]
+
+    def launch(self) -> None:
+        """Issue the reductions; call right after the stage's last backward of
+        the step was enqueued (e.g. after run_step returned)."""
+        if not self.active:
+            return
+        if not self.cuda:
+            for t in self.stage.grad_views().values():
+                self.dist.all_reduce(t, group=self.group)
+            return
+        with torch.cuda.stream(self.side):
+            for b in reversed(range(len(self.off) - 1)):
+                self.stage.bucket_wait(b, self.side)
+                g = self.grad[self.off[b]:self.off[b + 1]]
+                if self.zero and self.native:
+                    w = self.dist.reduce_scatter_tensor(self._slice(g), g, group=self.group, async_op=True)
+                else:
+                    w = self.dist.all_reduce(g, group=self.group, async_op=True)
+                self.works.append(w)
+
+    def finish(self) -> None:
+        """The current stream waits for every reduction (before the optimizer)."""
+        for w in self.works:
+            w.wait()
+        self.works = []
+
+    def after_step(self) -> None:
+        """ZeRO-1: all-gather the updated master slices, then re-derive the
+        working copies."""
+        if not self.zero:
+            return
+        for b in range(len(self.off) - 1):
+            m = self.master[self.off[b]:self.off[b + 1]]
+            mine = self._slice(m)
+            if self.native:
+                self.dist.all_gather_into_tensor(m, mine, group=self.group)
+            else:
+                parts = list(m.chunk(self.R))
+                self.dist.all_gather(parts, mine.clone(), group=self.group)
+                m.copy_(torch.cat(parts))
+        self.stage.sync_weights()
+
+
 def allreduce_grads(stage, group, replicas: int) -> None:
-    """Data-parallel gradient average of one stage over its replicas (NCCL
-    all-reduce on B200s), in place on the stage's accumulated gradients."""
+    """Blocking per-tensor sum of one stage's gradients over its replicas
+    (the un-bucketed baseline; GradSync is the overlapped path)."""
     if group is None or replicas <= 1:
         return
     import torch.distributed as dist
     for t in stage.grad_views().values():
         dist.all_reduce(t, group=group)
-        t.mul_(1.0 / replicas)
 
 
 class DistributedPipeline:
@@ -270,11 +360,13 @@ class DistributedPipeline:
         pending.append((self.dist.isend(t, dst=dst, group=group), t))
         self.p2p_bytes += t.numel() * t.element_size()
 
-    def run_step(self, plan: Plan, tokens: Sequence[np.ndarray], staged: Optional[_ChunkTokens] = None) -> dict:
+    def run_step(self, plan: Plan, tokens: Sequence[np.ndarray], staged: Optional[_ChunkTokens] = None,
+                 total_targets: Optional[int] = None) -> dict:
         p, dp = self.rank, self.world
         if dp != plan.pp_degree:
             raise ValueError(f"plan is for {plan.pp_degree} stages, world size is {dp}")
         toks = staged or _ChunkTokens(plan, tokens, self.device, need_ids=(p == 0), need_targets=(p == dp - 1))
+        self._targets = total_targets
         for unit in plan.units:
             if self.p2p:
                 self._run_unit_p2p(plan, unit, toks)
@@ -285,7 +377,7 @@ class DistributedPipeline:
     def _run_unit_p2p(self, plan: Plan, unit, toks: _ChunkTokens):
         p, dp, ch = self.rank, self.world, self.ch
         for kind, pos in stage_ops(len(unit.chunks), unit.n_prefill, dp, p + 1, unit.backward_order):
-            op = _op(plan, unit, pos, p, toks)
+            op = _op(plan, unit, pos, p, toks, self._targets)
             nbytes = self.stage.act_bytes(op)
             if kind == "F":
                 src = ch["fin"].recv_wait(nbytes) if p > 0 else None
@@ -311,7 +403,7 @@ class DistributedPipeline:
         pending = []
         for kind, pos in stage_ops(len(unit.chunks), unit.n_prefill, dp, p + 1, unit.backward_order):
             T = plan.chunks[unit.chunks[pos]].tokens
-            op = _op(plan, unit, pos, p, toks)
+            op = _op(plan, unit, pos, p, toks, self._targets)
             if kind == "F":
                 act_in = self._recv(T, self.ranks[p - 1], self.fwd_groups[p - 1]) if p > 0 else None
                 out = self.stage.forward(op, act_in)

@@ -79,6 +79,11 @@ def lib():
             "epp_stage_memory": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)],
             "epp_gpu_profile": [i32],
             "epp_stage_trace": [vp, i32, vp],
+            "epp_stage_arena": [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(i64)],
+            "epp_stage_buckets": [vp, ctypes.POINTER(i64), i32, ctypes.POINTER(i32)],
+            "epp_stage_grad_events": [vp, i32],
+            "epp_stage_bucket_wait": [vp, i32, vp],
+            "epp_stage_opt_shard": [vp, i32, i32, ctypes.POINTER(i64)],
             "epp_stage_trace_read": [vp, ctypes.POINTER(TraceEvent), i32, ctypes.POINTER(i32)],
             "epp_stage_chunk_loss": [vp, i32, ctypes.POINTER(ctypes.c_double), vp],
             "epp_gpu_profile_read": [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
@@ -297,6 +302,40 @@ class CudaStage:
         collectives, e.g. the data-parallel all-reduce)."""
         return {name: _wrap_ptr(p["grad"], p["numel"], torch.float32, self.device)
                 for name, p in self.params().items()}
+
+    # -- data-parallel buckets (include/epp_gpu.h, data parallelism) ---------
+    def arena(self) -> Dict[str, torch.Tensor]:
+        """Zero-copy flat views of the fp32 master and gradient arenas."""
+        m, w, g, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64()
+        check(lib().epp_stage_arena(self.h, ctypes.byref(m), ctypes.byref(w), ctypes.byref(g), ctypes.byref(n)))
+        return {"master": _wrap_ptr(m.value, n.value, torch.float32, self.device),
+                "grad": _wrap_ptr(g.value, n.value, torch.float32, self.device)}
+
+    def buckets(self):
+        """Arena element offsets of the gradient buckets ([embedding],
+        layers, [head]): nbuckets + 1 values."""
+        nb = ctypes.c_int32()
+        check(lib().epp_stage_buckets(self.h, None, 0, ctypes.byref(nb)))
+        arr = (ctypes.c_int64 * (nb.value + 1))()
+        check(lib().epp_stage_buckets(self.h, arr, nb.value + 1, ctypes.byref(nb)))
+        return list(arr)
+
+    def grad_events(self, enable: bool = True):
+        check(lib().epp_stage_grad_events(self.h, int(enable)))
+
+    def bucket_wait(self, bucket: int, stream: Optional[torch.cuda.Stream] = None):
+        """`stream` waits until bucket's gradients of the latest backward are final."""
+        check(lib().epp_stage_bucket_wait(self.h, int(bucket), stream_ptr(stream)))
+
+    def opt_shard(self, rank: int, nranks: int) -> int:
+        """ZeRO-1: keep Adam state for slice `rank` of `nranks` of every bucket;
+        returns the state elements held."""
+        n = ctypes.c_int64()
+        check(lib().epp_stage_opt_shard(self.h, int(rank), int(nranks), ctypes.byref(n)))
+        return n.value
+
+    def sync_weights(self):
+        check(lib().epp_stage_sync_weights(self.h, stream_ptr()))
 
     def zero_grads(self):
         check(lib().epp_stage_zero_grads(self.h, stream_ptr()))

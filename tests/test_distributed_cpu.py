@@ -95,7 +95,7 @@ LENGTHS_B = [120, 260, 33, 75, 9, 140]
 
 
 def dp_worker(rank, world, pp, port, docs, q):
-    from paper_2509_21275_b200.executor import allreduce_grads, pipeline_groups
+    from paper_2509_21275_b200.executor import GradSync, pipeline_groups
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
     replicas = world // pp
@@ -107,16 +107,24 @@ def dp_worker(rank, world, pp, port, docs, q):
     first, num = stage_layers(MODEL.layers, pp, p)
     st = O.TorchStage(spec(), params, first, num, p == 0, p == pp - 1)
     drv = DistributedPipeline(st, p, pp, torch.device("cpu"), MODEL.hidden, torch.float32, pipe=pipes[replica])
-    drv.run_step(plan, S.synthetic_tokens(lengths, MODEL.vocab, seed=11 + replica))
-    allreduce_grads(st, dp_groups[p], replicas)
+    sync = GradSync(st, dp_groups[p], replicas)
+    drv.run_step(plan, S.synthetic_tokens(lengths, MODEL.vocab, seed=11 + replica), total_targets=global_targets())
+    sync.launch()
+    sync.finish()
     q.put((rank, {k: v.numpy().copy() for k, v in st.grads().items()}))   # by value: the worker exits
     torch.distributed.barrier()
     torch.distributed.destroy_process_group()
 
 
+def global_targets():
+    return sum(max(0, n - 1) for n in LENGTHS + LENGTHS_B)
+
+
 def test_gloo_pipeline_data_parallel_replicas():
-    """pp 2 x dp 2: each replica pipelines its own batch, then the stage
-    gradients are averaged across replicas (allreduce_grads)."""
+    """pp 2 x dp 2: each replica pipelines its own batch with the loss
+    normalised by the targets of the WHOLE global batch, then the stage
+    gradients are summed across replicas (GradSync): the global per-token
+    mean, whatever each replica's share of targets."""
     from paper_2509_21275_b200 import planner
     pp, world = 2, 4
     cfg = M.planner_config(MODEL, pp, mem_capacity=1e12, reserve_bytes=0)
@@ -139,15 +147,16 @@ def test_gloo_pipeline_data_parallel_replicas():
         stages = [O.TorchStage(spec(), params, *stage_layers(MODEL.layers, pp, p), p == 0, p == pp - 1)
                   for p in range(pp)]
         LocalPipeline(stages, torch.device("cpu")).run_step(S.parse_plan(docs[replica], lengths),
-                                                           S.synthetic_tokens(lengths, MODEL.vocab, seed=11 + replica))
+                                                           S.synthetic_tokens(lengths, MODEL.vocab, seed=11 + replica),
+                                                           total_targets=global_targets())
         for st in stages:
             for k, v in st.grads().items():
-                ref[k] = ref.get(k, 0) + v / 2
+                ref[k] = ref.get(k, 0) + v
     for rank in range(world):
         p = rank % pp
         for k, v in results[rank].items():
             assert torch.allclose(v, ref[k], rtol=1e-5, atol=1e-8), (rank, k)
-    # both replicas of a stage hold identical averaged gradients
+    # both replicas of a stage hold identical summed gradients
     for p in range(pp):
         for k in results[p]:
             assert torch.equal(results[p][k], results[pp + p][k])

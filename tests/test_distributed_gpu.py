@@ -169,3 +169,80 @@ def test_p2p_channel_roundtrip():
         tx.send(torch.empty(4 << 20, device="cuda", dtype=torch.uint8))
     rx.close()
     tx.close()
+
+
+LENGTHS_R1 = [300, 44, 610, 17, 128]
+
+
+def dp_worker(rank, world, port, docs, zero, q):
+    from paper_2509_21275_b200.executor import GradSync, LocalPipeline
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    group = torch.distributed.new_group(list(range(world)))
+    lengths = (LENGTHS, LENGTHS_R1)[rank]
+    plan = S.parse_plan(docs[rank], lengths)
+    params = O.init_params(spec(), seed=5)
+    from paper_2509_21275_b200.gpu import CudaStage
+    st = CudaStage(MODEL, 0, MODEL.layers, True, True, dtype="f32")
+    st.load_weights(params)
+    sync = GradSync(st, group, world, zero=zero)
+    LocalPipeline([st], torch.device("cuda")).run_step(plan, S.synthetic_tokens(lengths, MODEL.vocab, seed=21 + rank),
+                                                       total_targets=targets_all())
+    sync.launch()
+    sync.finish()
+    grads = st.arena()["grad"].cpu().numpy().copy()
+    st.adamw_step(1e-3, 1)
+    sync.after_step()
+    torch.cuda.synchronize()
+    q.put((rank, grads, st.arena()["master"].cpu().numpy().copy(), sync.state_numel))
+    torch.distributed.barrier()
+    torch.distributed.destroy_process_group()
+
+
+def targets_all():
+    return sum(max(0, n - 1) for n in LENGTHS + LENGTHS_R1)
+
+
+@pytest.mark.parametrize("zero", [False, True])
+def test_data_parallel_gradsync(zero):
+    """dp 2 (two processes on cuda:0): bucketed gradient reduction over the
+    stage arenas (GradSync) after a step normalised by the global batch's
+    targets, then AdamW (ZeRO-1: each replica updates its half of every
+    bucket and the masters are all-gathered).  Equals one process running
+    both batches into one stage and stepping once."""
+    from paper_2509_21275_b200 import planner
+    from paper_2509_21275_b200.gpu import CudaStage
+    world = 2
+    cfg = M.planner_config(MODEL, 1, mem_capacity=1e12, reserve_bytes=0)
+    docs = [planner.make_plan_document(cfg, LENGTHS, 3, "main", 1),
+            planner.make_plan_document(cfg, LENGTHS_R1, 3, "main", 1)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=dp_worker, args=(r, world, port, docs, zero, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted(collect(q, procs, world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    params = O.init_params(spec(), seed=5)
+    st = CudaStage(MODEL, 0, MODEL.layers, True, True, dtype="f32")
+    st.load_weights(params)
+    drv = LocalPipeline([st], torch.device("cuda"))
+    for r, lengths in enumerate((LENGTHS, LENGTHS_R1)):
+        drv.run_step(S.parse_plan(docs[r], lengths), S.synthetic_tokens(lengths, MODEL.vocab, seed=21 + r),
+                     total_targets=targets_all())
+    ref_grad = st.arena()["grad"].cpu()
+    st.adamw_step(1e-3, 1)
+    ref_master = st.arena()["master"].cpu()
+    full = ref_master.numel()
+    for rank, g, m, state in results:
+        g, m = torch.from_numpy(g), torch.from_numpy(m)
+        if not zero:
+            assert float((g - ref_grad).norm() / ref_grad.norm()) < 1e-6
+        assert float((m - ref_master).norm() / ref_master.norm()) < 1e-6, rank
+        assert state == (full // 2 if zero else full)
+    assert torch.equal(torch.from_numpy(results[0][2]), torch.from_numpy(results[1][2]))
+    st.close()

@@ -26,6 +26,11 @@ CASES = {
     "seq4k": dict(H=16, Hkv=16, hd=128, segs=[(0, 4096, 0)]),
     "seq2k": dict(H=16, Hkv=16, hd=128, segs=[(0, 2048, 0)]),
     "seq1k_x8": dict(H=16, Hkv=16, hd=128, segs=[(i * 1024, 1024, 0) for i in range(8)]),
+    # GPT-7B (H=32, hd=128) at the default bench workload: a whole 16K
+    # sequence, and a split slice + packed short (14926 + 1316)
+    "gpt7b_16k": dict(H=32, Hkv=32, hd=128, segs=[(0, 16384, 0)]),
+    "gpt7b_hybrid": dict(H=32, Hkv=32, hd=128, segs=[(0, 14926, 0), (14926, 1316, 0)]),
+    "gpt7b_ctx": dict(H=32, Hkv=32, hd=128, segs=[(0, 5349, 10571)]),
 }
 
 
