@@ -774,13 +774,17 @@ __global__ void add_k(T* y, const T* x, long long n) {
         y[i] = from_f<T>(to_f(y[i]) + to_f(x[i]));
 }
 
-// Multi-tensor AdamW: float4 group i of the concatenated segments is found
-// by binary search over the segments' start4 prefix (a few hundred entries,
-// L1-resident), so the whole stage updates in one launch.
+// Multi-tensor AdamW: a block owns kAdamPer * blockDim consecutive float4
+// groups of the concatenated segments; each thread finds its first group's
+// segment by binary search over the start4 prefix (a few hundred entries,
+// L1-resident) and then only walks forward, so the whole stage updates in one
+// launch with independent, coalesced 16-byte accesses.
+constexpr int kAdamPer = 4;
 template <typename T>
-__global__ void adamw_multi_k(const AdamSeg* __restrict__ segs, int nseg, long long total4, float* master, T* work,
-                              float* grad, float* m, float* v, float lr, float b1, float b2, float eps, float wd,
-                              float bc1, float bc2) {
+__global__ void adamw_multi_k(const AdamSeg* __restrict__ segs, int nseg, long long total4,
+                              float* __restrict__ master, T* __restrict__ work, float* __restrict__ grad,
+                              float* __restrict__ m, float* __restrict__ v, float lr, float b1, float b2, float eps,
+                              float wd, float bc1, float bc2) {
     pdl_wait();
     pdl_trigger();
     const float ib1 = 1.f / bc1, ib2 = 1.f / bc2;
@@ -789,18 +793,20 @@ __global__ void adamw_multi_k(const AdamSeg* __restrict__ segs, int nseg, long l
         vi = b2 * vi + (1.f - b2) * g * g;
         p -= lr * (w * p + (mi * ib1) / (sqrtf(vi * ib2) + eps));
     };
-    int seg = 0;
-    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total4;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        if (i < __ldg(&segs[seg].start4) || (seg + 1 < nseg && i >= __ldg(&segs[seg + 1].start4))) {
-            int lo = 0, hi = nseg - 1;     // last segment with start4 <= i
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (__ldg(&segs[mid].start4) <= i) lo = mid;
-                else hi = mid - 1;
-            }
-            seg = lo;
-        }
+    const long long first = static_cast<long long>(blockIdx.x) * kAdamPer * blockDim.x + threadIdx.x;
+    if (first >= total4) return;
+    int lo = 0, hi = nseg - 1;     // last segment with start4 <= first
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(&segs[mid].start4) <= first) lo = mid;
+        else hi = mid - 1;
+    }
+    int seg = lo;
+#pragma unroll
+    for (int u = 0; u < kAdamPer; ++u) {
+        const long long i = first + static_cast<long long>(u) * blockDim.x;
+        if (i >= total4) break;
+        while (seg + 1 < nseg && __ldg(&segs[seg + 1].start4) <= i) ++seg;
         const long long local = i - __ldg(&segs[seg].start4);
         const long long e = __ldg(&segs[seg].off) / 4 + local;      // float4 index in the arenas
         const long long q = __ldg(&segs[seg].mv) / 4 + local;       // float4 index in the state
@@ -820,10 +826,10 @@ __global__ void adamw_multi_k(const AdamSeg* __restrict__ segs, int nseg, long l
         if constexpr (std::is_same<T, float>::value) {
             reinterpret_cast<float4*>(work)[e] = p;
         } else {
-            __nv_bfloat162 lo = __floats2bfloat162_rn(p.x, p.y), hi = __floats2bfloat162_rn(p.z, p.w);
+            __nv_bfloat162 lo2 = __floats2bfloat162_rn(p.x, p.y), hi2 = __floats2bfloat162_rn(p.z, p.w);
             uint2 raw;
-            raw.x = *reinterpret_cast<uint32_t*>(&lo);
-            raw.y = *reinterpret_cast<uint32_t*>(&hi);
+            raw.x = *reinterpret_cast<uint32_t*>(&lo2);
+            raw.y = *reinterpret_cast<uint32_t*>(&hi2);
             reinterpret_cast<uint2*>(work)[e] = raw;
         }
     }
@@ -1122,7 +1128,8 @@ void adamw_multi(const AdamSeg* segs, int nseg, long long total4, float* master,
     if (total4 == 0 || nseg == 0) return;
     dispatch_t(t, [&](auto z) {
         using E = decltype(z);
-        launch_k(adamw_multi_k<E>, grid_for(total4, 256), 256, 0, s, segs, nseg, total4, master,
+        const long long blocks = (total4 + kAdamPer * 256 - 1) / (kAdamPer * 256);
+        launch_k(adamw_multi_k<E>, dim3(static_cast<unsigned>(blocks)), 256, 0, s, segs, nseg, total4, master,
                  static_cast<E*>(work), grad, m, v, lr, b1, b2, eps, wd, bc1, bc2);
     });
     EPP_CHECK_LAUNCH();

@@ -164,7 +164,6 @@ struct LayerSaved {
     Buf x_out;        // output of this layer (= next layer's input); last layer -> act_out
     Buf mean1, rstd1, mean2, rstd2;
     Buf q, o, lse, x_mid, h;
-    Buf act;             // MLP activation gelu(h) / silu(g)*u: dW2's operand, kept
     bool full = false;   // q/o/lse/x_mid/h/act present
 };
 
@@ -697,7 +696,7 @@ private:
     long long kvw() const { return static_cast<long long>(Hkv_) * hd_; }
 
     void drop_full(LayerSaved& L) {
-        L.q.release(); L.o.release(); L.lse.release(); L.x_mid.release(); L.h.release(); L.act.release();
+        L.q.release(); L.o.release(); L.lse.release(); L.x_mid.release(); L.h.release();
         L.full = false;
     }
 
@@ -955,20 +954,24 @@ private:
         norm_fwd(dt_, llama_, L.x_mid.get(), work(P.ln2_w), P.ln2_b >= 0 ? work(P.ln2_b) : nullptr,
                  xn.get(), llama_ ? nullptr : L.mean2.get<float>(), L.rstd2.get<float>(), T, D_,
                  m_.norm_eps, s);
-        // the activation is kept for dW2 (also when recomputing a
-        // checkpointed layer), so the backward never re-derives it
-        L.act = Buf(&pool_, static_cast<size_t>(T) * F_ * e, s);
+        // The MLP activation is only W2's operand here: transient (the
+        // backward re-creates it from h for dW2), so a layer keeps 14 -> 10
+        // hidden-widths of activations per token (GPT) and the planner's
+        // checkpoint ladder has to recompute fewer layers.  A recompute
+        // (skip_out) only restores h.
+        Buf act;
+        if (!skip_out) act = Buf(&pool_, static_cast<size_t>(T) * F_ * e, s);
         GemmArgs up = mk(T, F1_, D_, xn.get(), D_, true, work(P.w1), D_, true, L.h.get(), F1_);
-        if (!llama_) {   // GELU fused into the up-projection epilogue
+        if (!llama_ && !skip_out) {   // GELU fused into the up-projection epilogue
             up.epi = Epi::StoreGelu;
-            up.C2 = L.act.get();
+            up.C2 = act.get();
             up.ldc2 = F_;
         }
         gemm(up, s);
         xn.release();
-        if (llama_) act_fwd(dt_, 1, L.h.get(), L.act.get(), T, F_, s);
         if (!skip_out) {
-            GemmArgs g2 = mk(T, D_, F_, L.act.get(), F_, true, work(P.w2), F_, true, out, D_);
+            if (llama_) act_fwd(dt_, 1, L.h.get(), act.get(), T, F_, s);
+            GemmArgs g2 = mk(T, D_, F_, act.get(), F_, true, work(P.w2), F_, true, out, D_);
             g2.epi = Epi::AddRes;
             g2.R = L.x_mid.get();
             g2.ldr = D_;
@@ -983,8 +986,11 @@ private:
         const size_t e = esz();
         const int Dq = H_ * hd_;
         // ---- MLP ----
-        wgrad(D_, F_, T, dy, D_, L.act.get(), F_, grad(P.w2), s);                          // dW2 += dY^T A
-        L.act.release();
+        {   // dW2 += dY^T A, A = act(h) re-created from the saved h
+            Buf act(&pool_, static_cast<size_t>(T) * F_ * e, s);
+            act_fwd(dt_, llama_ ? 1 : 0, L.h.get(), act.get(), T, F_, s);
+            wgrad(D_, F_, T, dy, D_, act.get(), F_, grad(P.w2), s);
+        }
         Buf dh(&pool_, static_cast<size_t>(T) * F1_ * e, s);
         if (llama_) {
             Buf da(&pool_, static_cast<size_t>(T) * F_ * e, s);

@@ -92,12 +92,12 @@ B200_MEM_CAPACITY = 180e9
 def activation_bytes_per_token(m: ModelConfig, elem_bytes: int = 2) -> float:
     """Bytes the CUDA stage keeps per token per NON-checkpointed layer until
     the chunk's backward (stage.cu LayerSaved + chunk-local K/V): layer output
-    x (D), q (H*hd), o (H*hd), x_mid (D), h (F or 2F), act (F), K and V (2*Hkv*hd),
-    plus fp32 norm stats and LSE."""
+    x (D), q (H*hd), o (H*hd), x_mid (D), h (F or 2F), K and V (2*Hkv*hd),
+    plus fp32 norm stats and LSE.  The MLP activation act(h) is transient (the
+    backward re-creates it from h for the W2 weight gradient)."""
     D, hd = m.hidden, m.head_dim
     f1 = 2 * m.ffn if m.llama else m.ffn
-    # ... + the MLP activation (ffn), kept for the W2 weight gradient
-    elems = D + m.heads * hd + m.heads * hd + D + f1 + m.ffn + 2 * m.kv_heads * hd
+    elems = D + m.heads * hd + m.heads * hd + D + f1 + 2 * m.kv_heads * hd
     return elems * elem_bytes + 4 * 4 + 4 * m.heads
 
 
