@@ -193,7 +193,9 @@ def global_targets(args, n_batches, world, replicas, seed0=1000):
 
 PROF_CLASSES = ((0, "gemm"), (1, "attn_fwd"), (2, "attn_bwd"), (3, "attn_bwd_dq"), (4, "attn_bwd_dkv"),
                 (5, "norm_fwd"), (6, "norm_bwd"), (7, "rope"), (8, "act"), (9, "cross_entropy"),
-                (10, "adamw"), (11, "embed"), (12, "copy_fill"))
+                (10, "adamw"), (11, "embed"), (12, "copy_fill"),
+                (13, "gemm_store"), (14, "gemm_wgrad_accum"), (15, "gemm_addres"), (16, "gemm_store_f32"),
+                (17, "gemm_up_gelu"), (18, "gemm_dgrad_gelu"), (19, "gemm_qkv_rope"))
 
 
 def read_profile(lib):
@@ -464,7 +466,8 @@ def run_ours(args):
                            for k, v in gemm_flops_class.items()},
         "instrumented_ms_per_step": prof_ms / nprof,
         "unattributed_ms_per_step": (prof_ms - sum(v["ms"] for k, v in prof.items()
-                                                   if k not in ("attn_bwd_dq", "attn_bwd_dkv"))) / nprof,
+                                                   if k not in ("attn_bwd_dq", "attn_bwd_dkv")
+                                                   and not k.startswith("gemm_"))) / nprof,
         "clocks": clk.summary(),
         "e2e": e2e,
         "trace": trace_block,

@@ -829,6 +829,7 @@ void gemm(const GemmArgs& g, cudaStream_t s) {
     EPP_REQUIRE(g.M >= 0 && g.N >= 0 && g.K >= 0, "gemm: negative extent");
     if (g.M == 0 || g.N == 0) return;
     ProfScope prof(kProfGemm, 2.0 * g.M * g.N * g.K, s);
+    ProfScope prof_epi(kProfGemmEpi0 + static_cast<int>(g.epi), 2.0 * g.M * g.N * g.K, s);
     if (g.dtype == DType::F32) {
         dim3 grid(ceil_div(g.N, 64), ceil_div(g.M, 64));
         launch_k(gemm_simt_kernel<float>, grid, 256, 0, s, g);
