@@ -219,8 +219,8 @@ int epp_kernel_gemm(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda,
                     int64_t ldc, const void* R, int64_t ldr, int32_t epi, int32_t dtype,
                     void* stream);
 /* Same with the fused MLP epilogues: epi 4 = StoreGelu (C = acc, C2 =
- * gelu_tanh(acc)), 5 = GeluBwd (C = acc * gelu_tanh'(R)); bf16 only for 4/5
- * outputs in the stage dtype. */
+ * gelu_tanh(acc)), 5 = GeluBwd (C = acc * gelu_tanh'(R), and C2 =
+ * gelu_tanh(R) when C2 is given); outputs in the stage dtype. */
 int epp_kernel_gemm_ex(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_kmajor,
                        const void* B, int64_t ldb, int32_t b_kmajor, void* C, int64_t ldc,
                        const void* R, int64_t ldr, void* C2, int64_t ldc2, int32_t epi, int32_t dtype,

@@ -131,6 +131,14 @@ __device__ __forceinline__ float gelu_tanh_fast_f(float x) {
     const float z = gelu_sigmoid_arg_(x, du);
     return __fdividef(x, 1.f + __expf(-z));
 }
+// gelu(x) and gelu'(x) from one sigmoid
+__device__ __forceinline__ float gelu_tanh_and_grad_fast_f(float x, float& grad) {
+    float du;
+    const float z = gelu_sigmoid_arg_(x, du);
+    const float s = __fdividef(1.f, 1.f + __expf(-z));
+    grad = fmaf(x * s * (1.f - s), du, s);
+    return x * s;
+}
 __device__ __forceinline__ float gelu_tanh_grad_fast_f(float x) {
     float du;
     const float z = gelu_sigmoid_arg_(x, du);

@@ -180,15 +180,32 @@ __device__ __forceinline__ void epilogue_plain(const TcParams& p, uint32_t taddr
         } else {
             if (EPI == static_cast<int>(Epi::AddRes) || EPI == static_cast<int>(Epi::GeluBwd)) {
                 const bf16* r = p.R + static_cast<long long>(row) * p.ldr + col;
+                // GeluBwd with C2: also emit gelu(R) (the MLP activation that
+                // dW2 needs), re-created here from the h already being read
+                bf16* dst2 = (EPI == static_cast<int>(Epi::GeluBwd) && p.C2)
+                                 ? p.C2 + static_cast<long long>(row) * p.ldc2 + col : nullptr;
 #pragma unroll
                 for (int i = 0; i < 32; i += 8) {
                     const uint4 raw = *reinterpret_cast<const uint4*>(r + i);
                     const bf16* rb = reinterpret_cast<const bf16*>(&raw);
+                    float a[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const float rv = __bfloat162float(rb[j]);
-                        if (EPI == static_cast<int>(Epi::AddRes)) v[i + j] += rv;
-                        else v[i + j] *= gelu_tanh_grad_fast_f(rv);
+                        if (EPI == static_cast<int>(Epi::AddRes)) {
+                            v[i + j] += rv;
+                        } else {
+                            float dg;
+                            a[j] = gelu_tanh_and_grad_fast_f(rv, dg);
+                            v[i + j] *= dg;
+                        }
+                    }
+                    if (EPI == static_cast<int>(Epi::GeluBwd) && dst2) {
+                        uint4 out;
+                        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&out);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) h2[j] = __floats2bfloat162_rn(a[2 * j], a[2 * j + 1]);
+                        *reinterpret_cast<uint4*>(dst2 + i) = out;
                     }
                 }
             }
@@ -813,8 +830,11 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
             } else {
                 if (g.epi == Epi::AddRes)
                     v += to_f(static_cast<const T*>(g.R)[static_cast<long long>(m) * g.ldr + n]);
-                if (g.epi == Epi::GeluBwd)
-                    v *= gelu_tanh_grad_f(to_f(static_cast<const T*>(g.R)[static_cast<long long>(m) * g.ldr + n]));
+                if (g.epi == Epi::GeluBwd) {
+                    const float rv = to_f(static_cast<const T*>(g.R)[static_cast<long long>(m) * g.ldr + n]);
+                    v *= gelu_tanh_grad_f(rv);
+                    if (g.C2) static_cast<T*>(g.C2)[static_cast<long long>(m) * g.ldc2 + n] = from_f<T>(gelu_tanh_f(rv));
+                }
                 if (g.epi == Epi::StoreGelu)
                     static_cast<T*>(g.C2)[static_cast<long long>(m) * g.ldc2 + n] = from_f<T>(gelu_tanh_f(v));
                 static_cast<T*>(g.C)[off] = from_f<T>(v);

@@ -24,7 +24,7 @@ enum class Epi : int {
     AddRes = 2,     // C = acc + R             (residual stream update)
     StoreF32 = 3,   // C(fp32) = acc
     StoreGelu = 4,  // C = acc, C2 = gelu_tanh(acc)          (MLP up-projection)
-    GeluBwd = 5,    // C = acc * gelu_tanh'(R)               (MLP dgrad -> dh)
+    GeluBwd = 5,    // C = acc * gelu_tanh'(R) [, C2 = gelu_tanh(R)]  (MLP dgrad -> dh [+ act for dW2])
     RopeScatter = 6,  // QKV projection: RoPE on q/k, q -> [T,H,hd], k/v -> the segments' KV rows
 };
 

@@ -986,23 +986,30 @@ private:
         const size_t e = esz();
         const int Dq = H_ * hd_;
         // ---- MLP ----
-        {   // dW2 += dY^T A, A = act(h) re-created from the saved h
-            Buf act(&pool_, static_cast<size_t>(T) * F_ * e, s);
-            act_fwd(dt_, llama_ ? 1 : 0, L.h.get(), act.get(), T, F_, s);
-            wgrad(D_, F_, T, dy, D_, act.get(), F_, grad(P.w2), s);
-        }
+        // The activation A = act(h) that dW2 needs is not kept from the
+        // forward: GPT re-creates it in the W2 data-gradient epilogue (which
+        // reads h for gelu' anyway), Llama in a pass over h.
+        Buf act(&pool_, static_cast<size_t>(T) * F_ * e, s);
         Buf dh(&pool_, static_cast<size_t>(T) * F1_ * e, s);
         if (llama_) {
+            act_fwd(dt_, 1, L.h.get(), act.get(), T, F_, s);
+            wgrad(D_, F_, T, dy, D_, act.get(), F_, grad(P.w2), s);                    // dW2 += dY^T A
+            act.release();
             Buf da(&pool_, static_cast<size_t>(T) * F_ * e, s);
             gemm(mk(T, F_, D_, dy, D_, true, work(P.w2), F_, false, da.get(), F_), s);    // dA = dY W2
             act_bwd(dt_, 1, L.h.get(), da.get(), dh.get(), T, F_, s);
         } else {
-            // dH = (dY W2) * gelu'(H), fused into the data-gradient epilogue
+            // dH = (dY W2) * gelu'(H) and A = gelu(H), fused into the
+            // data-gradient epilogue
             GemmArgs g = mk(T, F_, D_, dy, D_, true, work(P.w2), F_, false, dh.get(), F_);
             g.epi = Epi::GeluBwd;
             g.R = L.h.get();
             g.ldr = F_;
+            g.C2 = act.get();
+            g.ldc2 = F_;
             gemm(g, s);
+            wgrad(D_, F_, T, dy, D_, act.get(), F_, grad(P.w2), s);                    // dW2 += dY^T A
+            act.release();
         }
         Buf dxn(&pool_, static_cast<size_t>(T) * D_ * e, s);
         gemm(mk(T, D_, F1_, dh.get(), F1_, true, work(P.w1), D_, false, dxn.get(), D_), s);  // dXn2

@@ -82,7 +82,7 @@ def test_gemm_pair_epilogues(epi):
     """Every epilogue on the CTA-pair kernel (>= 60 pair tiles, N % 256 == 0)
     at the GPT-1.3B up-projection / W2-dgrad widths, with a ragged M edge:
     0 Store, 1 AccumF32 (wgrad, MN-major operands), 2 AddRes, 3 StoreF32,
-    4 StoreGelu (C and gelu(C)), 5 GeluBwd (C * gelu'(R)).  The fp32-output
+    4 StoreGelu (C and gelu(C)), 5 GeluBwd (C * gelu'(R) and gelu(R)).  The fp32-output
     epilogues (1, 3) are held to 1e-5 against an fp64 product of the same
     bf16 operands: only the accumulation order differs."""
     g = G()
@@ -108,7 +108,7 @@ def test_gemm_pair_epilogues(epi):
     C2 = torch.empty((M, N), device="cuda", dtype=torch.bfloat16)
     g.check(g.lib().epp_kernel_gemm_ex(M, N, K, A.data_ptr(), K, 1, B.data_ptr(), K, 1, C.data_ptr(), N,
                                        R.data_ptr() if epi in (2, 5) else None, N,
-                                       C2.data_ptr() if epi == 4 else None, N, epi, g.DTYPES["bf16"],
+                                       C2.data_ptr() if epi in (4, 5) else None, N, epi, g.DTYPES["bf16"],
                                        g.stream_ptr()))
     torch.cuda.synchronize()
     gelu = lambda x: torch.nn.functional.gelu(x, approximate="tanh")
@@ -123,7 +123,8 @@ def test_gemm_pair_epilogues(epi):
     else:
         r = R.double().requires_grad_()
         gelu(r).backward(torch.ones_like(r))
-        checks = [(C, acc * r.grad, 8e-3)]
+        # C2: the activation gelu(R) the W2 weight gradient re-uses
+        checks = [(C, acc * r.grad, 8e-3), (C2, gelu(R.double()), 8e-3)]
     for got, ref, tol in checks:
         err = float((got.double() - ref).norm() / ref.norm())
         assert err < tol, (epi, err)

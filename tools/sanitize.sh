@@ -13,10 +13,10 @@ for tool in racecheck synccheck memcheck; do
   log=gpurun_out/sanitize_${tool}.log
   extra=""
   [ "$tool" = racecheck ] && extra="--racecheck-report hazard"
-  timeout 1500 compute-sanitizer --tool $tool $extra --target-processes all --print-limit 50 \
+  timeout 1500 compute-sanitizer --tool $tool $extra --target-processes all --print-limit 400 \
     python -m pytest tests/test_gpu_kernels.py -q -x -k "$SEL" > "$log" 2>&1
   echo "$tool kernels rc=$?" >> "$log"
-  timeout 900 compute-sanitizer --tool $tool $extra --print-limit 50 \
+  timeout 900 compute-sanitizer --tool $tool $extra --print-limit 400 \
     python -c "import __graft_entry__ as g; g.smoke()" >> "$log" 2>&1
   echo "$tool smoke rc=$?" >> "$log"
   grep -E "ERROR SUMMARY|RACECHECK SUMMARY|passed|failed|rc=" "$log" | tail -8
