@@ -119,6 +119,14 @@ __device__ __forceinline__ void ex2_fma2(uint64_t x, float& p0, float& p1) {
     p1 = __int_as_float(__float_as_int(t1) * (1 << 23) + __float_as_int(q1));
 }
 
+// bf16 pair (a in the low half) for a tcgen05 operand, F2FP.BF16.PACK_AB.
+// (Packing on the integer pipes instead, IADD + PRMT with round half away
+// from zero, measured 2-3 % slower in every attention kernel.)
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
 __device__ __forceinline__ float max3(float a, float b, float c) {
     float d;
     asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
@@ -160,8 +168,7 @@ __device__ __forceinline__ float exp_pack_tmem(const float (&sv)[TK / 32][32], f
                 p1 = ex2(x1);
             }
             l4[(i >> 1) & 3] = fadd2(l4[(i >> 1) & 3], f2pack(p0, p1));
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-            pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+            pk[i >> 1] = pack_bf2(p0, p1);
         }
         tc::tmem_st16u(taddr + c * 16, pk);
     }
@@ -494,10 +501,6 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
     return d;
 }
-__device__ __forceinline__ uint32_t bf2(float a, float b) {
-    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&v);
-}
 
 constexpr int TB = 64;    // secondary tile (keys in dq, queries in dkv)
 constexpr int kDqStages = 7;    // K/V ring depth of the dq kernel
@@ -543,7 +546,7 @@ __device__ __forceinline__ void dq_ds_tile(const float (&p)[TB / 32][32], const 
         for (int i = 0; i < 32; i += 2) {
             float d0, d1;
             f2unpack(fmul2(f2pack(p[c][i], p[c][i + 1]), fsub2(f2pack(dp[c][i], dp[c][i + 1]), dl)), d0, d1);
-            pk[c * 16 + (i >> 1)] = bf2(d0, d1);
+            pk[c * 16 + (i >> 1)] = pack_bf2(d0, d1);
         }
     }
 }
@@ -866,7 +869,7 @@ __device__ __forceinline__ void dkv_p_tile(float (&s)[TB / 32][32], float c2, in
             }
             s[c][i] = p0;
             s[c][i + 1] = p1;
-            pk[c * 16 + (i >> 1)] = bf2(p0, p1);
+            pk[c * 16 + (i >> 1)] = pack_bf2(p0, p1);
         }
     }
 }
@@ -878,7 +881,7 @@ __device__ __forceinline__ void dkv_ds_tile(const float (&p)[TB / 32][32], const
         for (int i = 0; i < 32; i += 2) {
             float d0, d1;
             f2unpack(fmul2(f2pack(p[c][i], p[c][i + 1]), f2pack(dp[c][i], dp[c][i + 1])), d0, d1);
-            dk[c * 16 + (i >> 1)] = bf2(d0, d1);
+            dk[c * 16 + (i >> 1)] = pack_bf2(d0, d1);
         }
     }
 }
@@ -907,6 +910,105 @@ __device__ __forceinline__ uint64_t smem_desc_sw32(uint32_t addr) {
     d |= 1ull << 46;
     d |= 6ull << 61;
     return d;
+}
+
+// dK/dV epilogue of the key-parallel kernels: softmax group 0 takes dK
+// (scaled), group 1 dV, from the TMEM accumulators at colK / colV.
+template <int HD>
+__device__ __forceinline__ void dkv_epilogue(const AttnArgs& a, const AttnSeg& sg, int kvh, int k0, int nkeys,
+                                             int r, int grp, uint32_t lane_base, uint32_t kColK, uint32_t kColV) {
+    // group 0 adds dK (scaled), group 1 adds dV into the fp32 accumulators
+    const long long kvs = static_cast<long long>(a.Hkv) * HD;
+    float* base = grp == 0 ? sg.dk : sg.dv;
+    float* drow = base + a.layer * sg.dkv_layer_stride + kvh * HD + (k0 + min(r, nkeys - 1)) * kvs;
+    const float mul = grp == 0 ? a.scale : 1.f;
+    const uint32_t col = grp == 0 ? kColK : kColV;
+    if (a.dqkv_out != nullptr) {
+        // Rows of this chunk's own tokens are complete here (later slices,
+        // which also attend to them, ran their backward first): add the
+        // accumulated fp32 partials, undo RoPE (dK) and write bf16 straight
+        // into the k / v columns of dqkv.  Context rows (earlier slices)
+        // keep accumulating in fp32.
+        constexpr int HALF = HD / 2;
+        const int kp = k0 + r;
+        const bool valid = r < nkeys;
+        const bool own = valid && kp >= sg.kv_ctx;
+        const long long t_out = sg.q_start + (kp - sg.kv_ctx);
+        bf16* orow = static_cast<bf16*>(a.dqkv_out) + t_out * (a.H + 2 * a.Hkv) * HD +
+                     (grp == 0 ? a.H + kvh : a.H + a.Hkv + kvh) * HD;
+#pragma unroll 1
+        for (int cc = 0; cc < HALF; cc += 32) {
+            float g1[32], g2[32];
+            tc::tmem_ld32(lane_base + col + cc, g1);          // warp-collective: all lanes
+            tc::tmem_ld32(lane_base + col + HALF + cc, g2);
+            if (!valid) continue;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                g1[i] *= mul;
+                g2[i] *= mul;
+            }
+            if (sg.dkv_accum) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                    const float4 o1 = *reinterpret_cast<const float4*>(drow + cc + i);
+                    const float4 o2 = *reinterpret_cast<const float4*>(drow + HALF + cc + i);
+                    g1[i] += o1.x; g1[i + 1] += o1.y; g1[i + 2] += o1.z; g1[i + 3] += o1.w;
+                    g2[i] += o2.x; g2[i + 1] += o2.y; g2[i + 2] += o2.z; g2[i + 3] += o2.w;
+                }
+            }
+            if (!own) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                    *reinterpret_cast<float4*>(drow + cc + i) = make_float4(g1[i], g1[i + 1], g1[i + 2], g1[i + 3]);
+                    *reinterpret_cast<float4*>(drow + HALF + cc + i) =
+                        make_float4(g2[i], g2[i + 1], g2[i + 2], g2[i + 3]);
+                }
+                continue;
+            }
+            if (grp == 0) {   // dK: undo the rotation at position kp
+                const float4* c4 = reinterpret_cast<const float4*>(a.rope_cs + static_cast<long long>(kp) * HALF + cc);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const float4 cs = c4[k];
+                    const float x0 = g1[2 * k], y0 = g2[2 * k], x1 = g1[2 * k + 1], y1 = g2[2 * k + 1];
+                    g1[2 * k] = x0 * cs.x + y0 * cs.y;
+                    g2[2 * k] = y0 * cs.x - x0 * cs.y;
+                    g1[2 * k + 1] = x1 * cs.z + y1 * cs.w;
+                    g2[2 * k + 1] = y1 * cs.z - x1 * cs.w;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+                uint4 ra, rb;
+                __nv_bfloat162* ha = reinterpret_cast<__nv_bfloat162*>(&ra);
+                __nv_bfloat162* hb = reinterpret_cast<__nv_bfloat162*>(&rb);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    ha[j] = __floats2bfloat162_rn(g1[i + 2 * j], g1[i + 2 * j + 1]);
+                    hb[j] = __floats2bfloat162_rn(g2[i + 2 * j], g2[i + 2 * j + 1]);
+                }
+                *reinterpret_cast<uint4*>(orow + cc + i) = ra;
+                *reinterpret_cast<uint4*>(orow + HALF + cc + i) = rb;
+            }
+        }
+    } else {
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+            float v[32];
+            tc::tmem_ld32(lane_base + col + c * 32, v);    // warp-collective: all lanes
+            if (r < nkeys) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                    float4 x = make_float4(v[i] * mul, v[i + 1] * mul, v[i + 2] * mul, v[i + 3] * mul);
+                    if (sg.dkv_accum) {   // later slices' contributions are already there
+                        const float4 o = *reinterpret_cast<const float4*>(drow + c * 32 + i);
+                        x.x += o.x; x.y += o.y; x.z += o.z; x.w += o.w;
+                    }
+                    *reinterpret_cast<float4*>(drow + c * 32 + i) = x;
+                }
+            }
+        }
+    }
 }
 
 template <int HD>
@@ -1162,98 +1264,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
         }
         tc::mbar_wait(acc_full, 0);
         tc::fence_after();
-        // group 0 adds dK (scaled), group 1 adds dV into the fp32 accumulators
-        const long long kvs = static_cast<long long>(a.Hkv) * HD;
-        float* base = grp == 0 ? sg.dk : sg.dv;
-        float* drow = base + a.layer * sg.dkv_layer_stride + kvh * HD + (k0 + min(r, nkeys - 1)) * kvs;
-        const float mul = grp == 0 ? a.scale : 1.f;
-        const uint32_t col = grp == 0 ? kColK : kColV;
-        if (a.dqkv_out != nullptr) {
-            // Rows of this chunk's own tokens are complete here (later slices,
-            // which also attend to them, ran their backward first): add the
-            // accumulated fp32 partials, undo RoPE (dK) and write bf16 straight
-            // into the k / v columns of dqkv.  Context rows (earlier slices)
-            // keep accumulating in fp32.
-            constexpr int HALF = HD / 2;
-            const int kp = k0 + r;
-            const bool valid = r < nkeys;
-            const bool own = valid && kp >= sg.kv_ctx;
-            const long long t_out = sg.q_start + (kp - sg.kv_ctx);
-            bf16* orow = static_cast<bf16*>(a.dqkv_out) + t_out * (a.H + 2 * a.Hkv) * HD +
-                         (grp == 0 ? a.H + kvh : a.H + a.Hkv + kvh) * HD;
-#pragma unroll 1
-            for (int cc = 0; cc < HALF; cc += 32) {
-                float g1[32], g2[32];
-                tc::tmem_ld32(lane_base + col + cc, g1);          // warp-collective: all lanes
-                tc::tmem_ld32(lane_base + col + HALF + cc, g2);
-                if (!valid) continue;
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    g1[i] *= mul;
-                    g2[i] *= mul;
-                }
-                if (sg.dkv_accum) {
-#pragma unroll
-                    for (int i = 0; i < 32; i += 4) {
-                        const float4 o1 = *reinterpret_cast<const float4*>(drow + cc + i);
-                        const float4 o2 = *reinterpret_cast<const float4*>(drow + HALF + cc + i);
-                        g1[i] += o1.x; g1[i + 1] += o1.y; g1[i + 2] += o1.z; g1[i + 3] += o1.w;
-                        g2[i] += o2.x; g2[i + 1] += o2.y; g2[i + 2] += o2.z; g2[i + 3] += o2.w;
-                    }
-                }
-                if (!own) {
-#pragma unroll
-                    for (int i = 0; i < 32; i += 4) {
-                        *reinterpret_cast<float4*>(drow + cc + i) = make_float4(g1[i], g1[i + 1], g1[i + 2], g1[i + 3]);
-                        *reinterpret_cast<float4*>(drow + HALF + cc + i) =
-                            make_float4(g2[i], g2[i + 1], g2[i + 2], g2[i + 3]);
-                    }
-                    continue;
-                }
-                if (grp == 0) {   // dK: undo the rotation at position kp
-                    const float4* c4 = reinterpret_cast<const float4*>(a.rope_cs + static_cast<long long>(kp) * HALF + cc);
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const float4 cs = c4[k];
-                        const float x0 = g1[2 * k], y0 = g2[2 * k], x1 = g1[2 * k + 1], y1 = g2[2 * k + 1];
-                        g1[2 * k] = x0 * cs.x + y0 * cs.y;
-                        g2[2 * k] = y0 * cs.x - x0 * cs.y;
-                        g1[2 * k + 1] = x1 * cs.z + y1 * cs.w;
-                        g2[2 * k + 1] = y1 * cs.z - x1 * cs.w;
-                    }
-                }
-#pragma unroll
-                for (int i = 0; i < 32; i += 8) {
-                    uint4 ra, rb;
-                    __nv_bfloat162* ha = reinterpret_cast<__nv_bfloat162*>(&ra);
-                    __nv_bfloat162* hb = reinterpret_cast<__nv_bfloat162*>(&rb);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        ha[j] = __floats2bfloat162_rn(g1[i + 2 * j], g1[i + 2 * j + 1]);
-                        hb[j] = __floats2bfloat162_rn(g2[i + 2 * j], g2[i + 2 * j + 1]);
-                    }
-                    *reinterpret_cast<uint4*>(orow + cc + i) = ra;
-                    *reinterpret_cast<uint4*>(orow + HALF + cc + i) = rb;
-                }
-            }
-        } else {
-#pragma unroll 1
-            for (int c = 0; c < HD / 32; ++c) {
-                float v[32];
-                tc::tmem_ld32(lane_base + col + c * 32, v);    // warp-collective: all lanes
-                if (r < nkeys) {
-#pragma unroll
-                    for (int i = 0; i < 32; i += 4) {
-                        float4 x = make_float4(v[i] * mul, v[i + 1] * mul, v[i + 2] * mul, v[i + 3] * mul);
-                        if (sg.dkv_accum) {   // later slices' contributions are already there
-                            const float4 o = *reinterpret_cast<const float4*>(drow + c * 32 + i);
-                            x.x += o.x; x.y += o.y; x.z += o.z; x.w += o.w;
-                        }
-                        *reinterpret_cast<float4*>(drow + c * 32 + i) = x;
-                    }
-                }
-            }
-        }
+        dkv_epilogue<HD>(a, sg, kvh, k0, nkeys, r, grp, lane_base, kColK, kColV);
         tc::fence_before();
     }
     __syncthreads();
