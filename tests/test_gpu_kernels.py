@@ -91,13 +91,16 @@ def test_gemm_pair_epilogues(epi):
     if epi == 1:
         A = torch.randn((K, M), device="cuda").bfloat16()
         B = torch.randn((K, N), device="cuda").bfloat16()
-        C = torch.randn((M, N), device="cuda")
-        C0 = C.clone()
-        g.check(g.lib().epp_kernel_gemm(M, N, K, A.data_ptr(), M, 0, B.data_ptr(), N, 0, C.data_ptr(), N,
+        # C is a column slice of a wider buffer (ldc > N): the TMA reduce-add
+        # epilogue must respect the row pitch and leave the other columns alone
+        Cw = torch.randn((M, N + 64), device="cuda")
+        Cw0 = Cw.clone()
+        g.check(g.lib().epp_kernel_gemm(M, N, K, A.data_ptr(), M, 0, B.data_ptr(), N, 0, Cw.data_ptr(), N + 64,
                                         None, 0, 1, g.DTYPES["bf16"], g.stream_ptr()))
         torch.cuda.synchronize()
-        ref = C0.double() + A.double().T @ B.double()
-        assert ((C.double() - ref).norm() / ref.norm()) < 1e-5
+        ref = Cw0[:, :N].double() + A.double().T @ B.double()
+        assert ((Cw[:, :N].double() - ref).norm() / ref.norm()) < 1e-5
+        assert torch.equal(Cw[:, N:], Cw0[:, N:])
         return
     A = torch.randn((M, K), device="cuda").bfloat16()
     B = torch.randn((N, K), device="cuda").bfloat16() * 0.05
