@@ -472,6 +472,14 @@ def run_ours(args):
         "e2e": e2e,
         "trace": trace_block,
     }
+    # HBM: what the planner was told against what the stage actually used
+    # (weights/grads/Adam state + the activation pool's high-water mark)
+    free_b, total_b = torch.cuda.mem_get_info()
+    _, pool_peak = stage.memory()
+    out["memory"] = {"device_total_bytes": total_b, "planner_mem_capacity": cfg["cluster"]["mem_capacity"],
+                     "planner_stage_state_bytes": cfg["model"]["stage_state_bytes"][prank],
+                     "planner_token_act_bytes": cfg["model"]["token_act_bytes"],
+                     "stage_state_bytes": stage.state_bytes(), "activation_pool_peak_bytes": pool_peak}
     if world > 1:
         # stage-to-stage activations/gradients (this rank's sends; rank 0 is a
         # first stage, so its sends are the forward activations of one hop)
