@@ -84,9 +84,15 @@ MODELS: Dict[str, ModelConfig] = {
 }
 
 
-# Planner memory capacity of one B200 stage (mem_capacity =
-# 180e9), used by both benchmark arms so they plan identical documents.
-B200_MEM_CAPACITY = 180e9
+# Planner memory capacity of one B200 stage, used by both benchmark arms so
+# they plan identical documents: the device's HBM as cudaMemGetInfo reports
+# it on this pool's B200s (191,502,876,672 bytes), rounded down to 191.0e9.
+# SURVEY §8d's 180e9 (the marketing "180 GB") left 11.5 GB of every GPU
+# unplanned, which at GPT-7B / 16K on one GPU made the checkpoint MILP re-run
+# ~51 layer forwards per step.
+# Workspaces, allocator slack and the CUDA context stay covered by the 12 GB
+# reserve in stage_state_bytes; bench.py checks the device is at least this big.
+B200_MEM_CAPACITY = 191.0e9
 
 
 def activation_bytes_per_token(m: ModelConfig, elem_bytes: int = 2) -> float:
