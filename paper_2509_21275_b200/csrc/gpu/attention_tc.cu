@@ -248,7 +248,10 @@ __global__ void __launch_bounds__(kThreadsFwd, 1) attn_fwd_tc(const AttnArgs a,
     const AttnSeg sg = a.segs[w.seg];
     const int h = EPP_HEAD_INDEX;
     const int kvh = h / (a.H / a.Hkv);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp index broadcast from lane 0: the compiler then knows it is warp-uniform
+    // and keeps the role branches and the MMA warp's loop state on the uniform
+    // datapath (no R2UR before every tcgen05.mma)
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const int q0 = w.block * 2 * TQ;
     const int rows0 = min(TQ, sg.q_len - q0);
     const int rows1 = max(0, min(TQ, sg.q_len - q0 - TQ));
@@ -589,7 +592,10 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
     const AttnSeg sg = a.segs[w.seg];
     const int h = EPP_HEAD_INDEX;
     const int kvh = h / (a.H / a.Hkv);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp index broadcast from lane 0: the compiler then knows it is warp-uniform
+    // and keeps the role branches and the MMA warp's loop state on the uniform
+    // datapath (no R2UR before every tcgen05.mma)
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const int q0 = w.block * TQ;
     const int rows = min(TQ, sg.q_len - q0);
     const int kv_end = sg.kv_ctx + q0 + rows;
@@ -1057,7 +1063,10 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
     const AttnSeg sg = a.segs[w.seg];
     const int kvh = EPP_HEAD_INDEX;
     const int group = a.H / a.Hkv;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp index broadcast from lane 0: the compiler then knows it is warp-uniform
+    // and keeps the role branches and the MMA warp's loop state on the uniform
+    // datapath (no R2UR before every tcgen05.mma)
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const int k0 = w.block * TK;
     const int kv_len = sg.kv_ctx + sg.q_len;
     const int nkeys = min(TK, kv_len - k0);
