@@ -753,6 +753,12 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dq_tc(const AttnArgs 
             const int b = grp;
             tc::mbar_wait(&s_full[b], (j >> 1) & 1);
             tc::fence_after();
+#ifdef EPP_BWD_MMA_ONLY   // pipeline experiment: no softmax work at all (wrong results)
+            tc::mbar_wait(&dp_full[b], (j >> 1) & 1);
+            tc::fence_before();
+            tc::mbar_arrive(&p_full[b]);
+            continue;
+#endif
             const int key0 = j * TB;
             const bool need_mask = (key0 + TB - 1 > first_q) || rows < TQ;
             uint32_t pk[32];
@@ -1240,6 +1246,14 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
             const bool need_mask = (k0 + TK - 1 > first_q) || rows < TB;
             tc::mbar_wait(&s_full[b], (it >> 1) & 1);
             tc::fence_after();
+#ifdef EPP_BWD_MMA_ONLY
+            tc::fence_before();
+            tc::mbar_arrive(&pt_full[b]);
+            tc::mbar_wait(&dp_full[b], (it >> 1) & 1);
+            tc::fence_before();
+            tc::mbar_arrive(&p_full[b]);
+            continue;
+#endif
             uint32_t pk[32], dk[32];
             float sall[TB / 32][32], dall[TB / 32][32];
 #pragma unroll

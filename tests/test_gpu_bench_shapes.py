@@ -3,7 +3,8 @@ checked against the fp32 oracle (oracle/numerics.py) evaluated on the GPU in
 fp32 with TF32 off.
 
 Two transformer layers at GPT-1.3B width (D 2048, 16 heads of 128, FFN 8192,
-V 50304) and at Llama-7B width (D 4096, GQA 32/8, SwiGLU 11008, V 32000),
+V 50304), at Llama-7B width (D 4096, GQA 32/8, SwiGLU 11008, V 32000) and at
+GPT-7B width (D 4096, 32 heads, FFN 16384, V 50304; bf16 only),
 on a planned batch with one 20K-token sequence split into 4 slices (the last
 one, a Hybrid chunk, at 16.8-17.1K context followed by packed documents) and
 a Batched chunk of short documents.  Chunks hold 3.9-8.2K tokens, so every
@@ -45,6 +46,10 @@ WIDTHS = {
                               vocab=50304),
     "llama-7b": M.ModelConfig("llama-7b-w", "llama", layers=2, hidden=4096, heads=32, kv_heads=8, ffn=11008,
                               vocab=32000),
+    # the headline benchmark's model (bench.py default): LayerNorm / GELU at
+    # D 4096, 32 MHA heads, FFN 16384
+    "gpt-7b": M.ModelConfig("gpt-7b-w", "gpt", layers=2, hidden=4096, heads=32, kv_heads=32, ffn=16384,
+                            vocab=50304),
 }
 LENGTHS = [20480, 2300, 1500, 900, 610, 300, 129, 77]
 SLICES = 4
@@ -149,14 +154,15 @@ def assert_bench_variants(arch, dtype):
         return
     pair = [k for k in ks if "gemm_tc2_kernel<" in k and ks[k] > 0]
     epis = {k.split("gemm_tc2_kernel<")[1].split(">")[0].split(",")[-1].strip() for k in pair}
-    want = {"6", "2", "1"} | ({"4", "5"} if arch == "gpt-1.3b" else set())
+    want = {"6", "2", "1"} | ({"4", "5"} if WIDTHS[arch].arch == "gpt" else set())
     assert want <= epis, (sorted(epis), pair)
     assert "norm_fwd_row_k" in names and "norm_bwd_dx_row_k" in names, names
     for k in ("attn_fwd_tc", "attn_bwd_dq_tc", "attn_bwd_dkv_tc"):
         assert k in names, (k, names)
 
 
-@pytest.mark.parametrize("arch,dp,tight", [("gpt-1.3b", 1, False), ("gpt-1.3b", 2, True), ("llama-7b", 2, False)])
+@pytest.mark.parametrize("arch,dp,tight", [("gpt-1.3b", 1, False), ("gpt-1.3b", 2, True), ("llama-7b", 2, False),
+                                           ("gpt-7b", 1, False)])
 def test_bf16_at_bench_width(planner, arch, dp, tight):
     m = WIDTHS[arch]
     plan = make_plan(planner, m, dp, tight)
