@@ -17,9 +17,9 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 OUT = ROOT / "gpurun_out"
 PROF = ROOT / "profiles"
-CLASS = {"gemm_tc2_kernel": "gemm", "attn_fwd_tc": "attn_fwd", "attn_bwd_dq_tc": "attn_bwd_dq",
-         "attn_bwd_dkv_tc": "attn_bwd_dkv", "norm_bwd_dx_row_k": "norm_bwd", "norm_fwd_row_k": "norm_fwd",
-         "rope_gather_grad_k": "rope"}
+CLASS = {"gemm_tc2_kernel": "gemm", "gemm_tc2_wgrad": "gemm_wgrad_accum", "attn_fwd_tc": "attn_fwd",
+         "attn_bwd_dq_tc": "attn_bwd_dq", "attn_bwd_dkv_tc": "attn_bwd_dkv", "norm_bwd_dx_row_k": "norm_bwd",
+         "norm_fwd_row_k": "norm_fwd", "ce_k": "cross_entropy", "adamw_multi_k": "adamw"}
 KEYS = {"duration": "gpu__time_duration.sum",
         "dram_read_bytes": "dram__bytes_read.sum", "dram_write_bytes": "dram__bytes_write.sum",
         "tensor_pipe_active_pct": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
@@ -39,10 +39,11 @@ def raw(rep):
 
 def main():
     tag = sys.argv[1]
-    summ = {"round": 1, "tag": tag,
+    summ = {"round": 2, "tag": tag,
             "note": "ncu --set full --clock-control none, one launch per kernel class from `python bench.py "
-                    "--steps 1 --warmup 1 --seqs-per-gpu 32` (GPT-1.3B, d_p=1); launch list: "
-                    "--metrics gpu__time_duration.sum, same command (cold-cache, serialised: compare shares)",
+                    "--steps 1 --warmup 1 --seqs-per-gpu 16 --prof-steps 1` (GPT-7B, github_like <= 16K, "
+                    "d_p=1; tools/ncu_capture.sh); launch list: --metrics gpu__time_duration.sum, same command "
+                    "(cold-cache, serialised: compare shares)",
             "kernels": {}, "dram_bytes_per_launch": {}}
     for k, cls in CLASS.items():
         rep = OUT / f"prof_{tag}_{k}.ncu-rep"
