@@ -90,10 +90,16 @@ __device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
 #ifndef EPP_FWD_EMU
 #define EPP_FWD_EMU 3
 #endif
-#ifndef EPP_BWD_EMU
-#define EPP_BWD_EMU 0
+// Backward: the dQ kernel gains from 2/8 (+2-4 %, its softmax loads the XU
+// pipe with the exponentials and the dS packing), the dK/dV kernel (bound by
+// the shared-memory port of its SS score MMAs) loses 2 % with any.
+#ifndef EPP_DQ_EMU
+#define EPP_DQ_EMU 2
 #endif
-constexpr int kEmuFwd = EPP_FWD_EMU, kEmuBwd = EPP_BWD_EMU;
+#ifndef EPP_DKV_EMU
+#define EPP_DKV_EMU 0
+#endif
+constexpr int kEmuFwd = EPP_FWD_EMU, kEmuDq = EPP_DQ_EMU, kEmuDkv = EPP_DKV_EMU;
 template <int E>
 __device__ __forceinline__ constexpr bool emu_pair(int q) {   // q: pair index within a 32-column chunk
     return (q & 7) >= 8 - E;
@@ -522,7 +528,7 @@ __device__ __forceinline__ void dq_p_tile(float (&s)[TB / 32][32], float c2, flo
         for (int i = 0; i < 32; i += 2) {
             const uint64_t x = ffma2(f2pack(s[c][i], s[c][i + 1]), c2x, nl);
             float p0, p1;
-            if (emu_pair<kEmuBwd>(i >> 1)) {
+            if (emu_pair<kEmuDq>(i >> 1)) {
                 ex2_fma2(x, p0, p1);
             } else {
                 float x0, x1;
@@ -866,7 +872,7 @@ __device__ __forceinline__ void dkv_p_tile(float (&s)[TB / 32][32], float c2, in
         for (int i = 0; i < 32; i += 2) {
             const uint64_t x = fmul2(f2pack(s[c][i], s[c][i + 1]), c2x);
             float p0, p1;
-            if (emu_pair<kEmuBwd>(i >> 1)) {
+            if (emu_pair<kEmuDkv>(i >> 1)) {
                 ex2_fma2(x, p0, p1);
             } else {
                 float x0, x1;

@@ -944,9 +944,12 @@ void gemm(const GemmArgs& g, cudaStream_t s) {
     // use 128-wide tiles to expose more CTAs.
     const long long tiles256 = static_cast<long long>(ceil_div(g.N, 256)) * ceil_div(g.M, kBM);
     const long long pair_tiles = static_cast<long long>(ceil_div(g.N, 256)) * ceil_div(g.M, 2 * kBM);
-    if (g.K > 0 && g.N % 256 == 0 && pair_tiles >= 60)
+    // A ragged last column tile (N % 256 != 0, e.g. the LM head's V = 50304)
+    // is fine: TMA zero-fills the B rows past N (the box still completes its
+    // full byte count) and the epilogue stores only columns < N.
+    if (g.K > 0 && pair_tiles >= 60)
         dispatch_epi2<256, 6>(g, s);      // CTA pairs: 256 x 256 tiles
-    else if (g.N % 256 == 0 && tiles256 >= 120)
+    else if (tiles256 >= 120)
         dispatch_epi<256, 4>(g, s);
     else
         dispatch_epi<128, 6>(g, s);

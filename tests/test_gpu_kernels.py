@@ -77,6 +77,30 @@ def test_gemm_epilogues(dtype):
     assert ((C2.float() - ref2).norm() / ref2.norm()) < (8e-3 if dtype == "bf16" else 1e-5)
 
 
+
+@pytest.mark.parametrize("ak,bk", [(1, 1), (0, 0)])
+def test_gemm_pair_ragged_n(ak, bk):
+    """The CTA-pair kernel with N % 256 != 0 (the LM head: N = V = 50304;
+    the last column tile is half empty): K-major operands (head forward) and
+    MN-major ones (weight-gradient layout), bf16 store against fp64."""
+    g = G()
+    torch.manual_seed(3)
+    M, N, K = 1528, 50304, 512   # ragged M as well (1528 = 5 x 256 + 248)
+    A = torch.randn((M, K) if ak else (K, M), device="cuda").bfloat16()
+    B = (torch.randn((N, K) if bk else (K, N), device="cuda") * 0.05).bfloat16()
+    C = torch.full((M, N + 32), 7.0, device="cuda").bfloat16()
+    before = g.kernel_stats()
+    g.check(g.lib().epp_kernel_gemm(M, N, K, A.data_ptr(), A.shape[1], ak, B.data_ptr(), B.shape[1], bk,
+                                    C.data_ptr(), N + 32, None, 0, 0, g.DTYPES["bf16"], g.stream_ptr()))
+    torch.cuda.synchronize()
+    Ad = A.double() if ak else A.double().T
+    Bd = B.double().T if bk else B.double()
+    ref = Ad @ Bd
+    assert ((C[:, :N].double() - ref).norm() / ref.norm()) < 8e-3
+    assert torch.all(C[:, N:] == 7.0)
+    after = g.kernel_stats()
+    assert any("gemm_tc2_kernel<" in k and after[k] > before.get(k, 0) for k in after), "pair kernel not used"
+
 @pytest.mark.parametrize("epi", [0, 1, 2, 3, 4, 5])
 def test_gemm_pair_epilogues(epi):
     """Every epilogue on the CTA-pair kernel (>= 60 pair tiles, N % 256 == 0)
