@@ -48,6 +48,7 @@ import torch  # noqa: E402
 METRIC = "training tokens/s + MFU, skewed-length GPT EPP at 1/2/4/8 B200"
 DATA = "synthetic (seeded github_like lengths, uniform tokens, random-init weights)"
 REF_SO = ROOT / "oracle" / "_ref" / "libepp_ref.so"
+E2E_SEED0 = 7000   # the e2e leg's batches: fresh seeds (never trained on)
 
 
 def parse():
@@ -256,10 +257,23 @@ def run_ours(args):
     stage.init_weights(1234)
     timed_stage = calibrate.TimedStage(stage)
 
+    # P2P mailboxes (N > 1) hold two of the largest messages any plan of
+    # this run sends: the pre-planned batches, the e2e leg's batches (planned
+    # again inside its timed region) and 1.5x headroom for --replan's refit.
+    if dp > 1:
+        e2e_lengths = [] if args.no_e2e else [b[0] for b in make_batches(args, args.steps, dp, m.vocab, replica,
+                                                                         seed0=E2E_SEED0)]
+        biggest = max(lay.tokens for pl in plans for lay in pl.chunks.values())
+        for lengths in e2e_lengths:
+            pl = schedule.parse_plan(planner.make_plan_document(cfg, lengths, args.slices or None, "main", jobs),
+                                     lengths)
+            biggest = max(biggest, max(lay.tokens for lay in pl.chunks.values()))
+        max_tokens = max(int(1.5 * biggest), args.cap)
+
     def make_driver(st):
         if dp > 1:
             return DistributedPipeline(st, prank, dp, dev, m.hidden, gpu.TORCH_DTYPES[args.dtype],
-                                       pipe=pipes[replica])
+                                       pipe=pipes[replica], max_tokens=max_tokens)
         return LocalPipeline([st], dev)
 
     driver = make_driver(stage)
@@ -388,9 +402,8 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         # fresh batches (never trained on): the per-step losses are honest
-        e2e_seed0 = 7000
-        e2e_batches = make_batches(args, args.steps, dp, m.vocab, replica, seed0=e2e_seed0)
-        e2e_targets = global_targets(args, args.steps, dp, replicas, seed0=e2e_seed0)
+        e2e_batches = make_batches(args, args.steps, dp, m.vocab, replica, seed0=E2E_SEED0)
+        e2e_targets = global_targets(args, args.steps, dp, replicas, seed0=E2E_SEED0)
 
         def e2e_run(k, plan, tokens):
             out = driver.run_step(plan, tokens, total_targets=e2e_targets[k] if replicas > 1 else None)

@@ -39,19 +39,21 @@ class TimedStage:
     def __getattr__(self, name):
         return getattr(self.stage, name)
 
-    def _timed(self, phase, fn, op, x):
+    def _timed(self, phase, fn, op, x, **kw):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        out = fn(op, x)
+        out = fn(op, x, **kw)
         b.record()
         self.records.append((op, phase, a, b))
         return out
 
-    def forward(self, op, act_in):
-        return self._timed("forward", self.stage.forward, op, act_in)
+    # keyword arguments (e.g. out_ptr, the P2P mailbox the stage writes into)
+    # pass through to the wrapped stage
+    def forward(self, op, act_in, **kw):
+        return self._timed("forward", self.stage.forward, op, act_in, **kw)
 
-    def backward(self, op, grad_in):
-        return self._timed("backward", self.stage.backward, op, grad_in)
+    def backward(self, op, grad_in, **kw):
+        return self._timed("backward", self.stage.backward, op, grad_in, **kw)
 
     def samples(self) -> List[Dict]:
         """Fit samples.  A backward that first re-ran `ckpt` of the stage's
