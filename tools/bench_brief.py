@@ -9,7 +9,7 @@ for f in sys.argv[1:]:
     except Exception as e:  # noqa: BLE001
         print(f, "unreadable:", e)
         continue
-    print(f"{f}: {d['value']:.0f} tok/s  e2e {d.get('e2e', {}).get('value', 0):.0f}  mfu {d.get('mfu', 0):.3f}  "
+    print(f"{f}: {d['value']:.0f} tok/s  e2e {(d.get('e2e') or {}).get('value', 0):.0f}  mfu {d.get('mfu', 0):.3f}  "
           f"{d['ms_per_step']:.0f} ms/step  clock {d.get('clocks', {}).get('sm_mhz')}  "
           f"ckpt {d['config'].get('ckpt_layers_per_step')}  loss {d.get('loss', 0):.4f}")
     for k, v in d.get("kernel_classes", {}).items():
