@@ -196,7 +196,8 @@ PROF_CLASSES = ((0, "gemm"), (1, "attn_fwd"), (2, "attn_bwd"), (3, "attn_bwd_dq"
                 (5, "norm_fwd"), (6, "norm_bwd"), (7, "rope"), (8, "act"), (9, "cross_entropy"),
                 (10, "adamw"), (11, "embed"), (12, "copy_fill"),
                 (13, "gemm_store"), (14, "gemm_wgrad_accum"), (15, "gemm_addres"), (16, "gemm_store_f32"),
-                (17, "gemm_up_gelu"), (18, "gemm_dgrad_gelu"), (19, "gemm_qkv_rope"))
+                (17, "gemm_up_gelu"), (18, "gemm_dgrad_gelu"), (19, "gemm_qkv_rope"), (20, "gemm_up_swiglu"),
+                (21, "gemm_dgrad_swiglu"))
 
 
 def read_profile(lib):

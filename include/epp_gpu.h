@@ -220,7 +220,11 @@ int epp_kernel_gemm(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda,
                     void* stream);
 /* Same with the fused MLP epilogues: epi 4 = StoreGelu (C = acc, C2 =
  * gelu_tanh(acc)), 5 = GeluBwd (C = acc * gelu_tanh'(R), and C2 =
- * gelu_tanh(R) when C2 is given); outputs in the stage dtype. */
+ * gelu_tanh(R) when C2 is given), 7 = SwiGlu (N = 2F, B = [gate; up]
+ * K-major: C = [g | u], C2 = silu(g) u), 8 = SwiGluBwd (acc = dA [M, F],
+ * R = h = [g | u] with ldr >= 2F: C = dh = [dA u silu'(g) | dA silu(g)]
+ * with ldc >= 2F, C2 = silu(g) u); outputs in the stage dtype.  7 / 8 run
+ * on the CTA-pair kernel only (bf16, >= 60 pair tiles, F % 128 == 0 for 7). */
 int epp_kernel_gemm_ex(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_kmajor,
                        const void* B, int64_t ldb, int32_t b_kmajor, void* C, int64_t ldc,
                        const void* R, int64_t ldr, void* C2, int64_t ldc2, int32_t epi, int32_t dtype,

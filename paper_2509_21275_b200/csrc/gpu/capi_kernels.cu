@@ -131,10 +131,11 @@ int epp_kernel_gemm_ex(int32_t M, int32_t N, int32_t K, const void* A, int64_t l
         g.B = B; g.ldb = ldb; g.b_kmajor = b_kmajor != 0;
         g.C = C; g.ldc = ldc; g.R = R; g.ldr = ldr;
         g.C2 = C2; g.ldc2 = ldc2;
-        EPP_REQUIRE(epi >= 0 && epi <= 5, "bad epilogue");
+        EPP_REQUIRE((epi >= 0 && epi <= 5) || epi == 7 || epi == 8, "bad epilogue");
         g.epi = static_cast<eppk::Epi>(epi);
         EPP_REQUIRE(g.epi != eppk::Epi::StoreGelu || C2 != nullptr, "StoreGelu needs C2");
         EPP_REQUIRE(g.epi != eppk::Epi::GeluBwd || R != nullptr, "GeluBwd needs R (the pre-activation)");
+        EPP_REQUIRE(epi < 7 || eppk::gemm_swiglu_fusable(g), "SwiGlu epilogue: shape not taken by the pair kernel");
         g.dtype = static_cast<eppk::DType>(dtype);
         eppk::gemm(g, static_cast<cudaStream_t>(stream));
     });

@@ -144,10 +144,115 @@ __device__ __forceinline__ void epilogue_rope(const TcParams& p, uint32_t taddr,
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_plain(const TcParams& p, uint32_t taddr, int row, int n0, bool have_acc);
 
+__device__ __forceinline__ float silu_sig(float g, float& sg) {
+    sg = __fdividef(1.f, 1.f + __expf(-g));
+    return g * sg;
+}
+__device__ __forceinline__ void store32_bf16(bf16* dst, const float (&v)[32]) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+        uint4 raw;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(v[i + 2 * j], v[i + 2 * j + 1]);
+        *reinterpret_cast<uint4*>(dst + i) = raw;
+    }
+}
+
+// Epi::SwiGlu: the tile's accumulator columns [0, BN/2) are gate features
+// j0.., [BN/2, BN) the up features j0.. (the producer loaded w13 rows j0..
+// and F+j0.. for the two CTAs' B halves).  h keeps the [gate | up] layout.
+template <int BN>
+__device__ __forceinline__ void epilogue_swiglu(const TcParams& p, uint32_t taddr, int row, int j0) {
+    const int F = p.N / 2;
+#pragma unroll 1
+    for (int c = 0; c < BN / 2; c += 32) {
+        float g[32], u[32];
+        tc::tmem_ld32(taddr + c, g);
+        tc::tmem_ld32(taddr + BN / 2 + c, u);
+        const int col = j0 + c;
+        if (row >= p.M || col >= F) continue;
+        bf16* h = static_cast<bf16*>(p.C) + static_cast<long long>(row) * p.ldc + col;
+        store32_bf16(h, g);
+        store32_bf16(h + F, u);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            float sg;
+            g[i] = silu_sig(g[i], sg) * u[i];
+        }
+        store32_bf16(p.C2 + static_cast<long long>(row) * p.ldc2 + col, g);
+    }
+}
+
+// Epi::SwiGluBwd: acc = dA [., F]; R = h = [g | u].
+template <int BN>
+__device__ __forceinline__ void epilogue_swiglu_bwd(const TcParams& p, uint32_t taddr, int row, int n0) {
+    const int F = p.N;
+    // h of chunk c+1 is loaded before chunk c is processed (the row-strided
+    // loads are latency-bound; one chunk of lookahead doubles the bytes in
+    // flight per thread)
+    const bf16* hrow = p.R + static_cast<long long>(min(row, p.M - 1)) * p.ldr + n0;
+    uint4 ng[4], nu[4];
+    auto load_h = [&](int c) {
+        if (row < p.M && n0 + c < F) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                ng[i] = *reinterpret_cast<const uint4*>(hrow + c + 8 * i);
+                nu[i] = *reinterpret_cast<const uint4*>(hrow + F + c + 8 * i);
+            }
+        }
+    };
+    load_h(0);
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+        uint4 cg[4], cu[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            cg[i] = ng[i];
+            cu[i] = nu[i];
+        }
+        if (c + 32 < BN) load_h(c + 32);
+        float d[32];
+        tc::tmem_ld32(taddr + c, d);
+        const int col = n0 + c;
+        if (row >= p.M || col >= F) continue;
+        float dg[32], du[32], a[32];
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+            const uint4 rg = cg[i / 8];
+            const uint4 ru = cu[i / 8];
+            const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&rg);
+            const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&ru);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 gf = __bfloat1622float2(g2[j]), uf = __bfloat1622float2(u2[j]);
+                const float gv[2] = {gf.x, gf.y}, uv[2] = {uf.x, uf.y};
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int e = i + 2 * j + k;
+                    float sg;
+                    const float si = silu_sig(gv[k], sg);
+                    a[e] = si * uv[k];
+                    du[e] = d[e] * si;
+                    dg[e] = d[e] * uv[k] * sg * (1.f + gv[k] * (1.f - sg));
+                }
+            }
+        }
+        bf16* dh = static_cast<bf16*>(p.C) + static_cast<long long>(row) * p.ldc + col;
+        store32_bf16(dh, dg);
+        store32_bf16(dh + F, du);
+        store32_bf16(p.C2 + static_cast<long long>(row) * p.ldc2 + col, a);
+    }
+}
+
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t taddr, int row, int n0, bool have_acc) {
     if constexpr (EPI == static_cast<int>(Epi::RopeScatter)) {
         epilogue_rope<BN>(p, taddr, row, n0);
+    } else if constexpr (EPI == static_cast<int>(Epi::SwiGlu)) {
+        epilogue_swiglu<BN>(p, taddr, row, n0);
+    } else if constexpr (EPI == static_cast<int>(Epi::SwiGluBwd)) {
+        epilogue_swiglu_bwd<BN>(p, taddr, row, n0);
     } else {
         epilogue_plain<BN, EPI>(p, taddr, row, n0, have_acc);
     }
@@ -155,8 +260,24 @@ __device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t taddr,
 
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_plain(const TcParams& p, uint32_t taddr, int row, int n0, bool have_acc) {
+    // AddRes / GeluBwd read R: chunk c+1's R is loaded before chunk c is
+    // processed (one chunk of lookahead for the row-strided loads)
+    constexpr bool kR = EPI == static_cast<int>(Epi::AddRes) || EPI == static_cast<int>(Epi::GeluBwd);
+    const bf16* rrow = kR ? p.R + static_cast<long long>(min(row, p.M - 1)) * p.ldr + n0 : nullptr;
+    uint4 nr[4];
+    auto load_r = [&](int c) {
+        if (kR && row < p.M && n0 + c < p.N) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) nr[i] = *reinterpret_cast<const uint4*>(rrow + c + 8 * i);
+        }
+    };
+    load_r(0);
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
+        uint4 cr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cr[i] = nr[i];
+        if (c + 32 < BN) load_r(c + 32);
         float v[32];
         if (have_acc) {
             tc::tmem_ld32(taddr + c, v);
@@ -178,15 +299,14 @@ __device__ __forceinline__ void epilogue_plain(const TcParams& p, uint32_t taddr
                 *reinterpret_cast<float4*>(dst + i) = o;
             }
         } else {
-            if (EPI == static_cast<int>(Epi::AddRes) || EPI == static_cast<int>(Epi::GeluBwd)) {
-                const bf16* r = p.R + static_cast<long long>(row) * p.ldr + col;
+            if (kR) {
                 // GeluBwd with C2: also emit gelu(R) (the MLP activation that
                 // dW2 needs), re-created here from the h already being read
                 bf16* dst2 = (EPI == static_cast<int>(Epi::GeluBwd) && p.C2)
                                  ? p.C2 + static_cast<long long>(row) * p.ldc2 + col : nullptr;
 #pragma unroll
                 for (int i = 0; i < 32; i += 8) {
-                    const uint4 raw = *reinterpret_cast<const uint4*>(r + i);
+                    const uint4 raw = cr[i / 8];
                     const bf16* rb = reinterpret_cast<const bf16*>(&raw);
                     float a[8];
 #pragma unroll
@@ -510,7 +630,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     const int nk = (p.K + kBK - 1) / kBK;
-    const TileSched sched{(p.M + 2 * kBM - 1) / (2 * kBM), (p.N + BN - 1) / BN};
+    // SwiGlu: a tile covers BN/2 gate and the same BN/2 up features
+    constexpr bool kSwi = EPI == static_cast<int>(Epi::SwiGlu);
+    static_assert(!kSwi || !B_MN, "SwiGlu: K-major w13");
+    constexpr int kTileN = kSwi ? BN / 2 : BN;
+    const int n_logical = kSwi ? p.N / 2 : p.N;
+    const TileSched sched{(p.M + 2 * kBM - 1) / (2 * kBM), (n_logical + kTileN - 1) / kTileN};
     const int ntiles = sched.tiles_m * sched.tiles_n;
     const int cluster_id = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
 
@@ -548,7 +673,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int t = cluster_id; t < ntiles; t += nclusters) {
                 int mb, nb;
                 sched.coords(t, mb, nb);
-                const int m0 = mb * 2 * kBM + rank * kBM, n0 = nb * BN + rank * (BN / 2);
+                const int m0 = mb * 2 * kBM + rank * kBM;
+                const int n0 = kSwi ? nb * kTileN + rank * (p.N / 2) : nb * BN + rank * (BN / 2);
                 for (int kb = 0; kb < nk; ++kb) {
                     tc::mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) tc::mbar_expect_tx(&full[stage], 2 * L::kStageBytes);
@@ -615,7 +741,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int mb, nb;
             sched.coords(t, mb, nb);
             const int row = mb * 2 * kBM + rank * kBM + quarter * 32 + lane;
-            const int n0 = nb * BN;
+            const int n0 = nb * kTileN;
             const int acc = local & 1;
             tc::mbar_wait(&acc_full[acc], (local >> 1) & 1);
             tc::fence_after();
@@ -776,6 +902,10 @@ void dispatch_epi(const GemmArgs& g, cudaStream_t s) {
             EPP_REQUIRE(g.a_kmajor && g.b_kmajor && g.rope, "RopeScatter: K-major operands and rope args");
             launch_tc<BN, STAGES, false, false, 6>(g, s);
             break;
+        case Epi::SwiGlu:
+        case Epi::SwiGluBwd:
+            EPP_REQUIRE(false, "SwiGlu epilogues run on the CTA-pair kernel only (gemm_swiglu_fusable)");
+            break;
     }
 }
 
@@ -832,6 +962,12 @@ void dispatch_epi2(const GemmArgs& g, cudaStream_t s) {
         case Epi::RopeScatter:
             EPP_REQUIRE(g.a_kmajor && g.b_kmajor && g.rope, "RopeScatter: K-major operands and rope args");
             launch_tc2<BN, STAGES, false, false, 6>(g, s);
+            break;
+        case Epi::SwiGlu:
+            launch_tc2<BN, STAGES, false, false, 7>(g, s);
+            break;
+        case Epi::SwiGluBwd:
+            dispatch_major2<BN, STAGES, 8>(g, s);
             break;
     }
 }
@@ -917,6 +1053,16 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
 
 }  // namespace
 
+bool gemm_swiglu_fusable(const GemmArgs& g) {
+    if (g.dtype != DType::BF16 || g.K <= 0 || g.M <= 0 || !g.C2) return false;
+    const long long mt = ceil_div(g.M, 2 * kBM);
+    if (g.epi == Epi::SwiGlu)   // gate / up tiles must not straddle the F boundary
+        return g.a_kmajor && g.b_kmajor && g.N % 256 == 0 && mt * (g.N / 256) >= 60;
+    if (g.epi == Epi::SwiGluBwd)
+        return g.a_kmajor && g.R && g.N % 32 == 0 && g.ldc >= 2LL * g.N && mt * ceil_div(g.N, 256) >= 60;
+    return false;
+}
+
 void gemm(const GemmArgs& g, cudaStream_t s) {
     EPP_REQUIRE(g.M >= 0 && g.N >= 0 && g.K >= 0, "gemm: negative extent");
     if (g.M == 0 || g.N == 0) return;
@@ -942,6 +1088,11 @@ void gemm(const GemmArgs& g, cudaStream_t s) {
     }
     // Wide tiles keep the tensor pipe fed (128x256 per MMA); narrow problems
     // use 128-wide tiles to expose more CTAs.
+    if (g.epi == Epi::SwiGlu || g.epi == Epi::SwiGluBwd) {
+        EPP_REQUIRE(gemm_swiglu_fusable(g), "gemm: SwiGlu epilogue on a problem the pair kernel does not take");
+        dispatch_epi2<256, 6>(g, s);
+        return;
+    }
     const long long tiles256 = static_cast<long long>(ceil_div(g.N, 256)) * ceil_div(g.M, kBM);
     const long long pair_tiles = static_cast<long long>(ceil_div(g.N, 256)) * ceil_div(g.M, 2 * kBM);
     // A ragged last column tile (N % 256 != 0, e.g. the LM head's V = 50304)

@@ -26,6 +26,11 @@ enum class Epi : int {
     StoreGelu = 4,  // C = acc, C2 = gelu_tanh(acc)          (MLP up-projection)
     GeluBwd = 5,    // C = acc * gelu_tanh'(R) [, C2 = gelu_tanh(R)]  (MLP dgrad -> dh [+ act for dW2])
     RopeScatter = 6,  // QKV projection: RoPE on q/k, q -> [T,H,hd], k/v -> the segments' KV rows
+    // SwiGLU (Llama MLP), CTA-pair kernel only (gemm_swiglu_fusable):
+    SwiGlu = 7,       // up-projection, N = 2F (B = w13 = [gate; up], K-major): each tile pairs gate
+                      // rows j..j+127 with up rows F+j..: C = h = [g | u] (ldc 2F), C2 = silu(g)*u
+    SwiGluBwd = 8,    // dA = dY W2 (N = F): C = dh = [dA*u*silu'(g) | dA*silu(g)] (ldc 2F),
+                      // R = h (ldr 2F), C2 = silu(g)*u (W2's weight-gradient operand)
 };
 
 struct AttnSeg;
@@ -54,6 +59,9 @@ struct GemmArgs {
 };
 
 void gemm(const GemmArgs& a, cudaStream_t s);
+// True when gemm() runs `a` on the CTA-pair kernel and the SwiGlu /
+// SwiGluBwd epilogues apply (the caller otherwise runs the separate pass).
+bool gemm_swiglu_fusable(const GemmArgs& a);
 // Number of GEMM kernel launches issued so far on this process (bench counter).
 long long gemm_launch_count();
 

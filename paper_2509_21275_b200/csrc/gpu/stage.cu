@@ -966,11 +966,19 @@ private:
             up.epi = Epi::StoreGelu;
             up.C2 = act.get();
             up.ldc2 = F_;
+        } else if (llama_ && !skip_out) {   // SwiGLU fused (CTA-pair tiles pair gate and up rows)
+            up.epi = Epi::SwiGlu;
+            up.C2 = act.get();
+            up.ldc2 = F_;
+            if (!gemm_swiglu_fusable(up)) {
+                up.epi = Epi::Store;
+                up.C2 = nullptr;
+            }
         }
         gemm(up, s);
         xn.release();
         if (!skip_out) {
-            if (llama_) act_fwd(dt_, 1, L.h.get(), act.get(), T, F_, s);
+            if (llama_ && up.epi != Epi::SwiGlu) act_fwd(dt_, 1, L.h.get(), act.get(), T, F_, s);
             GemmArgs g2 = mk(T, D_, F_, act.get(), F_, true, work(P.w2), F_, true, out, D_);
             g2.epi = Epi::AddRes;
             g2.R = L.x_mid.get();
@@ -991,7 +999,17 @@ private:
         // reads h for gelu' anyway), Llama in a pass over h.
         Buf act(&pool_, static_cast<size_t>(T) * F_ * e, s);
         Buf dh(&pool_, static_cast<size_t>(T) * F1_ * e, s);
-        if (llama_) {
+        GemmArgs swb = mk(T, F_, D_, dy, D_, true, work(P.w2), F_, false, dh.get(), F1_);   // dA = dY W2
+        swb.epi = Epi::SwiGluBwd;   // -> dh = [dA u silu'(g) | dA silu(g)], A = silu(g) u
+        swb.R = L.h.get();
+        swb.ldr = F1_;
+        swb.C2 = act.get();
+        swb.ldc2 = F_;
+        if (llama_ && gemm_swiglu_fusable(swb)) {
+            gemm(swb, s);
+            wgrad(D_, F_, T, dy, D_, act.get(), F_, grad(P.w2), s);                    // dW2 += dY^T A
+            act.release();
+        } else if (llama_) {
             act_fwd(dt_, 1, L.h.get(), act.get(), T, F_, s);
             wgrad(D_, F_, T, dy, D_, act.get(), F_, grad(P.w2), s);                    // dW2 += dY^T A
             act.release();

@@ -145,7 +145,7 @@ def rel(a, b):
 def assert_bench_variants(arch, dtype):
     """The benchmark's kernel variants really ran (demangled template args:
     gemm_tc2_kernel<BN, STAGES, A_MN, B_MN, EPI>, EPI 6 RopeScatter,
-    4 StoreGelu, 5 GeluBwd, 2 AddRes, 1 AccumF32)."""
+    4 StoreGelu, 5 GeluBwd, 7 SwiGlu, 8 SwiGluBwd, 2 AddRes, 1 AccumF32)."""
     from paper_2509_21275_b200.gpu import kernel_stats
     ks = kernel_stats()
     names = " ".join(k for k, v in ks.items() if v > 0)
@@ -154,7 +154,7 @@ def assert_bench_variants(arch, dtype):
         return
     pair = [k for k in ks if "gemm_tc2_kernel<" in k and ks[k] > 0]
     epis = {k.split("gemm_tc2_kernel<")[1].split(">")[0].split(",")[-1].strip() for k in pair}
-    want = {"6", "2", "1"} | ({"4", "5"} if WIDTHS[arch].arch == "gpt" else set())
+    want = {"6", "2", "1"} | ({"4", "5"} if WIDTHS[arch].arch == "gpt" else {"7", "8"})
     assert want <= epis, (sorted(epis), pair)
     assert "norm_fwd_row_k" in names and "norm_bwd_dx_row_k" in names, names
     for k in ("attn_fwd_tc", "attn_bwd_dq_tc", "attn_bwd_dkv_tc"):

@@ -78,6 +78,44 @@ def test_gemm_epilogues(dtype):
 
 
 
+
+def test_gemm_swiglu_epilogues():
+    """The fused SwiGLU epilogues at Llama-7B's FFN width (F = 11008) against
+    fp64: the up-projection (tiles pair w13's gate rows j.. with its up rows
+    F+j..; C = h = [g | u], C2 = silu(g) u) and the W2 data gradient (acc =
+    dA; dh = [dA u silu'(g) | dA silu(g)], C2 = silu(g) u from the bf16 h)."""
+    g = G()
+    torch.manual_seed(4)
+    M, F, D = 2000, 11008, 512
+    x = torch.randn((M, D), device="cuda").bfloat16()
+    w13 = (torch.randn((2 * F, D), device="cuda") * 0.05).bfloat16()
+    h = torch.empty((M, 2 * F), device="cuda", dtype=torch.bfloat16)
+    act = torch.empty((M, F), device="cuda", dtype=torch.bfloat16)
+    g.check(g.lib().epp_kernel_gemm_ex(M, 2 * F, D, x.data_ptr(), D, 1, w13.data_ptr(), D, 1, h.data_ptr(), 2 * F,
+                                       None, 0, act.data_ptr(), F, 7, g.DTYPES["bf16"], g.stream_ptr()))
+    torch.cuda.synchronize()
+    hd = x.double() @ w13.double().T
+    assert ((h.double() - hd).norm() / hd.norm()) < 8e-3
+    ga, ua = hd[:, :F], hd[:, F:]
+    ref_act = torch.nn.functional.silu(ga) * ua
+    assert ((act.double() - ref_act).norm() / ref_act.norm()) < 1e-2
+    # backward: dA = dY W2 with W2 = [D, F] (MN-major B), R = the bf16 h
+    dy = torch.randn((M, D), device="cuda").bfloat16()
+    w2 = (torch.randn((D, F), device="cuda") * 0.05).bfloat16()
+    dh = torch.full((M, 2 * F), 3.0, device="cuda").bfloat16()
+    act2 = torch.empty((M, F), device="cuda", dtype=torch.bfloat16)
+    g.check(g.lib().epp_kernel_gemm_ex(M, F, D, dy.data_ptr(), D, 1, w2.data_ptr(), F, 0, dh.data_ptr(), 2 * F,
+                                       h.data_ptr(), 2 * F, act2.data_ptr(), F, 8, g.DTYPES["bf16"],
+                                       g.stream_ptr()))
+    torch.cuda.synchronize()
+    da = dy.double() @ w2.double()
+    gh, uh = h.double()[:, :F], h.double()[:, F:]
+    sg = torch.sigmoid(gh)
+    ref_dg = da * uh * sg * (1 + gh * (1 - sg))
+    ref_du = da * gh * sg
+    for got, ref in ((dh.double()[:, :F], ref_dg), (dh.double()[:, F:], ref_du), (act2.double(), gh * sg * uh)):
+        assert ((got - ref).norm() / ref.norm()) < 1e-2
+
 @pytest.mark.parametrize("ak,bk", [(1, 1), (0, 0)])
 def test_gemm_pair_ragged_n(ak, bk):
     """The CTA-pair kernel with N % 256 != 0 (the LM head: N = V = 50304;

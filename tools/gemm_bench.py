@@ -53,6 +53,31 @@ def main():
         a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
         gpu.check(lib.epp_gpu_profile_read(0, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), 1))
         out[name] = {"ms": round(a.value / c.value, 4), "tflops": round(b.value / a.value / 1e9, 1)}
+    # fused-epilogue data gradients: GELU' (R = h, C2 = gelu(h)) and SwiGLU'
+    # (R = h = [g | u], C = dh [T, 2F], C2 = silu(g) u)
+    for name, epi in (("dgrad_gelu", 5), ("dgrad_swiglu", 8)):
+        M, N, K = T, F, D
+        dy = torch.randn((M, K), device="cuda").to(bf)
+        W = torch.randn((K, N), device="cuda").to(bf)
+        h = torch.randn((M, 2 * N if epi == 8 else N), device="cuda").to(bf)
+        C = torch.empty((M, 2 * N if epi == 8 else N), device="cuda", dtype=bf)
+        C2 = torch.empty((M, N), device="cuda", dtype=bf)
+
+        def once2():
+            gpu.check(lib.epp_kernel_gemm_ex(M, N, K, dy.data_ptr(), K, 1, W.data_ptr(), N, 0, C.data_ptr(),
+                                             C.shape[1], h.data_ptr(), h.shape[1], C2.data_ptr(), N, epi, 1,
+                                             gpu.stream_ptr()))
+
+        once2()
+        torch.cuda.synchronize()
+        lib.epp_gpu_profile(1)
+        for _ in range(args.reps):
+            once2()
+        torch.cuda.synchronize()
+        lib.epp_gpu_profile(0)
+        a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        gpu.check(lib.epp_gpu_profile_read(0, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), 1))
+        out[name] = {"ms": round(a.value / c.value, 4), "tflops": round(b.value / a.value / 1e9, 1)}
     print(json.dumps(out))
 
 
