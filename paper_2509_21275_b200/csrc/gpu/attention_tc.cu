@@ -87,6 +87,9 @@ __device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
 
 // Share of exponentials (in eighths of the pairs) computed on the FMA pipe
 // instead of MUFU.EX2; tuned with tools/attn_bench.py.
+#ifndef EPP_DKV_PAIR
+#define EPP_DKV_PAIR 0
+#endif
 #ifndef EPP_FWD_EMU
 #define EPP_FWD_EMU 3
 #endif
@@ -1303,6 +1306,372 @@ __global__ void __launch_bounds__(kThreadsBwd, 1) attn_bwd_dkv_tc(const AttnArgs
     }
 }
 
+// ---------------------------------------------------------------------------
+// dK/dV on CTA pairs (cta_group::2, hd 128): two CTAs of a cluster take 256
+// consecutive keys of a head (128 each, the M halves of M=256 MMAs issued by
+// the leader CTA).  The score MMAs S^T = K Q^T / dP^T = V dO^T read their A
+// operand (the CTA's K / V rows) from shared memory; at N=64 the single-CTA
+// kernel's MMA reads 4 KB of A + 2 KB of B per K16 step, more than the
+// tensor core's 128 B/clk shared-memory port (48 instead of 32 cycles per
+// MMA, tools/micro/mma_issue_bench.cu).  Here each CTA supplies only half of
+// B (its 32 query rows of Q / dO; its 64 hd columns of dO^T / Q^T for dV / dK),
+// so a step reads 138 instead of 172 KB of shared memory per CTA.
+// Per stage each CTA stages two views of the same Q (and dO) tile:
+//   Qr: its 32 query rows x all hd   (S^T's B half: N = queries)
+//   Qc: all 64 query rows x its 64 hd (dK's B half: N = hd, MN-major)
+// Barriers live on the leader (rank 0) where the MMA warp waits: TMA loads
+// of both CTAs complete on the leader's barriers (peer bit cleared), the
+// softmax warps of both CTAs arrive there (peer: remote arrive), and MMA
+// commits multicast to both CTAs.
+//
+// MEASURED (tools/attn_bench.py, same box, A/B): correct (all attention
+// kernel tests pass) but SLOWER: 892-894 vs 1305 TFLOP/s at 16K causal, 809
+// vs 1190 at 5.3K context, 352 vs 483 on packed documents.  Every step now
+// waits on cross-CTA round trips (the peer's softmax arrives remotely at the
+// leader's barriers, commits multicast back), and the leader's MMA waits for
+// the slower of the two CTAs' softmax warps; the dependency chain, not the
+// shared-memory port, decides this kernel's speed.  Kept as an experiment
+// (build with -DEPP_DKV_PAIR=1, e.g. tools/ab_build.sh); the single-CTA
+// kernel above is the product.
+// ---------------------------------------------------------------------------
+#if EPP_DKV_PAIR
+__device__ __forceinline__ uint32_t cta_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma3_pair(uint32_t dst, const CUtensorMap* m, uint32_t leader_bar, int c0, int c1,
+                                          int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void tma4_pair(uint32_t dst, const CUtensorMap* m, uint32_t leader_bar, int c0, int c1,
+                                          int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+// arrive on the barrier at the same offset in the leader CTA (local when this is the leader)
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(tc::smem_u32(bar)));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+// expect_tx on this (the leader's) barrier for bytes that both CTAs' TMA loads deliver
+__device__ __forceinline__ void commit_pair_w(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            tc::smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+template <int A_STEP, int B_STEP>
+__device__ __forceinline__ void mma4_ss_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 a, b;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "mov.b64 a, %1;\n\tmov.b64 b, %2;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, p;\n\t"
+        "add.s64 a, a, %5;\n\tadd.s64 b, b, %6;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+        "add.s64 a, a, %5;\n\tadd.s64 b, b, %6;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+        "add.s64 a, a, %5;\n\tadd.s64 b, b, %6;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc0), "n"(A_STEP), "n"(B_STEP)
+        : "memory");
+}
+template <int A_COLS, int B_STEP>
+__device__ __forceinline__ void mma4_ts_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "mov.b32 a, %1;\n\tmov.b64 b, %2;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, p;\n\t"
+        "add.s32 a, a, %5;\n\tadd.s64 b, b, %6;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, 1;\n\t"
+        "add.s32 a, a, %5;\n\tadd.s64 b, b, %6;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, 1;\n\t"
+        "add.s32 a, a, %5;\n\tadd.s64 b, b, %6;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, 1;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc0), "n"(A_COLS), "n"(B_STEP)
+        : "memory");
+}
+__device__ __forceinline__ void mma_ss_pair_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+struct Dkv2Smem {   // hd 128, per CTA
+    static constexpr int HD = 128;
+    static constexpr int kStages = 4;
+    static constexpr int kBig = 128 * HD * 2;       // this CTA's K / V rows
+    static constexpr int kView = 32 * HD * 2;       // Qr / Or: 32 rows x 128 hd  (= 64 rows x 64 hd for Qc / Oc)
+    static constexpr int kStage = 4 * kView;        // Qr Qc Or Oc
+    static constexpr int kK = 0;
+    static constexpr int kV = kK + kBig;
+    static constexpr int kRing = kV + kBig;
+    static constexpr int kKa = kRing + kStages * kStage;     // augmented K-step: K, V [128 x 16] (ones)
+    static constexpr int kVa = kKa + 128 * 32;
+    static constexpr int kQa = kVa + 128 * 32;               // Q, dO [32 x 16] per stage (this CTA's queries)
+    static constexpr int kOa = kQa + kStages * 32 * 32;
+    static constexpr int kBar = kOa + kStages * 32 * 32;
+    static constexpr int kBytes = kBar + 32 * 8 + 16;
+    static constexpr int kAlloc = kBytes + 1024;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsBwd, 1)
+    attn_bwd_dkv_tc2(const AttnArgs a, const __grid_constant__ AttnMaps mp) {
+    pdl_wait();
+    pdl_trigger();
+    using L = Dkv2Smem;
+    constexpr int HD = L::HD, NS = L::kStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const uint32_t sbase = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
+    uint64_t* kv_full = bar + 0;                      // leader: both CTAs' K / V
+    uint64_t* qd_full = bar + 1;                      // [NS] leader: both CTAs' Q / dO views + aug columns
+    uint64_t* qd_empty = qd_full + NS;                // [NS] each CTA (multicast commit)
+    uint64_t* s_full = qd_empty + NS;                 // [2] each CTA (multicast commit)
+    uint64_t* dp_full = s_full + 2;                   // [2] each CTA
+    uint64_t* pt_full = dp_full + 2;                  // [2] leader: P^T of both CTAs in TMEM (8 warps)
+    uint64_t* p_full = pt_full + 2;                   // [2] leader: dS^T of both CTAs (8 warps)
+    uint64_t* acc_full = p_full + 2;                  // each CTA: all MMAs retired
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+    const uint32_t rank = cta_rank();
+    const bool leader = rank == 0;
+    const AttnWork w = a.kwork256[blockIdx.x >> 1];
+    const AttnSeg sg = a.segs[w.seg];
+    const int kvh = blockIdx.y;
+    const int group = a.H / a.Hkv;
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    const int kp0 = w.block * 2 * TK;                 // first key of the pair
+    const int k0 = kp0 + static_cast<int>(rank) * TK; // this CTA's keys
+    const int kv_len = sg.kv_ctx + sg.q_len;
+    const int nkeys = min(TK, kv_len - k0);           // <= 0: the pair's second block is past the end
+    const int qb_first = max(0, kp0 - sg.kv_ctx) / TB;
+    const int nqb = (sg.q_len + TB - 1) / TB;
+    const int per_head = nqb - qb_first;
+    const int iters = per_head * group;
+
+    if (threadIdx.x == 0) {
+        tc::mbar_init(kv_full, 1);
+        for (int st = 0; st < NS; ++st) {
+            tc::mbar_init(&qd_full[st], 3);   // leader expect_tx + both CTAs' aug-column writes
+            tc::mbar_init(&qd_empty[st], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&s_full[b], 1);
+            tc::mbar_init(&dp_full[b], 1);
+            tc::mbar_init(&pt_full[b], 8);
+            tc::mbar_init(&p_full[b], 8);
+        }
+        tc::mbar_init(acc_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 8) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(tmem_slot)),
+                     "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    for (int i = threadIdx.x; i < (L::kBar - L::kKa) / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem + L::kKa)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    if (threadIdx.x < 128) {
+        *reinterpret_cast<uint32_t*>(smem + L::kKa + aug_off(threadIdx.x)) = 0x3F803F80u;   // bf16 (1, 1)
+        *reinterpret_cast<uint32_t*>(smem + L::kVa + aug_off(threadIdx.x)) = 0x3F803F80u;
+    }
+    tc::fence_proxy_async();
+    tc::fence_before();
+    cluster_sync();          // barrier inits, TMEM allocation and aug blocks visible to the pair
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+    constexpr uint32_t kColS = 0, kColP = 128, kColV = 256, kColK = 256 + HD;
+
+    if (warp >= 8) tc::setmaxnreg_dec<56>();
+    if (warp == 9) {
+        const uint32_t lead_kv = tc::smem_u32(kv_full) & 0xFEFFFFFFu;     // peer bit cleared
+        const uint32_t lead_qd0 = tc::smem_u32(qd_full) & 0xFEFFFFFFu;
+        if (lane == 0) {
+            if (leader) tc::mbar_expect_tx(kv_full, 2 * 2 * L::kBig);
+            const CUtensorMap* mk = &mp.kv128[2 * sg.tma_map];
+            const CUtensorMap* mv = &mp.kv128[2 * sg.tma_map + 1];
+#pragma unroll
+            for (int c = 0; c < HD / 64; ++c) {
+                tma4_pair(sbase + L::kK + c * 128 * 128, mk, lead_kv, c * 64, kvh, sg.kv_row0 + k0, a.layer);
+                tma4_pair(sbase + L::kV + c * 128 * 128, mv, lead_kv, c * 64, kvh, sg.kv_row0 + k0, a.layer);
+            }
+        }
+        // aug columns of this CTA's 32 queries of the tile: -lse/c2 (hi, lo), -delta (hi, lo)
+        const float inv_c2 = 1.f / (a.scale * kLog2e);
+        float lv = 0.f, dv = 0.f;
+        auto fetch = [&](int it) {
+            const int hq = kvh * group + it / per_head;
+            const int q0 = (qb_first + it % per_head) * TB + 32 * static_cast<int>(rank);
+            const long long base = static_cast<long long>(hq) * a.T + sg.q_start + q0;
+            const bool ok = q0 + lane < sg.q_len;
+            lv = ok ? a.lse[base + lane] : 0.f;
+            dv = ok ? a.delta[base + lane] : 0.f;
+        };
+        fetch(0);
+        for (int it = 0; it < iters; ++it) {
+            const int st = it % NS;
+            const int hq = kvh * group + it / per_head;
+            const int row0 = sg.q_start + (qb_first + it % per_head) * TB;
+            const uint32_t qa = bf_hilo(-lv * inv_c2), oa = bf_hilo(-dv);
+            if (it + 1 < iters) fetch(it + 1);
+            tc::mbar_wait(&qd_empty[st], ((it / NS) & 1) ^ 1);
+            if (lane == 0) {
+                if (leader) tc::mbar_expect_tx(&qd_full[st], 2 * L::kStage);
+                const uint32_t sq = sbase + L::kRing + st * L::kStage;
+                const uint32_t lb = lead_qd0 + st * 8;
+                const int rr = row0 + 32 * static_cast<int>(rank);
+                // Qr, Or: this CTA's 32 query rows, both 64-column hd blocks
+                tma3_pair(sq, &mp.q32, lb, 0, hq, rr);
+                tma3_pair(sq + 32 * 128, &mp.q32, lb, 64, hq, rr);
+                tma3_pair(sq + 2 * L::kView, &mp.do32, lb, 0, hq, rr);
+                tma3_pair(sq + 2 * L::kView + 32 * 128, &mp.do32, lb, 64, hq, rr);
+                // Qc, Oc: all 64 query rows, this CTA's hd block
+                tma3_pair(sq + L::kView, &mp.q64, lb, 64 * static_cast<int>(rank), hq, row0);
+                tma3_pair(sq + 3 * L::kView, &mp.do64, lb, 64 * static_cast<int>(rank), hq, row0);
+            }
+            *reinterpret_cast<uint32_t*>(smem + L::kQa + st * 32 * 32 + aug_off(lane)) = qa;
+            *reinterpret_cast<uint32_t*>(smem + L::kOa + st * 32 * 32 + aug_off(lane)) = oa;
+            tc::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) arrive_leader(&qd_full[st]);
+        }
+    } else if (warp == 8) {
+        if (tmem != 0) __trap();
+        if (leader) {
+            constexpr uint32_t tmem_u = 0;
+            constexpr uint32_t idS = tc::instr_desc_mn(2 * TK, TB, false, false);   // M 256, N 64
+            constexpr uint32_t idD = tc::instr_desc_mn(2 * TK, HD, false, true);    // M 256, N 128, B MN-major
+            const uint64_t dK = tc::smem_desc(sbase + L::kK, 16, 1024), dV = tc::smem_desc(sbase + L::kV, 16, 1024);
+            const uint32_t sKa = sbase + L::kKa, sVa = sbase + L::kVa;
+            auto grad = [&](int it) {   // dV += P^T dO ; dK += dS^T Q
+                const int b = it & 1, st = it % NS;
+                const uint32_t sq = sbase + L::kRing + st * L::kStage;
+                tc::mbar_wait(&pt_full[b], (it >> 1) & 1);
+                tc::fence_after();
+                mma4_ts_pair<8, 128>(tmem_u + kColV, tmem_u + kColS + b * TB,
+                                     tc::smem_desc(sq + 3 * L::kView, TB * 128, 1024), idD, it != 0);
+                tc::mbar_wait(&p_full[b], (it >> 1) & 1);
+                tc::fence_after();
+                mma4_ts_pair<8, 128>(tmem_u + kColK, tmem_u + kColP + b * TB,
+                                     tc::smem_desc(sq + L::kView, TB * 128, 1024), idD, it != 0);
+                commit_pair_w(&qd_empty[st]);
+            };
+            auto scores = [&](int it) {   // S^T = K Q^T, dP^T = V dO^T
+                const int b = it & 1, st = it % NS;
+                const uint32_t sq = sbase + L::kRing + st * L::kStage;
+                tc::mbar_wait(&qd_full[st], (it / NS) & 1);
+                tc::fence_after();
+                const uint64_t dq = tc::smem_desc(sq, 16, 1024), dO = tc::smem_desc(sq + 2 * L::kView, 16, 1024);
+#pragma unroll
+                for (int cb = 0; cb < HD / 64; ++cb)   // 64-column blocks: A +16 KB, B (32 rows) +4 KB
+                    mma4_ss_pair<2, 2>(tmem_u + kColS + b * TB, dK + cb * 1024, dq + cb * 256, idS, cb != 0);
+                mma_ss_pair_w(tmem_u + kColS + b * TB, smem_desc_sw32(sKa),
+                              smem_desc_sw32(sbase + L::kQa + st * 32 * 32), idS, 1);
+                commit_pair_w(&s_full[b]);
+#pragma unroll
+                for (int cb = 0; cb < HD / 64; ++cb)
+                    mma4_ss_pair<2, 2>(tmem_u + kColP + b * TB, dV + cb * 1024, dO + cb * 256, idS, cb != 0);
+                mma_ss_pair_w(tmem_u + kColP + b * TB, smem_desc_sw32(sVa),
+                              smem_desc_sw32(sbase + L::kOa + st * 32 * 32), idS, 1);
+                commit_pair_w(&dp_full[b]);
+            };
+            tc::mbar_wait(kv_full, 0);
+            tc::fence_after();
+            scores(0);
+            for (int it = 0; it < iters; ++it) {
+                if (it + 1 < iters) scores(it + 1);
+                grad(it);
+            }
+            commit_pair_w(acc_full);
+        }
+        __syncwarp();
+    } else if (warp < 8) {
+        tc::setmaxnreg_inc<224>();
+        const int grp = warp >> 2;
+        const int r = threadIdx.x & 127;      // key row == TMEM lane
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        const int kp = k0 + r;
+        const float c2 = a.scale * kLog2e;
+        for (int it = grp; it < iters; it += 2) {
+            const int b = grp;
+            const int q0 = (qb_first + it % per_head) * TB;
+            const int rows = min(TB, sg.q_len - q0);
+            const int first_q = sg.kv_ctx + q0;
+            const bool need_mask = (k0 + TK - 1 > first_q) || rows < TB;
+            tc::mbar_wait(&s_full[b], (it >> 1) & 1);
+            tc::fence_after();
+            uint32_t pk[32], dk[32];
+            float sall[TB / 32][32], dall[TB / 32][32];
+#pragma unroll
+            for (int c = 0; c < TB / 32; ++c) tc::tmem_ld32_async(lane_base + kColS + b * TB + c * 32, sall[c]);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < TB / 32; ++c) tc::reg_fence(sall[c]);
+            if (need_mask) dkv_p_tile<true>(sall, c2, kp - first_q, rows, pk);
+            else dkv_p_tile<false>(sall, c2, 0, TB, pk);
+            tc::tmem_st32u(lane_base + kColS + b * TB, pk);
+            tc::tmem_wait_st();
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_leader(&pt_full[b]);
+            tc::mbar_wait(&dp_full[b], (it >> 1) & 1);
+            tc::fence_after();
+#pragma unroll
+            for (int c = 0; c < TB / 32; ++c) tc::tmem_ld32_async(lane_base + kColP + b * TB + c * 32, dall[c]);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < TB / 32; ++c) tc::reg_fence(dall[c]);
+            dkv_ds_tile(sall, dall, dk);
+            tc::tmem_st32u(lane_base + kColP + b * TB, dk);
+            tc::tmem_wait_st();
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_leader(&p_full[b]);
+        }
+        tc::mbar_wait(acc_full, 0);
+        tc::fence_after();
+        if (nkeys > 0) dkv_epilogue<HD>(a, sg, kvh, k0, nkeys, r, grp, lane_base, kColK, kColV);
+        tc::fence_before();
+    }
+    __syncthreads();
+    cluster_sync();          // the leader's MMAs and the peer's arrivals are done on both sides
+    if (warp == 8) {
+        tc::fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+    }
+}
+#endif  // EPP_DKV_PAIR
+
 template <int HD>
 void launch_bwd_tc(const AttnArgs& a, cudaStream_t s) {
     static bool cfg = false;
@@ -1320,6 +1689,21 @@ void launch_bwd_tc(const AttnArgs& a, cudaStream_t s) {
         launch_k(attn_bwd_dq_tc<HD>, attn_grid(a.H, a.nqwork128), kThreadsBwd, DqSmem<HD>::kAlloc, s, b, *a.maps);
         EPP_CHECK_LAUNCH();
     }
+#if EPP_DKV_PAIR
+    if (HD == 128 && a.nkwork256 > 0 && a.kwork256) {
+        // CTA pairs: cluster (2 x 128 keys) per 256-key block, grid (2 x blocks, Hkv)
+        ProfScope prof(kProfAttnBwdDkv, 8.0 * a.H * a.hd * a.pairs, s);    // executed: 4 matmuls
+        static bool cfg2 = false;
+        if (!cfg2) {
+            EPP_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          Dkv2Smem::kAlloc));
+            cfg2 = true;
+        }
+        launch_k(attn_bwd_dkv_tc2, dim3(2 * a.nkwork256, a.Hkv), kThreadsBwd, Dkv2Smem::kAlloc, s, a, *a.maps);
+        EPP_CHECK_LAUNCH();
+        return;
+    }
+#endif
     if (a.nkwork128 > 0) {
         ProfScope prof(kProfAttnBwdDkv, 8.0 * a.H * a.hd * a.pairs, s);    // executed: 4 matmuls
         AttnArgs b = a;
@@ -1360,14 +1744,16 @@ void attn_maps_q(AttnMaps& m, const void* q, const void* dout, int T, int H, int
                                         static_cast<unsigned long long>(T)};
     const unsigned long long st[2] = {static_cast<unsigned long long>(hd) * 2,
                                       static_cast<unsigned long long>(H) * hd * 2};
-    const unsigned b128[3] = {64, 1, 128}, b64[3] = {64, 1, 64};
+    const unsigned b128[3] = {64, 1, 128}, b64[3] = {64, 1, 64}, b32[3] = {64, 1, 32};
     if (q) {
         m.q128 = make_tma_map(q, 3, dims, st, b128);
         m.q64 = make_tma_map(q, 3, dims, st, b64);
+        m.q32 = make_tma_map(q, 3, dims, st, b32);
     }
     if (dout) {
         m.do128 = make_tma_map(dout, 3, dims, st, b128);
         m.do64 = make_tma_map(dout, 3, dims, st, b64);
+        m.do32 = make_tma_map(dout, 3, dims, st, b32);
     }
 }
 

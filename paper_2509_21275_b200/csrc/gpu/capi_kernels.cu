@@ -39,7 +39,8 @@ struct AttnTables {
     void* qw128 = nullptr;
     void* kw128 = nullptr;
     void* qw256 = nullptr;
-    int nq = 0, nk = 0, nq128 = 0, nk128 = 0, nq256 = 0;
+    void* kw256 = nullptr;
+    int nq = 0, nk = 0, nq128 = 0, nk128 = 0, nq256 = 0, nk256 = 0;
     cudaStream_t s;
     AttnTables(int nseg, const int32_t* q_start, const int32_t* q_len, const int32_t* kv_ctx,
                const void* const* k, const void* const* v, float* const* dk, float* const* dv,
@@ -56,7 +57,7 @@ struct AttnTables {
             EPP_CUDA(cudaMemset(kcat, 0, 2 * total_rows * row_bytes));
         }
         long long row = 0;
-        std::vector<AttnWork> q, kk, q128, k128, q256;
+        std::vector<AttnWork> q, kk, q128, k128, q256, k256;
         for (int i = 0; i < nseg; ++i) {
             sg[i] = AttnSeg{};
             sg[i].dkv_accum = 1;   // kernel-level ABI: dK/dV accumulate into the caller's buffers
@@ -81,6 +82,7 @@ struct AttnTables {
             for (int b = 0; b * 128 < q_len[i]; ++b) q128.push_back({i, b});
             for (int b = 0; b * 128 < kv_ctx[i] + q_len[i]; ++b) k128.push_back({i, b});
             for (int b = 0; b * 256 < q_len[i]; ++b) q256.push_back({i, b});
+            for (int b = 0; b * 256 < kv_ctx[i] + q_len[i]; ++b) k256.push_back({i, b});
         }
         nq128 = static_cast<int>(q128.size());
         nk128 = static_cast<int>(k128.size());
@@ -91,6 +93,9 @@ struct AttnTables {
         nq256 = static_cast<int>(q256.size());
         EPP_CUDA(cudaMalloc(&qw256, sizeof(AttnWork) * (nq256 ? nq256 : 1)));
         EPP_CUDA(cudaMemcpy(qw256, q256.data(), sizeof(AttnWork) * nq256, cudaMemcpyHostToDevice));
+        nk256 = static_cast<int>(k256.size());
+        EPP_CUDA(cudaMalloc(&kw256, sizeof(AttnWork) * (nk256 ? nk256 : 1)));
+        EPP_CUDA(cudaMemcpy(kw256, k256.data(), sizeof(AttnWork) * nk256, cudaMemcpyHostToDevice));
         if (tc) {
             attn_maps_kv(maps, 1, kcat, static_cast<uint8_t*>(kcat) + total_rows * row_bytes, total_rows, 1, Hkv, hd);
             attn_maps_q(maps, qptr, dout, T, H, hd);
@@ -112,6 +117,7 @@ struct AttnTables {
         cudaFree(qw128);
         cudaFree(kw128);
         cudaFree(qw256);
+        cudaFree(kw256);
         if (kcat) cudaFree(kcat);
     }
 };
@@ -172,6 +178,8 @@ int epp_kernel_attention_fwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, floa
         a.nkwork128 = tb.nk128;
         a.qwork256 = static_cast<const eppk::AttnWork*>(tb.qw256);
         a.nqwork256 = tb.nq256;
+        a.kwork256 = static_cast<const eppk::AttnWork*>(tb.kw256);
+        a.nkwork256 = tb.nk256;
         a.T = T; a.H = H; a.Hkv = Hkv; a.hd = hd; a.layer = 0; a.scale = scale;
         a.dtype = static_cast<eppk::DType>(dtype);
         a.q = q; a.o = o; a.lse = lse;
@@ -205,6 +213,8 @@ int epp_kernel_attention_bwd(int32_t T, int32_t H, int32_t Hkv, int32_t hd, floa
         a.nkwork128 = tb.nk128;
         a.qwork256 = static_cast<const eppk::AttnWork*>(tb.qw256);
         a.nqwork256 = tb.nq256;
+        a.kwork256 = static_cast<const eppk::AttnWork*>(tb.kw256);
+        a.nkwork256 = tb.nk256;
         a.T = T; a.H = H; a.Hkv = Hkv; a.hd = hd; a.layer = 0; a.scale = scale;
         a.dtype = static_cast<eppk::DType>(dtype);
         a.q = q; a.o = const_cast<void*>(o); a.lse = const_cast<float*>(lse);

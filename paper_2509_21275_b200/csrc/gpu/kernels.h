@@ -91,8 +91,8 @@ struct AttnSeg {
 // sequence's KV buffer and the chunk-local one).  All bf16, 128-byte swizzle,
 // boxes of 64 hd-columns x 1 head x {64,128} rows.
 struct AttnMaps {
-    CUtensorMap q128, q64;       // Q with 128- / 64-row boxes
-    CUtensorMap do128, do64;     // dO
+    CUtensorMap q128, q64, q32;      // Q with 128- / 64- / 32-row boxes
+    CUtensorMap do128, do64, do32;   // dO
     CUtensorMap kv128[4];        // k0, v0, k1, v1 with 128-row boxes
     CUtensorMap kv64[4];         // ... 64-row boxes
 };
@@ -123,6 +123,8 @@ struct AttnArgs {
     int nkwork128 = 0;
     const AttnWork* qwork256 = nullptr;   // 256-row query blocks (tcgen05 forward: 2 tiles / CTA)
     int nqwork256 = 0;
+    const AttnWork* kwork256 = nullptr;   // 256-key blocks (CTA-pair dK/dV: 128 keys per CTA)
+    int nkwork256 = 0;
     int hfast = 0;                        // launch order: grid (head, work) instead of (work, head)
     int T = 0;
     int H = 0, Hkv = 0, hd = 0;

@@ -170,10 +170,10 @@ struct LayerSaved {
 struct ChunkState {
     int T = 0;
     std::vector<AttnSeg> segs;     // host copy
-    Buf segs_dev, tok_seg, tok_pos, qwork, kwork, qwork128, kwork128, qwork256;
+    Buf segs_dev, tok_seg, tok_pos, qwork, kwork, qwork128, kwork128, qwork256, kwork256;
     Buf kv_local;                  // [K|V][layer][T][Hkv*hd] rows of packed segments
     Buf dkv_local;                 // fp32 [dK|dV][T][Hkv*hd], one layer, re-zeroed per layer
-    int nqwork = 0, nkwork = 0, nqwork128 = 0, nkwork128 = 0, nqwork256 = 0;
+    int nqwork = 0, nkwork = 0, nqwork128 = 0, nkwork128 = 0, nqwork256 = 0, nkwork256 = 0;
     double pairs = 0;
     AttnMaps maps{};               // TMA descriptors (K/V per chunk, Q/dO per layer call)
     Buf x_in;                      // stage input (copy of act_in or embedding)
@@ -773,7 +773,7 @@ private:
                          Hkv_, hd_);
         }
         std::vector<int> tseg(cs.T), tpos(cs.T);
-        std::vector<AttnWork> qw, kw, qw128, kw128, qw256;
+        std::vector<AttnWork> qw, kw, qw128, kw128, qw256, kw256;
         for (int i = 0; i < static_cast<int>(cs.segs.size()); ++i) {
             const AttnSeg& sg = cs.segs[i];
             for (int t = 0; t < sg.q_len; ++t) {
@@ -785,6 +785,7 @@ private:
             for (int b = 0; b * 128 < sg.q_len; ++b) qw128.push_back({i, b});
             for (int b = 0; b * 128 < sg.kv_ctx + sg.q_len; ++b) kw128.push_back({i, b});
             for (int b = 0; b * 256 < sg.q_len; ++b) qw256.push_back({i, b});
+            for (int b = 0; b * 256 < sg.kv_ctx + sg.q_len; ++b) kw256.push_back({i, b});
         }
         cs.pairs = 0;
         for (const AttnSeg& sg : cs.segs)
@@ -813,6 +814,7 @@ private:
         std::sort(qw128.begin(), qw128.end(), by(qcost, 128));
         std::sort(kw128.begin(), kw128.end(), by(kcost, 128));
         std::sort(qw256.begin(), qw256.end(), by(qcost, 256));
+        std::sort(kw256.begin(), kw256.end(), by(kcost, 256));
         cs.nqwork = static_cast<int>(qw.size());
         cs.nkwork = static_cast<int>(kw.size());
         cs.tok_seg = upload(tseg.data(), tseg.size() * sizeof(int), s);
@@ -825,6 +827,8 @@ private:
         cs.kwork128 = upload(kw128.data(), kw128.size() * sizeof(AttnWork), s);
         cs.nqwork256 = static_cast<int>(qw256.size());
         cs.qwork256 = upload(qw256.data(), qw256.size() * sizeof(AttnWork), s);
+        cs.nkwork256 = static_cast<int>(kw256.size());
+        cs.kwork256 = upload(kw256.data(), kw256.size() * sizeof(AttnWork), s);
         cs.segs_dev = upload(cs.segs.data(), cs.segs.size() * sizeof(AttnSeg), s);
     }
 
@@ -874,6 +878,8 @@ private:
         a.nqwork128 = cs.nqwork128;
         a.kwork128 = cs.kwork128.get<AttnWork>();
         a.nkwork128 = cs.nkwork128;
+        a.kwork256 = cs.kwork256.get<AttnWork>();
+        a.nkwork256 = cs.nkwork256;
         a.qwork256 = cs.qwork256.get<AttnWork>();
         a.nqwork256 = cs.nqwork256;
         a.T = cs.T;
