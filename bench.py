@@ -498,7 +498,7 @@ def run_ours(args):
         # stage-to-stage activations/gradients (this rank's sends; rank 0 is a
         # first stage, so its sends are the forward activations of one hop)
         hop_bytes = p2p_bytes / args.steps
-        out["p2p"] = {"bytes_per_step_rank0": hop_bytes,
+        out["p2p"] = {"transport": getattr(driver, "transport", None), "bytes_per_step_rank0": hop_bytes,
                       "gbs_rank0_avg_over_step": hop_bytes / (sec / args.steps) / 1e9,
                       "nvlink_gbs_per_direction": 900.0,
                       "note": "rank 0's send volume over the whole step time (not per-transfer bandwidth)"}

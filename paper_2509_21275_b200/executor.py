@@ -320,30 +320,61 @@ class DistributedPipeline:
         self.p2p_bytes = 0
         self.p2p = bool(getattr(stage, "supports_p2p", False))
         self.ch = {}
+        self.transport = "torch.distributed"
         if self.p2p:
-            self._open_channels(max_tokens)
+            # every rank must agree on the transport: if any endpoint cannot
+            # map its peer (e.g. no CUDA IPC between the two processes), all
+            # ranks use torch.distributed (NCCL) send / recv instead
+            err = self._open_channels(max_tokens)
+            errs = [None] * self.dist.get_world_size()
+            self.dist.all_gather_object(errs, err)
+            bad = [e for e in errs if e]
+            if bad:
+                import sys
+                print(f"epp: P2P channels unavailable ({bad[0]}); stage transfers use torch.distributed",
+                      file=sys.stderr)
+                self.close()
+                self.p2p = False
+                self.transport = f"torch.distributed (P2P channels failed: {bad[0]})"
+            else:
+                self.transport = "epp_p2p channels (peer memory)"
 
-    def _open_channels(self, max_tokens: int):
+    def _open_channels(self, max_tokens: int) -> str:
         """Endpoints: 'fin' (activations from p-1), 'fout' (to p+1), 'bin'
-        (gradients from p+1), 'bout' (to p-1).  Receivers own the arenas."""
+        (gradients from p+1), 'bout' (to p-1).  Receivers own the arenas.
+        Every rank takes part in the handle exchange even if its own
+        endpoints failed; returns this rank's error ('' = fine)."""
         from .gpu import P2PChannel
         p, dp = self.rank, self.world
-        esz = torch.tensor([], dtype=self.act_dtype).element_size()
-        arena = 2 * max(1, int(max_tokens)) * self.hidden * esz
-        if p > 0:
-            self.ch["fin"] = P2PChannel("recv", arena)
-            self.ch["bout"] = P2PChannel("send")
-        if p + 1 < dp:
-            self.ch["fout"] = P2PChannel("send")
-            self.ch["bin"] = P2PChannel("recv", arena)
-        mine = {k: c.handle for k, c in self.ch.items()}
+        err = ""
+        try:
+            esz = torch.tensor([], dtype=self.act_dtype).element_size()
+            arena = 2 * max(1, int(max_tokens)) * self.hidden * esz
+            if p > 0:
+                self.ch["fin"] = P2PChannel("recv", arena)
+                self.ch["bout"] = P2PChannel("send")
+            if p + 1 < dp:
+                self.ch["fout"] = P2PChannel("send")
+                self.ch["bin"] = P2PChannel("recv", arena)
+            mine = {k: c.handle for k, c in self.ch.items()}
+        except Exception as e:  # noqa: BLE001
+            err, mine = f"{type(e).__name__}: {e}", None
         got = [None] * self.dist.get_world_size()
         self.dist.all_gather_object(got, (self.ranks[p], mine))
         by_rank = {r: h for (r, h) in got}
+        if err:
+            return err
         peer = {"fin": (p - 1, "fout"), "bout": (p - 1, "bin"), "fout": (p + 1, "fin"), "bin": (p + 1, "bout")}
-        for k, c in self.ch.items():
-            q, their = peer[k]
-            c.open(by_rank[self.ranks[q]][their])
+        try:
+            for k, c in self.ch.items():
+                q, their = peer[k]
+                h = by_rank[self.ranks[q]]
+                if h is None:
+                    return f"stage {q} has no P2P endpoints"
+                c.open(h[their])
+        except Exception as e:  # noqa: BLE001
+            return f"{type(e).__name__}: {e}"
+        return ""
 
     def close(self):
         for c in self.ch.values():

@@ -33,14 +33,24 @@ def counts_for(world):
     return [3, 1] if world == 2 else None
 
 
-def worker(rank, world, port, doc, q):
+class ClaimsP2P(O.TorchStage):
+    """A CPU stage that claims the C-ABI P2P transport: opening the channels
+    fails here (no GPU), so every rank must fall back to torch.distributed
+    together."""
+    supports_p2p = True
+
+
+def worker(rank, world, port, doc, q, claim_p2p=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
     plan = S.parse_plan(doc, LENGTHS)
     params = O.init_params(spec(), seed=3)
     first, num = stage_layers(MODEL.layers, world, rank, counts_for(world))
-    st = O.TorchStage(spec(), params, first, num, rank == 0, rank == world - 1)
+    cls = ClaimsP2P if claim_p2p else O.TorchStage
+    st = cls(spec(), params, first, num, rank == 0, rank == world - 1)
     drv = DistributedPipeline(st, rank, world, torch.device("cpu"), MODEL.hidden, torch.float32)
+    if claim_p2p:
+        assert not drv.p2p and drv.transport.startswith("torch.distributed (P2P channels failed"), drv.transport
     drv.run_step(plan, S.synthetic_tokens(LENGTHS, MODEL.vocab, seed=11))
     # by value (numpy): shared-memory tensors would vanish with the exiting worker
     q.put((rank, {k: v.numpy().copy() for k, v in st.grads().items()}, float(st.loss_sum), drv.p2p_bytes))
@@ -56,13 +66,13 @@ def free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_gloo_pipeline_matches_local(world):
+@pytest.mark.parametrize("world,claim_p2p", [(2, False), (4, False), (2, True)])
+def test_gloo_pipeline_matches_local(world, claim_p2p):
     doc = plan_doc(world)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, world, port, doc, q)) for r in range(world)]
+    procs = [ctx.Process(target=worker, args=(r, world, port, doc, q, claim_p2p)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=300) for _ in range(world)]
