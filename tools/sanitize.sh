@@ -8,7 +8,7 @@
 set -u
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-SEL='test_gemm_pair_epilogues or (test_attention and bf16 and (packed or slice_ctx or hybrid))'
+SEL='test_gemm_pair_epilogues or test_gemm_swiglu_epilogues or test_gemm_pair_ragged_n or (test_attention and bf16 and (packed or slice_ctx or hybrid))'
 for tool in racecheck synccheck memcheck; do
   log=gpurun_out/sanitize_${tool}.log
   extra=""
