@@ -28,6 +28,7 @@ def main():
         gpu._LIB_PATH = Path(args.lib)
     torch.cuda.set_device(0)
     lib = gpu.lib()
+    gpu.pool_reserve(8 << 30)   # as the stage does: workspaces never wait on the driver to map memory
     T, D, F = args.T, args.D, args.F
     bf = torch.bfloat16
     out = {}
