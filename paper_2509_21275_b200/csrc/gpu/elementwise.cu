@@ -663,15 +663,19 @@ __global__ void ce_k(T* logits, const int32_t* targets, float* row_loss, int V, 
     T* lr = logits + row * V;
     const int tgt = targets[row];
     float m = -INFINITY, s = 0.f;
+    // online (max, sum) per 8-element vector: one rescale per vector instead
+    // of per element (9 exponentials per 8 logits instead of 16; the MUFU
+    // pipe and HBM otherwise co-limit this kernel)
     for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
         float v[8];
         load8(lr + c, v);
+        float mv = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])), fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
+        const float mn = fmaxf(m, mv);
+        float acc = 0.f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float mn = fmaxf(m, v[i]);
-            s = s * __expf(m - mn) + __expf(v[i] - mn);
-            m = mn;
-        }
+        for (int i = 0; i < 8; ++i) acc += __expf(v[i] - mn);
+        s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + acc;
+        m = mn;
     }
     // combine (m, s) across the block
 #pragma unroll
