@@ -968,7 +968,7 @@ __device__ __forceinline__ void dkv_epilogue(const AttnArgs& a, const AttnSeg& s
                 g1[i] *= mul;
                 g2[i] *= mul;
             }
-            if (sg.dkv_accum) {
+            if (sg.dkv_accum == 1) {
 #pragma unroll
                 for (int i = 0; i < 32; i += 4) {
                     const float4 o1 = *reinterpret_cast<const float4*>(drow + cc + i);
@@ -1021,7 +1021,7 @@ __device__ __forceinline__ void dkv_epilogue(const AttnArgs& a, const AttnSeg& s
 #pragma unroll
                 for (int i = 0; i < 32; i += 4) {
                     float4 x = make_float4(v[i] * mul, v[i + 1] * mul, v[i + 2] * mul, v[i + 3] * mul);
-                    if (sg.dkv_accum) {   // later slices' contributions are already there
+                    if (sg.dkv_accum == 1) {   // later slices' contributions are already there
                         const float4 o = *reinterpret_cast<const float4*>(drow + c * 32 + i);
                         x.x += o.x; x.y += o.y; x.z += o.z; x.w += o.w;
                     }
@@ -1758,14 +1758,15 @@ void attn_maps_q(AttnMaps& m, const void* q, const void* dout, int T, int H, int
 }
 
 void attn_maps_kv(AttnMaps& m, int which, const void* k, const void* v, long long rows, int layers, int Hkv,
-                  int hd) {
+                  int hd, long long stride_rows) {
     if (!k || rows <= 0) return;
+    if (stride_rows <= 0) stride_rows = rows;
     const unsigned long long dims[4] = {static_cast<unsigned long long>(hd), static_cast<unsigned long long>(Hkv),
                                         static_cast<unsigned long long>(rows),
                                         static_cast<unsigned long long>(layers)};
     const unsigned long long st[3] = {static_cast<unsigned long long>(hd) * 2,
                                       static_cast<unsigned long long>(Hkv) * hd * 2,
-                                      static_cast<unsigned long long>(rows) * Hkv * hd * 2};
+                                      static_cast<unsigned long long>(stride_rows) * Hkv * hd * 2};
     const unsigned b128[4] = {64, 1, 128, 1}, b64[4] = {64, 1, 64, 1};
     m.kv128[2 * which] = make_tma_map(k, 4, dims, st, b128);
     m.kv128[2 * which + 1] = make_tma_map(v, 4, dims, st, b128);

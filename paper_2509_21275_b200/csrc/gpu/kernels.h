@@ -77,6 +77,7 @@ struct AttnSeg {
     int tma_map;     // tcgen05 kernels: 0 -> AttnMaps::kv[0..1] (sequence), 1 -> kv[2..3]
     int kv_row0;     // row of key 0 in that map's row coordinate
     int dkv_accum;   // 1: dK/dV accumulate into a persistent (sequence) buffer;
+                     // 2: first writer of that buffer (tcgen05: the tail slice);
                      // 0: chunk-local scratch, written once (tcgen05 backward)
     const void* k;       // layer-0 base
     const void* v;
@@ -98,8 +99,10 @@ struct AttnMaps {
 };
 // Helpers filling AttnMaps (attention_tc.cu).
 void attn_maps_q(AttnMaps& m, const void* q, const void* dout, int T, int H, int hd);
+// rows: the map's row extent (reads past it return zeros); stride_rows: the
+// buffer's rows per layer (0 = rows)
 void attn_maps_kv(AttnMaps& m, int which, const void* k, const void* v, long long rows, int layers, int Hkv,
-                  int hd);
+                  int hd, long long stride_rows = 0);
 CUtensorMap make_tma_map(const void* base, int rank, const unsigned long long* dims,
                          const unsigned long long* strides_b, const unsigned* box);
 

@@ -716,15 +716,22 @@ private:
             SeqKV& sk = seqs_[c.seq];
             if (!sk.kv) {
                 sk.len = c.seq_len;
-                // zeroed: attention tiles may read rows of later (not yet written)
-                // slices; they are masked, and must be finite
-                sk.kv = Buf(&pool_, 2 * static_cast<size_t>(nl_) * sk.len * kvw() * esz(), s, /*zero=*/true);
+                // bf16: no zero fill (the chunk's TMA maps end at its last
+                // visible key, rows past it load as zeros); fp32 parity
+                // kernels never read past a query's position either, but
+                // keep the buffer defined for them
+                sk.kv = Buf(&pool_, 2 * static_cast<size_t>(nl_) * sk.len * kvw() * esz(), s,
+                            /*zero=*/dt_ != DType::BF16);
             }
             EPP_REQUIRE(sk.len == c.seq_len, "seq_len changed between slices");
         } else {
             EPP_REQUIRE(c.context == 0, "context without a sequence");
         }
-        cs.kv_local = Buf(&pool_, 2 * static_cast<size_t>(nl_) * T * kvw() * esz(), s, /*zero=*/true);
+        // chunk-local K/V of packed documents: every row a kernel reads is
+        // written by the layer's QKV epilogue first (rows past T load as
+        // zeros through the TMA map), so bf16 skips the zero fill (~8 GB per
+        // 15K-token GPT-7B chunk)
+        cs.kv_local = Buf(&pool_, 2 * static_cast<size_t>(nl_) * T * kvw() * esz(), s, /*zero=*/dt_ != DType::BF16);
         int max_pos = 0;
         long long q_start = 0;
         cs.segs.clear();
@@ -741,7 +748,11 @@ private:
                 sg.v = sk.kv.get<uint8_t>() + static_cast<size_t>(nl_) * sk.len * kvw() * esz();
                 sg.kv_layer_stride = sk.len * kvw();
                 sg.dkv_layer_stride = sk.len * kvw();
-                sg.dkv_accum = 1;
+                // the tail slice's backward is the sequence's first (later
+                // slices run first, pipeline.cpp:121-131): it WRITES every
+                // context row of the fp32 dK/dV buffer and has no partials for
+                // its own rows (2); earlier slices read-add (1)
+                sg.dkv_accum = (c.tail && dt_ == DType::BF16) ? 2 : 1;
             } else {
                 // Packed document: K/V rows in the chunk-local buffer (layer
                 // strided like the sequence buffers); dK/dV in a one-layer
@@ -764,9 +775,10 @@ private:
         if (dt_ == DType::BF16) {
             if (seq_chunk) {
                 const SeqKV& sk = seqs_[c.seq];
+                // rows end at the chunk's last visible key: tiles past it read zeros
                 attn_maps_kv(cs.maps, 0, sk.kv.get(),
-                             sk.kv.get<uint8_t>() + static_cast<size_t>(nl_) * sk.len * kvw() * esz(), sk.len,
-                             nl_, Hkv_, hd_);
+                             sk.kv.get<uint8_t>() + static_cast<size_t>(nl_) * sk.len * kvw() * esz(),
+                             c.context + c.slices[0], nl_, Hkv_, hd_, sk.len);
             }
             attn_maps_kv(cs.maps, 1, cs.kv_local.get(),
                          cs.kv_local.get<uint8_t>() + static_cast<size_t>(nl_) * T * kvw() * esz(), T, nl_,
@@ -852,9 +864,9 @@ private:
             AttnSeg& sg = cs.segs[i];
             if (i == 0 && c.seq >= 0) {
                 SeqKV& sk = seqs_[c.seq];
-                if (!sk.dkv)
+                if (!sk.dkv)   // bf16: the tail slice writes it first (dkv_accum 2), no zero fill
                     sk.dkv = Buf(&pool_, 2 * static_cast<size_t>(nl_) * sk.len * kvw() * sizeof(float),
-                                 s, /*zero=*/true);
+                                 s, /*zero=*/dt_ != DType::BF16);
                 sg.dk = sk.dkv.get<float>();
                 sg.dv = sk.dkv.get<float>() + static_cast<size_t>(nl_) * sk.len * kvw();
             } else {
