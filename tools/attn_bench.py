@@ -31,6 +31,9 @@ CASES = {
     "gpt7b_16k": dict(H=32, Hkv=32, hd=128, segs=[(0, 16384, 0)]),
     "gpt7b_hybrid": dict(H=32, Hkv=32, hd=128, segs=[(0, 14926, 0), (14926, 1316, 0)]),
     "gpt7b_ctx": dict(H=32, Hkv=32, hd=128, segs=[(0, 5349, 10571)]),
+    # Llama-7B (GQA 32/8) at 64K split into 8 slices: the last slice, and a middle one
+    "llama_ctx56k": dict(H=32, Hkv=8, hd=128, segs=[(0, 8192, 57344)]),
+    "llama_ctx24k": dict(H=32, Hkv=8, hd=128, segs=[(0, 8192, 24576)]),
 }
 
 
