@@ -507,6 +507,185 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   acc_full[b]  both CTAs: multicast commit after a tile's last MMA
 //   acc_empty[b] leader only: 4 epilogue warps x 2 CTAs arrive (peer: remote)
 // =========================================================================
+// TMA-staged bf16 epilogues of the pair kernel (Store, AddRes, StoreGelu,
+// GeluBwd, SwiGlu, SwiGluBwd).  An epilogue thread owns one accumulator row
+// (the tcgen05.ld 32x32b shape), so direct global stores / residual loads are
+// one 16-byte access per row and lane: 32 L1 wavefronts per warp instruction,
+// and every extra row-strided stream cost ~10 % of the GEMM at K = 2048
+// (tools/gemm_bench.py: store 1462, + residual load 1311, GELU' with h load
+// and gelu(h) store 1075 TFLOP/s) because those wavefronts share the SM's
+// L1 / shared-memory data path with the TMA writes and MMA reads of the main
+// loop.  Here each warp moves 32 x 32 bf16 boxes (64-byte swizzle) through
+// shared memory: residual / h boxes arrive by TMA (two slots, one group of
+// lookahead), outputs leave by TMA bulk stores; the warp's shared-memory
+// accesses are 4 wavefronts per instruction.
+template <int EPI>
+struct EpiTma {
+    static constexpr bool kOn = EPI == static_cast<int>(Epi::Store) || EPI == static_cast<int>(Epi::AddRes) ||
+                                EPI == static_cast<int>(Epi::StoreGelu) || EPI == static_cast<int>(Epi::GeluBwd) ||
+                                EPI == static_cast<int>(Epi::SwiGlu) || EPI == static_cast<int>(Epi::SwiGluBwd);
+    // R streams per 32-column group: residual, h, or SwiGLU's gate and up halves of h
+    static constexpr int kR = EPI == static_cast<int>(Epi::AddRes) || EPI == static_cast<int>(Epi::GeluBwd) ? 1
+                              : EPI == static_cast<int>(Epi::SwiGluBwd)                                   ? 2
+                                                                                                          : 0;
+    // output boxes per group: C (SwiGLU: both halves of h / dh) and C2
+    static constexpr int kOut = EPI == static_cast<int>(Epi::Store) || EPI == static_cast<int>(Epi::AddRes) ? 1
+                                : EPI == static_cast<int>(Epi::StoreGelu) || EPI == static_cast<int>(Epi::GeluBwd) ? 2
+                                : kOn ? 3 : 0;
+    static constexpr int kBox = 32 * 64;            // 32 rows x 32 bf16
+    static constexpr int kRSlots = kR ? 2 : 0;
+    static constexpr int kOutBufs = 2;
+    static constexpr int kWarpBytes = (kRSlots * kR + kOutBufs * kOut) * kBox;
+};
+
+// 64-byte swizzle: 16-byte chunk j of a 64-byte row r sits at j ^ ((r >> 1) & 3)
+__device__ __forceinline__ uint32_t sw64(int r, int j) { return r * 64 + ((j ^ ((r >> 1) & 3)) << 4); }
+
+__device__ __forceinline__ void box_store_row(uint8_t* box, int r, const float (&v)[32]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        uint4 raw;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
+        *reinterpret_cast<uint4*>(box + sw64(r, j)) = raw;
+    }
+}
+__device__ __forceinline__ void box_load_row(const uint8_t* box, int r, float (&v)[32]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(box + sw64(r, j));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float2 f = __bfloat1622float2(h[k]);
+            v[8 * j + 2 * k] = f.x;
+            v[8 * j + 2 * k + 1] = f.y;
+        }
+    }
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const uint8_t* box, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(tc::smem_u32(box))
+                 : "memory");
+}
+
+// Per-warp state of the TMA epilogue across tiles.
+struct EpiTmaState {
+    uint32_t r_used = 0;     // R groups consumed (slot = r_used & 1)
+    uint32_t stored = 0;     // output groups committed (buffer = stored & 1)
+};
+
+// One tile's epilogue for one warp: rows row0 .. row0 + 31 (this thread:
+// row0 + lane), accumulator columns [0, kCols) at taddr; output column of
+// accumulator column 0 = n0 (SwiGlu: gate feature j0 = n0).
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tma(const TcParams& p, const CUtensorMap* map_r, const CUtensorMap* map_c,
+                                             const CUtensorMap* map_c2, uint32_t taddr, uint8_t* ebuf,
+                                             uint64_t* rbar, int row0, int n0, int lane, EpiTmaState& st) {
+    using E = EpiTma<EPI>;
+    constexpr bool kSwi = EPI == static_cast<int>(Epi::SwiGlu);
+    constexpr bool kSwiB = EPI == static_cast<int>(Epi::SwiGluBwd);
+    constexpr int kCols = kSwi ? BN / 2 : BN;            // accumulator columns walked (SwiGlu: gate half)
+    const int nlog = kSwi ? p.N / 2 : p.N;                // columns of the logical output
+    const int F = kSwi ? p.N / 2 : p.N;                   // SwiGLU halves
+    const int groups = max(0, min(kCols, nlog - n0)) / 32;
+    const bool rows_live = row0 < p.M;
+    const bool has_c2 = p.C2 != nullptr;
+    uint8_t* rbase = ebuf;
+    uint8_t* obase = ebuf + E::kRSlots * E::kR * E::kBox;
+    auto issue_r = [&](int gi, uint32_t k) {   // lane 0: R boxes of group gi, the warp's k-th R group
+        const int slot = k & 1;
+        uint64_t* bar = rbar + slot;
+        tc::mbar_expect_tx(bar, E::kR * E::kBox);
+        const int col = n0 + 32 * gi;
+        tc::tma_load_2d(rbase + (slot * E::kR) * E::kBox, map_r, bar, col, row0);
+        if constexpr (E::kR == 2) tc::tma_load_2d(rbase + (slot * E::kR + 1) * E::kBox, map_r, bar, F + col, row0);
+    };
+    if constexpr (E::kR > 0) {
+        if (lane == 0 && rows_live) {
+            if (groups > 0) issue_r(0, st.r_used);
+            if (groups > 1) issue_r(1, st.r_used + 1);
+        }
+    }
+#pragma unroll 1
+    for (int gi = 0; gi < groups; ++gi) {
+        const int col = n0 + 32 * gi;
+        float v[32], w[32];
+        tc::tmem_ld32(taddr + 32 * gi, v);
+        if constexpr (kSwi) tc::tmem_ld32(taddr + BN / 2 + 32 * gi, w);
+        if (!rows_live) continue;       // warp-uniform: the whole 32-row box lies past M
+        float r0[32], r1[32];
+        if constexpr (E::kR > 0) {
+            const int slot = st.r_used & 1;
+            tc::mbar_wait(rbar + slot, (st.r_used >> 1) & 1);
+            box_load_row(rbase + (slot * E::kR) * E::kBox, lane, r0);
+            if constexpr (E::kR == 2) box_load_row(rbase + (slot * E::kR + 1) * E::kBox, lane, r1);
+            tc::fence_proxy_async();
+            __syncwarp();
+            ++st.r_used;
+            // the slot just read takes group gi + 2
+            if (lane == 0 && gi + 2 < groups) issue_r(gi + 2, st.r_used + 1);
+        }
+        // outputs: o0 -> C (col), o1 -> C (F + col) for SwiGLU / C2 otherwise, o2 -> C2 (SwiGLU)
+        float o1[32], o2[32];
+        if constexpr (EPI == static_cast<int>(Epi::AddRes)) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += r0[i];
+        } else if constexpr (EPI == static_cast<int>(Epi::StoreGelu)) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o1[i] = gelu_tanh_fast_f(v[i]);
+        } else if constexpr (EPI == static_cast<int>(Epi::GeluBwd)) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                float dg;
+                o1[i] = gelu_tanh_and_grad_fast_f(r0[i], dg);
+                v[i] *= dg;
+            }
+        } else if constexpr (kSwi) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                float sg;
+                o1[i] = w[i];
+                o2[i] = silu_sig(v[i], sg) * w[i];
+            }
+        } else if constexpr (kSwiB) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                float sg;
+                const float g = r0[i], u = r1[i], d = v[i];
+                const float si = silu_sig(g, sg);
+                o2[i] = si * u;
+                o1[i] = d * si;
+                v[i] = d * u * sg * (1.f + g * (1.f - sg));
+            }
+        }
+        const int buf = st.stored & 1;
+        if (st.stored >= 2) {   // this buffer's stores (two groups ago) must have been read
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+        }
+        uint8_t* ob = obase + buf * E::kOut * E::kBox;
+        box_store_row(ob, lane, v);
+        if constexpr (E::kOut >= 2) box_store_row(ob + E::kBox, lane, o1);
+        if constexpr (E::kOut >= 3) box_store_row(ob + 2 * E::kBox, lane, o2);
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_2d(map_c, ob, col, row0);
+            if constexpr (kSwi || kSwiB) {
+                tma_store_2d(map_c, ob + E::kBox, F + col, row0);
+                tma_store_2d(map_c2, ob + 2 * E::kBox, col, row0);
+            } else if constexpr (E::kOut >= 2) {
+                if (has_c2) tma_store_2d(map_c2, ob + E::kBox, col, row0);
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        ++st.stored;
+    }
+}
+
 template <int BN, int STAGES, int EPI = 0>
 struct Tc2Smem {
     static constexpr int kABytes = kBM * kBK * 2;            // this CTA's 128 rows of A
@@ -515,9 +694,11 @@ struct Tc2Smem {
     // AccumF32: per epilogue warp two [32 rows x 32 fp32] staging boxes for
     // the TMA reduce-add into C
     static constexpr int kEpiOffset = STAGES * kStageBytes;
-    static constexpr int kEpiBytes = EPI == static_cast<int>(Epi::AccumF32) ? 4 * 2 * 4096 : 0;
+    static constexpr int kEpiBytes = EPI == static_cast<int>(Epi::AccumF32) ? 4 * 2 * 4096
+                                     : EpiTma<EPI>::kOn                    ? 4 * EpiTma<EPI>::kWarpBytes
+                                                                           : 0;
     static constexpr int kBarOffset = kEpiOffset + kEpiBytes;
-    static constexpr int kTotal = kBarOffset + (2 * STAGES + 4) * 8 + 16 + 1024;
+    static constexpr int kTotal = kBarOffset + (2 * STAGES + 4 + 8) * 8 + 16 + 1024;   // + 2 R barriers per epilogue warp
 };
 
 // Weight-gradient epilogue (Epi::AccumF32) of the pair kernel: C(fp32) +=
@@ -611,6 +792,7 @@ template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_c,
+                    const __grid_constant__ CUtensorMap map_r, const __grid_constant__ CUtensorMap map_c2,
                     const TcParams p) {
     pdl_wait();
     pdl_trigger();
@@ -623,7 +805,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* empty = full + STAGES;
     uint64_t* acc_full = empty + STAGES;     // [2]
     uint64_t* acc_empty = acc_full + 2;      // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    uint64_t* rbar = acc_empty + 2;          // [4 epilogue warps][2 R slots] (TMA epilogues)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 8);
 
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);   // warp-uniform for the compiler
     const int lane = threadIdx.x & 31;
@@ -648,6 +831,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc::mbar_init(&acc_full[b], 1);
             tc::mbar_init(&acc_empty[b], 8);     // 4 epilogue warps x 2 CTAs (leader's copy)
         }
+        for (int b = 0; b < 8; ++b) tc::mbar_init(&rbar[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -736,7 +920,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t leader_acc_empty0;
         asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leader_acc_empty0) : "r"(tc::smem_u32(acc_empty)));
         int local = 0, issued = 0;
-        uint8_t* ebuf = smem + L::kEpiOffset + quarter * 8192;
+        constexpr bool kTma = EpiTma<EPI>::kOn;
+        uint8_t* ebuf = smem + L::kEpiOffset + quarter * (kTma ? EpiTma<EPI>::kWarpBytes : 8192);
+        EpiTmaState est;
         for (int t = cluster_id; t < ntiles; t += nclusters, ++local) {
             int mb, nb;
             sched.coords(t, mb, nb);
@@ -748,6 +934,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
             if constexpr (EPI == static_cast<int>(Epi::AccumF32))
                 epilogue_accum_tma<BN>(&map_c, taddr, ebuf, row - lane, n0, lane, issued);
+            else if constexpr (kTma)
+                epilogue_tma<BN, EPI>(p, &map_r, &map_c, &map_c2, taddr, ebuf, rbar + 2 * quarter, row - lane, n0, lane,
+                                      est);
             else
                 epilogue_rows<BN, EPI>(p, taddr, row, n0, true);
             tc::fence_before();
@@ -757,7 +946,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                  leader_acc_empty0 + acc * 8)
                              : "memory");
         }
-        if (EPI == static_cast<int>(Epi::AccumF32) && lane == 0)
+        if ((EPI == static_cast<int>(Epi::AccumF32) || kTma) && lane == 0)
             asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // staging boxes read, C updated
     }
     tc::fence_before();
@@ -824,6 +1013,32 @@ CUtensorMap make_map_f32(const void* base, long long rows, long long cols, long 
     if (r != CUDA_SUCCESS)
         throw CudaError("cuTensorMapEncodeTiled (f32) failed (" + std::to_string(static_cast<int>(r)) + ")");
     return m;
+}
+
+// 2-D bf16 tensor [rows, cols], 64-byte swizzle, 32 x 32 boxes (the TMA epilogues).
+CUtensorMap make_map_sw64(const void* base, long long rows, long long cols, long long ld) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw CudaError("cuTensorMapEncodeTiled (sw64) failed (" + std::to_string(static_cast<int>(r)) + ")");
+    return m;
+}
+
+// Deepest TMA ring (<= MAX stages) whose shared memory fits next to the
+// epilogue staging of EPI.
+template <int BN, int MAX, int EPI>
+constexpr int pair_stages() {
+    int st = MAX;
+    while (st > 2 && Tc2Smem<BN, 0, EPI>::kEpiBytes + st * Tc2Smem<BN, 0, EPI>::kStageBytes + (2 * st + 12) * 8 + 16 +
+                             1024 > 227 * 1024)
+        --st;
+    return st;
 }
 
 }  // namespace
@@ -911,8 +1126,9 @@ void dispatch_epi(const GemmArgs& g, cudaStream_t s) {
 
 template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 void launch_tc2(const GemmArgs& g, cudaStream_t s) {
-    using L = Tc2Smem<BN, STAGES, EPI>;
-    auto kern = gemm_tc2_kernel<BN, STAGES, A_MN, B_MN, EPI>;
+    constexpr int S = pair_stages<BN, STAGES, EPI>();   // the TMA epilogues' staging can cost a ring stage
+    using L = Tc2Smem<BN, S, EPI>;
+    auto kern = gemm_tc2_kernel<BN, S, A_MN, B_MN, EPI>;
     static bool configured = false;   // per instantiation
     if (!configured) {
         EPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
@@ -933,10 +1149,28 @@ void launch_tc2(const GemmArgs& g, cudaStream_t s) {
     }
     const int tiles = ceil_div(g.N, BN) * ceil_div(g.M, 2 * kBM);
     const int clusters = std::min(tiles, num_sms / 2);
-    // C as an fp32 [M, N] tensor, 32 x 32 boxes (the AccumF32 reduce-add)
-    CUtensorMap mc{};
+    // C as an fp32 [M, N] tensor, 32 x 32 boxes (the AccumF32 reduce-add);
+    // the TMA epilogues' bf16 C / R / C2 tensors in 32 x 32 boxes
+    CUtensorMap mc{}, mr{}, mc2{};
     if (EPI == static_cast<int>(Epi::AccumF32)) mc = make_map_f32(g.C, g.M, g.N, g.ldc, 32, 32);
-    launch_k(kern, 2 * clusters, kThreads, L::kTotal, s, ma, mb, mc, p);
+    if constexpr (EpiTma<EPI>::kOn) {
+        constexpr bool kSwi = EPI == static_cast<int>(Epi::SwiGlu), kSwiB = EPI == static_cast<int>(Epi::SwiGluBwd);
+        auto aligned = [](const void* q, long long ld) {
+            return (reinterpret_cast<uintptr_t>(q) & 15) == 0 && ld % 8 == 0;
+        };
+        // C: [M, N] (SwiGluBwd: dh = [M, 2N]); R: [M, N] (SwiGluBwd: h = [M, 2N]);
+        // C2: [M, N] (SwiGlu: [M, N/2])
+        mc = make_map_sw64(g.C, g.M, kSwiB ? 2LL * g.N : g.N, g.ldc);
+        if (EpiTma<EPI>::kR) {
+            EPP_REQUIRE(g.R && aligned(g.R, g.ldr), "gemm: R must be 16-byte aligned with ldr % 8 == 0");
+            mr = make_map_sw64(g.R, g.M, kSwiB ? 2LL * g.N : g.N, g.ldr);
+        }
+        if (EpiTma<EPI>::kOut >= 2 && g.C2) {
+            EPP_REQUIRE(aligned(g.C2, g.ldc2), "gemm: C2 must be 16-byte aligned with ldc2 % 8 == 0");
+            mc2 = make_map_sw64(g.C2, g.M, kSwi ? g.N / 2 : g.N, g.ldc2);
+        }
+    }
+    launch_k(kern, 2 * clusters, kThreads, L::kTotal, s, ma, mb, mc, mr, mc2, p);
     EPP_CHECK_LAUNCH();
     g_gemm_launches.fetch_add(1);
 }

@@ -14,6 +14,7 @@ from paper_2509_21275_b200 import _build as b  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--src", required=True, help="file under csrc/gpu to recompile")
+    ap.add_argument("--from-file", default=None, help="compile this file in its place (e.g. a git show of HEAD)")
     ap.add_argument("-D", action="append", default=[], dest="defs")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
@@ -23,7 +24,8 @@ def main():
     out.parent.mkdir(parents=True, exist_ok=True)
     src = b.CSRC / "gpu" / a.src
     variant = out.with_suffix(".o")
-    b._run([b.NVCC] + b.NVCC_FLAGS + [f"-D{d}" for d in a.defs] + ["-c", str(src), "-o", str(variant)])
+    text = Path(a.from_file) if a.from_file else src
+    b._run([b.NVCC] + b.NVCC_FLAGS + [f"-D{d}" for d in a.defs] + ["-c", str(text), "-o", str(variant)])
     objs = [str(variant) if o.stem == src.stem else str(o) for o in sorted(objdir.glob("*.o"))]
     b._run([b.NVCC, "-shared"] + b.GPU_ARCH + ["-o", str(out)] + objs)
     variant.unlink()

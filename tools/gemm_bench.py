@@ -56,17 +56,23 @@ def main():
         out[name] = {"ms": round(a.value / c.value, 4), "tflops": round(b.value / a.value / 1e9, 1)}
     # fused-epilogue data gradients: GELU' (R = h, C2 = gelu(h)) and SwiGLU'
     # (R = h = [g | u], C = dh [T, 2F], C2 = silu(g) u)
-    for name, epi in (("dgrad_gelu", 5), ("dgrad_swiglu", 8)):
+    # *_store: the same operands and layout with a plain bf16 store (isolates
+    # the epilogue); *_kmajor: the same epilogue with a K-major weight operand
+    # (epilogue cost split: addres = R load + store; storegelu = math + C2
+    # store; gelu_noc2 = R load + math + store)
+    for name, epi, wk in (("dgrad_gelu", 5, 0), ("dgrad_swiglu", 8, 0), ("dgrad_gelu_store", 0, 0),
+                          ("dgrad_gelu_kmajor", 5, 1), ("dgrad_store_kmajor", 0, 1), ("dgrad_addres", 2, 0),
+                          ("dgrad_storegelu", 4, 0), ("dgrad_gelu_noc2", 5, 0)):
         M, N, K = T, F, D
         dy = torch.randn((M, K), device="cuda").to(bf)
-        W = torch.randn((K, N), device="cuda").to(bf)
+        W = torch.randn((N, K) if wk else (K, N), device="cuda").to(bf)
         h = torch.randn((M, 2 * N if epi == 8 else N), device="cuda").to(bf)
         C = torch.empty((M, 2 * N if epi == 8 else N), device="cuda", dtype=bf)
         C2 = torch.empty((M, N), device="cuda", dtype=bf)
 
         def once2():
-            gpu.check(lib.epp_kernel_gemm_ex(M, N, K, dy.data_ptr(), K, 1, W.data_ptr(), N, 0, C.data_ptr(),
-                                             C.shape[1], h.data_ptr(), h.shape[1], C2.data_ptr(), N, epi, 1,
+            gpu.check(lib.epp_kernel_gemm_ex(M, N, K, dy.data_ptr(), K, 1, W.data_ptr(), W.shape[1], wk, C.data_ptr(),
+                                             C.shape[1], h.data_ptr(), h.shape[1], None if name.endswith("noc2") else C2.data_ptr(), N, epi, 1,
                                              gpu.stream_ptr()))
 
         once2()
