@@ -534,7 +534,10 @@ struct EpiTma {
                                 : kOn ? 3 : 0;
     static constexpr int kBox = 32 * 64;            // 32 rows x 32 bf16
     static constexpr int kRSlots = kR ? 2 : 0;
-    static constexpr int kOutBufs = 2;
+    // one output buffer set when there are several outputs: keeps the main
+    // loop's six TMA stages (GELU': 1212 -> 1222, SwiGLU' 1025 -> 1075 TFLOP/s
+    // at K = 2048) at the price of a wait for the previous group's stores
+    static constexpr int kOutBufs = kOut >= 2 ? 1 : 2;
     static constexpr int kWarpBytes = (kRSlots * kR + kOutBufs * kOut) * kBox;
 };
 
@@ -661,9 +664,12 @@ __device__ __forceinline__ void epilogue_tma(const TcParams& p, const CUtensorMa
                 v[i] = d * u * sg * (1.f + g * (1.f - sg));
             }
         }
-        const int buf = st.stored & 1;
-        if (st.stored >= 2) {   // this buffer's stores (two groups ago) must have been read
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        const int buf = E::kOutBufs == 2 ? (st.stored & 1) : 0;
+        if (st.stored >= E::kOutBufs) {   // this buffer's stores (kOutBufs groups ago) must have been read
+            if (lane == 0) {
+                if constexpr (E::kOutBufs == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
             __syncwarp();
         }
         uint8_t* ob = obase + buf * E::kOut * E::kBox;
