@@ -56,6 +56,7 @@ struct TcParams {
     bf16* C2;
     long long ldc2;
     RopeScatterArgs rope;
+    int defer;   // GemmArgs::defer_wait
 };
 
 // Persistent CTAs (one per SM) walk the output tiles in a grouped raster
@@ -359,7 +360,7 @@ template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, const TcParams p) {
-    pdl_wait();
+    if (!p.defer) pdl_wait();
     pdl_trigger();
     using L = TcSmem<BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
@@ -486,6 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) tc::mbar_arrive(&acc_empty[acc]);
         }
     }
+    if (p.defer) pdl_wait();   // completion of this grid implies the previous one's
     __syncthreads();
     if (warp == 1) {
         tc::fence_after();
@@ -800,7 +802,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_c,
                     const __grid_constant__ CUtensorMap map_r, const __grid_constant__ CUtensorMap map_c2,
                     const TcParams p) {
-    pdl_wait();
+    if (!p.defer) pdl_wait();   // deferred: see GemmArgs::defer_wait
     pdl_trigger();
     using L = Tc2Smem<BN, STAGES, EPI>;
     extern __shared__ uint8_t smem_raw[];
@@ -955,6 +957,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if ((EPI == static_cast<int>(Epi::AccumF32) || kTma) && lane == 0)
             asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // staging boxes read, C updated
     }
+    if (p.defer) pdl_wait();   // completion of this grid implies the previous one's
     tc::fence_before();
     cluster_sync_all();
     if (warp == 1) {
@@ -1087,7 +1090,7 @@ void launch_tc(const GemmArgs& g, cudaStream_t s) {
     const CUtensorMap mb = B_MN ? make_map(g.B, g.K, g.N, g.ldb, 64, kBK)
                                 : make_map(g.B, g.N, g.K, g.ldb, kBK, BN);
     TcParams p{g.M, g.N, g.K, g.C, g.ldc, static_cast<const bf16*>(g.R), g.ldr,
-               static_cast<bf16*>(g.C2), g.ldc2, g.rope ? *g.rope : RopeScatterArgs{}};
+               static_cast<bf16*>(g.C2), g.ldc2, g.rope ? *g.rope : RopeScatterArgs{}, g.defer_wait ? 1 : 0};
     static int num_sms = 0;
     if (!num_sms) {
         int dev = 0;
@@ -1146,7 +1149,7 @@ void launch_tc2(const GemmArgs& g, cudaStream_t s) {
     const CUtensorMap mb = B_MN ? make_map(g.B, g.K, g.N, g.ldb, 64, kBK)
                                 : make_map(g.B, g.N, g.K, g.ldb, kBK, BN / 2);
     TcParams p{g.M, g.N, g.K, g.C, g.ldc, static_cast<const bf16*>(g.R), g.ldr,
-               static_cast<bf16*>(g.C2), g.ldc2, g.rope ? *g.rope : RopeScatterArgs{}};
+               static_cast<bf16*>(g.C2), g.ldc2, g.rope ? *g.rope : RopeScatterArgs{}, g.defer_wait ? 1 : 0};
     static int num_sms = 0;
     if (!num_sms) {
         int dev = 0;

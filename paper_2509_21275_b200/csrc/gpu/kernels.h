@@ -56,6 +56,13 @@ struct GemmArgs {
     const RopeScatterArgs* rope = nullptr;   // Epi::RopeScatter
     Epi epi = Epi::Store;
     DType dtype = DType::BF16;
+    // Deferred dependency wait (tcgen05 kernels): the caller guarantees this
+    // GEMM neither reads nor writes anything the PREVIOUS kernel in the stream
+    // touches (e.g. a weight gradient behind an independent data gradient).
+    // The kernel then skips its programmatic-launch wait at entry and waits
+    // only before exiting, so its CTAs take the SMs the previous GEMM's last
+    // wave leaves idle; its completion still implies the previous kernel's.
+    bool defer_wait = false;
 };
 
 void gemm(const GemmArgs& a, cudaStream_t s);

@@ -270,6 +270,7 @@ public:
         EPP_REQUIRE(dt == DType::F32 || m.head_dim == 64 || m.head_dim == 128,
                     "bf16 attention supports head_dim 64 or 128");
         keep_pool_reserved();
+        if (const char* e = getenv("EPP_DEFER_WGRAD"); e && e[0] == '0') defer_wgrad_ = false;   // A/B switch
         if (const char* e = getenv("EPP_SMEM_PREF"); e && e[0] == '1')
             EPP_CUDA(cudaDeviceSetCacheConfig(cudaFuncCachePreferShared));
         D_ = m.hidden;
@@ -580,6 +581,7 @@ public:
             LayerSaved& L = cs.layers[j];
             const void* x = j == 0 ? cs.x_in.get() : cs.layers[j - 1].x_out.get();
             if (!L.full) {   // recompute
+                flush_wgrad(false, s);
                 cudaEvent_t ra = tr ? tracer_.record(s) : nullptr;
                 layer_forward(cs, j, x, L, nullptr, /*skip_out=*/true, s);
                 if (tr) tr->rec.emplace_back(ra, tracer_.record(s));
@@ -596,12 +598,14 @@ public:
                 dx_ptr = dx.get();
             }
             layer_backward(cs, j, x, L, dy_ptr, dx_ptr, s);
-            bucket_ready(layer_bucket(j), s);
+            if (pending_.live) pending_.bucket = layer_bucket(j);   // its dWqkv is still pending
+            else bucket_ready(layer_bucket(j), s);
             drop_full(L);
             L.x_out.release();
             dy = std::move(dx);
             dy_ptr = dx_ptr;
         }
+        flush_wgrad(false, s);
         if (has_embed_) {
             embed_bwd(dt_, c.token_ids, dy_ptr, grad(emb_), cs.T, D_, s);
             bucket_ready(0, s);
@@ -1023,11 +1027,22 @@ private:
         swb.ldr = F1_;
         swb.C2 = act.get();
         swb.ldc2 = F_;
+        Buf dxn(&pool_, static_cast<size_t>(T) * D_ * e, s);
+        auto dgrad_w1 = [&] {
+            gemm(mk(T, D_, F1_, dh.get(), F1_, true, work(P.w1), D_, false, dxn.get(), D_), s);  // dXn2
+        };
+        // Where the W2 data-gradient epilogue forms A, dW2 runs after the
+        // (independent) W1 data gradient and fills that GEMM's last wave.
+        bool w1_done = false;
         if (llama_ && gemm_swiglu_fusable(swb)) {
             gemm(swb, s);
-            wgrad(D_, F_, T, dy, D_, act.get(), F_, grad(P.w2), s);                    // dW2 += dY^T A
+            flush_wgrad(true, s);   // the previous layer's dWqkv
+            dgrad_w1();
+            w1_done = true;
+            wgrad(D_, F_, T, dy, D_, act.get(), F_, grad(P.w2), s, true);              // dW2 += dY^T A
             act.release();
         } else if (llama_) {
+            flush_wgrad(false, s);
             act_fwd(dt_, 1, L.h.get(), act.get(), T, F_, s);
             wgrad(D_, F_, T, dy, D_, act.get(), F_, grad(P.w2), s);                    // dW2 += dY^T A
             act.release();
@@ -1044,11 +1059,13 @@ private:
             g.C2 = act.get();
             g.ldc2 = F_;
             gemm(g, s);
-            wgrad(D_, F_, T, dy, D_, act.get(), F_, grad(P.w2), s);                    // dW2 += dY^T A
+            flush_wgrad(true, s);   // the previous layer's dWqkv
+            dgrad_w1();
+            w1_done = true;
+            wgrad(D_, F_, T, dy, D_, act.get(), F_, grad(P.w2), s, true);              // dW2 += dY^T A
             act.release();
         }
-        Buf dxn(&pool_, static_cast<size_t>(T) * D_ * e, s);
-        gemm(mk(T, D_, F1_, dh.get(), F1_, true, work(P.w1), D_, false, dxn.get(), D_), s);  // dXn2
+        if (!w1_done) dgrad_w1();
         // norm backward also re-creates xn = norm(x_mid) (one pass over x_mid)
         // for the dW1 weight gradient
         Buf xn(&pool_, static_cast<size_t>(T) * D_ * e, s);
@@ -1057,12 +1074,14 @@ private:
                  llama_ ? nullptr : L.mean2.get<float>(), L.rstd2.get<float>(), dy, dxm.get(),
                  grad(P.ln2_w), P.ln2_b >= 0 ? grad(P.ln2_b) : nullptr, T, D_, s,
                  P.ln2_b >= 0 ? work(P.ln2_b) : nullptr, xn.get());
-        wgrad(F1_, D_, T, dh.get(), F1_, xn.get(), D_, grad(P.w1), s);                     // dW1
-        dh.release();
         // ---- attention ----
+        // dW1 and dWo do not depend on the out-projection's data gradient:
+        // they follow it and fill its last wave (and each other's)
         Buf dout(&pool_, static_cast<size_t>(T) * Dq * e, s);
         gemm(mk(T, Dq, D_, dxm.get(), D_, true, work(P.wo), Dq, false, dout.get(), Dq), s);  // dO
-        wgrad(D_, Dq, T, dxm.get(), D_, L.o.get(), Dq, grad(P.wo), s);                       // dWo
+        wgrad(F1_, D_, T, dh.get(), F1_, xn.get(), D_, grad(P.w1), s, true);               // dW1
+        dh.release();
+        wgrad(D_, Dq, T, dxm.get(), D_, L.o.get(), Dq, grad(P.wo), s, true);               // dWo
         Buf delta(&pool_, sizeof(float) * static_cast<size_t>(H_) * T, s);
         Buf dqkv(&pool_, static_cast<size_t>(T) * Nqkv_ * e, s);
         AttnArgs a = attn_args(cs, j);
@@ -1101,9 +1120,33 @@ private:
                  L.rstd1.get<float>(), dxm.get(), dx, grad(P.ln1_w),
                  P.ln1_b >= 0 ? grad(P.ln1_b) : nullptr, T, D_, s,
                  P.ln1_b >= 0 ? work(P.ln1_b) : nullptr, xn.get());
-        wgrad(Nqkv_, D_, T, dqkv.get(), Nqkv_, xn.get(), D_, grad(P.wqkv), s);
-        dqkv.release();
-        xn.release();
+        // dWqkv waits for the next kernel that does not touch its operands
+        // (the next layer's first data gradient): flush_wgrad()
+        GemmArgs wq = mk(Nqkv_, D_, T, dqkv.get(), Nqkv_, false, xn.get(), D_, false, grad(P.wqkv), D_);
+        wq.epi = Epi::AccumF32;
+        pending_ = PendingWgrad{wq, std::move(dqkv), std::move(xn), -1, true};
+    }
+
+    // A weight gradient held back until an independent GEMM has been
+    // enqueued; it then follows that GEMM with a deferred dependency wait
+    // (GemmArgs::defer_wait) and fills its last wave.  `bucket`: the DP
+    // bucket whose gradients it completes (recorded after it runs).
+    struct PendingWgrad {
+        GemmArgs g;
+        Buf a, b;
+        int bucket = -1;
+        bool live = false;
+    };
+    PendingWgrad pending_;
+    void flush_wgrad(bool defer, cudaStream_t s) {
+        if (!pending_.live) return;
+        pending_.g.defer_wait = defer && defer_wgrad_;
+        gemm(pending_.g, s);
+        pending_.a.release();
+        pending_.b.release();
+        pending_.live = false;
+        if (pending_.bucket >= 0) bucket_ready(pending_.bucket, s);
+        pending_.bucket = -1;
     }
 
     // Last stage: final norm, LM head, cross-entropy and its backward through
@@ -1131,7 +1174,7 @@ private:
             // dXf = dLogits Wlm ; dWlm += dLogits^T Xf
             gemm(mk(n, D_, V, logits.get(), V, true, work(lm_), D_, false,
                     cs.dxf.get<uint8_t>() + static_cast<size_t>(r0) * D_ * e, D_), s);
-            wgrad(V, D_, n, logits.get(), V, xr, D_, grad(lm_), s);
+            wgrad(V, D_, n, logits.get(), V, xr, D_, grad(lm_), s, true);   // independent of dXf
         }
         auto slot = loss_slot_.find(c.id);
         if (slot == loss_slot_.end()) {
@@ -1153,10 +1196,13 @@ private:
         return g;
     }
     // dW[M,N] += sum_t dY[t, m] X[t, n]  (both operands MN-major)
+    // defer: the previous kernel in the stream is independent of this one
+    // (GemmArgs::defer_wait): the weight gradient fills its last wave.
     void wgrad(int M, int N, int T, const void* dy, long long ldy, const void* x, long long ldx,
-               float* dw, cudaStream_t s) const {
+               float* dw, cudaStream_t s, bool defer = false) const {
         GemmArgs g = mk(M, N, T, dy, ldy, false, x, ldx, false, dw, N);
         g.epi = Epi::AccumF32;
+        g.defer_wait = defer && defer_wgrad_;
         gemm(g, s);
     }
 
@@ -1166,6 +1212,7 @@ private:
     DType dt_;
     int D_ = 0, H_ = 0, Hkv_ = 0, hd_ = 0, F_ = 0, F1_ = 0, Nqkv_ = 0;
     bool llama_ = false;
+    bool defer_wgrad_ = true;
     std::vector<Param> params_;
     static constexpr long long kBucketAlign = 4096;
     std::vector<long long> bucket_off_;
