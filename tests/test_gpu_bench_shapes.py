@@ -207,3 +207,22 @@ def test_f32_at_bench_width(planner, arch):
         assert n == n_ref and abs(s - s_ref) <= 1e-5 * abs(s_ref), (cid, s, s_ref)
     for name, g in ref_grads.items():
         assert rel(grads[name], g) < 1e-3, (name, rel(grads[name], g))
+
+
+@pytest.mark.parametrize("arch,dp", [("gpt-1.3b", 2), ("llama-7b", 1)])
+def test_deferred_wgrad_bit_identical(planner, monkeypatch, arch, dp):
+    """Weight gradients launched with a deferred dependency wait
+    (GemmArgs::defer_wait: they overlap the preceding independent data
+    gradient) give the same bits as the fully ordered stream (the stage reads
+    EPP_DEFER_WGRAD when it is created)."""
+    m = WIDTHS[arch]
+    plan = make_plan(planner, m, dp, False)
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("EPP_DEFER_WGRAD", flag)
+        out[flag] = run_cuda(m, plan, "bf16")
+    (l0, c0, g0, k0), (l1, c1, g1, k1) = out["0"], out["1"]
+    assert (l0, c0) == (l1, c1)
+    assert k0 == k1
+    for name, g in g0.items():
+        assert torch.equal(g, g1[name]), name
