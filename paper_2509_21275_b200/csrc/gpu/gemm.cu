@@ -67,7 +67,10 @@ struct TileSched {
     __device__ __forceinline__ void coords(int t, int& mb, int& nb) const {
         // groups of 8 M-blocks: consecutive tiles share the same B column
         // panel while sweeping a small set of A row panels (L2 reuse).
-        constexpr int G = 8;
+#ifndef EPP_RASTER_G
+#define EPP_RASTER_G 8
+#endif
+        constexpr int G = EPP_RASTER_G;
         const int per_group = G * tiles_n;
         const int g = t / per_group;
         const int first_m = g * G;
