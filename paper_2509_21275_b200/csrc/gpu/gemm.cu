@@ -67,6 +67,10 @@ struct TileSched {
     __device__ __forceinline__ void coords(int t, int& mb, int& nb) const {
         // groups of 8 M-blocks: consecutive tiles share the same B column
         // panel while sweeping a small set of A row panels (L2 reuse).
+        // 8 measured best in the step (profiles/r02_raster_group_ab.json):
+        // 16 re-reads B panels half as often and is +2.5 % on isolated
+        // forward GEMMs, but neutral-to-worse in the power-capped step; 32
+        // overflows L2 with A panels (-4 %)
 #ifndef EPP_RASTER_G
 #define EPP_RASTER_G 8
 #endif
