@@ -131,8 +131,9 @@ class ClockSampler:
         load = [int(r[1]) for r in rows if float(r[3] or 0) > 200] or sm
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        pw = [float(r[3]) for r in rows if float(r[3] or 0) > 200]
         return {"sm_mhz": statistics.median(load), "sm_max_mhz": int(rows[0][2]), "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(rows), "power_w": statistics.median(pw) if pw else None}
 
 
 def step_flops(m, plan):
@@ -484,8 +485,16 @@ def run_ours(args):
                                                    and not k.startswith("gemm_"))) / nprof,
         "clocks": clk.summary(),
         "e2e": e2e,
+        # the step runs at the board's power cap (sw_power_cap): throughput
+        # is energy per token, which this reports (median board power under
+        # load x device time per token)
+        "energy": None,
         "trace": trace_block,
     }
+    if out["clocks"] and out["clocks"].get("power_w") and out["value"]:
+        # rank 0's board power, taken as every rank's (whole-job tokens/s)
+        out["energy"] = {"power_w_per_gpu": out["clocks"]["power_w"],
+                         "joules_per_token": out["clocks"]["power_w"] * world / out["value"]}
     # HBM: what the planner was told against what the stage actually used
     # (weights/grads/Adam state + the activation pool's high-water mark)
     free_b, total_b = torch.cuda.mem_get_info()
